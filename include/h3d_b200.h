@@ -1,0 +1,157 @@
+/*
+ * h3d_b200 — C-ABI of the B200-native HODLR3D engine (drop-in boundary).
+ *
+ * The reference has no C ABI; its operator surface for this path is the C++
+ * free-function API of /root/reference/proj/include/h3d/hmatrix.hpp and
+ * parallel.hpp. Each entry point below names the reference interface it
+ * replaces. Plain pointers and sizes only; no torch types. The C++ host layer
+ * (paper_2307_16303_b200/csrc/h3d_b200.hpp) restores the reference's C++
+ * signatures and exception types on top of this header.
+ *
+ * Error convention: every int-returning call returns H3D_OK (0) or a status
+ * below; h3d_last_error() returns the thread-local message. Status codes map
+ * to the reference exceptions:
+ *   H3D_EINVAL       -> std::invalid_argument
+ *   H3D_EDEGEN_GEOM  -> h3d::DegenerateGeometryError   (kernel.hpp:64-66)
+ *   H3D_EDEGEN_DIST  -> h3d::DegenerateDistributionError (octree.hpp:41-43)
+ *   H3D_ECUDA / H3D_ENCCL / H3D_ENOMEM -> std::runtime_error
+ *   H3D_EUNSUPPORTED -> std::invalid_argument (e.g. custom std::function kernels,
+ *                       kernel.hpp:56-57, cannot cross to the device)
+ */
+#ifndef H3D_B200_H
+#define H3D_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define H3D_B200_ABI_VERSION 1
+
+enum h3d_status {
+  H3D_OK = 0,
+  H3D_EINVAL = 1,
+  H3D_EDEGEN_GEOM = 2,
+  H3D_EDEGEN_DIST = 3,
+  H3D_ECUDA = 4,
+  H3D_ENCCL = 5,
+  H3D_ENOMEM = 6,
+  H3D_EUNSUPPORTED = 7
+};
+
+/* Kernel ids follow h3d::KernelId (reference kernel.hpp:42). */
+enum h3d_kernel { H3D_LAPLACE3D = 0, H3D_R4 = 1, H3D_HELMHOLTZ_RE = 2 };
+
+/* Near-field (dense leaf block) storage; mirrors h3d::DenseMode
+ * (reference hmatrix.hpp:12-14): Cached stores the blocks at initialize,
+ * OnTheFly regenerates them in every matvec. */
+enum h3d_near_mode { H3D_NEAR_STORED = 0, H3D_NEAR_MATRIX_FREE = 1 };
+
+/* Options; the first six fields are h3d::HmatOptions (hmatrix.hpp:16-22) and
+ * KernelSpec (kernel.hpp:46-53). */
+typedef struct {
+  int kernel_id;        /* h3d_kernel */
+  double diagonal;      /* KernelSpec::diagonal, entry (i,i) */
+  int n_max;            /* leaf threshold: depth = min l with max occupancy < n_max */
+  double epsilon;       /* ACA tolerance */
+  int depth_cap;        /* Morton resolution / DegenerateDistributionError cap */
+  int64_t max_rank;     /* 0: min(|X|,|Y|) per block */
+  int near_mode;        /* h3d_near_mode */
+  int device;           /* CUDA device ordinal */
+  int shard_rank;       /* Morton-subtree row ownership (parallel.hpp:9-30 analogue) */
+  int shard_world;      /* 1 = single GPU owns every row */
+  int64_t reserved[8];
+} h3d_options;
+
+/* Per-call matvec timing, milliseconds (CUDA events on the engine stream);
+ * analogue of h3d::MatvecTiming (hmatrix.hpp:60-66). */
+typedef struct {
+  double total_ms;      /* whole call incl. copies */
+  double h2d_ms;        /* host x -> device (host mode only) */
+  double gather_ms;     /* x permutation to Morton order */
+  double exchange_ms;   /* multi-GPU all-gather of x (0 on one GPU) */
+  double phase1_ms;     /* V^T x over the factor pool (+ partial reduce) */
+  double phase2_ms;     /* near field + U t, fused un-permute */
+  double d2h_ms;        /* device b -> host (host mode only) */
+  int64_t launches;     /* kernels launched by this call */
+} h3d_timing;
+
+/* Representation statistics; superset of h3d::RepStats (hmatrix.hpp:73-85). */
+typedef struct {
+  int depth;
+  int max_rank;
+  int64_t n;
+  int64_t lowrank_blocks;     /* ordered admissible blocks (reference lr_levels total) */
+  int64_t aca_pairs;          /* unordered pairs compressed (symmetric storage) */
+  int64_t sum_rank;           /* sum over pairs */
+  int64_t factor_doubles;     /* sum over pairs of r (m + n): the factor pool */
+  int64_t factor_bytes_alloc; /* W incl. padding */
+  int64_t tvec_doubles;       /* S pool */
+  int64_t near_blocks;        /* dense leaf blocks (reference dense_blocks) */
+  int64_t near_entries;       /* sum |X||Y| over dense blocks */
+  int64_t near_bytes_stored;  /* 0 in matrix-free mode */
+  uint64_t ref_float_count;   /* reference RepStats::float_count convention: sum r^2 (ordered
+                                 blocks, each pair counted twice) + dense areas */
+  uint64_t ref_int_count;     /* 2 * sum r over ordered blocks */
+  double compression_ratio;   /* ref_float_count / N^2 */
+  double build_ms_tree;
+  double build_ms_lists;
+  double build_ms_aca_rank;
+  double build_ms_aca_write;
+  double build_ms_total;
+  int64_t phase1_items;
+  int64_t owned_row_begin;    /* shard rows [begin, end) in Morton order */
+  int64_t owned_row_end;
+  int64_t reserved[6];
+} h3d_stats;
+
+typedef struct h3d_dev h3d_dev;
+
+const char* h3d_last_error(void);
+int h3d_abi_version(void);
+void h3d_default_options(h3d_options* opt);
+
+/* Input generation, bit-identical to the reference:
+ * generate_points(UniformRandom, n, seed) (kernel.cpp:88-95), AoS xyz[3n];
+ * the CLI right-hand side mt19937_64(seed), 2u-1 (tools/h3d.cpp:135-137). */
+int h3d_generate_points(int64_t n, uint64_t seed, double* xyz);
+void h3d_random_vector(int64_t n, uint64_t seed, double* out);
+
+/* Replaces h3d::initialize(PointSet, KernelSpec, Variant::Hodlr3d, HmatOptions)
+ * (hmatrix.hpp:57-58 / hmatrix.cpp:52-151): octree + lists + batched ACA on
+ * the device. xyz is host AoS (Point3[n]). */
+int h3d_dev_create(const double* xyz, int64_t n, const h3d_options* opt, h3d_dev** out);
+void h3d_dev_destroy(h3d_dev* dev);
+
+/* Replaces h3d::matvec(rep, x, MatvecTiming*) (hmatrix.hpp:70-71): b = A~ x in
+ * ORIGINAL point order. where = 0: x/b are host pointers (copies included,
+ * returns after b is written); where = 1: device pointers on dev's GPU
+ * (returns after the result is complete). timing may be NULL. */
+int h3d_dev_matvec(h3d_dev* dev, const double* x, double* b, int where, h3d_timing* timing);
+
+/* Replaces h3d::stats(rep) (hmatrix.hpp:85). */
+int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out);
+
+/* Parity exports (tree and lists are bit-exact with reference octree.cpp):
+ * perm[n] (permuted position -> original index, Octree::perm, octree.hpp:61);
+ * offsets[8^level + 1] (node m = [off[m], off[m+1]), Octree::levels). */
+int h3d_dev_export_tree(const h3d_dev* dev, int32_t* perm, int level, int64_t* offsets);
+/* Interaction list CSR at a level, kind 0 inter / 1 near_edge / 2 near_face
+ * (NodeLists, octree.hpp:88-93). ids may be NULL to query *count. */
+int h3d_dev_export_list(const h3d_dev* dev, int level, int kind, int32_t* offsets,
+                        int32_t* ids, int64_t* count);
+/* Compressed pairs at a level: (X, Y, rank) with X < Y (Morton ids). */
+int h3d_dev_export_pairs(const h3d_dev* dev, int level, int32_t* x, int32_t* y, int32_t* rank,
+                         int64_t* count);
+
+/* Multi-GPU (Morton-subtree ownership; replaces parallel_matvec,
+ * parallel.hpp:65-66). One process per GPU: rank 0 calls h3d_nccl_get_id and
+ * broadcasts the 128 bytes; every rank attaches before its first matvec. */
+int h3d_nccl_get_id(void* id128);
+int h3d_dev_attach_nccl(h3d_dev* dev, const void* id128, int rank, int world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* H3D_B200_H */

@@ -1091,3 +1091,25 @@ int orc_exact_rows(const double* xyz, int64_t n, int kernel_id, double diag,
   }
   return bad;
 }
+
+/* Raw uniform01 stream (kernel.hpp:24-26), for reproducing the reference
+ * tests' geometries (test_lowrank.cpp:13-21 unit_cube_points). */
+void orc_uniform_stream(int64_t n, uint64_t seed, double* out) {
+  mt64 g;
+  mt64_seed(&g, seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = uniform01(&g);
+}
+
+/* Tree and lists only (no ACA): for bit-exact parity at full BASELINE sizes. */
+int orc_tree_lists(const double* xyz, int64_t n, int n_max, int depth_cap, orc_rep** out) {
+  *out = NULL;
+  orc_rep* rep = (orc_rep*)calloc(1, sizeof(orc_rep));
+  int st = build_tree(rep, xyz, n, n_max, depth_cap);
+  if (st != ORC_OK) {
+    orc_free(rep);
+    return st;
+  }
+  build_lists(rep);
+  *out = rep;
+  return ORC_OK;
+}

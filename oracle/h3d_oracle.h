@@ -78,6 +78,11 @@ int orc_exact_rows(const double* xyz, int64_t n, int kernel_id, double diag,
 
 void orc_set_threads(int n);
 
+/* raw uniform01 stream of mt19937_64(seed) (kernel.hpp:24-26) */
+void orc_uniform_stream(int64_t n, uint64_t seed, double* out);
+/* build_tree + build_interaction_lists only (octree.cpp:76-260), no ACA */
+int orc_tree_lists(const double* xyz, int64_t n, int n_max, int depth_cap, orc_rep** out);
+
 #ifdef __cplusplus
 }
 #endif

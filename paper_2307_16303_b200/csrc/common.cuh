@@ -1,0 +1,100 @@
+// Shared device helpers for the B200 HODLR3D engine (sm_100a only).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "h3d_b200 targets sm_100a only"
+#endif
+
+namespace h3db {
+
+// Kernel ids follow h3d::KernelId (reference kernel.hpp:42).
+enum KernelKind : int { kLaplace = 0, kR4 = 1, kHelmholtz = 2 };
+
+// Device status flags (bitwise OR'ed by kernels, read by the host).
+enum DevFlag : unsigned {
+  kFlagDegenGeom = 1u,    // r < 1e-14 between distinct points (kernel.cpp:59-71)
+  kFlagAcaOverflow = 2u,  // ACA workspace rank capacity exhausted
+  kFlagOutOfDomain = 4u,  // point outside [-1,1]^3 (octree.cpp:91-97)
+};
+
+constexpr double kCoincidentTol2 = 1e-14 * 1e-14;
+
+// Radial map on r^2 (reference lowrank.cpp:51-62: LaplaceF, QuarticF,
+// HelmholtzF). Laplace uses the fp64 reciprocal square root (<= 1 ulp from
+// 1/sqrt(r2)); parity is tolerance-based (north_star: 10x ACA tol).
+template <int K>
+__device__ __forceinline__ double kernel_r2(double r2) {
+  if constexpr (K == kLaplace) {
+    return rsqrt(r2);
+  } else if constexpr (K == kR4) {
+    return 1.0 / (r2 * r2);
+  } else {
+    const double r = sqrt(r2);
+    return cos(r) / r;
+  }
+}
+
+__device__ __forceinline__ double sq3(double dx, double dy, double dz) {
+  return fma(dz, dz, fma(dy, dy, dx * dx));
+}
+
+// Deterministic warp reductions (fixed butterfly order).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// argmax with ties to the lowest index; idx < 0 means "no candidate".
+__device__ __forceinline__ void argmax_combine(double& v, long long& i, double v2,
+                                               long long i2) {
+  if (i2 >= 0 && (i < 0 || v2 > v || (v2 == v && i2 < i))) {
+    v = v2;
+    i = i2;
+  }
+}
+
+__device__ __forceinline__ void warp_argmax(double& v, long long& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    argmax_combine(v, i, v2, i2);
+  }
+}
+
+__device__ __forceinline__ long long warp_min_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    v = v2 < v ? v2 : v;
+  }
+  return v;
+}
+
+// Streaming 16-byte load that bypasses L1 allocation (factor pools are read
+// once per matvec phase and are far larger than L2).
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ double ld_stream1(const double* p) {
+  double r;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
+}  // namespace h3db
+
+#define H3D_CUDA_CHECK(expr)                                                   \
+  do {                                                                         \
+    cudaError_t e_ = (expr);                                                   \
+    if (e_ != cudaSuccess) throw ::h3db::CudaError(e_, #expr, __FILE__, __LINE__); \
+  } while (0)

@@ -1,0 +1,153 @@
+// Launch interfaces of the sm_100a kernels (host-callable, no torch types).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace h3db {
+
+struct CudaError : std::runtime_error {
+  CudaError(cudaError_t e, const char* expr, const char* file, int line)
+      : std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(e) + " at " + file +
+                           ":" + std::to_string(line) + " (" + expr + ")"),
+        code(e) {}
+  cudaError_t code;
+};
+
+// ---------------------------------------------------------------- tree.cu
+// Morton codes at depth_cap (reference octree.cpp:67-72, 99-108), fp64
+// binning with round-to-nearest multiplies exactly as the reference.
+void launch_morton_codes(const double* xyz, std::int64_t n, int depth_cap,
+                         unsigned long long* codes, std::int32_t* idx, unsigned* flags,
+                         cudaStream_t s);
+std::size_t radix_sort_temp_bytes(std::int64_t n, int end_bit);
+void radix_sort_pairs(void* tmp, std::size_t tmp_bytes, const unsigned long long* kin,
+                      unsigned long long* kout, const std::int32_t* vin, std::int32_t* vout,
+                      std::int64_t n, int end_bit, cudaStream_t s);
+// max run length of (code >> 3(cap-l)) for every l in [0, cap] (octree.cpp:110-130)
+void launch_depth_scan(const unsigned long long* codes, std::int64_t n, int depth_cap,
+                       unsigned long long* maxocc, cudaStream_t s);
+// node offsets at `level`: off[m] = first sorted index with prefix >= m, m in [0, 8^l]
+void launch_node_offsets(const unsigned long long* codes, std::int64_t n, int depth_cap,
+                         int level, std::int64_t* off, cudaStream_t s);
+void launch_permute_points(const double* xyz, const std::int32_t* perm, std::int64_t n,
+                           double* px, double* py, double* pz, cudaStream_t s);
+
+// --------------------------------------------------------------- lists.cu
+// HODLR3D lists at one level (octree.cpp:197-260): kind 0 inter (vertex +
+// well-separated), 1 near_edge, 2 near_face. counts: 3 x 8^l.
+void launch_list_counts(int level, std::int32_t* counts, cudaStream_t s);
+void launch_list_fill(int level, const std::int32_t* offsets, std::int32_t* ids0,
+                      std::int32_t* ids1, std::int32_t* ids2, cudaStream_t s);
+// exclusive scan of n int32 into int32 (n+1 outputs, last = total)
+std::size_t scan_temp_bytes(std::int64_t n);
+void exclusive_scan_i32(void* tmp, std::size_t tmp_bytes, const std::int32_t* in,
+                        std::int32_t* out, std::int64_t n, cudaStream_t s);
+
+// ----------------------------------------------------------------- aca.cu
+struct AcaArgs {
+  std::int64_t npairs = 0;
+  const std::int64_t* xb = nullptr;  // row range begin (permuted index)
+  const std::int32_t* m = nullptr;
+  const std::int64_t* yb = nullptr;  // column range begin
+  const std::int32_t* n = nullptr;
+  const double *px = nullptr, *py = nullptr, *pz = nullptr;
+  int kernel = 0;
+  double diag = 0.0;
+  double eps = 1e-7;
+  std::int64_t max_rank = 0;
+  // workspace: one slot per resident CTA
+  double* ws = nullptr;
+  std::int64_t slot_doubles = 0;
+  int cap_ws = 0;     // rank capacity of a slot
+  int ms = 0, ns = 0; // column strides of U (m) and V (n) in a slot
+  std::int32_t* rank_out = nullptr;
+  // factor write-back (pass 2); null in the rank pass
+  double* W = nullptr;
+  const std::int64_t* wx = nullptr;  // W offset of U's (row 0, col 0)
+  const std::int32_t* rx = nullptr;  // U row stride
+  const std::int64_t* wy = nullptr;
+  const std::int32_t* ry = nullptr;
+  // optional pivot/LU write-back (matrix-free mode)
+  std::int32_t* piv_row = nullptr;
+  std::int32_t* piv_col = nullptr;
+  double* lu = nullptr;
+  const std::int64_t* piv_off = nullptr;
+  const std::int64_t* lu_off = nullptr;
+  unsigned* flags = nullptr;
+  unsigned long long* counter = nullptr;
+};
+// threads in {32, 128, 256, 512}; grid = number of workspace slots
+void launch_aca(const AcaArgs& a, int threads, int grid, cudaStream_t s);
+std::size_t aca_smem_bytes(int threads, int cap_ws);
+int aca_blocks_per_sm(int threads, int kernel, std::size_t smem);
+
+// -------------------------------------------------------------- matvec.cu
+void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp,
+                   cudaStream_t s);
+
+struct P1Item {
+  std::int32_t node;   // global node id
+  std::int32_t row0;   // first row (local to the node)
+  std::int32_t nrows;
+  std::int32_t col0;   // first column (local), multiple of 256
+  std::int32_t ncols;  // <= 256
+  std::int32_t pad;
+  std::int64_t pslot;  // -1: write to S directly; else partial buffer base
+};
+
+struct P1Reduce {
+  std::int32_t node;
+  std::int32_t ncols;
+  std::int32_t nchunks;
+  std::int32_t pad;
+  std::int64_t pbase;  // partials: pbase + chunk * ncols + c
+};
+
+struct NodeTable {
+  const std::int64_t* rowbeg = nullptr;  // first permuted row of global node g
+  const std::int32_t* rows = nullptr;    // number of points
+  const std::int64_t* woff = nullptr;    // factor matrix W_g (rows x rpad, row-major)
+  const std::int32_t* rpad = nullptr;
+  const std::int64_t* soff = nullptr;    // S_g (rpad entries)
+};
+
+void launch_phase1(const P1Item* items, std::int64_t nitems, NodeTable nt, const double* W,
+                   const double* xp, const std::int32_t* spos, double* S, double* P,
+                   cudaStream_t s);
+void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
+                          const std::int32_t* spos, const double* P, double* S,
+                          cudaStream_t s);
+
+struct Phase2Args {
+  int depth = 0;
+  std::int64_t nleaves = 0;  // leaves processed by this launch
+  std::int64_t leaf0 = 0;    // first leaf (Morton id) of this launch
+  const std::int64_t* leaf_off = nullptr;  // 8^L + 1
+  const std::int64_t* node_base = nullptr; // global id base per level (host-side values copied)
+  NodeTable nt;
+  const double* W = nullptr;
+  const double* S = nullptr;
+  const double* xp = nullptr;
+  const double *px = nullptr, *py = nullptr, *pz = nullptr;
+  const std::int32_t* perm = nullptr;
+  // leaf near lists: self + near_edge + near_face (non-empty), CSR
+  const std::int32_t* near_off = nullptr;
+  const std::int32_t* near_ids = nullptr;
+  // stored near field (near_mode 0): per leaf a row-major m x (sum n) block
+  const std::int64_t* nf_off = nullptr;  // per leaf offset into NF (or null: matrix-free)
+  const double* NF = nullptr;
+  int kernel = 0;
+  double diag = 0.0;
+  double* b = nullptr;  // output, original order
+  std::int64_t lbase[24] = {0};  // node_base per level (by value)
+};
+void launch_phase2(const Phase2Args& a, cudaStream_t s);
+
+// Build-time near-field scan: coincidence check (and optional store).
+void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s);
+
+}  // namespace h3db

@@ -1,0 +1,355 @@
+"""Python host mirror of the reference HODLR3D C++ API over the C-ABI.
+
+The reference operator surface for this path (proj/include/h3d/hmatrix.hpp)::
+
+    HMatrixRep initialize(const PointSet&, const KernelSpec&, Variant, const HmatOptions&)
+    std::vector<double> matvec(const HMatrixRep&, std::span<const double> x, MatvecTiming*)
+    RepStats stats(const HMatrixRep&)
+
+is mirrored here with the same names, argument meaning and error behaviour
+(``std::invalid_argument`` -> ``ValueError``; ``DegenerateGeometryError`` and
+``DegenerateDistributionError`` keep their names). Everything runs through
+``lib/libh3d_b200.so`` (include/h3d_b200.h); there is no CPU fallback: without
+the built library, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from pathlib import Path
+from typing import Optional
+
+import numpy as np
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libh3d_b200.so"
+
+KERNELS = {"laplace3d": 0, "r4": 1, "helmholtz-re": 2}
+NEAR_STORED, NEAR_MATRIX_FREE = 0, 1
+
+
+class DegenerateGeometryError(RuntimeError):
+    """Coincident distinct points (reference kernel.hpp:64-66)."""
+
+
+class DegenerateDistributionError(RuntimeError):
+    """Depth cap exceeded (reference octree.hpp:41-43)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL / allocation failure inside the engine."""
+
+
+class _Options(C.Structure):
+    _fields_ = [
+        ("kernel_id", C.c_int),
+        ("diagonal", C.c_double),
+        ("n_max", C.c_int),
+        ("epsilon", C.c_double),
+        ("depth_cap", C.c_int),
+        ("max_rank", C.c_int64),
+        ("near_mode", C.c_int),
+        ("device", C.c_int),
+        ("shard_rank", C.c_int),
+        ("shard_world", C.c_int),
+        ("reserved", C.c_int64 * 8),
+    ]
+
+
+class _Timing(C.Structure):
+    _fields_ = [
+        ("total_ms", C.c_double),
+        ("h2d_ms", C.c_double),
+        ("gather_ms", C.c_double),
+        ("exchange_ms", C.c_double),
+        ("phase1_ms", C.c_double),
+        ("phase2_ms", C.c_double),
+        ("d2h_ms", C.c_double),
+        ("launches", C.c_int64),
+    ]
+
+
+class _Stats(C.Structure):
+    _fields_ = [
+        ("depth", C.c_int),
+        ("max_rank", C.c_int),
+        ("n", C.c_int64),
+        ("lowrank_blocks", C.c_int64),
+        ("aca_pairs", C.c_int64),
+        ("sum_rank", C.c_int64),
+        ("factor_doubles", C.c_int64),
+        ("factor_bytes_alloc", C.c_int64),
+        ("tvec_doubles", C.c_int64),
+        ("near_blocks", C.c_int64),
+        ("near_entries", C.c_int64),
+        ("near_bytes_stored", C.c_int64),
+        ("ref_float_count", C.c_uint64),
+        ("ref_int_count", C.c_uint64),
+        ("compression_ratio", C.c_double),
+        ("build_ms_tree", C.c_double),
+        ("build_ms_lists", C.c_double),
+        ("build_ms_aca_rank", C.c_double),
+        ("build_ms_aca_write", C.c_double),
+        ("build_ms_total", C.c_double),
+        ("phase1_items", C.c_int64),
+        ("owned_row_begin", C.c_int64),
+        ("owned_row_end", C.c_int64),
+        ("reserved", C.c_int64 * 6),
+    ]
+
+
+_EXPORTS = [
+    "h3d_last_error", "h3d_abi_version", "h3d_default_options", "h3d_generate_points",
+    "h3d_random_vector", "h3d_dev_create", "h3d_dev_destroy", "h3d_dev_matvec",
+    "h3d_dev_stats", "h3d_dev_export_tree", "h3d_dev_export_list", "h3d_dev_export_pairs",
+    "h3d_nccl_get_id", "h3d_dev_attach_nccl",
+]
+
+
+def _load():
+    if not _LIB_PATH.exists():
+        raise ImportError(
+            f"{_LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (or `make -C paper_2307_16303_b200/csrc`). There is no CPU fallback.")
+    L = C.CDLL(str(_LIB_PATH))
+    P = C.c_void_p
+    L.h3d_last_error.restype = C.c_char_p
+    L.h3d_default_options.argtypes = [C.POINTER(_Options)]
+    L.h3d_generate_points.argtypes = [C.c_int64, C.c_uint64, P]
+    L.h3d_random_vector.argtypes = [C.c_int64, C.c_uint64, P]
+    L.h3d_dev_create.argtypes = [P, C.c_int64, C.POINTER(_Options), C.POINTER(P)]
+    L.h3d_dev_destroy.argtypes = [P]
+    L.h3d_dev_matvec.argtypes = [P, P, P, C.c_int, C.POINTER(_Timing)]
+    L.h3d_dev_stats.argtypes = [P, C.POINTER(_Stats)]
+    L.h3d_dev_export_tree.argtypes = [P, P, C.c_int, P]
+    L.h3d_dev_export_list.argtypes = [P, C.c_int, C.c_int, P, P, C.POINTER(C.c_int64)]
+    L.h3d_dev_export_pairs.argtypes = [P, C.c_int, P, P, P, C.POINTER(C.c_int64)]
+    L.h3d_nccl_get_id.argtypes = [P]
+    L.h3d_dev_attach_nccl.argtypes = [P, P, C.c_int, C.c_int]
+    return L
+
+
+_L = _load()
+
+
+def library_path() -> str:
+    return str(_LIB_PATH)
+
+
+def exported_symbols():
+    return list(_EXPORTS)
+
+
+def _raise(code: int):
+    msg = _L.h3d_last_error().decode()
+    if code == 1 or code == 7:
+        raise ValueError(msg)
+    if code == 2:
+        raise DegenerateGeometryError(msg)
+    if code == 3:
+        raise DegenerateDistributionError(msg)
+    raise DeviceError(f"[status {code}] {msg}")
+
+
+def _check(code: int):
+    if code != 0:
+        _raise(code)
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data)
+
+
+# ---------------------------------------------------------------- inputs
+def generate_points(n: int, seed: int) -> np.ndarray:
+    """generate_points(UniformRandom, n, seed) (reference kernel.cpp:88-95), (n, 3)."""
+    out = np.empty((n, 3), dtype=np.float64)
+    _check(_L.h3d_generate_points(n, seed, _ptr(out)))
+    return out
+
+
+def random_vector(n: int, seed: int) -> np.ndarray:
+    """mt19937_64(seed), 2u-1 (reference tools/h3d.cpp:135-137)."""
+    out = np.empty(n, dtype=np.float64)
+    _L.h3d_random_vector(n, seed, _ptr(out))
+    return out
+
+
+# ---------------------------------------------------------------- options
+@dataclasses.dataclass
+class KernelSpec:
+    """Built-in radial kernel (reference kernel.hpp:46-53)."""
+
+    name: str = "laplace3d"
+    diagonal: float = 0.0
+
+    @property
+    def id(self) -> int:
+        if self.name not in KERNELS:
+            raise ValueError(f"unknown kernel: {self.name}")
+        return KERNELS[self.name]
+
+
+def make_kernel(name: str, diagonal: float = 0.0) -> KernelSpec:
+    """parse_kernel (reference kernel.cpp:52-57): laplace3d, r4, helmholtz-re."""
+    if name not in KERNELS:
+        raise ValueError(f"unknown kernel: {name}")
+    return KernelSpec(name, diagonal)
+
+
+@dataclasses.dataclass
+class HmatOptions:
+    """Reference hmatrix.hpp:16-22. dense_mode: "cached" stores the near field,
+    "on-the-fly" recomputes it every matvec (matrix-free)."""
+
+    n_max: int = 216
+    epsilon: float = 1e-7
+    dense_mode: str = "on-the-fly"
+    depth_cap: int = 12
+    max_rank: int = 0
+
+
+@dataclasses.dataclass
+class MatvecTiming:
+    total_ms: float = 0.0
+    h2d_ms: float = 0.0
+    gather_ms: float = 0.0
+    exchange_ms: float = 0.0
+    phase1_ms: float = 0.0
+    phase2_ms: float = 0.0
+    d2h_ms: float = 0.0
+    launches: int = 0
+
+
+class HMatrixRep:
+    """Device-resident HODLR3D representation (reference hmatrix.hpp:37-55)."""
+
+    def __init__(self, points, kernel: KernelSpec, options: HmatOptions, device: int = 0,
+                 shard_rank: int = 0, shard_world: int = 1):
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        o = _Options()
+        _L.h3d_default_options(C.byref(o))
+        o.kernel_id = kernel.id
+        o.diagonal = float(kernel.diagonal)
+        o.n_max = int(options.n_max)
+        o.epsilon = float(options.epsilon)
+        o.depth_cap = int(options.depth_cap)
+        o.max_rank = int(options.max_rank)
+        if options.dense_mode not in ("cached", "on-the-fly"):
+            raise ValueError(f"unknown dense_mode: {options.dense_mode}")
+        o.near_mode = NEAR_STORED if options.dense_mode == "cached" else NEAR_MATRIX_FREE
+        o.device = int(device)
+        o.shard_rank = int(shard_rank)
+        o.shard_world = int(shard_world)
+        h = C.c_void_p()
+        self._h = None
+        _check(_L.h3d_dev_create(_ptr(pts), len(pts), C.byref(o), C.byref(h)))
+        self._h = h
+        self.kernel = kernel
+        self.options = options
+        self.n = len(pts)
+        self.device = device
+        self.shard_rank, self.shard_world = shard_rank, shard_world
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _L.h3d_dev_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # --- matvec -------------------------------------------------------------
+    def matvec(self, x, out: Optional[np.ndarray] = None, timing: Optional[MatvecTiming] = None):
+        """b = A~ x in original point order (reference hmatrix.cpp:153-226)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.ndim != 1 or len(x) != self.n:
+            raise ValueError("matvec: vector length != N")
+        b = out if out is not None else np.empty(self.n, dtype=np.float64)
+        t = _Timing()
+        _check(_L.h3d_dev_matvec(self._h, _ptr(x), _ptr(b), 0, C.byref(t)))
+        if timing is not None:
+            for f, _ in _Timing._fields_:
+                setattr(timing, f, getattr(t, f))
+        return b
+
+    def matvec_ptr(self, x_ptr: int, b_ptr: int, host: bool, timing: Optional[MatvecTiming] = None):
+        """Raw-pointer matvec (device pointers for torch CUDA tensors, or pinned host)."""
+        t = _Timing()
+        _check(_L.h3d_dev_matvec(self._h, C.c_void_p(x_ptr), C.c_void_p(b_ptr), 0 if host else 1,
+                                 C.byref(t)))
+        if timing is not None:
+            for f, _ in _Timing._fields_:
+                setattr(timing, f, getattr(t, f))
+        return t
+
+    # --- introspection ------------------------------------------------------
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(_L.h3d_dev_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in _Stats._fields_ if f != "reserved"}
+
+    @property
+    def depth(self) -> int:
+        return self.stats()["depth"]
+
+    def perm(self) -> np.ndarray:
+        p = np.empty(self.n, np.int32)
+        _check(_L.h3d_dev_export_tree(self._h, _ptr(p), -1, None))
+        return p
+
+    def offsets(self, level: int) -> np.ndarray:
+        o = np.empty((1 << (3 * level)) + 1, np.int64)
+        _check(_L.h3d_dev_export_tree(self._h, None, level, _ptr(o)))
+        return o
+
+    def list(self, level: int, kind: int):
+        """Interaction list CSR (kind 0 inter, 1 near_edge, 2 near_face)."""
+        nn = 1 << (3 * level)
+        off = np.empty(nn + 1, np.int32)
+        cnt = C.c_int64(0)
+        _check(_L.h3d_dev_export_list(self._h, level, kind, _ptr(off), None, C.byref(cnt)))
+        ids = np.empty(max(cnt.value, 1), np.int32)
+        _check(_L.h3d_dev_export_list(self._h, level, kind, _ptr(off), _ptr(ids), C.byref(cnt)))
+        return off, ids[: cnt.value]
+
+    def pairs(self, level: int):
+        cnt = C.c_int64(0)
+        _check(_L.h3d_dev_export_pairs(self._h, level, None, None, None, C.byref(cnt)))
+        k = cnt.value
+        x, y, r = (np.empty(max(k, 1), np.int32) for _ in range(3))
+        _check(_L.h3d_dev_export_pairs(self._h, level, _ptr(x), _ptr(y), _ptr(r), C.byref(cnt)))
+        return x[:k], y[:k], r[:k]
+
+    # --- multi-GPU ----------------------------------------------------------
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int):
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        _check(_L.h3d_dev_attach_nccl(self._h, C.cast(buf, C.c_void_p), rank, world))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_char * 128)()
+    _check(_L.h3d_nccl_get_id(C.cast(buf, C.c_void_p)))
+    return bytes(buf)
+
+
+def initialize(points, kernel: KernelSpec, variant: str = "hodlr3d",
+               options: Optional[HmatOptions] = None, device: int = 0, shard_rank: int = 0,
+               shard_world: int = 1) -> HMatrixRep:
+    """Reference hmatrix.hpp:57-58. Only the HODLR3D variant is on the device path."""
+    if variant != "hodlr3d":
+        raise ValueError(f"variant {variant!r} is not on the B200 path (hodlr3d only)")
+    if len(np.asarray(points).reshape(-1, 3)) == 0:
+        raise ValueError("initialize: empty point set")
+    return HMatrixRep(points, kernel, options or HmatOptions(), device, shard_rank, shard_world)
+
+
+def matvec(rep: HMatrixRep, x, timing: Optional[MatvecTiming] = None) -> np.ndarray:
+    return rep.matvec(x, timing=timing)
+
+
+def stats(rep: HMatrixRep) -> dict:
+    return rep.stats()

@@ -1,0 +1,61 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE ITSELF.
+
+Runs the unmodified reference (oracle/_ref/libh3dref.so, built in place from
+/root/reference/proj/src by `make -C oracle ref`) on seeded inputs and stores
+its outputs: permutation, node offsets, interaction lists, per-block ranks,
+its matvec output b_ref and the exact direct sum b_exact.
+
+Only runnable where /root/reference was mounted at build time; the fixtures
+are committed so the GPU box (no /root/reference) can use them.
+
+    python tests/golden/make_golden.py
+"""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+from oracle_lib import RefLib  # noqa: E402
+
+# name: (N, kernel, n_max, eps, seed)  -- C1 is BASELINE.json configs[0]
+CONFIGS = {
+    "c1_n4096_laplace_nmax64_eps1e-10": (4096, "laplace3d", 64, 1e-10, 1),
+    "n3000_r4_nmax100_eps1e-6": (3000, "r4", 100, 1e-6, 29),
+    "n3000_helm_nmax100_eps1e-6": (3000, "helmholtz-re", 100, 1e-6, 29),
+    "n150_laplace_depth0": (150, "laplace3d", 216, 1e-7, 19),
+    "n2197_laplace_nmax64_eps1e-7": (2197, "laplace3d", 64, 1e-7, 13),
+}
+
+
+def main():
+    ref = RefLib()
+    ref.set_threads(8)
+    for name, (n, kern, n_max, eps, seed) in CONFIGS.items():
+        pts = ref.generate_points(n, seed)
+        x = ref.random_vector(n, seed + 17)
+        rep = ref.initialize(pts, kern, n_max=n_max, eps=eps)
+        out = dict(n=n, kernel=kern, n_max=n_max, eps=eps, seed=seed, depth=rep.depth,
+                   perm=rep.perm(), x=x)
+        for l in range(rep.depth + 1):
+            out[f"off{l}"] = rep.offsets(l)
+            for k, kn in enumerate(["inter", "edge", "face"]):
+                o, ids = rep.list(l, k)
+                out[f"{kn}_off{l}"] = o
+                out[f"{kn}_ids{l}"] = ids
+            if l >= 1:
+                t, s, r = rep.lr_blocks(l)
+                out[f"lr_t{l}"], out[f"lr_s{l}"], out[f"lr_r{l}"] = t, s, r
+        out["b_ref"] = rep.matvec(x)
+        out["b_exact"] = ref.dense_matvec(pts, x, kern)
+        out["ref_error"] = rep.reference_error(x, out["b_ref"])
+        st = rep.stats()
+        out["stats"] = np.array([st["float_count"], st["int_count"], st["memory_bytes"],
+                                 st["max_rank"], st["depth"]], dtype=np.uint64)
+        np.savez_compressed(HERE / f"{name}.npz", **out)
+        print(name, "depth", rep.depth, "err", out["ref_error"])
+
+
+if __name__ == "__main__":
+    main()

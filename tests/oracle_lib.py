@@ -70,10 +70,23 @@ class Oracle:
         L.orc_dense_matvec.argtypes = [_D, C.c_int64, C.c_int, C.c_double, _D, _D]
         L.orc_exact_rows.argtypes = [_D, C.c_int64, C.c_int, C.c_double, _D, _I64, C.c_int64, _D]
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_uniform_stream.argtypes = [C.c_int64, C.c_uint64, _D]
+        L.orc_tree_lists.argtypes = [_D, C.c_int64, C.c_int, C.c_int, C.POINTER(_P)]
 
     def _check(self, st):
         if st != 0:
             raise CheckerError(st, self.L.orc_last_error().decode())
+
+    def uniform_stream(self, n: int, seed: int) -> np.ndarray:
+        out = np.empty(n, dtype=np.float64)
+        self.L.orc_uniform_stream(n, seed, out)
+        return out
+
+    def tree_lists(self, pts, n_max=216, depth_cap=12) -> "OracleRep":
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1)
+        h = _P()
+        self._check(self.L.orc_tree_lists(pts, len(pts) // 3, n_max, depth_cap, C.byref(h)))
+        return OracleRep(self, h, len(pts) // 3)
 
     def set_threads(self, n: int):
         self.L.orc_set_threads(n)
