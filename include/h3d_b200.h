@@ -130,6 +130,16 @@ void h3d_dev_destroy(h3d_dev* dev);
  * (returns after the result is complete). timing may be NULL. */
 int h3d_dev_matvec(h3d_dev* dev, const double* x, double* b, int where, h3d_timing* timing);
 
+/* Stream-ordered variant for device-resident vectors: enqueue one matvec on
+ * the caller's cudaStream_t (may be the caller's framework stream) and return
+ * without synchronising. Same numerics as h3d_dev_matvec. */
+int h3d_dev_matvec_async(h3d_dev* dev, const double* x_dev, double* b_dev, void* stream);
+/* Per-phase CUDA-event timing of async matvecs: enable (resets) with room for
+ * `capacity` calls; read = synchronise and sum the phases over the recorded
+ * calls (*steps). Used by bench.py for live per-kernel durations. */
+int h3d_dev_profile(h3d_dev* dev, int enable, int64_t capacity);
+int h3d_dev_profile_read(h3d_dev* dev, h3d_timing* sum, int64_t* steps);
+
 /* Replaces h3d::stats(rep) (hmatrix.hpp:85). */
 int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out);
 

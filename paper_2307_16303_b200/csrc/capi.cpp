@@ -116,6 +116,28 @@ int h3d_dev_matvec(h3d_dev* dev, const double* x, double* b, int where, h3d_timi
   });
 }
 
+int h3d_dev_matvec_async(h3d_dev* dev, const double* x_dev, double* b_dev, void* stream) {
+  return guarded([&] {
+    if (!dev) throw h3db::InvalidArgument("matvec: null handle");
+    std::lock_guard<std::mutex> lk(eng(dev)->mu);
+    eng(dev)->matvec_async(x_dev, b_dev, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int h3d_dev_profile(h3d_dev* dev, int enable, int64_t capacity) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(eng(dev)->mu);
+    eng(dev)->profile(enable, capacity);
+  });
+}
+
+int h3d_dev_profile_read(h3d_dev* dev, h3d_timing* sum, int64_t* steps) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(eng(dev)->mu);
+    eng(dev)->profile_read(sum, steps);
+  });
+}
+
 int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out) {
   return guarded([&] { eng(dev)->stats(out); });
 }

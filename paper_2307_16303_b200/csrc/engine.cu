@@ -121,6 +121,8 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
 }
 
 Engine::~Engine() {
+  for (auto e : prof_ev_)
+    if (e) cudaEventDestroy(e);
   if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
@@ -655,48 +657,38 @@ void Engine::near_scan() {
 }
 
 // ---------------------------------------------------------------- matvec
-void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
-  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
-  if (world_ > 1 && nccl_comm_ == nullptr)
-    throw InvalidArgument("matvec: sharded engine needs h3d_dev_attach_nccl first");
+// Enqueue one matvec on stream s: x (original order, device) -> b (original
+// order, device). ev (optional, 4 events) brackets gather/exchange, phase 1,
+// phase 2. Returns the number of kernels launched.
+std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev) {
   std::int64_t launches = 0;
-  cudaEventRecord(ev_[0], stream_);
-  const double* xin = x;
-  if (host) {
-    H3D_CUDA_CHECK(cudaMemcpyAsync(x_.get(), x, n_ * 8, cudaMemcpyHostToDevice, stream_));
-    xin = x_.get();
-  }
-  cudaEventRecord(ev_[1], stream_);
+  if (ev) cudaEventRecord(ev[0], s);
   if (world_ == 1) {
-    launch_gather(xin, perm_.get(), n_, xp_.get(), stream_);
+    launch_gather(xin, perm_.get(), n_, xp_.get(), s);
     ++launches;
-    cudaEventRecord(ev_[2], stream_);
-    cudaEventRecord(ev_[3], stream_);
   } else {
     // own slice of x in Morton order, then the all-gather of x over NVLink
     if (row1_ > row0_) {
-      launch_gather(xin, perm_.get() + row0_, row1_ - row0_, xp_.get() + row0_, stream_);
+      launch_gather(xin, perm_.get() + row0_, row1_ - row0_, xp_.get() + row0_, s);
       ++launches;
     }
-    cudaEventRecord(ev_[2], stream_);
     auto comm = static_cast<ncclComm_t>(nccl_comm_);
     NCCL_CHECK(ncclGroupStart());
     for (int r = 0; r < world_; ++r) {
       const std::int64_t c = rank_row1_[r] - rank_row0_[r];
       if (c > 0)
         NCCL_CHECK(ncclBroadcast(xp_.get() + rank_row0_[r], xp_.get() + rank_row0_[r],
-                                 static_cast<std::size_t>(c), ncclDouble, r, comm, stream_));
+                                 static_cast<std::size_t>(c), ncclDouble, r, comm, s));
     }
     NCCL_CHECK(ncclGroupEnd());
-    cudaEventRecord(ev_[3], stream_);
   }
+  if (ev) cudaEventRecord(ev[1], s);
   NodeTable nt{rowbeg_.get(), rows_.get(), woff_.get(), rpad_.get(), soff_.get()};
-  launch_phase1(p1_items_.get(), n_p1_, nt, W_.get(), xp_.get(), spos_.get(), S_.get(), P_.get(), stream_);
+  launch_phase1(p1_items_.get(), n_p1_, nt, W_.get(), xp_.get(), spos_.get(), S_.get(), P_.get(), s);
   launches += n_p1_ > 0;
-  launch_phase1_reduce(p1_red_.get(), n_red_, nt, spos_.get(), P_.get(), S_.get(), stream_);
+  launch_phase1_reduce(p1_red_.get(), n_red_, nt, spos_.get(), P_.get(), S_.get(), s);
   launches += n_red_ > 0;
-  cudaEventRecord(ev_[4], stream_);
-  double* bout = host ? b_.get() : b;
+  if (ev) cudaEventRecord(ev[2], s);
   if (leaf1_ > leaf0_) {
     Phase2Args a;
     a.depth = L_;
@@ -721,12 +713,27 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
     a.diag = opt_.diagonal;
     a.b = bout;
     for (int l = 0; l <= L_ && l < 24; ++l) a.lbase[l] = node_base_[l];
-    launch_phase2(a, stream_);
+    launch_phase2(a, s);
     ++launches;
   }
-  cudaEventRecord(ev_[5], stream_);
+  if (ev) cudaEventRecord(ev[3], s);
+  return launches;
+}
+
+void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  if (world_ > 1 && nccl_comm_ == nullptr)
+    throw InvalidArgument("matvec: sharded engine needs h3d_dev_attach_nccl first");
+  cudaEventRecord(ev_[0], stream_);
+  const double* xin = x;
+  if (host) {
+    H3D_CUDA_CHECK(cudaMemcpyAsync(x_.get(), x, n_ * 8, cudaMemcpyHostToDevice, stream_));
+    xin = x_.get();
+  }
+  double* bout = host ? b_.get() : b;
+  const std::int64_t launches = enqueue(xin, bout, stream_, ev_ + 1);
   if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
-  cudaEventRecord(ev_[6], stream_);
+  cudaEventRecord(ev_[5], stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   if (t) {
     float v = 0;
@@ -734,15 +741,64 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
       cudaEventElapsedTime(&v, ev_[a], ev_[bb]);
       return static_cast<double>(v);
     };
-    t->total_ms = el(0, 6);
+    std::memset(t, 0, sizeof(*t));
+    t->total_ms = el(0, 5);
     t->h2d_ms = el(0, 1);
-    t->gather_ms = el(1, 2);
-    t->exchange_ms = el(2, 3);
-    t->phase1_ms = el(3, 4);
-    t->phase2_ms = el(4, 5);
-    t->d2h_ms = el(5, 6);
+    if (world_ == 1) t->gather_ms = el(1, 2);
+    else t->exchange_ms = el(1, 2);
+    t->phase1_ms = el(2, 3);
+    t->phase2_ms = el(3, 4);
+    t->d2h_ms = el(4, 5);
     t->launches = launches;
   }
+}
+
+void Engine::matvec_async(const double* x, double* b, cudaStream_t s) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  if (world_ > 1 && nccl_comm_ == nullptr)
+    throw InvalidArgument("matvec: sharded engine needs h3d_dev_attach_nccl first");
+  cudaEvent_t* ev = nullptr;
+  if (prof_on_) {
+    if (prof_used_ >= prof_ev_.size() / 4) throw InvalidArgument("profile ring full; read it first");
+    ev = prof_ev_.data() + 4 * prof_used_;
+    ++prof_used_;
+  }
+  prof_launches_ += enqueue(x, b, s, ev);
+}
+
+void Engine::profile(int enable, std::int64_t capacity) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  prof_on_ = enable != 0;
+  prof_used_ = 0;
+  prof_launches_ = 0;
+  const std::size_t need = static_cast<std::size_t>(4 * std::max<std::int64_t>(capacity, 1));
+  if (prof_on_ && prof_ev_.size() < need) {
+    for (auto e : prof_ev_) cudaEventDestroy(e);
+    prof_ev_.assign(need, nullptr);
+    for (auto& e : prof_ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
+  }
+}
+
+void Engine::profile_read(h3d_timing* sum, std::int64_t* steps) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  std::memset(sum, 0, sizeof(*sum));
+  for (std::size_t k = 0; k < prof_used_; ++k) {
+    cudaEvent_t* ev = prof_ev_.data() + 4 * k;
+    H3D_CUDA_CHECK(cudaEventSynchronize(ev[3]));
+    float a = 0, b = 0, c = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    if (world_ == 1) sum->gather_ms += a;
+    else sum->exchange_ms += a;
+    sum->phase1_ms += b;
+    sum->phase2_ms += c;
+    sum->total_ms += a + b + c;
+  }
+  sum->launches = prof_launches_;
+  *steps = static_cast<std::int64_t>(prof_used_);
+  prof_used_ = 0;
+  prof_launches_ = 0;
 }
 
 void Engine::attach_nccl(const void* id128, int rank, int world) {

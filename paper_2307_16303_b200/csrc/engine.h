@@ -67,6 +67,9 @@ class Engine {
   ~Engine();
 
   void matvec(const double* x, double* b, bool host, h3d_timing* t);
+  void matvec_async(const double* x, double* b, cudaStream_t s);
+  void profile(int enable, std::int64_t capacity);
+  void profile_read(h3d_timing* sum, std::int64_t* steps);
   void stats(h3d_stats* out) const;
   void export_tree(std::int32_t* perm, int level, std::int64_t* offsets) const;
   std::int64_t export_list(int level, int kind, std::int32_t* offsets, std::int32_t* ids) const;
@@ -84,6 +87,7 @@ class Engine {
   void build_matvec_plan();
   void near_scan();
   void check_flags(const char* where);
+  std::int64_t enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev);
   bool owned(int level, std::int64_t m) const;
   std::int64_t gid(int level, std::int64_t m) const { return node_base_[level] + m; }
   std::int64_t node_size(int level, std::int64_t m) const {
@@ -151,6 +155,12 @@ class Engine {
   int world_ = 1, rank_ = 0;
   std::vector<std::int64_t> rank_row0_, rank_row1_;
   DevBuf<double> bperm_;
+
+  // profiling ring for async matvecs (4 events per step)
+  bool prof_on_ = false;
+  std::vector<cudaEvent_t> prof_ev_;
+  std::size_t prof_used_ = 0;
+  std::int64_t prof_launches_ = 0;
 
   // timings
   double ms_tree_ = 0, ms_lists_ = 0, ms_aca_rank_ = 0, ms_aca_write_ = 0, ms_total_ = 0;

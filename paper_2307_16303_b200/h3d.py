@@ -102,7 +102,8 @@ _EXPORTS = [
     "h3d_last_error", "h3d_abi_version", "h3d_default_options", "h3d_generate_points",
     "h3d_random_vector", "h3d_dev_create", "h3d_dev_destroy", "h3d_dev_matvec",
     "h3d_dev_stats", "h3d_dev_export_tree", "h3d_dev_export_list", "h3d_dev_export_pairs",
-    "h3d_nccl_get_id", "h3d_dev_attach_nccl",
+    "h3d_nccl_get_id", "h3d_dev_attach_nccl", "h3d_dev_matvec_async", "h3d_dev_profile",
+    "h3d_dev_profile_read",
 ]
 
 
@@ -124,6 +125,9 @@ def _load():
     L.h3d_dev_export_tree.argtypes = [P, P, C.c_int, P]
     L.h3d_dev_export_list.argtypes = [P, C.c_int, C.c_int, P, P, C.POINTER(C.c_int64)]
     L.h3d_dev_export_pairs.argtypes = [P, C.c_int, P, P, P, C.POINTER(C.c_int64)]
+    L.h3d_dev_matvec_async.argtypes = [P, P, P, P]
+    L.h3d_dev_profile.argtypes = [P, C.c_int, C.c_int64]
+    L.h3d_dev_profile_read.argtypes = [P, C.POINTER(_Timing), C.POINTER(C.c_int64)]
     L.h3d_nccl_get_id.argtypes = [P]
     L.h3d_dev_attach_nccl.argtypes = [P, P, C.c_int, C.c_int]
     return L
@@ -285,6 +289,24 @@ class HMatrixRep:
             for f, _ in _Timing._fields_:
                 setattr(timing, f, getattr(t, f))
         return t
+
+    def matvec_async(self, x_ptr: int, b_ptr: int, stream: int = 0):
+        """Enqueue b = A~ x on a CUDA stream (device pointers, no sync)."""
+        _check(_L.h3d_dev_matvec_async(self._h, C.c_void_p(x_ptr), C.c_void_p(b_ptr),
+                                       C.c_void_p(stream)))
+
+    def profile(self, enable: bool, capacity: int = 1024):
+        _check(_L.h3d_dev_profile(self._h, int(enable), int(capacity)))
+
+    def profile_read(self):
+        """(summed MatvecTiming over recorded async calls, number of calls)."""
+        t = _Timing()
+        steps = C.c_int64(0)
+        _check(_L.h3d_dev_profile_read(self._h, C.byref(t), C.byref(steps)))
+        out = MatvecTiming()
+        for f, _ in _Timing._fields_:
+            setattr(out, f, getattr(t, f))
+        return out, steps.value
 
     # --- introspection ------------------------------------------------------
     def stats(self) -> dict:
