@@ -36,7 +36,8 @@ def load_golden(name):
         return {k: z[k] for k in z.files}
 
 
-GOLDEN_NAMES = sorted(p.stem for p in GOLDEN.glob("*.npz"))
+GOLDEN_NAMES = sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith("large_"))
+LARGE_NAMES = sorted(p.stem[len("large_"):] for p in GOLDEN.glob("large_*.npz"))
 
 
 @pytest.fixture(scope="session")
