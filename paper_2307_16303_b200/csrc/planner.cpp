@@ -1,0 +1,344 @@
+// Host planning (see planner.h). Reference mapping:
+//   build_pairs  <- the per-level ACA job list of initialize (hmatrix.cpp:74-98),
+//                   halved to unordered pairs X < Y (lists swap-symmetric,
+//                   test_octree.cpp:167-181; kernels symmetric, kernel.cpp:7-21)
+//   near lists   <- the dense leaf block list (hmatrix.cpp:105-120): self, edge, face
+//   ownership    <- Morton-subtree analogue of plan_partition (parallel.cpp:34-74)
+#include "planner.h"
+
+#include <algorithm>
+
+namespace h3db {
+
+namespace {
+constexpr std::int64_t kRowChunk = 2048;  // phase-1 stream: rows per item
+constexpr int kColChunk = 256;            // phase-1: columns (targets) per item
+constexpr std::int64_t kSrcChunk = 2048;  // phase-1 proxy: source points per item
+}  // namespace
+
+std::vector<int> default_modes(int depth, std::int64_t n, int policy) {
+  std::vector<int> m(depth + 1, kModeStream);
+  if (policy == 0 || depth == 0) return m;  // all streamed
+  // policy 1 (hybrid): leaf level exact, then alternate compute/stream so the
+  // FP64 pipes and HBM work concurrently (cost model: DESIGN.md section 4).
+  m[depth] = kModeDirect;
+  for (int l = 1; l < depth; ++l) m[l] = kModeProxy;
+  (void)n;
+  return m;
+}
+
+Planner::Planner(int depth, std::int64_t n, std::vector<std::vector<std::int64_t>> off,
+                 std::vector<LevelLists> lists, int rank, int world, std::vector<int> modes)
+    : L_(depth), n_(n), off_(std::move(off)), lists_(std::move(lists)), rank_(rank),
+      world_(world), mode_(std::move(modes)) {
+  if (static_cast<int>(off_.size()) != L_ + 1 || static_cast<int>(lists_.size()) != L_ + 1)
+    throw std::invalid_argument("planner: offsets/lists do not match the depth");
+  if (!(world_ == 1 || world_ == 2 || world_ == 4 || world_ == 8))
+    throw std::invalid_argument("planner: shard_world must be 1, 2, 4 or 8");
+  if (rank_ < 0 || rank_ >= world_) throw std::invalid_argument("planner: shard_rank out of range");
+  if (static_cast<int>(mode_.size()) != L_ + 1) mode_.assign(L_ + 1, kModeStream);
+  for (int l = 1; l <= L_; ++l) {
+    if (mode_[l] < 0 || mode_[l] > 2) throw std::invalid_argument("planner: bad level mode");
+    if (mode_[l] == kModeDirect && l != L_)
+      throw std::invalid_argument("planner: direct mode is only valid at the leaf level");
+  }
+  oct0_ = 8 * rank_ / world_;
+  oct1_ = 8 * (rank_ + 1) / world_;
+  node_base_.assign(L_ + 2, 0);
+  for (int l = 0; l <= L_; ++l) node_base_[l + 1] = node_base_[l] + (1LL << (3 * l));
+  if (L_ == 0) {
+    row0 = 0;
+    row1 = rank_ == 0 ? n_ : 0;
+  } else {
+    row0 = off_[1][oct0_];
+    row1 = off_[1][oct1_];
+  }
+  rank_row0.resize(world_);
+  rank_row1.resize(world_);
+  for (int r = 0; r < world_; ++r) {
+    if (L_ == 0) {
+      rank_row0[r] = 0;
+      rank_row1[r] = r == 0 ? n_ : 0;
+    } else {
+      rank_row0[r] = off_[1][8 * r / world_];
+      rank_row1[r] = off_[1][8 * (r + 1) / world_];
+    }
+  }
+  build_pairs();
+}
+
+bool Planner::owned(int level, std::int64_t m) const {
+  if (level == 0) return rank_ == 0;
+  const std::int64_t oct = m >> (3 * (level - 1));
+  return oct >= oct0_ && oct < oct1_;
+}
+
+// Admissible blocks with both nodes non-empty (hmatrix.cpp:74-98); one ACA per
+// unordered pair X < Y, on every shard that owns X or Y (cross pairs are
+// compressed redundantly, like the reference's shared nodes, parallel.cpp:308-380).
+void Planner::build_pairs() {
+  pairs_.assign(L_ + 1, LevelPairs{});
+  entry_pair_.assign(L_ + 1, {});
+  entry_col_.assign(L_ + 1, {});
+  sizes.nblocks_ordered = 0;
+  for (int l = 1; l <= L_; ++l) {
+    const std::int64_t cnt = 1LL << (3 * l);
+    const auto& off = lists_[l].off[0];
+    const auto& ids = lists_[l].ids[0];
+    auto& ep = entry_pair_[l];
+    ep.assign(ids.size(), -1);
+    auto& P = pairs_[l];
+    for (std::int64_t X = 0; X < cnt; ++X) {
+      if (node_size(l, X) == 0) continue;
+      for (std::int32_t e = off[X]; e < off[X + 1]; ++e) {
+        const std::int32_t Y = ids[e];
+        if (node_size(l, Y) == 0) continue;
+        ++sizes.nblocks_ordered;
+        if (mode_[l] == kModeDirect) continue;
+        if (Y <= X || !(owned(l, X) || owned(l, Y))) continue;
+        ep[e] = static_cast<std::int32_t>(P.X.size());
+        P.X.push_back(static_cast<std::int32_t>(X));
+        P.Y.push_back(Y);
+        P.eX.push_back(e);
+        const int m = static_cast<int>(node_size(l, X)), nn = static_cast<int>(node_size(l, Y));
+        P.max_m = std::max(P.max_m, m);
+        P.max_n = std::max(P.max_n, nn);
+        P.max_mn = std::max(P.max_mn, std::min(m, nn));
+      }
+    }
+    P.eY.assign(P.X.size(), -1);
+    for (std::int64_t Z = 0; Z < cnt; ++Z) {
+      if (node_size(l, Z) == 0) continue;
+      for (std::int32_t e = off[Z]; e < off[Z + 1]; ++e) {
+        const std::int32_t k = ids[e];
+        if (k >= Z || node_size(l, k) == 0 || mode_[l] == kModeDirect ||
+            !(owned(l, Z) || owned(l, k)))
+          continue;
+        const auto b = ids.begin() + off[k], en = ids.begin() + off[k + 1];
+        const auto it = std::lower_bound(b, en, static_cast<std::int32_t>(Z));
+        if (it == en || *it != Z) throw std::logic_error("interaction lists not swap-symmetric");
+        const std::int32_t p = ep[static_cast<std::size_t>(it - ids.begin())];
+        ep[e] = p;
+        P.eY[p] = e;
+      }
+    }
+    P.rank.assign(P.X.size(), 0);
+    const double mbar = static_cast<double>(n_) / static_cast<double>(cnt);
+    P.threads = mbar <= 64 ? 32 : mbar <= 512 ? 128 : mbar <= 4096 ? 256 : 512;
+  }
+  sizes.npairs = 0;
+  for (const auto& P : pairs_) sizes.npairs += static_cast<std::int64_t>(P.X.size());
+}
+
+void Planner::layout() {
+  const std::int64_t T = total_nodes();
+  woff.assign(T, 0);
+  soff.assign(T, 0);
+  rowbeg.assign(T, 0);
+  rpad.assign(T, 0);
+  rows.assign(T, 0);
+  for (int l = 0; l <= L_; ++l) {
+    const std::int64_t cnt = 1LL << (3 * l);
+    for (std::int64_t z = 0; z < cnt; ++z) {
+      rowbeg[gid(l, z)] = off_[l][z];
+      rows[gid(l, z)] = static_cast<std::int32_t>(node_size(l, z));
+    }
+  }
+  PlanSizes& S = sizes;
+  S.w_doubles = S.s_doubles = S.piv_total = S.lu_total = 0;
+  S.factor_doubles = S.proxy_units = S.sum_rank = 0;
+  S.max_rank = 0;
+  S.ref_float_count = S.ref_int_count = 0;
+  pair_wx.assign(L_ + 1, {});
+  pair_wy.assign(L_ + 1, {});
+  pair_rx.assign(L_ + 1, {});
+  pair_ry.assign(L_ + 1, {});
+  pair_piv.assign(L_ + 1, {});
+  pair_lu.assign(L_ + 1, {});
+  for (int l = 1; l <= L_; ++l) {
+    const auto& P = pairs_[l];
+    const std::int64_t cnt = 1LL << (3 * l);
+    for (std::size_t p = 0; p < P.X.size(); ++p) {
+      const std::int64_t r = P.rank[p];
+      const std::int64_t units = r * (node_size(l, P.X[p]) + node_size(l, P.Y[p]));
+      S.sum_rank += r;
+      if (mode_[l] == kModeStream) S.factor_doubles += units;
+      else S.proxy_units += units;
+      S.max_rank = std::max(S.max_rank, P.rank[p]);
+      S.ref_float_count += 2ull * static_cast<std::uint64_t>(r * r);
+      S.ref_int_count += 4ull * static_cast<std::uint64_t>(r);
+    }
+    if (mode_[l] == kModeProxy) {
+      pair_piv[l].resize(P.X.size());
+      pair_lu[l].resize(P.X.size());
+      for (std::size_t p = 0; p < P.X.size(); ++p) {
+        const std::int64_t r = P.rank[p];
+        pair_piv[l][p] = S.piv_total;
+        pair_lu[l][p] = S.lu_total;
+        S.piv_total += 2 * r;
+        S.lu_total += r * r;
+      }
+    }
+    const auto& off = lists_[l].off[0];
+    const auto& ep = entry_pair_[l];
+    auto& ec = entry_col_[l];
+    ec.assign(ep.size(), -1);
+    for (std::int64_t z = 0; z < cnt; ++z) {
+      std::int32_t cols = 0;
+      bool any = false;
+      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
+        if (ep[e] < 0) continue;
+        ec[e] = cols;
+        cols += P.rank[ep[e]];
+        any = true;
+      }
+      const std::int64_t g = gid(l, z);
+      const std::int32_t rp = any ? cols + (cols & 1) : 0;
+      rpad[g] = rp;
+      soff[g] = S.s_doubles;
+      S.s_doubles += rp;
+      if (mode_[l] == kModeStream) {
+        woff[g] = S.w_doubles;
+        S.w_doubles += node_size(l, z) * rp;
+      }
+    }
+    if (mode_[l] == kModeStream) {
+      pair_wx[l].resize(P.X.size());
+      pair_wy[l].resize(P.X.size());
+      pair_rx[l].resize(P.X.size());
+      pair_ry[l].resize(P.X.size());
+      for (std::size_t p = 0; p < P.X.size(); ++p) {
+        const std::int64_t gx = gid(l, P.X[p]), gy = gid(l, P.Y[p]);
+        pair_wx[l][p] = woff[gx] + ec[P.eX[p]];
+        pair_rx[l][p] = rpad[gx];
+        pair_wy[l][p] = woff[gy] + ec[P.eY[p]];
+        pair_ry[l][p] = rpad[gy];
+      }
+    }
+  }
+  if (S.s_doubles > 0x7fffffffLL) throw std::invalid_argument("planner: t-vector pool exceeds int32");
+
+  // spos: column c of node z's layout (partner k) -> S slot of the mirrored
+  // block (target k, partner z). Only owned targets run phase 2.
+  spos.assign(std::max<std::int64_t>(S.s_doubles, 1), -1);
+  proxy_segs.clear();
+  for (int l = 1; l <= L_; ++l) {
+    const std::int64_t cnt = 1LL << (3 * l);
+    const auto& off = lists_[l].off[0];
+    const auto& ids = lists_[l].ids[0];
+    const auto& ep = entry_pair_[l];
+    const auto& ec = entry_col_[l];
+    const auto& P = pairs_[l];
+    for (std::int64_t z = 0; z < cnt; ++z) {
+      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
+        const std::int32_t p = ep[e];
+        if (p < 0) continue;
+        const std::int32_t k = ids[e];
+        const int r = P.rank[p];
+        const std::int64_t so = soff[gid(l, z)] + ec[e];
+        if (mode_[l] == kModeProxy) {
+          ProxySeg sg{};
+          sg.so = so;
+          sg.base = off_[l][k];
+          sg.piv_off = pair_piv[l][p];
+          sg.lu_off = pair_lu[l][p];
+          sg.r = r;
+          sg.side = (P.X[p] == z) ? 0 : 1;
+          sg.solve = owned(l, z) ? 1 : 0;
+          proxy_segs.push_back(sg);
+        }
+        if (!owned(l, k)) continue;
+        const std::int32_t e2 = (P.X[p] == z) ? P.eY[p] : P.eX[p];
+        const std::int64_t dst = soff[gid(l, k)] + ec[e2];
+        for (int a = 0; a < r; ++a) spos[so + a] = static_cast<std::int32_t>(dst + a);
+      }
+    }
+  }
+
+  // phase-1 items: stream levels (rows x 256 columns of W_Z), proxy levels
+  // (256 proxy targets x <= 2048 source points of Z)
+  items.clear();
+  reds.clear();
+  std::int64_t ptot = 0;
+  for (int l = 1; l <= L_; ++l) {
+    if (mode_[l] == kModeDirect) continue;
+    const std::int64_t cnt = 1LL << (3 * l);
+    const std::int64_t chunk = mode_[l] == kModeStream ? kRowChunk : kSrcChunk;
+    for (std::int64_t z = 0; z < cnt; ++z) {
+      const std::int64_t g = gid(l, z);
+      const int rp = rpad[g];
+      if (rp == 0) continue;
+      const std::int64_t nr = node_size(l, z);
+      const std::int64_t nrc = (nr + chunk - 1) / chunk;
+      const int ncc = (rp + kColChunk - 1) / kColChunk;
+      const std::int64_t pbase = ptot;
+      if (nrc > 1) {
+        ptot += nrc * rp;
+        reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rp, static_cast<std::int32_t>(nrc), 0, pbase});
+      }
+      for (std::int64_t k = 0; k < nrc; ++k)
+        for (int cc = 0; cc < ncc; ++cc) {
+          P1Item it{};
+          it.node = static_cast<std::int32_t>(g);
+          it.row0 = static_cast<std::int32_t>(k * chunk);
+          it.nrows = static_cast<std::int32_t>(std::min<std::int64_t>(chunk, nr - k * chunk));
+          it.col0 = cc * kColChunk;
+          it.ncols = std::min(kColChunk, rp - cc * kColChunk);
+          it.kind = mode_[l];
+          it.pslot = nrc > 1 ? pbase + k * rp + cc * kColChunk : -1;
+          items.push_back(it);
+        }
+    }
+  }
+  S.p_doubles = ptot;
+
+  // leaf plan: owned leaves; near lists = self, near_edge, near_face (the
+  // reference's dense blocks), plus the leaf-level admissible partners when
+  // that level is evaluated directly
+  const std::int64_t nl = 1LL << (3 * L_);
+  if (L_ == 0) {
+    leaf0 = 0;
+    leaf1 = rank_ == 0 ? 1 : 0;
+  } else {
+    leaf0 = static_cast<std::int64_t>(oct0_) << (3 * (L_ - 1));
+    leaf1 = static_cast<std::int64_t>(oct1_) << (3 * (L_ - 1));
+  }
+  near_off.assign(nl + 1, 0);
+  near_ids.clear();
+  nf_off.assign(nl + 1, 0);
+  nf_total = 0;
+  S.near_blocks = S.near_entries = S.direct_evals = 0;
+  for (std::int64_t x = 0; x < nl; ++x) {
+    near_off[x] = static_cast<std::int32_t>(near_ids.size());
+    nf_off[x] = nf_total;
+    const std::int64_t mx = node_size(L_, x);
+    if (mx == 0 || x < leaf0 || x >= leaf1) continue;
+    std::int64_t ntot = 0;
+    auto add = [&](std::int64_t y, bool dense) {
+      const std::int64_t ny = node_size(L_, y);
+      if (ny == 0) return;
+      near_ids.push_back(static_cast<std::int32_t>(y));
+      ntot += ny;
+      if (dense) {
+        ++S.near_blocks;
+        S.near_entries += mx * ny;
+      } else {
+        S.direct_evals += mx * ny;
+      }
+    };
+    add(x, true);
+    if (L_ > 0) {
+      for (int k = 1; k <= 2; ++k)
+        for (std::int32_t e = lists_[L_].off[k][x]; e < lists_[L_].off[k][x + 1]; ++e)
+          add(lists_[L_].ids[k][e], true);
+      if (mode_[L_] == kModeDirect)
+        for (std::int32_t e = lists_[L_].off[0][x]; e < lists_[L_].off[0][x + 1]; ++e)
+          add(lists_[L_].ids[0][e], false);
+    }
+    nf_total += mx * ntot;
+  }
+  near_off[nl] = static_cast<std::int32_t>(near_ids.size());
+  nf_off[nl] = nf_total;
+}
+
+}  // namespace h3db

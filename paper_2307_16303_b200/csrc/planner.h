@@ -1,0 +1,139 @@
+// Host-side planning of the HODLR3D representation and of the matvec launch
+// plan (pure C++, no CUDA): which pairs a shard compresses, the node-major
+// column layout shared by the factor pool W, the t-vector pool S and the
+// proxy lists, the phase-1 work items, the triangular-solve segments and the
+// leaf near lists. Exposed through the C-ABI (h3d_plan_*) so the multi-GPU
+// shard logic is testable on CPU (tests/test_shard_plan.py, gloo world 2).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace h3db {
+
+// How the admissible blocks of one level are applied in the matvec.
+enum LevelMode : int {
+  kModeStream = 0,  // explicit ACA factors streamed from the pool W (2 x 8 r(m+n) B)
+  kModeProxy = 1,   // matrix-free: pivots + packed LU (reference lowrank.cpp:291-327),
+                    //   2 r(m+n) kernel evaluations + 2 r^2 solve FMAs per pair
+  kModeDirect = 2,  // exact dense evaluation (leaf level only): 2 m n evaluations per pair
+};
+
+struct LevelLists {
+  // CSR per kind: 0 inter, 1 near_edge, 2 near_face (reference NodeLists)
+  std::vector<std::int32_t> off[3];
+  std::vector<std::int32_t> ids[3];
+};
+
+struct LevelPairs {
+  std::vector<std::int32_t> X, Y;  // Morton ids, X < Y
+  std::vector<std::int32_t> rank;
+  std::vector<std::int32_t> eX, eY;  // inter-list entry of Y in X's list / X in Y's list
+  int threads = 32;                  // ACA CTA size (fixed per level: determinism)
+  int max_m = 0, max_n = 0, max_mn = 0;
+};
+
+// phase-1 work item (both stream and proxy kinds)
+struct P1Item {
+  std::int32_t node;   // global node id
+  std::int32_t row0;   // stream: first row; proxy: first source point (local)
+  std::int32_t nrows;
+  std::int32_t col0;   // first column (local to the node's column layout)
+  std::int32_t ncols;  // <= 256
+  std::int32_t kind;   // kModeStream / kModeProxy
+  std::int64_t pslot;  // -1: write to S through spos; else partial buffer base
+};
+
+struct P1Reduce {
+  std::int32_t node;
+  std::int32_t ncols;
+  std::int32_t nchunks;
+  std::int32_t pad;
+  std::int64_t pbase;  // partials: pbase + chunk * ncols + c
+};
+
+// One ordered proxy block (target Z, partner k): its S segment, pivots, LU.
+struct ProxySeg {
+  std::int64_t so;       // S-space offset of the segment (soff[Z] + column offset)
+  std::int64_t base;     // first permuted point index of the partner node k
+  std::int64_t piv_off;  // offset of the pair's pivots (row pivots at piv_off, col at piv_off + r... see engine)
+  std::int64_t lu_off;   // offset of the pair's packed LU (row-major r x r)
+  std::int32_t r;
+  std::int32_t side;     // 0: Z is the pair's row side X (proxies = col pivots tau in k)
+                         // 1: Z is the pair's col side Y (proxies = row pivots sigma in k)
+  std::int32_t solve;    // 1 if Z is owned here (its S segment is solved before phase 2)
+  std::int32_t pad;
+};
+
+struct PlanSizes {
+  std::int64_t w_doubles = 0, s_doubles = 0, p_doubles = 0, piv_total = 0, lu_total = 0;
+  std::int64_t factor_doubles = 0, proxy_units = 0, direct_evals = 0, sum_rank = 0,
+               npairs = 0, nblocks_ordered = 0;
+  std::int64_t near_blocks = 0, near_entries = 0;
+  int max_rank = 0;
+  std::uint64_t ref_float_count = 0, ref_int_count = 0;
+};
+
+class Planner {
+ public:
+  Planner(int depth, std::int64_t n, std::vector<std::vector<std::int64_t>> off,
+          std::vector<LevelLists> lists, int rank, int world, std::vector<int> modes);
+
+  int depth() const { return L_; }
+  int mode(int l) const { return mode_[l]; }
+  bool owned(int level, std::int64_t m) const;
+  std::int64_t gid(int level, std::int64_t m) const { return node_base_[level] + m; }
+  std::int64_t node_size(int level, std::int64_t m) const {
+    return off_[level][m + 1] - off_[level][m];
+  }
+  std::int64_t total_nodes() const { return node_base_.back(); }
+  const std::vector<std::int64_t>& node_base() const { return node_base_; }
+  const std::vector<std::vector<std::int64_t>>& offsets() const { return off_; }
+  const std::vector<LevelLists>& lists() const { return lists_; }
+
+  LevelPairs& pairs(int l) { return pairs_[l]; }
+  const LevelPairs& pairs(int l) const { return pairs_[l]; }
+
+  // After every level's ranks are set: column layout, S, spos, per-pair write
+  // offsets, proxy segments, phase-1 items, leaf plan.
+  void layout();
+
+  // results ----------------------------------------------------------------
+  std::vector<std::int64_t> woff, soff, rowbeg;
+  std::vector<std::int32_t> rpad, rows;
+  std::vector<std::int32_t> spos;
+  // per level, per pair: W write offsets (stream levels) or pivot/LU offsets (proxy)
+  std::vector<std::vector<std::int64_t>> pair_wx, pair_wy, pair_piv, pair_lu;
+  std::vector<std::vector<std::int32_t>> pair_rx, pair_ry;
+  std::vector<ProxySeg> proxy_segs;
+  std::vector<P1Item> items;
+  std::vector<P1Reduce> reds;
+  std::int64_t leaf0 = 0, leaf1 = 0;
+  std::vector<std::int32_t> near_off, near_ids;
+  std::vector<std::int64_t> nf_off;  // stored near field offsets (per leaf)
+  std::int64_t nf_total = 0;
+  std::int64_t row0 = 0, row1 = 0;  // owned permuted rows
+  std::vector<std::int64_t> rank_row0, rank_row1;
+  PlanSizes sizes;
+
+ private:
+  void build_pairs();
+
+  int L_;
+  std::int64_t n_;
+  std::vector<std::vector<std::int64_t>> off_;
+  std::vector<LevelLists> lists_;
+  int rank_, world_, oct0_, oct1_;
+  std::vector<int> mode_;
+  std::vector<std::int64_t> node_base_;
+  std::vector<LevelPairs> pairs_;
+  std::vector<std::vector<std::int32_t>> entry_pair_, entry_col_;
+};
+
+// Cost-model default for the per-level modes: the leaf level
+// is evaluated directly when its blocks are smaller than their factors.
+std::vector<int> default_modes(int depth, std::int64_t n, int policy);
+
+}  // namespace h3db
