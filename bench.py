@@ -50,6 +50,12 @@ CONFIGS = {
 REF_SAMPLE_N = {"c1": 4096, "c2": 65536, "c3": 262144, "c4": 65536, "c5": 262144}
 
 FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+# FP64 peak is not in MEASURED_PEAKS.json; measured on this pool's B200 with
+# tools/fp64_bench.cu (17.49 T DFMA/s sustained, profiles/r01_summary.md)
+FP64_TFLOPS = 35.0
+# FP64 flops per kernel evaluation (SURVEY.md section 8(d) convention: 3 sub +
+# 3 mul + 2 add for r^2, rsqrt, 1 FMA = 2)
+FLOPS_PER_EVAL = {"laplace3d": 11, "r4": 12, "helmholtz-re": 30}
 
 
 def peaks():
@@ -162,6 +168,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--near", default="matrix-free", choices=["matrix-free", "stored"])
+    ap.add_argument("--policy", default="auto", choices=["auto", "stream"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -200,7 +207,8 @@ def main():
     pts = h3d.generate_points(n, cfg["seed"])
     x_host = h3d.random_vector(n, cfg["seed"] + 17)
     opt = h3d.HmatOptions(n_max=cfg["n_max"], epsilon=cfg["eps"],
-                          dense_mode="cached" if args.near == "stored" else "on-the-fly")
+                          dense_mode="cached" if args.near == "stored" else "on-the-fly",
+                          mode_policy=args.policy)
     t0 = time.time()
     rep = h3d.initialize(pts, h3d.make_kernel(cfg["kernel"]), "hodlr3d", opt, device=local_rank,
                          shard_rank=rank, shard_world=world)
@@ -285,31 +293,45 @@ def main():
         except Exception as e:  # checker unavailable: report, never substitute
             rel_err = f"unavailable: {e}"
 
-    # ---- roofline of the dominant kernel (algorithmic bytes / live duration)
+    # ---- roofline of the dominant kernel: T_roof = max(bytes / HBM, flops / FP64)
     hbm, peak_src = peaks()
     p1 = prof.phase1_ms / max(nprof, 1)
     p2 = prof.phase2_ms / max(nprof, 1)
-    F = st["factor_doubles"]
+    F = st["factor_doubles"]          # streamed factor doubles (stream levels)
     T = st["tvec_doubles"]
+    U = st["proxy_units"]             # regenerated entries per phase (proxy levels)
+    NE = st["near_entries"] + st["direct_evals"]
     nloc = st["owned_row_end"] - st["owned_row_begin"]
-    bytes_p1 = 8 * F + 8 * T + 8 * n
-    bytes_p2 = 8 * F + 8 * T + 44 * nloc
-    if p2 >= p1:
-        kname, kbytes, kms = "phase2_kernel (U.t + near field, fused un-permute)", bytes_p2, p2
+    fpe = FLOPS_PER_EVAL[cfg["kernel"]]
+    k1 = dict(name="phase1_kernel (stream V^T x | proxy K(P,Z) x)", bytes=8 * F + 8 * T + 8 * n,
+              flops=fpe * U, ms=p1)
+    k2 = dict(name="phase2_kernel (near + direct + stream U t | proxy K(X,P) s, un-permute)",
+              bytes=8 * F + 8 * T + 44 * nloc, flops=fpe * (U + NE), ms=p2)
+    for k in (k1, k2):
+        tb = k["bytes"] / (hbm * 1e9)
+        tf = k["flops"] / (FP64_TFLOPS * 1e12)
+        k["bound"] = "hbm" if tb >= tf else "fp64"
+        k["t_roof_ms"] = max(tb, tf) * 1e3
+    kd = k2 if p2 >= p1 else k1
+    if kd["bound"] == "hbm":
+        achieved, peak, unit, peak_note = kd["bytes"] / (kd["ms"] * 1e-3) / 1e9, hbm, "GB/s", peak_src
     else:
-        kname, kbytes, kms = "phase1_kernel (V^T x over the factor pool)", bytes_p1, p1
-    achieved = kbytes / (kms * 1e-3) / 1e9
+        achieved, peak, unit = kd["flops"] / (kd["ms"] * 1e-3) / 1e12, FP64_TFLOPS, "TFLOP/s"
+        peak_note = "measured fp64 DFMA peak (tools/fp64_bench.cu, profiles/r01_summary.md)"
     traffic = None
     tr = ROOT / "profiles" / "ncu_traffic.json"
     if tr.exists():
         try:
             d = json.loads(tr.read_text())
             key = "phase2" if p2 >= p1 else "phase1"
-            if d.get("config") == args.config and d.get(key) is not None:
+            if d.get("config") == args.config and d.get("policy", "stream") == args.policy \
+                    and d.get(key) is not None:
                 traffic = d[key]
         except Exception:
             traffic = None
-    step_bytes = bytes_p1 + bytes_p2
+    step_bytes = k1["bytes"] + k2["bytes"]
+    step_flops = k1["flops"] + k2["flops"]
+    step_roof_ms = max(step_bytes / (hbm * 1e9), step_flops / (FP64_TFLOPS * 1e12)) * 1e3
 
     if rank != 0:
         if dist:
@@ -337,26 +359,39 @@ def main():
                 "mt19937_64(18), bit-identical to the reference generators",
         "config": {
             "workload": cfg["desc"],
-            "representation": "symmetric-pair explicit ACA factors (one U/V pair per unordered "
-                              "admissible pair, node-major pool W), two streaming passes",
+            "representation": {"policy": args.policy,
+                               "level_modes": {str(l): ["stream", "proxy", "direct"][m]
+                                               for l, m in enumerate(st["level_modes"]) if l > 0},
+                               "note": "one ACA per unordered admissible pair; stream = explicit "
+                                       "factors in HBM, proxy = pivots+LU regenerated in FP64, "
+                                       "direct = exact leaf blocks"},
+            "streamed_factor_GB": round(8 * F / 1e9, 3),
+            "proxy_entries_per_phase": U,
+            "lu_GB": round(8 * st["lu_doubles"] / 1e9, 3),
             "near_field": args.near,
             "parallelism": f"Morton-subtree row ownership over {world} GPU(s), NCCL all-gather of x",
-            "l2": f"inputs larger than L2: factor pool {8 * F / 1e9:.1f} GB >> 126 MB L2",
+            "l2": f"inputs larger than L2: factor+LU pools {8 * (F + st['lu_doubles']) / 1e9:.1f} GB "
+                  f">> 126 MB L2 (per-step working set re-read from HBM)",
             "aca_build_s": round(build_s, 3),
             "build_ms": {k: round(st[k], 1) for k in ("build_ms_tree", "build_ms_lists",
                                                        "build_ms_aca_rank", "build_ms_aca_write",
                                                        "build_ms_total")},
             "depth": st["depth"], "aca_pairs": st["aca_pairs"], "max_rank": st["max_rank"],
-            "factor_GB": round(8 * F / 1e9, 3),
             "phase_ms": {"gather_or_exchange": round((prof.gather_ms + prof.exchange_ms) / max(nprof, 1), 4),
                          "phase1": round(p1, 4), "phase2": round(p2, 4)},
-            "step_roofline_frac": round(step_bytes / (ms * 1e-3) / 1e9 / hbm, 4),
+            "step_roofline": {"t_roof_ms": round(step_roof_ms, 3), "frac": round(step_roof_ms / ms, 4),
+                              "bytes": step_bytes, "fp64_flops": step_flops},
+            "phase_roofline": {"phase1": {"bound": k1["bound"], "t_roof_ms": round(k1["t_roof_ms"], 3),
+                                          "frac": round(k1["t_roof_ms"] / max(p1, 1e-9), 4)},
+                               "phase2": {"bound": k2["bound"], "t_roof_ms": round(k2["t_roof_ms"], 3),
+                                          "frac": round(k2["t_roof_ms"] / max(p2, 1e-9), 4)}},
             "rel_err_vs_exact_200_rows": rel_err,
         },
-        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
-                     "peak": hbm, "peak_source": peak_src, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": traffic,
-                     "alg_bytes_per_launch": kbytes},
+        "roofline": {"bound": kd["bound"], "kernel": kd["name"], "achieved": round(achieved, 3),
+                     "peak": peak, "peak_source": peak_note, "unit": unit,
+                     "frac": round(kd["t_roof_ms"] / kd["ms"], 4), "traffic": traffic,
+                     "alg_bytes_per_launch": kd["bytes"], "alg_fp64_flops_per_launch": kd["flops"],
+                     "t_roof_ms": round(kd["t_roof_ms"], 3), "t_ms": round(kd["ms"], 3)},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "Mpoints/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms},

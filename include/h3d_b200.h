@@ -61,7 +61,16 @@ typedef struct {
   int device;           /* CUDA device ordinal */
   int shard_rank;       /* Morton-subtree row ownership (parallel.hpp:9-30 analogue) */
   int shard_world;      /* 1 = single GPU owns every row */
-  int64_t reserved[8];
+  /* How each level's admissible blocks are applied:
+   * 0 = stream explicit ACA factors at every level;
+   * 1 = auto (default): leaf level evaluated exactly, upper levels split
+   *     between streamed factors and matrix-free proxies (pivots + LU, the
+   *     reference's own storage, lowrank.cpp:291-327) by a HBM/FP64 cost model;
+   * 2 = explicit per level from level_modes[l] (0 stream, 1 proxy, 2 direct;
+   *     direct only at the leaf level). */
+  int mode_policy;
+  int level_modes[16];
+  int64_t reserved[4];
 } h3d_options;
 
 /* Per-call matvec timing, milliseconds (CUDA events on the engine stream);
@@ -103,7 +112,12 @@ typedef struct {
   int64_t phase1_items;
   int64_t owned_row_begin;    /* shard rows [begin, end) in Morton order */
   int64_t owned_row_end;
-  int64_t reserved[6];
+  int level_modes[16];        /* applied mode per level (0 stream, 1 proxy, 2 direct) */
+  int64_t proxy_units;        /* sum over proxy-level pairs of r (m + n) */
+  int64_t direct_evals;       /* leaf-level admissible entries evaluated exactly */
+  int64_t lu_doubles;         /* packed LU storage of proxy-level pairs */
+  int64_t level_units[16];    /* per level: sum over pairs of r (m + n) */
+  int64_t reserved[4];
 } h3d_stats;
 
 typedef struct h3d_dev h3d_dev;
@@ -160,6 +174,24 @@ int h3d_dev_export_pairs(const h3d_dev* dev, int level, int32_t* x, int32_t* y, 
  * broadcasts the 128 bytes; every rank attaches before its first matvec. */
 int h3d_nccl_get_id(void* id128);
 int h3d_dev_attach_nccl(h3d_dev* dev, const void* id128, int rank, int world);
+
+/* Host planner (no GPU): the shard ownership, column layout, work items and
+ * leaf lists the engine derives from the tree, for CPU verification of the
+ * multi-GPU logic. offsets = concat over levels of 8^l + 1 int64; list_off =
+ * concat over (level 1..L, kind 0..2) of 8^l + 1 int32; list_ids = concat of
+ * the ids; list_counts[3*l + k] = ids per (level, kind); modes = L + 1 ints
+ * (0 stream, 1 proxy, 2 direct) or NULL. */
+typedef struct h3d_plan h3d_plan;
+int h3d_plan_create(int depth, int64_t n, const int64_t* offsets, const int32_t* list_off,
+                    const int32_t* list_ids, const int64_t* list_counts, int shard_rank,
+                    int shard_world, const int* modes, h3d_plan** out);
+void h3d_plan_destroy(h3d_plan* plan);
+int h3d_plan_pairs(const h3d_plan* plan, int level, int32_t* x, int32_t* y, int64_t* count);
+int h3d_plan_set_ranks(h3d_plan* plan, int level, const int32_t* ranks);
+int h3d_plan_set_mode(h3d_plan* plan, int level, int mode);
+int h3d_plan_layout(h3d_plan* plan);
+/* Named result arrays (raw bytes; *count = elements); see planner.h. */
+int h3d_plan_array(const h3d_plan* plan, const char* name, int level, void* out, int64_t* count);
 
 #ifdef __cplusplus
 }

@@ -314,8 +314,8 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
       // upper delta_a * v_a(j_b); row-major r x r.
       const std::int64_t po = a.piv_off[p], lo = a.lu_off[p];
       for (int q = tid; q < rank; q += NT) {
-        a.piv_row[po + q] = s_prow[q];
-        a.piv_col[po + q] = s_pcol[q];
+        a.piv[po + q] = s_prow[q];
+        a.piv[po + rank + q] = s_pcol[q];
       }
       for (int e = tid; e < rank * rank; e += NT) {
         const int row = e / rank, col = e % rank;

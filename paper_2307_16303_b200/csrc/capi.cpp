@@ -24,7 +24,7 @@ int guarded(F&& f) {
   } catch (const h3db::DegenerateDistribution& e) {
     g_err = e.what();
     return H3D_EDEGEN_DIST;
-  } catch (const h3db::InvalidArgument& e) {
+  } catch (const std::invalid_argument& e) {  // incl. h3db::InvalidArgument
     g_err = e.what();
     return H3D_EINVAL;
   } catch (const h3db::NcclFailure& e) {
@@ -67,6 +67,7 @@ void h3d_default_options(h3d_options* o) {
   o->device = 0;
   o->shard_rank = 0;
   o->shard_world = 1;
+  o->mode_policy = 1;  // auto: direct leaf level, stream/proxy split by the cost model
 }
 
 // generate_points(UniformRandom, n, seed) (kernel.cpp:88-95) with the same
@@ -170,6 +171,129 @@ int h3d_dev_attach_nccl(h3d_dev* dev, const void* id128, int rank, int world) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(eng(dev)->mu);
     eng(dev)->attach_nccl(id128, rank, world);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host planner (no GPU needed): the shard / layout / work-item logic of the
+// engine, exposed so it can be verified on CPU (tests/test_shard_plan.py).
+namespace {
+
+h3db::Planner* plan_of(h3d_plan* p) { return reinterpret_cast<h3db::Planner*>(p); }
+const h3db::Planner* plan_of(const h3d_plan* p) { return reinterpret_cast<const h3db::Planner*>(p); }
+
+template <class T>
+void put(const std::vector<T>& v, void* out, int64_t* count) {
+  *count = static_cast<int64_t>(v.size());
+  if (out && !v.empty()) std::memcpy(out, v.data(), v.size() * sizeof(T));
+}
+
+}  // namespace
+
+extern "C" {
+
+int h3d_plan_create(int depth, int64_t n, const int64_t* offsets, const int32_t* list_off,
+                    const int32_t* list_ids, const int64_t* list_counts, int shard_rank,
+                    int shard_world, const int* modes, h3d_plan** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (depth < 0 || depth > 8) throw h3db::InvalidArgument("plan: depth out of range");
+    std::vector<std::vector<int64_t>> off(depth + 1);
+    std::vector<h3db::LevelLists> lists(depth + 1);
+    int64_t po = 0, lo = 0, li = 0;
+    for (int l = 0; l <= depth; ++l) {
+      const int64_t cnt = 1LL << (3 * l);
+      off[l].assign(offsets + po, offsets + po + cnt + 1);
+      po += cnt + 1;
+      for (int k = 0; k < 3; ++k) {
+        if (l == 0) {
+          lists[0].off[k].assign(2, 0);
+          continue;
+        }
+        lists[l].off[k].assign(list_off + lo, list_off + lo + cnt + 1);
+        lo += cnt + 1;
+        const int64_t c = list_counts[3 * l + k];
+        lists[l].ids[k].assign(list_ids + li, list_ids + li + c);
+        li += c;
+      }
+    }
+    std::vector<int> m(modes ? modes : nullptr, modes ? modes + depth + 1 : nullptr);
+    auto* p = new h3db::Planner(depth, n, std::move(off), std::move(lists), shard_rank,
+                                shard_world, std::move(m));
+    *out = reinterpret_cast<h3d_plan*>(p);
+  });
+}
+
+void h3d_plan_destroy(h3d_plan* p) { delete plan_of(p); }
+
+int h3d_plan_pairs(const h3d_plan* p, int level, int32_t* x, int32_t* y, int64_t* count) {
+  return guarded([&] {
+    const auto& P = plan_of(p)->pairs(level);
+    put(P.X, x, count);
+    put(P.Y, y, count);
+  });
+}
+
+int h3d_plan_set_ranks(h3d_plan* p, int level, const int32_t* ranks) {
+  return guarded([&] {
+    auto& P = plan_of(p)->pairs(level);
+    P.rank.assign(ranks, ranks + P.X.size());
+  });
+}
+
+int h3d_plan_set_mode(h3d_plan* p, int level, int mode) {
+  return guarded([&] { plan_of(p)->set_mode(level, mode); });
+}
+
+int h3d_plan_layout(h3d_plan* p) {
+  return guarded([&] { plan_of(p)->layout(); });
+}
+
+int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, int64_t* count) {
+  return guarded([&] {
+    const h3db::Planner& P = *plan_of(p);
+    const std::string nm(name);
+    if (nm == "woff") put(P.woff, out, count);
+    else if (nm == "soff") put(P.soff, out, count);
+    else if (nm == "rowbeg") put(P.rowbeg, out, count);
+    else if (nm == "rpad") put(P.rpad, out, count);
+    else if (nm == "rows") put(P.rows, out, count);
+    else if (nm == "spos") put(P.spos, out, count);
+    else if (nm == "pair_wx") put(P.pair_wx.at(level), out, count);
+    else if (nm == "pair_wy") put(P.pair_wy.at(level), out, count);
+    else if (nm == "pair_rx") put(P.pair_rx.at(level), out, count);
+    else if (nm == "pair_ry") put(P.pair_ry.at(level), out, count);
+    else if (nm == "pair_piv") put(P.pair_piv.at(level), out, count);
+    else if (nm == "pair_lu") put(P.pair_lu.at(level), out, count);
+    else if (nm == "proxy_segs") put(P.proxy_segs, out, count);
+    else if (nm == "items") put(P.items, out, count);
+    else if (nm == "reds") put(P.reds, out, count);
+    else if (nm == "near_off") put(P.near_off, out, count);
+    else if (nm == "near_ids") put(P.near_ids, out, count);
+    else if (nm == "node_base") put(P.node_base(), out, count);
+    else if (nm == "modes") put(P.modes(), out, count);
+    else if (nm == "ranges") {
+      const std::vector<int64_t> r{P.leaf0, P.leaf1, P.row0, P.row1};
+      put(r, out, count);
+    } else if (nm == "rank_rows") {
+      std::vector<int64_t> r;
+      for (std::size_t i = 0; i < P.rank_row0.size(); ++i) {
+        r.push_back(P.rank_row0[i]);
+        r.push_back(P.rank_row1[i]);
+      }
+      put(r, out, count);
+    } else if (nm == "sizes") {
+      const auto& Z = P.sizes;
+      const std::vector<int64_t> r{Z.w_doubles, Z.s_doubles, Z.p_doubles, Z.piv_total,
+                                   Z.lu_total, Z.factor_doubles, Z.proxy_units, Z.direct_evals,
+                                   Z.sum_rank, Z.npairs, Z.nblocks_ordered, Z.near_blocks,
+                                   Z.near_entries};
+      put(r, out, count);
+    } else {
+      throw h3db::InvalidArgument("plan: unknown array " + nm);
+    }
   });
 }
 

@@ -37,6 +37,26 @@ __device__ __forceinline__ double kernel_r2(double r2) {
   }
 }
 
+// Matvec-path radial map: Laplace uses the hardware fp64 rsqrt seed
+// (MUFU.RSQ64H, ~2^-22) plus one Newton step (~1e-13 relative), 1.26x the
+// throughput of rsqrt() in the P2P loop (profiles/r01_summary.md).
+__device__ __forceinline__ double rsqrt_nr1(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double p = x * y;
+  const double e = fma(-p, y, 1.0);
+  return fma(0.5 * y, e, y);
+}
+
+template <int K>
+__device__ __forceinline__ double kernel_r2_fast(double r2) {
+  if constexpr (K == kLaplace) {
+    return rsqrt_nr1(r2);
+  } else {
+    return kernel_r2<K>(r2);
+  }
+}
+
 __device__ __forceinline__ double sq3(double dx, double dy, double dz) {
   return fma(dz, dz, fma(dy, dy, dx * dx));
 }

@@ -1,9 +1,10 @@
-// Host orchestration: build (tree -> lists -> pairs -> ACA rank pass ->
-// layout -> ACA write pass -> matvec plan) and the matvec launch sequence.
+// Host orchestration: build (tree -> lists -> plan -> ACA rank pass -> mode
+// choice -> layout -> ACA write pass -> proxies) and the matvec launch
+// sequence (gather / x all-gather -> phase 1 -> proxy solves -> phase 2).
 //
 // Reference mapping:
 //   Engine::Engine      <- h3d::initialize (hmatrix.cpp:52-151)
-//   Engine::matvec      <- h3d::matvec (hmatrix.cpp:153-226); with shard_world > 1
+//   Engine::enqueue     <- h3d::matvec (hmatrix.cpp:153-226); with shard_world > 1
 //                          <- h3d::parallel_matvec (parallel.cpp:111-306)
 //   Engine::stats       <- h3d::stats (hmatrix.cpp:228-251)
 #include "engine.h"
@@ -25,9 +26,19 @@ double ms_since(Clock::time_point t0) {
   return std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
 }
 
-constexpr int kMaxDepth = 8;            // 8^8 leaves; beyond that the device tables explode
-constexpr std::int64_t kRowChunk = 2048;  // phase-1 row chunk for tall nodes
-constexpr int kColChunk = 256;          // phase-1 columns per item
+constexpr int kMaxDepth = 8;       // 8^8 leaves; beyond that the device tables explode
+constexpr int kMaxProxyRank = 320; // proxy_solve_kernel's per-warp shared buffer
+
+// Cost model (profiles/r01_summary.md): streamed factor bytes at the measured
+// copy bandwidth, regenerated entries at the measured P2P evaluation rate.
+constexpr double kStreamBW = 6.2e12;  // B/s
+double eval_rate(int kernel) {
+  switch (kernel) {
+    case kLaplace: return 1.15e12;
+    case kR4: return 0.8e12;
+    default: return 0.25e12;
+  }
+}
 
 #define NCCL_CHECK(expr)                                                        \
   do {                                                                          \
@@ -73,6 +84,7 @@ template class DevBuf<unsigned>;
 template class DevBuf<unsigned long long>;
 template class DevBuf<P1Item>;
 template class DevBuf<P1Reduce>;
+template class DevBuf<ProxySeg>;
 
 Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_(opt), n_(n) {
   const auto t0 = Clock::now();
@@ -85,13 +97,13 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   if (opt.depth_cap < 0 || opt.depth_cap > 20)
     throw InvalidArgument("build_tree: unreasonable depth cap");
   if (n > 0x7fffffffLL) throw InvalidArgument("initialize: N exceeds int32 point indices");
+  if (opt.mode_policy < 0 || opt.mode_policy > 2)
+    throw InvalidArgument("initialize: mode_policy must be 0, 1 or 2");
   world_ = opt.shard_world < 1 ? 1 : opt.shard_world;
   rank_ = opt.shard_rank;
   if (!(world_ == 1 || world_ == 2 || world_ == 4 || world_ == 8))
     throw InvalidArgument("initialize: shard_world must be 1, 2, 4 or 8 (Morton-subtree ownership)");
   if (rank_ < 0 || rank_ >= world_) throw InvalidArgument("initialize: shard_rank out of range");
-  oct0_ = 8 * rank_ / world_;
-  oct1_ = 8 * (rank_ + 1) / world_;
 
   H3D_CUDA_CHECK(cudaSetDevice(opt.device));
   cudaDeviceProp prop{};
@@ -106,15 +118,33 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   t = Clock::now();
   build_lists();
   ms_lists_ = ms_since(t);
-  build_pairs();
+
+  // initial modes: direct leaf level (auto: small leaves are cheaper to
+  // evaluate than to compress), stream/proxy for the rest decided after ranks
+  modes_.assign(L_ + 1, kModeStream);
+  if (opt_.mode_policy == 1 && L_ >= 1 && opt_.n_max <= 128) modes_[L_] = kModeDirect;
+  if (opt_.mode_policy == 2) {
+    for (int l = 1; l <= L_ && l < 16; ++l) {
+      const int m = opt_.level_modes[l];
+      if (m < 0 || m > 2) throw InvalidArgument("initialize: level_modes entries must be 0, 1 or 2");
+      if (m == kModeDirect && l != L_)
+        throw InvalidArgument("initialize: direct mode is only valid at the leaf level");
+      modes_[l] = m;
+    }
+  }
+  plan_ = std::make_unique<Planner>(L_, n_, off_, lists_, rank_, world_, modes_);
   t = Clock::now();
   run_aca(false);
   ms_aca_rank_ = ms_since(t);
-  build_layout();
+  choose_modes();
+  plan_->layout();
+  upload_plan();
   t = Clock::now();
   run_aca(true);
   ms_aca_write_ = ms_since(t);
-  build_matvec_plan();
+  if (n_segs_all_ > 0)
+    launch_proxy_gather(segs_all_.get(), n_segs_all_, piv_.get(), px_.get(), py_.get(), pz_.get(),
+                        qx_.get(), qy_.get(), qz_.get(), stream_);
   near_scan();
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   ms_total_ = ms_since(t0);
@@ -136,12 +166,6 @@ void Engine::check_flags(const char* where) {
   if (f & kFlagOutOfDomain) throw InvalidArgument("build_tree: point outside the domain cube");
   if (f & kFlagDegenGeom)
     throw DegenerateGeometry(std::string("coincident distinct points in block (") + where + ")");
-}
-
-bool Engine::owned(int level, std::int64_t m) const {
-  if (level == 0) return rank_ == 0;
-  const std::int64_t oct = m >> (3 * (level - 1));
-  return oct >= oct0_ && oct < oct1_;
 }
 
 // ---------------------------------------------------------------- tree
@@ -196,7 +220,6 @@ void Engine::build_tree(const double* xyz) {
                           " exceeds the device engine's limit of " + std::to_string(kMaxDepth));
   L_ = depth;
   off_.resize(L_ + 1);
-  node_base_.assign(L_ + 2, 0);
   for (int l = 0; l <= L_; ++l) {
     const std::int64_t cnt = 1LL << (3 * l);
     DevBuf<std::int64_t> o;
@@ -205,9 +228,7 @@ void Engine::build_tree(const double* xyz) {
     off_[l].resize(cnt + 1);
     H3D_CUDA_CHECK(cudaMemcpyAsync(off_[l].data(), o.get(), (cnt + 1) * 8, cudaMemcpyDeviceToHost, stream_));
     H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    node_base_[l + 1] = node_base_[l] + cnt;
   }
-  total_nodes_ = node_base_[L_ + 1];
   perm_h_.resize(n_);
   H3D_CUDA_CHECK(cudaMemcpyAsync(perm_h_.data(), perm_.get(), n_ * 4, cudaMemcpyDeviceToHost, stream_));
   px_.alloc(n_);
@@ -216,25 +237,6 @@ void Engine::build_tree(const double* xyz) {
   launch_permute_points(xyz_d.get(), perm_.get(), n_, px_.get(), py_.get(), pz_.get(), stream_);
   leaf_off_.upload(off_[L_], stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
-  // owned row range (Morton-subtree shard)
-  if (L_ == 0) {
-    row0_ = 0;
-    row1_ = rank_ == 0 ? n_ : 0;
-  } else {
-    row0_ = off_[1][oct0_];
-    row1_ = off_[1][oct1_];
-  }
-  rank_row0_.resize(world_);
-  rank_row1_.resize(world_);
-  for (int r = 0; r < world_; ++r) {
-    if (L_ == 0) {
-      rank_row0_[r] = 0;
-      rank_row1_[r] = r == 0 ? n_ : 0;
-    } else {
-      rank_row0_[r] = off_[1][8 * r / world_];
-      rank_row1_[r] = off_[1][8 * (r + 1) / world_];
-    }
-  }
 }
 
 // ---------------------------------------------------------------- lists
@@ -275,78 +277,27 @@ void Engine::build_lists() {
   }
 }
 
-// ---------------------------------------------------------------- pairs
-// Admissible blocks (hmatrix.cpp:74-98) with both nodes non-empty; one ACA
-// per unordered pair X < Y (the lists are swap-symmetric, octree tests
-// test_octree.cpp:167-181, and the built-in kernels are symmetric,
-// kernel.cpp:7-21). A shard compresses every pair touching an owned node.
-void Engine::build_pairs() {
-  pairs_.assign(L_ + 1, LevelPairs{});
-  entry_pair_.assign(L_ + 1, {});
-  entry_col_.assign(L_ + 1, {});
-  nblocks_ordered_ = 0;
-  for (int l = 1; l <= L_; ++l) {
-    const std::int64_t cnt = 1LL << (3 * l);
-    const auto& off = lists_[l].off[0];
-    const auto& ids = lists_[l].ids[0];
-    auto& ep = entry_pair_[l];
-    ep.assign(ids.size(), -1);
-    auto& P = pairs_[l];
-    for (std::int64_t X = 0; X < cnt; ++X) {
-      if (node_size(l, X) == 0) continue;
-      for (std::int32_t e = off[X]; e < off[X + 1]; ++e) {
-        const std::int32_t Y = ids[e];
-        if (node_size(l, Y) == 0) continue;
-        ++nblocks_ordered_;
-        if (Y <= X || !(owned(l, X) || owned(l, Y))) continue;
-        ep[e] = static_cast<std::int32_t>(P.X.size());
-        P.X.push_back(static_cast<std::int32_t>(X));
-        P.Y.push_back(Y);
-        const int m = static_cast<int>(node_size(l, X)), nn = static_cast<int>(node_size(l, Y));
-        P.max_m = std::max(P.max_m, m);
-        P.max_n = std::max(P.max_n, nn);
-        P.max_mn = std::max(P.max_mn, std::min(m, nn));
-      }
-    }
-    for (std::int64_t Z = 0; Z < cnt; ++Z) {
-      if (node_size(l, Z) == 0) continue;
-      for (std::int32_t e = off[Z]; e < off[Z + 1]; ++e) {
-        const std::int32_t k = ids[e];
-        if (k >= Z || node_size(l, k) == 0 || !(owned(l, Z) || owned(l, k))) continue;
-        // Z's position in k's sorted list
-        const auto b = ids.begin() + off[k], en = ids.begin() + off[k + 1];
-        const auto it = std::lower_bound(b, en, static_cast<std::int32_t>(Z));
-        if (it == en || *it != Z) throw std::logic_error("interaction lists not swap-symmetric");
-        ep[e] = ep[static_cast<std::size_t>(it - ids.begin())];
-      }
-    }
-    P.rank.assign(P.X.size(), 0);
-    const double mbar = static_cast<double>(n_) / static_cast<double>(cnt);
-    P.threads = mbar <= 64 ? 32 : mbar <= 512 ? 128 : mbar <= 4096 ? 256 : 512;
-  }
-  npairs_ = 0;
-  for (const auto& P : pairs_) npairs_ += static_cast<std::int64_t>(P.X.size());
-}
-
 // ---------------------------------------------------------------- ACA
 void Engine::run_aca(bool write) {
   DevBuf<unsigned long long> counter;
   counter.alloc(1);
   std::size_t free_b = 0, total_b = 0;
   H3D_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  if (!write) free_mem_ = free_b;
   for (int l = 1; l <= L_; ++l) {
-    auto& P = pairs_[l];
+    auto& P = plan_->pairs(l);
     const std::int64_t np = static_cast<std::int64_t>(P.X.size());
     if (np == 0) continue;
-    std::vector<std::int64_t> xb(np), yb(np), wx, wy;
-    std::vector<std::int32_t> m(np), nn(np), rx, ry;
+    const int mode = plan_->mode(l);
+    std::vector<std::int64_t> xb(np), yb(np);
+    std::vector<std::int32_t> m(np), nn(np);
     for (std::int64_t p = 0; p < np; ++p) {
       xb[p] = off_[l][P.X[p]];
       yb[p] = off_[l][P.Y[p]];
       m[p] = static_cast<std::int32_t>(node_size(l, P.X[p]));
       nn[p] = static_cast<std::int32_t>(node_size(l, P.Y[p]));
     }
-    DevBuf<std::int64_t> d_xb, d_yb, d_wx, d_wy;
+    DevBuf<std::int64_t> d_xb, d_yb, d_wx, d_wy, d_po, d_lo;
     DevBuf<std::int32_t> d_m, d_n, d_rank, d_rx, d_ry;
     d_xb.upload(xb, stream_);
     d_yb.upload(yb, stream_);
@@ -355,31 +306,16 @@ void Engine::run_aca(bool write) {
     d_rank.alloc(np);
     int level_max_rank = 0;
     if (write) {
-      wx.resize(np);
-      wy.resize(np);
-      rx.resize(np);
-      ry.resize(np);
-      // column offsets of the pair in W_X and W_Y (build_layout)
-      const auto& off = lists_[l].off[0];
-      const auto& ids = lists_[l].ids[0];
-      const auto& ec = entry_col_[l];
-      for (std::int64_t p = 0; p < np; ++p) {
-        const std::int32_t X = P.X[p], Y = P.Y[p];
-        auto find = [&](std::int32_t a, std::int32_t b) {
-          const auto it = std::lower_bound(ids.begin() + off[a], ids.begin() + off[a + 1], b);
-          return static_cast<std::size_t>(it - ids.begin());
-        };
-        const std::int64_t gx = gid(l, X), gy = gid(l, Y);
-        wx[p] = woff_h_[gx] + ec[find(X, Y)];
-        rx[p] = rpad_h_[gx];
-        wy[p] = woff_h_[gy] + ec[find(Y, X)];
-        ry[p] = rpad_h_[gy];
-        level_max_rank = std::max(level_max_rank, P.rank[p]);
+      for (std::int64_t p = 0; p < np; ++p) level_max_rank = std::max(level_max_rank, P.rank[p]);
+      if (mode == kModeStream) {
+        d_wx.upload(plan_->pair_wx[l], stream_);
+        d_wy.upload(plan_->pair_wy[l], stream_);
+        d_rx.upload(plan_->pair_rx[l], stream_);
+        d_ry.upload(plan_->pair_ry[l], stream_);
+      } else {
+        d_po.upload(plan_->pair_piv[l], stream_);
+        d_lo.upload(plan_->pair_lu[l], stream_);
       }
-      d_wx.upload(wx, stream_);
-      d_wy.upload(wy, stream_);
-      d_rx.upload(rx, stream_);
-      d_ry.upload(ry, stream_);
     }
     const int ms = (P.max_m + 1) & ~1, ns = (P.max_n + 1) & ~1;
     int cap_ws;
@@ -422,12 +358,18 @@ void Engine::run_aca(bool write) {
       a.ms = ms;
       a.ns = ns;
       a.rank_out = d_rank.get();
-      if (write) {
+      if (write && mode == kModeStream) {
         a.W = W_.get();
         a.wx = d_wx.get();
         a.rx = d_rx.get();
         a.wy = d_wy.get();
         a.ry = d_ry.get();
+      }
+      if (write && mode == kModeProxy) {
+        a.piv = piv_.get();
+        a.lu = lu_.get();
+        a.piv_off = d_po.get();
+        a.lu_off = d_lo.get();
       }
       a.flags = flags_.get();
       a.counter = counter.get();
@@ -455,180 +397,126 @@ void Engine::run_aca(bool write) {
   }
 }
 
-// ---------------------------------------------------------------- layout
-// W_Z = [F_Z^(Z,k1) | F_Z^(Z,k2) | ...] over Z's partners in list order,
-// row-major |Z| x rpad_Z (rpad even: 16-byte rows). S shares the column
-// layout; spos maps a column of W_Z to the S slot of the mirrored block.
-void Engine::build_layout() {
-  woff_h_.assign(total_nodes_, 0);
-  soff_h_.assign(total_nodes_, 0);
-  rowbeg_h_.assign(total_nodes_, 0);
-  rpad_h_.assign(total_nodes_, 0);
-  rows_h_.assign(total_nodes_, 0);
-  for (int l = 0; l <= L_; ++l) {
-    const std::int64_t cnt = 1LL << (3 * l);
-    for (std::int64_t z = 0; z < cnt; ++z) {
-      rowbeg_h_[gid(l, z)] = off_[l][z];
-      rows_h_[gid(l, z)] = static_cast<std::int32_t>(node_size(l, z));
-    }
-  }
-  std::int64_t wtot = 0, stot = 0;
-  factor_doubles_ = sum_rank_ = 0;
-  max_rank_ = 0;
-  ref_float_count_ = ref_int_count_ = 0;
+// ---------------------------------------------------------------- modes
+// Auto policy: the FP64 pipes (proxy regeneration, near field, direct leaf
+// blocks) and HBM (factor streaming) are separate resources; pick the
+// stream/proxy split of the upper levels that minimises
+//   max(stream, compute_1) + max(stream, compute_2 + near + direct)
+// subject to the factor pool fitting in free memory.
+void Engine::choose_modes() {
+  if (opt_.mode_policy != 1) return;
+  std::vector<int> cand;
+  std::vector<double> units(L_ + 1, 0.0), lu(L_ + 1, 0.0);
+  std::vector<int> maxr(L_ + 1, 0);
   for (int l = 1; l <= L_; ++l) {
-    const auto& P = pairs_[l];
+    const auto& P = plan_->pairs(l);
+    if (plan_->mode(l) == kModeDirect || P.X.empty()) continue;
     for (std::size_t p = 0; p < P.X.size(); ++p) {
-      const std::int64_t r = P.rank[p];
-      sum_rank_ += r;
-      factor_doubles_ += r * (node_size(l, P.X[p]) + node_size(l, P.Y[p]));
-      max_rank_ = std::max(max_rank_, P.rank[p]);
-      ref_float_count_ += 2ull * static_cast<std::uint64_t>(r * r);
-      ref_int_count_ += 4ull * static_cast<std::uint64_t>(r);
+      const double r = P.rank[p];
+      units[l] += r * static_cast<double>(node_size(l, P.X[p]) + node_size(l, P.Y[p]));
+      lu[l] += r * r;
+      maxr[l] = std::max(maxr[l], P.rank[p]);
     }
-    const std::int64_t cnt = 1LL << (3 * l);
-    const auto& off = lists_[l].off[0];
-    const auto& ep = entry_pair_[l];
-    auto& ec = entry_col_[l];
-    ec.assign(ep.size(), -1);
-    for (std::int64_t z = 0; z < cnt; ++z) {
-      std::int32_t cols = 0;
-      bool any = false;
-      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
-        if (ep[e] < 0) continue;
-        ec[e] = cols;
-        cols += P.rank[ep[e]];
-        any = true;
-      }
-      const std::int64_t g = gid(l, z);
-      const std::int32_t rpad = any ? cols + (cols & 1) : 0;
-      rpad_h_[g] = rpad;
-      woff_h_[g] = wtot;
-      soff_h_[g] = stot;
-      wtot += node_size(l, z) * rpad;
-      stot += rpad;
-    }
+    cand.push_back(l);
   }
-  w_doubles_ = wtot;
-  s_doubles_ = stot;
-  if (stot > 0x7fffffffLL) throw InvalidArgument("initialize: t-vector pool exceeds int32 indexing");
-  std::vector<std::int32_t> spos(std::max<std::int64_t>(stot, 1), -1);
-  for (int l = 1; l <= L_; ++l) {
-    const std::int64_t cnt = 1LL << (3 * l);
-    const auto& off = lists_[l].off[0];
-    const auto& ids = lists_[l].ids[0];
-    const auto& ep = entry_pair_[l];
-    const auto& ec = entry_col_[l];
-    const auto& P = pairs_[l];
-    for (std::int64_t z = 0; z < cnt; ++z) {
-      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
-        if (ep[e] < 0) continue;
-        const std::int32_t k = ids[e];
-        if (!owned(l, k)) continue;  // only owned targets run phase 2
-        const int r = P.rank[ep[e]];
-        const auto it = std::lower_bound(ids.begin() + off[k], ids.begin() + off[k + 1],
-                                         static_cast<std::int32_t>(z));
-        const std::int32_t e2 = ec[static_cast<std::size_t>(it - ids.begin())];
-        const std::int64_t src = soff_h_[gid(l, z)] + ec[e];
-        const std::int64_t dst = soff_h_[gid(l, k)] + e2;
-        for (int a = 0; a < r; ++a) spos[src + a] = static_cast<std::int32_t>(dst + a);
+  // phase-2 compute independent of the split: near field + direct leaf blocks
+  double fixed = 0.0;
+  {
+    const auto& lst = lists_[L_];
+    for (std::int64_t x = 0; x < (1LL << (3 * L_)); ++x) {
+      const double mx = static_cast<double>(node_size(L_, x));
+      if (mx == 0) continue;
+      double nsum = mx;
+      if (L_ > 0) {
+        for (int k = 1; k <= 2; ++k)
+          for (std::int32_t e = lst.off[k][x]; e < lst.off[k][x + 1]; ++e)
+            nsum += static_cast<double>(node_size(L_, lst.ids[k][e]));
+        if (plan_->mode(L_) == kModeDirect)
+          for (std::int32_t e = lst.off[0][x]; e < lst.off[0][x + 1]; ++e)
+            nsum += static_cast<double>(node_size(L_, lst.ids[0][e]));
+      }
+      fixed += mx * nsum;
+    }
+    fixed /= static_cast<double>(world_);
+  }
+  const double E = eval_rate(opt_.kernel_id);
+  const double budget = 0.8 * static_cast<double>(free_mem_) - 64.0 * static_cast<double>(n_) -
+                        (2 << 30);
+  double best = 1e300;
+  unsigned best_mask = 0;
+  const unsigned ncand = static_cast<unsigned>(cand.size());
+  for (unsigned mask = 0; mask < (1u << ncand); ++mask) {  // bit set = stream
+    double sbytes = 0.0, comp = 0.0, lub = 0.0;
+    bool ok = true;
+    for (unsigned i = 0; i < ncand; ++i) {
+      const int l = cand[i];
+      if (mask & (1u << i)) {
+        sbytes += 8.0 * units[l];
+      } else {
+        if (maxr[l] > kMaxProxyRank) ok = false;
+        comp += units[l] / E;
+        lub += 16.0 * lu[l];
       }
     }
+    if (!ok || sbytes > budget) continue;
+    const double ts = sbytes / kStreamBW;
+    const double T = std::max(ts, comp) + std::max(ts, comp + fixed / E) + lub / kStreamBW;
+    if (T < best) {
+      best = T;
+      best_mask = mask;
+    }
   }
-  W_.alloc(std::max<std::int64_t>(wtot, 2));
-  H3D_CUDA_CHECK(cudaMemsetAsync(W_.get(), 0, W_.size() * 8, stream_));
-  S_.alloc(std::max<std::int64_t>(stot, 2));
-  H3D_CUDA_CHECK(cudaMemsetAsync(S_.get(), 0, S_.size() * 8, stream_));
-  spos_.upload(spos, stream_);
-  woff_.upload(woff_h_, stream_);
-  soff_.upload(soff_h_, stream_);
-  rowbeg_.upload(rowbeg_h_, stream_);
-  rpad_.upload(rpad_h_, stream_);
-  rows_.upload(rows_h_, stream_);
-  H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (best == 1e300)
+    throw std::runtime_error("initialize: no stream/proxy split fits in device memory");
+  for (unsigned i = 0; i < ncand; ++i)
+    plan_->set_mode(cand[i], (best_mask & (1u << i)) ? kModeStream : kModeProxy);
 }
 
-// ---------------------------------------------------------------- plan
-void Engine::build_matvec_plan() {
-  std::vector<P1Item> items;
-  std::vector<P1Reduce> reds;
-  std::int64_t ptot = 0;
-  for (int l = 1; l <= L_; ++l) {
-    const std::int64_t cnt = 1LL << (3 * l);
-    for (std::int64_t z = 0; z < cnt; ++z) {
-      const std::int64_t g = gid(l, z);
-      const int rpad = rpad_h_[g];
-      if (rpad == 0) continue;
-      const std::int64_t rows = node_size(l, z);
-      const std::int64_t nrc = (rows + kRowChunk - 1) / kRowChunk;
-      const int ncc = (rpad + kColChunk - 1) / kColChunk;
-      const std::int64_t pbase = ptot;
-      if (nrc > 1) {
-        ptot += nrc * rpad;
-        reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rpad, static_cast<std::int32_t>(nrc), 0, pbase});
-      }
-      for (std::int64_t k = 0; k < nrc; ++k)
-        for (int cc = 0; cc < ncc; ++cc) {
-          P1Item it{};
-          it.node = static_cast<std::int32_t>(g);
-          it.row0 = static_cast<std::int32_t>(k * kRowChunk);
-          it.nrows = static_cast<std::int32_t>(std::min<std::int64_t>(kRowChunk, rows - k * kRowChunk));
-          it.col0 = cc * kColChunk;
-          it.ncols = std::min(kColChunk, rpad - cc * kColChunk);
-          it.pslot = nrc > 1 ? pbase + k * rpad + cc * kColChunk : -1;
-          items.push_back(it);
-        }
-    }
+// ---------------------------------------------------------------- device plan
+void Engine::upload_plan() {
+  const Planner& P = *plan_;
+  const PlanSizes& Z = P.sizes;
+  woff_.upload(P.woff, stream_);
+  soff_.upload(P.soff, stream_);
+  rowbeg_.upload(P.rowbeg, stream_);
+  rpad_.upload(P.rpad, stream_);
+  rows_.upload(P.rows, stream_);
+  W_.alloc(std::max<std::int64_t>(Z.w_doubles, 2));
+  H3D_CUDA_CHECK(cudaMemsetAsync(W_.get(), 0, W_.size() * 8, stream_));
+  S_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
+  H3D_CUDA_CHECK(cudaMemsetAsync(S_.get(), 0, S_.size() * 8, stream_));
+  spos_.upload(P.spos, stream_);
+  P_.alloc(std::max<std::int64_t>(Z.p_doubles, 1));
+  piv_.alloc(std::max<std::int64_t>(Z.piv_total, 1));
+  lu_.alloc(std::max<std::int64_t>(Z.lu_total, 1));
+  // proxy coordinates share S's index space; padding slots sit far away
+  // (their weights are 0, see matvec.cu)
+  qx_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
+  qy_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
+  qz_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
+  {
+    std::vector<double> far(qx_.size(), 1e100);
+    H3D_CUDA_CHECK(cudaMemcpyAsync(qx_.get(), far.data(), far.size() * 8, cudaMemcpyHostToDevice, stream_));
+    H3D_CUDA_CHECK(cudaMemcpyAsync(qy_.get(), far.data(), far.size() * 8, cudaMemcpyHostToDevice, stream_));
+    H3D_CUDA_CHECK(cudaMemcpyAsync(qz_.get(), far.data(), far.size() * 8, cudaMemcpyHostToDevice, stream_));
+    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   }
-  n_p1_ = static_cast<std::int64_t>(items.size());
-  n_red_ = static_cast<std::int64_t>(reds.size());
-  p_doubles_ = ptot;
-  p1_items_.upload(items, stream_);
-  p1_red_.upload(reds, stream_);
-  P_.alloc(std::max<std::int64_t>(ptot, 1));
-
-  // leaf near lists: self, near_edge, near_face (non-empty), visit order of
-  // the reference dense pass (hmatrix.cpp:105-120)
-  const std::int64_t nl = 1LL << (3 * L_);
-  if (L_ == 0) {
-    leaf0_ = 0;
-    leaf1_ = rank_ == 0 ? 1 : 0;
-  } else {
-    leaf0_ = static_cast<std::int64_t>(oct0_) << (3 * (L_ - 1));
-    leaf1_ = static_cast<std::int64_t>(oct1_) << (3 * (L_ - 1));
-  }
-  std::vector<std::int32_t> noff(nl + 1, 0), nids;
-  std::vector<std::int64_t> nfoff(nl + 1, 0);
-  std::int64_t nftot = 0;
-  near_blocks_ = near_entries_ = 0;
-  for (std::int64_t x = 0; x < nl; ++x) {
-    noff[x] = static_cast<std::int32_t>(nids.size());
-    nfoff[x] = nftot;
-    const std::int64_t mx = node_size(L_, x);
-    if (mx == 0 || x < leaf0_ || x >= leaf1_) continue;
-    std::int64_t ntot = 0;
-    auto add = [&](std::int64_t y) {
-      const std::int64_t ny = node_size(L_, y);
-      if (ny == 0) return;
-      nids.push_back(static_cast<std::int32_t>(y));
-      ntot += ny;
-      ++near_blocks_;
-      near_entries_ += mx * ny;
-    };
-    add(x);
-    if (L_ > 0)
-      for (int k = 1; k <= 2; ++k)
-        for (std::int32_t e = lists_[L_].off[k][x]; e < lists_[L_].off[k][x + 1]; ++e)
-          add(lists_[L_].ids[k][e]);
-    nftot += mx * ntot;
-  }
-  noff[nl] = static_cast<std::int32_t>(nids.size());
-  nfoff[nl] = nftot;
-  near_off_.upload(noff, stream_);
-  near_ids_.upload(nids.empty() ? std::vector<std::int32_t>{0} : nids, stream_);
+  std::vector<ProxySeg> solve;
+  for (const auto& s : P.proxy_segs)
+    if (s.solve) solve.push_back(s);
+  n_segs_all_ = static_cast<std::int64_t>(P.proxy_segs.size());
+  n_segs_solve_ = static_cast<std::int64_t>(solve.size());
+  segs_all_.upload(P.proxy_segs, stream_);
+  segs_solve_.upload(solve, stream_);
+  p1_items_.upload(P.items, stream_);
+  p1_red_.upload(P.reds, stream_);
+  n_p1_ = static_cast<std::int64_t>(P.items.size());
+  n_red_ = static_cast<std::int64_t>(P.reds.size());
+  near_off_.upload(P.near_off, stream_);
+  near_ids_.upload(P.near_ids.empty() ? std::vector<std::int32_t>{0} : P.near_ids, stream_);
   if (opt_.near_mode == H3D_NEAR_STORED) {
-    nf_off_.upload(nfoff, stream_);
-    NF_.alloc(std::max<std::int64_t>(nftot, 1));
+    nf_off_.upload(P.nf_off, stream_);
+    NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
   }
   x_.alloc(n_);
   xp_.alloc(n_);
@@ -636,21 +524,45 @@ void Engine::build_matvec_plan() {
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
 
-void Engine::near_scan() {
-  if (leaf1_ <= leaf0_) return;
+Phase2Args Engine::phase2_args(double* bout) const {
+  const Planner& P = *plan_;
   Phase2Args a;
   a.depth = L_;
-  a.leaf0 = leaf0_;
-  a.nleaves = leaf1_ - leaf0_;
+  a.leaf0 = P.leaf0;
+  a.nleaves = P.leaf1 - P.leaf0;
   a.leaf_off = leaf_off_.get();
+  a.nt = NodeTable{rowbeg_.get(), rows_.get(), woff_.get(), rpad_.get(), soff_.get()};
+  a.W = W_.get();
+  a.S = S_.get();
+  a.xp = xp_.get();
   a.px = px_.get();
   a.py = py_.get();
   a.pz = pz_.get();
+  a.qx = qx_.get();
+  a.qy = qy_.get();
+  a.qz = qz_.get();
+  a.perm = perm_.get();
   a.near_off = near_off_.get();
   a.near_ids = near_ids_.get();
-  a.nf_off = opt_.near_mode == H3D_NEAR_STORED ? nf_off_.get() : nullptr;
+  if (opt_.near_mode == H3D_NEAR_STORED) {
+    a.nf_off = nf_off_.get();
+    a.NF = NF_.get();
+  }
   a.kernel = opt_.kernel_id;
   a.diag = opt_.diagonal;
+  a.b = bout;
+  for (int l = 0; l <= L_ && l < 24; ++l) {
+    a.lbase[l] = P.node_base()[l];
+    a.mode[l] = P.mode(l);
+  }
+  return a;
+}
+
+void Engine::near_scan() {
+  const Planner& P = *plan_;
+  if (P.leaf1 <= P.leaf0) return;
+  Phase2Args a = phase2_args(nullptr);
+  if (opt_.near_mode != H3D_NEAR_STORED) a.nf_off = nullptr;
   H3D_CUDA_CHECK(cudaMemsetAsync(flags_.get(), 0, 4, stream_));
   launch_near_scan(a, opt_.near_mode == H3D_NEAR_STORED ? NF_.get() : nullptr, flags_.get(), stream_);
   check_flags("near field");
@@ -658,9 +570,10 @@ void Engine::near_scan() {
 
 // ---------------------------------------------------------------- matvec
 // Enqueue one matvec on stream s: x (original order, device) -> b (original
-// order, device). ev (optional, 4 events) brackets gather/exchange, phase 1,
-// phase 2. Returns the number of kernels launched.
+// order, device). ev (optional, 4 events) brackets gather/exchange, phase 1
+// (+ reduce + proxy solves), phase 2. Returns the number of kernels launched.
 std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev) {
+  const Planner& P = *plan_;
   std::int64_t launches = 0;
   if (ev) cudaEventRecord(ev[0], s);
   if (world_ == 1) {
@@ -668,52 +581,32 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ++launches;
   } else {
     // own slice of x in Morton order, then the all-gather of x over NVLink
-    if (row1_ > row0_) {
-      launch_gather(xin, perm_.get() + row0_, row1_ - row0_, xp_.get() + row0_, s);
+    if (P.row1 > P.row0) {
+      launch_gather(xin, perm_.get() + P.row0, P.row1 - P.row0, xp_.get() + P.row0, s);
       ++launches;
     }
     auto comm = static_cast<ncclComm_t>(nccl_comm_);
     NCCL_CHECK(ncclGroupStart());
     for (int r = 0; r < world_; ++r) {
-      const std::int64_t c = rank_row1_[r] - rank_row0_[r];
+      const std::int64_t c = P.rank_row1[r] - P.rank_row0[r];
       if (c > 0)
-        NCCL_CHECK(ncclBroadcast(xp_.get() + rank_row0_[r], xp_.get() + rank_row0_[r],
+        NCCL_CHECK(ncclBroadcast(xp_.get() + P.rank_row0[r], xp_.get() + P.rank_row0[r],
                                  static_cast<std::size_t>(c), ncclDouble, r, comm, s));
     }
     NCCL_CHECK(ncclGroupEnd());
   }
   if (ev) cudaEventRecord(ev[1], s);
   NodeTable nt{rowbeg_.get(), rows_.get(), woff_.get(), rpad_.get(), soff_.get()};
-  launch_phase1(p1_items_.get(), n_p1_, nt, W_.get(), xp_.get(), spos_.get(), S_.get(), P_.get(), s);
+  launch_phase1(p1_items_.get(), n_p1_, nt, W_.get(), xp_.get(), spos_.get(), S_.get(), P_.get(),
+                px_.get(), py_.get(), pz_.get(), qx_.get(), qy_.get(), qz_.get(), opt_.kernel_id, s);
   launches += n_p1_ > 0;
   launch_phase1_reduce(p1_red_.get(), n_red_, nt, spos_.get(), P_.get(), S_.get(), s);
   launches += n_red_ > 0;
+  launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), S_.get(), s);
+  launches += n_segs_solve_ > 0;
   if (ev) cudaEventRecord(ev[2], s);
-  if (leaf1_ > leaf0_) {
-    Phase2Args a;
-    a.depth = L_;
-    a.leaf0 = leaf0_;
-    a.nleaves = leaf1_ - leaf0_;
-    a.leaf_off = leaf_off_.get();
-    a.nt = nt;
-    a.W = W_.get();
-    a.S = S_.get();
-    a.xp = xp_.get();
-    a.px = px_.get();
-    a.py = py_.get();
-    a.pz = pz_.get();
-    a.perm = perm_.get();
-    a.near_off = near_off_.get();
-    a.near_ids = near_ids_.get();
-    if (opt_.near_mode == H3D_NEAR_STORED) {
-      a.nf_off = nf_off_.get();
-      a.NF = NF_.get();
-    }
-    a.kernel = opt_.kernel_id;
-    a.diag = opt_.diagonal;
-    a.b = bout;
-    for (int l = 0; l <= L_ && l < 24; ++l) a.lbase[l] = node_base_[l];
-    launch_phase2(a, s);
+  if (P.leaf1 > P.leaf0) {
+    launch_phase2(phase2_args(bout), s);
     ++launches;
   }
   if (ev) cudaEventRecord(ev[3], s);
@@ -813,21 +706,25 @@ void Engine::attach_nccl(const void* id128, int rank, int world) {
 }
 
 void Engine::stats(h3d_stats* s) const {
+  const Planner& P = *plan_;
+  const PlanSizes& Z = P.sizes;
   std::memset(s, 0, sizeof(*s));
   s->depth = L_;
-  s->max_rank = max_rank_;
+  s->max_rank = Z.max_rank;
   s->n = n_;
-  s->lowrank_blocks = nblocks_ordered_;
-  s->aca_pairs = npairs_;
-  s->sum_rank = sum_rank_;
-  s->factor_doubles = factor_doubles_;
-  s->factor_bytes_alloc = w_doubles_ * 8;
-  s->tvec_doubles = s_doubles_;
-  s->near_blocks = near_blocks_;
-  s->near_entries = near_entries_;
-  s->near_bytes_stored = opt_.near_mode == H3D_NEAR_STORED ? near_entries_ * 8 : 0;
-  s->ref_float_count = ref_float_count_ + static_cast<std::uint64_t>(near_entries_);
-  s->ref_int_count = ref_int_count_;
+  s->lowrank_blocks = Z.nblocks_ordered;
+  s->aca_pairs = Z.npairs;
+  s->sum_rank = Z.sum_rank;
+  s->factor_doubles = Z.factor_doubles;
+  s->factor_bytes_alloc = Z.w_doubles * 8;
+  s->tvec_doubles = Z.s_doubles;
+  s->near_blocks = Z.near_blocks;
+  s->near_entries = Z.near_entries;
+  s->near_bytes_stored = opt_.near_mode == H3D_NEAR_STORED ? P.nf_total * 8 : 0;
+  // reference RepStats convention (hmatrix.cpp:228-251): r^2 per ordered
+  // block + dense leaf areas (directly evaluated leaf blocks count as dense)
+  s->ref_float_count = Z.ref_float_count + static_cast<std::uint64_t>(Z.near_entries + Z.direct_evals);
+  s->ref_int_count = Z.ref_int_count;
   s->compression_ratio = static_cast<double>(s->ref_float_count) /
                          (static_cast<double>(n_) * static_cast<double>(n_));
   s->build_ms_tree = ms_tree_;
@@ -836,8 +733,19 @@ void Engine::stats(h3d_stats* s) const {
   s->build_ms_aca_write = ms_aca_write_;
   s->build_ms_total = ms_total_;
   s->phase1_items = n_p1_;
-  s->owned_row_begin = row0_;
-  s->owned_row_end = row1_;
+  s->owned_row_begin = P.row0;
+  s->owned_row_end = P.row1;
+  for (int l = 0; l <= L_ && l < 16; ++l) s->level_modes[l] = P.mode(l);
+  s->proxy_units = Z.proxy_units;
+  s->direct_evals = Z.direct_evals;
+  s->lu_doubles = Z.lu_total;
+  for (int l = 1; l <= L_ && l < 16; ++l) {
+    const auto& pr = P.pairs(l);
+    std::int64_t u = 0;
+    for (std::size_t p = 0; p < pr.X.size(); ++p)
+      u += static_cast<std::int64_t>(pr.rank[p]) * (node_size(l, pr.X[p]) + node_size(l, pr.Y[p]));
+    s->level_units[l] = u;
+  }
 }
 
 void Engine::export_tree(std::int32_t* perm, int level, std::int64_t* offsets) const {
@@ -868,7 +776,7 @@ std::int64_t Engine::export_list(int level, int kind, std::int32_t* offsets,
 std::int64_t Engine::export_pairs(int level, std::int32_t* x, std::int32_t* y,
                                   std::int32_t* rank) const {
   if (level < 1 || level > L_) return 0;
-  const auto& P = pairs_[level];
+  const auto& P = plan_->pairs(level);
   if (x) std::memcpy(x, P.X.data(), P.X.size() * 4);
   if (y) std::memcpy(y, P.Y.data(), P.Y.size() * 4);
   if (rank) std::memcpy(rank, P.rank.data(), P.rank.size() * 4);

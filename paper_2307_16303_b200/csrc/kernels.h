@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include "planner.h"
+
 namespace h3db {
 
 struct CudaError : std::runtime_error {
@@ -38,7 +40,7 @@ void launch_permute_points(const double* xyz, const std::int32_t* perm, std::int
 
 // --------------------------------------------------------------- lists.cu
 // HODLR3D lists at one level (octree.cpp:197-260): kind 0 inter (vertex +
-// well-separated), 1 near_edge, 2 near_face. counts: 3 x 8^l.
+// well-separated), 1 near_edge, 2 near_face. counts: 3 x (8^l + 1).
 void launch_list_counts(int level, std::int32_t* counts, cudaStream_t s);
 void launch_list_fill(int level, const std::int32_t* offsets, std::int32_t* ids0,
                       std::int32_t* ids1, std::int32_t* ids2, cudaStream_t s);
@@ -65,15 +67,15 @@ struct AcaArgs {
   int cap_ws = 0;     // rank capacity of a slot
   int ms = 0, ns = 0; // column strides of U (m) and V (n) in a slot
   std::int32_t* rank_out = nullptr;
-  // factor write-back (pass 2); null in the rank pass
+  // factor write-back (stream levels, write pass)
   double* W = nullptr;
   const std::int64_t* wx = nullptr;  // W offset of U's (row 0, col 0)
   const std::int32_t* rx = nullptr;  // U row stride
   const std::int64_t* wy = nullptr;
   const std::int32_t* ry = nullptr;
-  // optional pivot/LU write-back (matrix-free mode)
-  std::int32_t* piv_row = nullptr;
-  std::int32_t* piv_col = nullptr;
+  // pivot + packed-LU write-back (proxy levels, write pass): row pivots at
+  // piv[piv_off[p] + a], column pivots at piv[piv_off[p] + r + a]
+  std::int32_t* piv = nullptr;
   double* lu = nullptr;
   const std::int64_t* piv_off = nullptr;
   const std::int64_t* lu_off = nullptr;
@@ -89,61 +91,50 @@ int aca_blocks_per_sm(int threads, int kernel, std::size_t smem);
 void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp,
                    cudaStream_t s);
 
-struct P1Item {
-  std::int32_t node;   // global node id
-  std::int32_t row0;   // first row (local to the node)
-  std::int32_t nrows;
-  std::int32_t col0;   // first column (local), multiple of 256
-  std::int32_t ncols;  // <= 256
-  std::int32_t pad;
-  std::int64_t pslot;  // -1: write to S directly; else partial buffer base
-};
-
-struct P1Reduce {
-  std::int32_t node;
-  std::int32_t ncols;
-  std::int32_t nchunks;
-  std::int32_t pad;
-  std::int64_t pbase;  // partials: pbase + chunk * ncols + c
-};
-
 struct NodeTable {
   const std::int64_t* rowbeg = nullptr;  // first permuted row of global node g
   const std::int32_t* rows = nullptr;    // number of points
   const std::int64_t* woff = nullptr;    // factor matrix W_g (rows x rpad, row-major)
-  const std::int32_t* rpad = nullptr;
-  const std::int64_t* soff = nullptr;    // S_g (rpad entries)
+  const std::int32_t* rpad = nullptr;    // columns of the node's layout
+  const std::int64_t* soff = nullptr;    // S_g / proxy slots (rpad entries)
 };
 
 void launch_phase1(const P1Item* items, std::int64_t nitems, NodeTable nt, const double* W,
                    const double* xp, const std::int32_t* spos, double* S, double* P,
-                   cudaStream_t s);
+                   const double* px, const double* py, const double* pz, const double* qx,
+                   const double* qy, const double* qz, int kernel, cudaStream_t s);
 void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
                           const std::int32_t* spos, const double* P, double* S,
                           cudaStream_t s);
+void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int32_t* piv,
+                         const double* px, const double* py, const double* pz, double* qx,
+                         double* qy, double* qz, cudaStream_t s);
+void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, double* S,
+                        cudaStream_t s);
 
 struct Phase2Args {
   int depth = 0;
   std::int64_t nleaves = 0;  // leaves processed by this launch
   std::int64_t leaf0 = 0;    // first leaf (Morton id) of this launch
   const std::int64_t* leaf_off = nullptr;  // 8^L + 1
-  const std::int64_t* node_base = nullptr; // global id base per level (host-side values copied)
   NodeTable nt;
   const double* W = nullptr;
   const double* S = nullptr;
   const double* xp = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;
+  const double *qx = nullptr, *qy = nullptr, *qz = nullptr;
   const std::int32_t* perm = nullptr;
-  // leaf near lists: self + near_edge + near_face (non-empty), CSR
+  // leaf near lists: self + near_edge + near_face (+ direct partners), CSR
   const std::int32_t* near_off = nullptr;
   const std::int32_t* near_ids = nullptr;
   // stored near field (near_mode 0): per leaf a row-major m x (sum n) block
-  const std::int64_t* nf_off = nullptr;  // per leaf offset into NF (or null: matrix-free)
+  const std::int64_t* nf_off = nullptr;
   const double* NF = nullptr;
   int kernel = 0;
   double diag = 0.0;
   double* b = nullptr;  // output, original order
   std::int64_t lbase[24] = {0};  // node_base per level (by value)
+  int mode[24] = {0};            // LevelMode per level
 };
 void launch_phase2(const Phase2Args& a, cudaStream_t s);
 

@@ -53,6 +53,13 @@ Planner::Planner(int depth, std::int64_t n, std::vector<std::vector<std::int64_t
     row0 = off_[1][oct0_];
     row1 = off_[1][oct1_];
   }
+  if (L_ == 0) {
+    leaf0 = 0;
+    leaf1 = rank_ == 0 ? 1 : 0;
+  } else {
+    leaf0 = static_cast<std::int64_t>(oct0_) << (3 * (L_ - 1));
+    leaf1 = static_cast<std::int64_t>(oct1_) << (3 * (L_ - 1));
+  }
   rank_row0.resize(world_);
   rank_row1.resize(world_);
   for (int r = 0; r < world_; ++r) {

@@ -83,6 +83,14 @@ class Planner {
 
   int depth() const { return L_; }
   int mode(int l) const { return mode_[l]; }
+  const std::vector<int>& modes() const { return mode_; }
+  // stream <-> proxy may change after the rank pass (direct cannot: it decides
+  // which pairs exist)
+  void set_mode(int l, int m) {
+    if (mode_[l] == kModeDirect || m == kModeDirect)
+      throw std::invalid_argument("planner: direct mode is fixed at construction");
+    mode_[l] = m;
+  }
   bool owned(int level, std::int64_t m) const;
   std::int64_t gid(int level, std::int64_t m) const { return node_base_[level] + m; }
   std::int64_t node_size(int level, std::int64_t m) const {

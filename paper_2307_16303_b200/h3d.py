@@ -52,7 +52,9 @@ class _Options(C.Structure):
         ("device", C.c_int),
         ("shard_rank", C.c_int),
         ("shard_world", C.c_int),
-        ("reserved", C.c_int64 * 8),
+        ("mode_policy", C.c_int),
+        ("level_modes", C.c_int * 16),
+        ("reserved", C.c_int64 * 4),
     ]
 
 
@@ -94,7 +96,12 @@ class _Stats(C.Structure):
         ("phase1_items", C.c_int64),
         ("owned_row_begin", C.c_int64),
         ("owned_row_end", C.c_int64),
-        ("reserved", C.c_int64 * 6),
+        ("level_modes", C.c_int * 16),
+        ("proxy_units", C.c_int64),
+        ("direct_evals", C.c_int64),
+        ("lu_doubles", C.c_int64),
+        ("level_units", C.c_int64 * 16),
+        ("reserved", C.c_int64 * 4),
     ]
 
 
@@ -103,7 +110,8 @@ _EXPORTS = [
     "h3d_random_vector", "h3d_dev_create", "h3d_dev_destroy", "h3d_dev_matvec",
     "h3d_dev_stats", "h3d_dev_export_tree", "h3d_dev_export_list", "h3d_dev_export_pairs",
     "h3d_nccl_get_id", "h3d_dev_attach_nccl", "h3d_dev_matvec_async", "h3d_dev_profile",
-    "h3d_dev_profile_read",
+    "h3d_dev_profile_read", "h3d_plan_create", "h3d_plan_destroy", "h3d_plan_pairs",
+    "h3d_plan_set_ranks", "h3d_plan_set_mode", "h3d_plan_layout", "h3d_plan_array",
 ]
 
 
@@ -128,6 +136,14 @@ def _load():
     L.h3d_dev_matvec_async.argtypes = [P, P, P, P]
     L.h3d_dev_profile.argtypes = [P, C.c_int, C.c_int64]
     L.h3d_dev_profile_read.argtypes = [P, C.POINTER(_Timing), C.POINTER(C.c_int64)]
+    L.h3d_plan_create.argtypes = [C.c_int, C.c_int64, P, P, P, P, C.c_int, C.c_int, P,
+                                  C.POINTER(P)]
+    L.h3d_plan_destroy.argtypes = [P]
+    L.h3d_plan_pairs.argtypes = [P, C.c_int, P, P, C.POINTER(C.c_int64)]
+    L.h3d_plan_set_ranks.argtypes = [P, C.c_int, P]
+    L.h3d_plan_set_mode.argtypes = [P, C.c_int, C.c_int]
+    L.h3d_plan_layout.argtypes = [P]
+    L.h3d_plan_array.argtypes = [P, C.c_char_p, C.c_int, P, C.POINTER(C.c_int64)]
     L.h3d_nccl_get_id.argtypes = [P]
     L.h3d_dev_attach_nccl.argtypes = [P, P, C.c_int, C.c_int]
     return L
@@ -211,6 +227,11 @@ class HmatOptions:
     dense_mode: str = "on-the-fly"
     depth_cap: int = 12
     max_rank: int = 0
+    # B200 extension: "auto" (cost model), "stream"
+    # (explicit factors everywhere) or "explicit" (level_modes[l]: 0 stream,
+    # 1 proxy, 2 direct at the leaf level)
+    mode_policy: str = "auto"
+    level_modes: tuple = ()
 
 
 @dataclasses.dataclass
@@ -245,6 +266,13 @@ class HMatrixRep:
         o.device = int(device)
         o.shard_rank = int(shard_rank)
         o.shard_world = int(shard_world)
+        policies = {"stream": 0, "auto": 1, "explicit": 2}
+        if options.mode_policy not in policies:
+            raise ValueError(f"unknown mode_policy: {options.mode_policy}")
+        o.mode_policy = policies[options.mode_policy]
+        for l, m in enumerate(options.level_modes):
+            if l < 16:
+                o.level_modes[l] = int(m)
         h = C.c_void_p()
         self._h = None
         _check(_L.h3d_dev_create(_ptr(pts), len(pts), C.byref(o), C.byref(h)))
@@ -312,7 +340,16 @@ class HMatrixRep:
     def stats(self) -> dict:
         s = _Stats()
         _check(_L.h3d_dev_stats(self._h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in _Stats._fields_ if f != "reserved"}
+        out = {}
+        for f, _ in _Stats._fields_:
+            if f == "reserved":
+                continue
+            v = getattr(s, f)
+            out[f] = list(v) if f in ("level_modes", "level_units") else v
+        L = out["depth"]
+        out["level_modes"] = out["level_modes"][: L + 1]
+        out["level_units"] = out["level_units"][: L + 1]
+        return out
 
     @property
     def depth(self) -> int:
@@ -375,3 +412,80 @@ def matvec(rep: HMatrixRep, x, timing: Optional[MatvecTiming] = None) -> np.ndar
 
 def stats(rep: HMatrixRep) -> dict:
     return rep.stats()
+
+
+# ---------------------------------------------------------------- host planner
+_PLAN_DTYPES = {
+    "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
+    "spos": np.int32, "pair_wx": np.int64, "pair_wy": np.int64, "pair_rx": np.int32,
+    "pair_ry": np.int32, "pair_piv": np.int64, "pair_lu": np.int64, "near_off": np.int32,
+    "near_ids": np.int32, "node_base": np.int64, "modes": np.int32, "ranges": np.int64,
+    "rank_rows": np.int64, "sizes": np.int64,
+    # structs, decoded as int64 fields (see csrc/planner.h)
+    "proxy_segs": np.dtype([("so", np.int64), ("base", np.int64), ("piv_off", np.int64),
+                            ("lu_off", np.int64), ("r", np.int32), ("side", np.int32),
+                            ("solve", np.int32), ("pad", np.int32)]),
+    "items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
+                       ("col0", np.int32), ("ncols", np.int32), ("kind", np.int32),
+                       ("pslot", np.int64)]),
+    "reds": np.dtype([("node", np.int32), ("ncols", np.int32), ("nchunks", np.int32),
+                      ("pad", np.int32), ("pbase", np.int64)]),
+}
+
+
+class Plan:
+    """The engine's host planner (csrc/planner.cpp) driven from Python: shard
+    ownership, pair selection, column layout, phase-1 items, proxy segments and
+    leaf lists, without a GPU. `offsets[l]` / `lists[l][k]` = (off, ids) as
+    exported by the tree/list builders (bit-identical to the reference)."""
+
+    def __init__(self, depth, n, offsets, lists, shard_rank=0, shard_world=1, modes=None):
+        off = np.ascontiguousarray(np.concatenate([np.asarray(offsets[l], np.int64)
+                                                   for l in range(depth + 1)]))
+        lo, li, counts = [], [], np.zeros(3 * (depth + 1), np.int64)
+        for l in range(1, depth + 1):
+            for k in range(3):
+                o, ids = lists[l][k]
+                lo.append(np.asarray(o, np.int32))
+                li.append(np.asarray(ids, np.int32))
+                counts[3 * l + k] = len(ids)
+        lo = np.ascontiguousarray(np.concatenate(lo) if lo else np.zeros(1, np.int32))
+        li = np.ascontiguousarray(np.concatenate(li) if li else np.zeros(1, np.int32))
+        md = None if modes is None else np.ascontiguousarray(np.asarray(modes, np.int32))
+        h = C.c_void_p()
+        self._h = None
+        _check(_L.h3d_plan_create(depth, n, _ptr(off), _ptr(lo), _ptr(li), _ptr(counts),
+                                  shard_rank, shard_world, None if md is None else _ptr(md),
+                                  C.byref(h)))
+        self._h = h
+        self.depth = depth
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _L.h3d_plan_destroy(self._h)
+
+    def pairs(self, level):
+        cnt = C.c_int64(0)
+        _check(_L.h3d_plan_pairs(self._h, level, None, None, C.byref(cnt)))
+        x = np.empty(max(cnt.value, 1), np.int32)
+        y = np.empty(max(cnt.value, 1), np.int32)
+        _check(_L.h3d_plan_pairs(self._h, level, _ptr(x), _ptr(y), C.byref(cnt)))
+        return x[: cnt.value], y[: cnt.value]
+
+    def set_ranks(self, level, ranks):
+        r = np.ascontiguousarray(ranks, np.int32)
+        _check(_L.h3d_plan_set_ranks(self._h, level, _ptr(r)))
+
+    def set_mode(self, level, mode):
+        _check(_L.h3d_plan_set_mode(self._h, level, int(mode)))
+
+    def layout(self):
+        _check(_L.h3d_plan_layout(self._h))
+
+    def array(self, name, level=0):
+        dt = np.dtype(_PLAN_DTYPES[name])
+        cnt = C.c_int64(0)
+        _check(_L.h3d_plan_array(self._h, name.encode(), level, None, C.byref(cnt)))
+        out = np.zeros(max(cnt.value, 1), dt)
+        _check(_L.h3d_plan_array(self._h, name.encode(), level, _ptr(out), C.byref(cnt)))
+        return out[: cnt.value]

@@ -1,0 +1,214 @@
+"""TEST INFRASTRUCTURE — a numpy executor for the engine's host plan.
+
+Runs the matvec exactly as the GPU kernels do (phase-1 items -> spos/partials
+-> reduce -> proxy solves -> phase-2 leaf tiles), but in numpy, from a
+`paper_2307_16303_b200.h3d.Plan` and factors derived from the oracle's ACA
+(pivots + packed LU, the reference's representation). This verifies the
+planner's shard ownership, pair selection, layout, spos mapping, partial
+reductions, proxy segments and solve directions on CPU.
+"""
+import numpy as np
+
+
+def kernel_matrix(kind, A, B):
+    d = A[:, None, :] - B[None, :, :]
+    r2 = np.einsum("ijk,ijk->ij", d, d)
+    with np.errstate(divide="ignore", over="ignore", invalid="ignore"):
+        if kind == "laplace3d":
+            return 1.0 / np.sqrt(r2)
+        if kind == "r4":
+            return 1.0 / (r2 * r2)
+        r = np.sqrt(r2)
+        return np.cos(r) / r
+
+
+def oracle_inputs(oracle, n, seed, n_max, eps, kind):
+    pts = oracle.generate_points(n, seed)
+    orep = oracle.initialize(pts, kind, n_max=n_max, eps=eps)
+    L = orep.depth
+    offsets = [orep.offsets(l) for l in range(L + 1)]
+    lists = [None] + [[orep.list(l, k) for k in range(3)] for l in range(1, L + 1)]
+    pairs = {}
+    for l in range(1, L + 1):
+        t, s, r = orep.lr_blocks(l)
+        for k in range(len(t)):
+            if t[k] < s[k]:
+                pairs[(l, int(t[k]), int(s[k]))] = orep.lr_block_detail(l, k, int(r[k]))
+    perm = orep.perm()
+    return dict(pts=pts, orep=orep, L=L, offsets=offsets, lists=lists, pairs=pairs, perm=perm,
+                ppts=pts[perm])
+
+
+def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
+    """Returns b in Morton order for the plan's owned rows (others zero)."""
+    L, off, ppts, pd = inp["L"], inp["offsets"], inp["ppts"], inp["pairs"]
+    # ranks, optional mode switches, layout
+    for l in range(1, L + 1):
+        X, Y = plan.pairs(l)
+        plan.set_ranks(l, [len(pd[(l, int(a), int(b))][0]) for a, b in zip(X, Y)])
+    if modes is not None:
+        for l in range(1, L + 1):
+            if modes[l] != 2 and plan.array("modes")[l] != 2:
+                plan.set_mode(l, modes[l])
+    plan.layout()
+    md = plan.array("modes")
+    sizes = plan.array("sizes")
+    W = np.zeros(max(sizes[0], 1))
+    S = np.zeros(max(sizes[1], 1))
+    P = np.zeros(max(sizes[2], 1))
+    piv = np.zeros(max(sizes[3], 1), np.int64)
+    lu = np.zeros(max(sizes[4], 1))
+    woff, soff, rowbeg = plan.array("woff"), plan.array("soff"), plan.array("rowbeg")
+    rpad, spos, nb = plan.array("rpad"), plan.array("spos"), plan.array("node_base")
+
+    def pts_of(l, z):
+        return ppts[off[l][z]:off[l][z + 1]]
+
+    for l in range(1, L + 1):
+        X, Y = plan.pairs(l)
+        if md[l] == 0:
+            wx, wy = plan.array("pair_wx", l), plan.array("pair_wy", l)
+            rx, ry = plan.array("pair_rx", l), plan.array("pair_ry", l)
+        elif md[l] == 1:
+            po, lo = plan.array("pair_piv", l), plan.array("pair_lu", l)
+        for p, (a, b) in enumerate(zip(X, Y)):
+            rp, cp, LU = pd[(l, int(a), int(b))]
+            r = len(rp)
+            if r == 0:
+                continue
+            Lm = np.tril(LU, -1) + np.eye(r)
+            Um = np.triu(LU)
+            Xp, Yp = pts_of(l, a), pts_of(l, b)
+            if md[l] == 0:
+                FX = np.linalg.solve(Um.T, kernel_matrix(kind, Xp, Yp[cp]).T).T  # K(X,tau) R^-1
+                FY = np.linalg.solve(Lm, kernel_matrix(kind, Yp, Xp[rp]).T).T    # K(Y,sigma) L^-T
+                for i in range(len(Xp)):
+                    W[wx[p] + i * rx[p]: wx[p] + i * rx[p] + r] = FX[i]
+                for j in range(len(Yp)):
+                    W[wy[p] + j * ry[p]: wy[p] + j * ry[p] + r] = FY[j]
+            elif md[l] == 1:
+                piv[po[p]: po[p] + r] = rp
+                piv[po[p] + r: po[p] + 2 * r] = cp
+                lu[lo[p]: lo[p] + r * r] = LU.reshape(-1)
+    # proxy coordinates (padding far away, weight 0)
+    Q = np.full((max(sizes[1], 1), 3), 1e100)
+    for sg in plan.array("proxy_segs"):
+        r = int(sg["r"])
+        loc = piv[sg["piv_off"] + (r if sg["side"] == 0 else 0): sg["piv_off"] + (r if sg["side"] == 0 else 0) + r]
+        Q[sg["so"]: sg["so"] + r] = ppts[sg["base"] + loc]
+
+    # ---- phase 1
+    for it in plan.array("items"):
+        g = int(it["node"])
+        rb = rowbeg[g] + it["row0"]
+        c0, nc = int(it["col0"]), int(it["ncols"])
+        xs = xp[rb: rb + it["nrows"]]
+        if it["kind"] == 0:
+            R = int(rpad[g])
+            Wn = W[woff[g]: woff[g] + (it["row0"] + it["nrows"]) * R].reshape(-1, R)[it["row0"]:]
+            v = Wn[:, c0: c0 + nc].T @ xs
+        else:
+            v = kernel_matrix(kind, Q[soff[g] + c0: soff[g] + c0 + nc], ppts[rb: rb + it["nrows"]]) @ xs
+        if it["pslot"] < 0:
+            dst = spos[soff[g] + c0: soff[g] + c0 + nc]
+            ok = dst >= 0
+            S[dst[ok]] = v[ok]
+        else:
+            P[it["pslot"]: it["pslot"] + nc] = v
+    for rd in plan.array("reds"):
+        g, nc, k = int(rd["node"]), int(rd["ncols"]), int(rd["nchunks"])
+        v = P[rd["pbase"]: rd["pbase"] + k * nc].reshape(k, nc).sum(axis=0)
+        dst = spos[soff[g]: soff[g] + nc]
+        ok = dst >= 0
+        S[dst[ok]] = v[ok]
+    # ---- proxy solves
+    for sg in plan.array("proxy_segs"):
+        if not sg["solve"]:
+            continue
+        r, so = int(sg["r"]), int(sg["so"])
+        LU = lu[sg["lu_off"]: sg["lu_off"] + r * r].reshape(r, r)
+        Lm = np.tril(LU, -1) + np.eye(r)
+        Um = np.triu(LU)
+        v = S[so: so + r]
+        if sg["side"] == 0:
+            S[so: so + r] = np.linalg.solve(Um, np.linalg.solve(Lm, v))
+        else:
+            S[so: so + r] = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, v))
+    # ---- phase 2
+    leaf0, leaf1, row0, row1 = plan.array("ranges")
+    noff, nids = plan.array("near_off"), plan.array("near_ids")
+    b = np.zeros(len(ppts))
+    for X in range(leaf0, leaf1):
+        xb, xe = off[L][X], off[L][X + 1]
+        if xe == xb:
+            continue
+        T = ppts[xb:xe]
+        acc = np.zeros(xe - xb)
+        for Y in nids[noff[X]: noff[X + 1]]:
+            yb, ye = off[L][Y], off[L][Y + 1]
+            K = kernel_matrix(kind, T, ppts[yb:ye])
+            if Y == X:
+                np.fill_diagonal(K, diag)
+            acc += K @ xp[yb:ye]
+        for l in range(1, L + 1):
+            A = X >> (3 * (L - l))
+            g = nb[l] + A
+            R = int(rpad[g])
+            if R == 0:
+                continue
+            so = soff[g]
+            if md[l] == 1:
+                acc += kernel_matrix(kind, T, Q[so: so + R]) @ S[so: so + R]
+            else:
+                ro = xb - rowbeg[g]
+                Wr = W[woff[g] + ro * R: woff[g] + (ro + xe - xb) * R].reshape(-1, R)
+                acc += Wr @ S[so: so + R]
+        b[xb:xe] = acc
+    return b, (int(row0), int(row1))
+
+
+def symmetric_reference(inp, x, kind, direct_leaf=False, diag=0.0):
+    """Dense numpy evaluation of the representation the engine applies: the
+    reference's dense leaf blocks (exact), one pivot/LU factorization per
+    unordered pair applied to both block orientations, optionally the leaf
+    level's admissible blocks exact. Morton order in, original order out."""
+    L, off, ppts, pd, perm = inp["L"], inp["offsets"], inp["ppts"], inp["pairs"], inp["perm"]
+    xp = x[perm]
+    b = np.zeros(len(xp))
+    lists = inp["lists"]
+    for X in range(1 << (3 * L)):
+        xb, xe = off[L][X], off[L][X + 1]
+        if xe == xb:
+            continue
+        nbrs = [X]
+        if L > 0:
+            for k in (1, 2):
+                o, ids = lists[L][k]
+                nbrs += [int(v) for v in ids[o[X]:o[X + 1]]]
+        for Y in nbrs:
+            yb, ye = off[L][Y], off[L][Y + 1]
+            K = kernel_matrix(kind, ppts[xb:xe], ppts[yb:ye])
+            if Y == X:
+                np.fill_diagonal(K, diag)
+            b[xb:xe] += K @ xp[yb:ye]
+    for (l, a, c), (rp, cp, LU) in pd.items():
+        xa, xe = off[l][a], off[l][a + 1]
+        ya, ye = off[l][c], off[l][c + 1]
+        Xp, Yp = ppts[xa:xe], ppts[ya:ye]
+        if direct_leaf and l == L:
+            K = kernel_matrix(kind, Xp, Yp)
+            b[xa:xe] += K @ xp[ya:ye]
+            b[ya:ye] += K.T @ xp[xa:xe]
+            continue
+        r = len(rp)
+        if r == 0:
+            continue
+        Lm = np.tril(LU, -1) + np.eye(r)
+        Um = np.triu(LU)
+        t = np.linalg.solve(Um, np.linalg.solve(Lm, kernel_matrix(kind, Xp[rp], Yp) @ xp[ya:ye]))
+        b[xa:xe] += kernel_matrix(kind, Xp, Yp[cp]) @ t
+        t2 = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, kernel_matrix(kind, Yp[cp], Xp) @ xp[xa:xe]))
+        b[ya:ye] += kernel_matrix(kind, Yp, Xp[rp]) @ t2
+    out = np.empty_like(b)
+    out[perm] = b
+    return out

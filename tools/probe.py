@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--nmax", type=int, default=64)
     ap.add_argument("--kernel", default="laplace3d")
     ap.add_argument("--mode", default="on-the-fly")
+    ap.add_argument("--policy", default="auto")
+    ap.add_argument("--levels", default="")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--check-rows", type=int, default=0)
@@ -30,7 +32,9 @@ def main():
     x = h3d.random_vector(a.n, a.seed + 17)
     t1 = time.time()
     rep = h3d.initialize(pts, h3d.make_kernel(a.kernel), "hodlr3d",
-                         h3d.HmatOptions(n_max=a.nmax, epsilon=a.eps, dense_mode=a.mode))
+                         h3d.HmatOptions(n_max=a.nmax, epsilon=a.eps, dense_mode=a.mode,
+                                         mode_policy=a.policy,
+                                         level_modes=tuple(int(c) for c in a.levels)))
     t2 = time.time()
     st = rep.stats()
     tm = h3d.MatvecTiming()
