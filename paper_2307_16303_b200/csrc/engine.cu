@@ -110,7 +110,12 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   H3D_CUDA_CHECK(cudaGetDeviceProperties(&prop, opt.device));
   sms_ = prop.multiProcessorCount;
   H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
   for (auto& e : ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
+  for (int k = 0; k < 2; ++k) {
+    H3D_CUDA_CHECK(cudaEventCreateWithFlags(&fork_[k], cudaEventDisableTiming));
+    H3D_CUDA_CHECK(cudaEventCreateWithFlags(&join_[k], cudaEventDisableTiming));
+  }
 
   auto t = Clock::now();
   build_tree(xyz);
@@ -156,6 +161,11 @@ Engine::~Engine() {
   if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
+  for (int k = 0; k < 2; ++k) {
+    if (fork_[k]) cudaEventDestroy(fork_[k]);
+    if (join_[k]) cudaEventDestroy(join_[k]);
+  }
+  if (stream2_) cudaStreamDestroy(stream2_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -508,12 +518,26 @@ void Engine::upload_plan() {
   n_segs_solve_ = static_cast<std::int64_t>(solve.size());
   segs_all_.upload(P.proxy_segs, stream_);
   segs_solve_.upload(solve, stream_);
-  p1_items_.upload(P.items, stream_);
+  // phase-1 items split by resource: HBM-bound stream items and FP64-bound
+  // proxy items run as two concurrent persistent kernels
+  std::vector<P1Item> si, pi;
+  for (const auto& it : P.items) (it.kind == kModeStream ? si : pi).push_back(it);
+  p1_stream_items_.upload(si, stream_);
+  p1_proxy_items_.upload(pi, stream_);
+  n_p1s_ = static_cast<std::int64_t>(si.size());
+  n_p1p_ = static_cast<std::int64_t>(pi.size());
   p1_red_.upload(P.reds, stream_);
-  n_p1_ = static_cast<std::int64_t>(P.items.size());
   n_red_ = static_cast<std::int64_t>(P.reds.size());
   near_off_.upload(P.near_off, stream_);
   near_ids_.upload(P.near_ids.empty() ? std::vector<std::int32_t>{0} : P.near_ids, stream_);
+  near_dense_.upload(P.near_dense, stream_);
+  has_stream_levels_ = false;
+  for (int l = 1; l <= L_; ++l)
+    if (P.mode(l) == kModeStream && !P.pairs(l).X.empty()) has_stream_levels_ = true;
+  if (has_stream_levels_) {
+    cpart_.alloc(n_);
+    spart_.alloc(n_);
+  }
   if (opt_.near_mode == H3D_NEAR_STORED) {
     nf_off_.upload(P.nf_off, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
@@ -544,6 +568,7 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.perm = perm_.get();
   a.near_off = near_off_.get();
   a.near_ids = near_ids_.get();
+  a.near_dense = near_dense_.get();
   if (opt_.near_mode == H3D_NEAR_STORED) {
     a.nf_off = nf_off_.get();
     a.NF = NF_.get();
@@ -551,6 +576,10 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.kernel = opt_.kernel_id;
   a.diag = opt_.diagonal;
   a.b = bout;
+  if (has_stream_levels_) {
+    a.spart = spart_.get();
+    a.cpart_out = cpart_.get();
+  }
   for (int l = 0; l <= L_ && l < 24; ++l) {
     a.lbase[l] = P.node_base()[l];
     a.mode[l] = P.mode(l);
@@ -596,18 +625,65 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     NCCL_CHECK(ncclGroupEnd());
   }
   if (ev) cudaEventRecord(ev[1], s);
+  // ---- phase 1: HBM-bound stream items on s, FP64-bound proxy items on
+  // stream2_, persistent CTAs sized to co-reside on every SM
   NodeTable nt{rowbeg_.get(), rows_.get(), woff_.get(), rpad_.get(), soff_.get()};
-  launch_phase1(p1_items_.get(), n_p1_, nt, W_.get(), xp_.get(), spos_.get(), S_.get(), P_.get(),
-                px_.get(), py_.get(), pz_.get(), qx_.get(), qy_.get(), qz_.get(), opt_.kernel_id, s);
-  launches += n_p1_ > 0;
+  P1Args a1;
+  a1.nt = nt;
+  a1.W = W_.get();
+  a1.xp = xp_.get();
+  a1.spos = spos_.get();
+  a1.S = S_.get();
+  a1.P = P_.get();
+  a1.px = px_.get();
+  a1.py = py_.get();
+  a1.pz = pz_.get();
+  a1.qx = qx_.get();
+  a1.qy = qy_.get();
+  a1.qz = qz_.get();
+  const bool both1 = n_p1s_ > 0 && n_p1p_ > 0;
+  if (both1) {
+    H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
+    H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[0], 0));
+  }
+  if (n_p1s_ > 0) {
+    a1.items = p1_stream_items_.get();
+    a1.nitems = n_p1s_;
+    launch_p1_stream(a1, sms_, both1 ? 2 : 4, s);
+    ++launches;
+  }
+  if (n_p1p_ > 0) {
+    a1.items = p1_proxy_items_.get();
+    a1.nitems = n_p1p_;
+    launch_p1_proxy(a1, opt_.kernel_id, sms_, both1 ? 2 : 4, both1 ? stream2_ : s);
+    ++launches;
+  }
+  if (both1) {
+    H3D_CUDA_CHECK(cudaEventRecord(join_[0], stream2_));
+    H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
+  }
   launch_phase1_reduce(p1_red_.get(), n_red_, nt, spos_.get(), P_.get(), S_.get(), s);
   launches += n_red_ > 0;
   launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), S_.get(), s);
   launches += n_segs_solve_ > 0;
   if (ev) cudaEventRecord(ev[2], s);
+  // ---- phase 2: FP64 part (near + direct + proxy levels) on stream2_, HBM
+  // part (stream levels) on s, combined into b in original order
   if (P.leaf1 > P.leaf0) {
-    launch_phase2(phase2_args(bout), s);
-    ++launches;
+    const Phase2Args a2 = phase2_args(bout);
+    if (has_stream_levels_) {
+      H3D_CUDA_CHECK(cudaEventRecord(fork_[1], s));
+      H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[1], 0));
+      launch_p2_compute(a2, sms_, 2, stream2_);
+      launch_p2_stream(a2, sms_, 2, s);
+      H3D_CUDA_CHECK(cudaEventRecord(join_[1], stream2_));
+      H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
+      launch_combine(cpart_.get(), spart_.get(), perm_.get(), P.row0, P.row1, bout, s);
+      launches += 3;
+    } else {
+      launch_p2_compute(a2, sms_, 4, s);
+      ++launches;
+    }
   }
   if (ev) cudaEventRecord(ev[3], s);
   return launches;
@@ -732,7 +808,7 @@ void Engine::stats(h3d_stats* s) const {
   s->build_ms_aca_rank = ms_aca_rank_;
   s->build_ms_aca_write = ms_aca_write_;
   s->build_ms_total = ms_total_;
-  s->phase1_items = n_p1_;
+  s->phase1_items = n_p1s_ + n_p1p_;
   s->owned_row_begin = P.row0;
   s->owned_row_end = P.row1;
   for (int l = 0; l <= L_ && l < 16; ++l) s->level_modes[l] = P.mode(l);

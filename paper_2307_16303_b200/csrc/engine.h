@@ -111,10 +111,14 @@ class Engine {
   DevBuf<double> qx_, qy_, qz_;
   DevBuf<ProxySeg> segs_all_, segs_solve_;
   std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
-  DevBuf<P1Item> p1_items_;
+  DevBuf<P1Item> p1_stream_items_, p1_proxy_items_;
   DevBuf<P1Reduce> p1_red_;
-  std::int64_t n_p1_ = 0, n_red_ = 0;
-  DevBuf<std::int32_t> near_off_, near_ids_;
+  std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_ = 0;
+  bool has_stream_levels_ = false;
+  DevBuf<std::int32_t> near_off_, near_ids_, near_dense_;
+  DevBuf<double> cpart_, spart_;
+  cudaStream_t stream2_ = nullptr;          // concurrent HBM / FP64 kernels
+  cudaEvent_t fork_[2] = {}, join_[2] = {};  // per phase
   DevBuf<std::int64_t> nf_off_;
   DevBuf<double> NF_;
 

@@ -99,10 +99,21 @@ struct NodeTable {
   const std::int64_t* soff = nullptr;    // S_g / proxy slots (rpad entries)
 };
 
-void launch_phase1(const P1Item* items, std::int64_t nitems, NodeTable nt, const double* W,
-                   const double* xp, const std::int32_t* spos, double* S, double* P,
-                   const double* px, const double* py, const double* pz, const double* qx,
-                   const double* qy, const double* qz, int kernel, cudaStream_t s);
+struct P1Args {
+  const P1Item* items = nullptr;  // one kind per launch
+  std::int64_t nitems = 0;
+  NodeTable nt;
+  const double* W = nullptr;
+  const double* xp = nullptr;
+  const std::int32_t* spos = nullptr;
+  double* S = nullptr;
+  double* P = nullptr;
+  const double *px = nullptr, *py = nullptr, *pz = nullptr;  // permuted points
+  const double *qx = nullptr, *qy = nullptr, *qz = nullptr;  // proxy points (S-space)
+};
+// persistent CTAs: grid = SMs x per_sm (capped by occupancy and work)
+void launch_p1_stream(const P1Args& a, int sms, int per_sm, cudaStream_t s);
+void launch_p1_proxy(const P1Args& a, int kernel, int sms, int per_sm, cudaStream_t s);
 void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
                           const std::int32_t* spos, const double* P, double* S,
                           cudaStream_t s);
@@ -127,16 +138,22 @@ struct Phase2Args {
   // leaf near lists: self + near_edge + near_face (+ direct partners), CSR
   const std::int32_t* near_off = nullptr;
   const std::int32_t* near_ids = nullptr;
-  // stored near field (near_mode 0): per leaf a row-major m x (sum n) block
+  const std::int32_t* near_dense = nullptr;  // per leaf: leading dense entries (self/edge/face)
+  // stored near field (near_mode 0): per leaf a column-major m x (sum n) block
   const std::int64_t* nf_off = nullptr;
   const double* NF = nullptr;
   int kernel = 0;
   double diag = 0.0;
-  double* b = nullptr;  // output, original order
+  double* b = nullptr;          // output, original order
+  double* spart = nullptr;      // stream-level partial sums (Morton order), or null
+  double* cpart_out = nullptr;  // compute partial sums (Morton order) when spart != null
   std::int64_t lbase[24] = {0};  // node_base per level (by value)
   int mode[24] = {0};            // LevelMode per level
 };
-void launch_phase2(const Phase2Args& a, cudaStream_t s);
+void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
+void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
+void launch_combine(const double* cpart, const double* spart, const std::int32_t* perm,
+                    std::int64_t row0, std::int64_t row1, double* b, cudaStream_t s);
 
 // Build-time near-field scan: coincidence check (and optional store).
 void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s);

@@ -5,22 +5,28 @@
 // triangular factor of the pivot LU (reference lowrank.cpp:291-327). Per node Z
 // the partner segments share one column layout (rpad_Z columns):
 //
-//   stream levels : W_Z = [F_Z^(Z,k1) | ...] stored row-major, streamed;
-//   proxy levels  : only the proxy coordinates (q*) + pivots + LU are stored,
-//                   the entries K(Z, P_Z) are regenerated in FP64;
+//   stream levels : W_Z = [F_Z^(Z,k1) | ...] stored row-major and streamed (HBM);
+//   proxy levels  : only proxy coordinates + pivots + LU are stored and the
+//                   entries K(Z, P_Z) are regenerated (FP64 pipes);
 //   direct (leaf) : leaf-level admissible blocks are evaluated exactly and
 //                   join the near field.
 //
-//   phase 1  per node: T_Z = W_Z^T x_Z (stream) or v_Z = K(P_Z, Z) x_Z (proxy),
-//            scattered through spos into S (target-major t-vectors);
-//   solve    per ordered proxy block: s = (LU)^-1 v or (U^T L^T)^-1 v in place;
-//   phase 2  per leaf tile X (one CTA): b_X = near/direct P2P
-//            + sum over ancestor levels of W_A[rows] S_A (stream) or
-//              K(X, P_A) S_A (proxy); one writer per b entry, fused un-permute.
+// Two resources, two kernels per phase, run concurrently on two CUDA streams
+// as persistent CTAs that co-reside on every SM:
 //
-// Streaming uses 16-byte L1::no_allocate loads; P2P uses lanes over sources
-// and 4 register-resident target rows per warp. No atomics anywhere: results
-// are bitwise reproducible run to run (reference hmatrix.hpp:68-69).
+//   phase 1  p1_stream_kernel : T_Z = W_Z^T x_Z           (HBM)
+//            p1_proxy_kernel  : v_Z = K(P_Z, Z) x_Z         (FP64, lane = target)
+//            -> scattered through spos into S (target-major t-vectors),
+//               partial sums of tall nodes reduced in fixed order;
+//   solve    proxy_solve_kernel: s = (LU)^-1 v or (U^T L^T)^-1 v in place;
+//   phase 2  p2_stream_kernel : rows of W_A(l) . S_A(l) over stream levels (HBM)
+//            p2_compute_kernel: near field + direct leaf blocks + K(X, P_A) s_A
+//                               over proxy levels, one continuous source walk
+//                               per warp, lane = target row (FP64)
+//            combine_kernel   : b[perm[p]] = compute + stream (fused un-permute).
+//
+// Every output has one writer and a fixed accumulation order (no atomics), so
+// matvecs are bitwise reproducible (reference hmatrix.hpp:68-69).
 #include "common.cuh"
 #include "kernels.h"
 
@@ -29,6 +35,11 @@ namespace h3db {
 namespace {
 
 constexpr double kFar = 1e100;  // coordinate of padding / inactive targets
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kP1Cols = 256;    // phase-1 columns per item
+constexpr int kChunk = 256;     // phase-1 proxy: sources staged per round
+constexpr int kMaxRanges = 256; // phase-2 compute: source ranges per tile
 
 __global__ void gather_kernel(const double* __restrict__ x, const std::int32_t* __restrict__ perm,
                               std::int64_t n, double* __restrict__ xp) {
@@ -36,89 +47,31 @@ __global__ void gather_kernel(const double* __restrict__ x, const std::int32_t* 
   if (p < n) xp[p] = __ldg(x + perm[p]);
 }
 
-// acc[r] += sum_j K(t_r, s_j) w_j over sources [0, ns), lanes striding j.
-template <int K, int R>
-__device__ __forceinline__ void p2p_rows(const double (&tx)[R], const double (&ty)[R],
-                                         const double (&tz)[R], double (&acc)[R],
-                                         const double* __restrict__ sx,
-                                         const double* __restrict__ sy,
-                                         const double* __restrict__ sz,
-                                         const double* __restrict__ sw, int ns, int lane) {
-  int j = lane;
-  for (; j + 32 < ns; j += 64) {
-    const double x0 = __ldg(sx + j), y0 = __ldg(sy + j), z0 = __ldg(sz + j), w0 = __ldg(sw + j);
-    const double x1 = __ldg(sx + j + 32), y1 = __ldg(sy + j + 32), z1 = __ldg(sz + j + 32),
-                 w1 = __ldg(sw + j + 32);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double a0 = sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0);
-      const double a1 = sq3(tx[r] - x1, ty[r] - y1, tz[r] - z1);
-      acc[r] = fma(kernel_r2_fast<K>(a0), w0, acc[r]);
-      acc[r] = fma(kernel_r2_fast<K>(a1), w1, acc[r]);
-    }
-  }
-  if (j < ns) {
-    const double x0 = __ldg(sx + j), y0 = __ldg(sy + j), z0 = __ldg(sz + j), w0 = __ldg(sw + j);
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-      acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0)), w0, acc[r]);
+__device__ __forceinline__ void p1_write(const P1Item& it, std::int64_t g, int c, double v,
+                                         const P1Args& a) {
+  if (it.pslot < 0) {
+    const std::int32_t dst = a.spos[a.nt.soff[g] + it.col0 + c];
+    if (dst >= 0) a.S[dst] = v;
+  } else {
+    a.P[it.pslot + c] = v;
   }
 }
 
-// Self block: the diagonal entry is KernelSpec::diagonal (kernel.cpp:73-80).
-template <int K, int R>
-__device__ __forceinline__ void p2p_rows_self(const double (&tx)[R], const double (&ty)[R],
-                                              const double (&tz)[R], const int (&ti)[R],
-                                              double (&acc)[R], const double* __restrict__ sx,
-                                              const double* __restrict__ sy,
-                                              const double* __restrict__ sz,
-                                              const double* __restrict__ sw, int ns, int lane,
-                                              double diag) {
-  for (int j = lane; j < ns; j += 32) {
-    const double x0 = sx[j], y0 = sy[j], z0 = sz[j], w0 = sw[j];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const double k = ti[r] == j ? diag : kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
-      acc[r] = fma(k, w0, acc[r]);
-    }
-  }
-}
-
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kP1Cols = 256;  // 32 lanes x 2 doubles x 4 groups
-constexpr int kRows = 4;      // P2P target rows per warp
-
-struct P1Args {
-  const P1Item* items;
-  NodeTable nt;
-  const double* W;
-  const double* xp;
-  const std::int32_t* spos;
-  double* S;
-  double* P;
-  const double *px, *py, *pz;  // permuted points
-  const double *qx, *qy, *qz;  // proxy points (S-space)
-};
-
-template <int K>
-__global__ void __launch_bounds__(kThreads) phase1_kernel(const P1Args a) {
+// ---- phase 1, stream levels: T = W_Z^T x_Z over <= 2048 rows x 256 columns
+__global__ void __launch_bounds__(kThreads, 2) p1_stream_kernel(const P1Args a) {
   __shared__ double red[kWarps][kP1Cols + 2];
-  __shared__ double outv[kP1Cols];
-  const P1Item it = a.items[blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::int64_t g = it.node;
-  const std::int64_t rb = a.nt.rowbeg[g] + it.row0;
-  if (it.kind == 0) {
-    // ---- stream: T = W_Z^T x_Z over rows [row0, row0+nrows), 256 columns
+  for (std::int64_t k = blockIdx.x; k < a.nitems; k += gridDim.x) {
+    const P1Item it = a.items[k];
+    const std::int64_t g = it.node;
     const int rpad = a.nt.rpad[g];
     const double* __restrict__ Wn =
         a.W + a.nt.woff[g] + static_cast<std::int64_t>(it.row0) * rpad + it.col0;
-    const double* __restrict__ xn = a.xp + rb;
+    const double* __restrict__ xn = a.xp + a.nt.rowbeg[g] + it.row0;
     const int ng = (it.ncols + 63) >> 6;
     double acc[4][2];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k][0] = acc[k][1] = 0.0;
+    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
     int i = warp;
     for (; i + kWarps < it.nrows; i += 2 * kWarps) {
       const double x0 = xn[i], x1 = xn[i + kWarps];
@@ -127,35 +80,36 @@ __global__ void __launch_bounds__(kThreads) phase1_kernel(const P1Args a) {
           reinterpret_cast<const double2*>(Wn + static_cast<std::int64_t>(i + kWarps) * rpad);
       double2 w0[4], w1[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const bool ok = k < ng && (2 * lane + 64 * k) < it.ncols;
-        w0[k] = ok ? ld_stream(r0 + lane + 32 * k) : make_double2(0.0, 0.0);
-        w1[k] = ok ? ld_stream(r1 + lane + 32 * k) : make_double2(0.0, 0.0);
+      for (int q = 0; q < 4; ++q) {
+        const bool ok = q < ng && (2 * lane + 64 * q) < it.ncols;
+        w0[q] = ok ? ld_stream(r0 + lane + 32 * q) : make_double2(0.0, 0.0);
+        w1[q] = ok ? ld_stream(r1 + lane + 32 * q) : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        acc[k][0] = fma(w0[k].x, x0, acc[k][0]);
-        acc[k][1] = fma(w0[k].y, x0, acc[k][1]);
-        acc[k][0] = fma(w1[k].x, x1, acc[k][0]);
-        acc[k][1] = fma(w1[k].y, x1, acc[k][1]);
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] = fma(w0[q].x, x0, acc[q][0]);
+        acc[q][1] = fma(w0[q].y, x0, acc[q][1]);
+        acc[q][0] = fma(w1[q].x, x1, acc[q][0]);
+        acc[q][1] = fma(w1[q].y, x1, acc[q][1]);
       }
     }
     for (; i < it.nrows; i += kWarps) {
       const double x0 = xn[i];
       const double2* r0 = reinterpret_cast<const double2*>(Wn + static_cast<std::int64_t>(i) * rpad);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (k < ng && (2 * lane + 64 * k) < it.ncols) {
-          const double2 w = ld_stream(r0 + lane + 32 * k);
-          acc[k][0] = fma(w.x, x0, acc[k][0]);
-          acc[k][1] = fma(w.y, x0, acc[k][1]);
+      for (int q = 0; q < 4; ++q) {
+        if (q < ng && (2 * lane + 64 * q) < it.ncols) {
+          const double2 w = ld_stream(r0 + lane + 32 * q);
+          acc[q][0] = fma(w.x, x0, acc[q][0]);
+          acc[q][1] = fma(w.y, x0, acc[q][1]);
         }
       }
     }
+    __syncthreads();  // red reuse across items
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      red[warp][2 * lane + 64 * k] = acc[k][0];
-      red[warp][2 * lane + 64 * k + 1] = acc[k][1];
+    for (int q = 0; q < 4; ++q) {
+      red[warp][2 * lane + 64 * q] = acc[q][0];
+      red[warp][2 * lane + 64 * q + 1] = acc[q][1];
     }
     __syncthreads();
     const int c = threadIdx.x;
@@ -163,44 +117,48 @@ __global__ void __launch_bounds__(kThreads) phase1_kernel(const P1Args a) {
       double v = 0.0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) v += red[w][c];
-      outv[c] = v;
+      p1_write(it, g, c, v, a);
     }
-  } else {
-    // ---- proxy: v_c = sum_j K(P_c, z_j) x_j, targets = proxy columns
-    const std::int64_t qb = a.nt.soff[g] + it.col0;
-    for (int t0 = warp * 32; t0 < it.ncols; t0 += kWarps * 32) {
-      for (int grp = 0; grp < 32 && t0 + grp < it.ncols; grp += kRows) {
-        double tx[kRows], ty[kRows], tz[kRows], acc[kRows];
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-          const int c = t0 + grp + r;
-          const bool ok = c < it.ncols;
-          tx[r] = ok ? a.qx[qb + c] : kFar;
-          ty[r] = ok ? a.qy[qb + c] : kFar;
-          tz[r] = ok ? a.qz[qb + c] : kFar;
-          acc[r] = 0.0;
-        }
-        p2p_rows<K, kRows>(tx, ty, tz, acc, a.px + rb, a.py + rb, a.pz + rb, a.xp + rb, it.nrows,
-                           lane);
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-          const double v = warp_sum(acc[r]);
-          const int c = t0 + grp + r;
-          if (lane == 0 && c < it.ncols) outv[c] = v;
-        }
+  }
+}
+
+// ---- phase 1, proxy levels: v_c = sum_j K(P_c, z_j) x_j, thread = target,
+// sources staged in shared memory and read as broadcasts.
+template <int K>
+__global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
+  __shared__ double2 src[2 * kChunk];  // (x, y), (z, w)
+  for (std::int64_t k = blockIdx.x; k < a.nitems; k += gridDim.x) {
+    const P1Item it = a.items[k];
+    const std::int64_t g = it.node;
+    const std::int64_t rb = a.nt.rowbeg[g] + it.row0;
+    const int c = threadIdx.x;
+    const std::int64_t qi = a.nt.soff[g] + it.col0 + c;
+    const bool active = c < it.ncols;
+    const double tx = active ? a.qx[qi] : kFar, ty = active ? a.qy[qi] : kFar,
+                 tz = active ? a.qz[qi] : kFar;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int j0 = 0; j0 < it.nrows; j0 += kChunk) {
+      const int nj = min(kChunk, it.nrows - j0);
+      __syncthreads();
+      if (threadIdx.x < nj) {
+        const std::int64_t p = rb + j0 + threadIdx.x;
+        src[2 * threadIdx.x] = make_double2(a.px[p], a.py[p]);
+        src[2 * threadIdx.x + 1] = make_double2(a.pz[p], a.xp[p]);
+      }
+      __syncthreads();
+      int j = 0;
+      for (; j + 1 < nj; j += 2) {
+        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
+        const double2 u0 = src[2 * j + 2], u1 = src[2 * j + 3];
+        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
+        acc1 = fma(kernel_r2_fast<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x)), u1.y, acc1);
+      }
+      if (j < nj) {
+        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
+        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
       }
     }
-    __syncthreads();
-  }
-  const int c = threadIdx.x;
-  if (c < it.ncols) {
-    const double v = outv[c];
-    if (it.pslot < 0) {
-      const std::int32_t dst = a.spos[a.nt.soff[g] + it.col0 + c];
-      if (dst >= 0) a.S[dst] = v;
-    } else {
-      a.P[it.pslot + c] = v;
-    }
+    if (active) p1_write(it, g, c, acc0 + acc1, a);
   }
 }
 
@@ -226,13 +184,13 @@ __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int6
   const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.y) + threadIdx.y;
   if (s >= nseg) return;
   const ProxySeg sg = segs[s];
-  for (int a = threadIdx.x; a < sg.r; a += blockDim.x) {
+  for (int q = threadIdx.x; q < sg.r; q += blockDim.x) {
     // side 0: Z = X, proxies = column pivots tau (in Y = k); side 1: row pivots sigma
-    const std::int32_t loc = piv[sg.piv_off + (sg.side == 0 ? sg.r : 0) + a];
+    const std::int32_t loc = piv[sg.piv_off + (sg.side == 0 ? sg.r : 0) + q];
     const std::int64_t idx = sg.base + loc;
-    qx[sg.so + a] = px[idx];
-    qy[sg.so + a] = py[idx];
-    qz[sg.so + a] = pz[idx];
+    qx[sg.so + q] = px[idx];
+    qy[sg.so + q] = py[idx];
+    qz[sg.so + q] = pz[idx];
   }
 }
 
@@ -250,133 +208,251 @@ __global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64
   const int r = sg.r;
   double* v = sh + warp * 320;  // r <= 320 (enforced on the host)
   double* Sg = S + sg.so;
-  for (int a = lane; a < r; a += 32) v[a] = Sg[a];
+  for (int q = lane; q < r; q += 32) v[q] = Sg[q];
   __syncwarp();
   const double* A = lu + sg.lu_off;
   if (sg.side == 0) {
-    for (int a = 0; a < r; ++a) {  // L (unit lower): v_b -= L[b][a] v_a
-      const double va = v[a];
+    for (int q = 0; q < r; ++q) {  // L (unit lower): v_b -= L[b][q] v_q
+      const double vq = v[q];
       __syncwarp();
-      for (int b = a + 1 + lane; b < r; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(b) * r + a], va, v[b]);
+      for (int b = q + 1 + lane; b < r; b += 32)
+        v[b] = fma(-A[static_cast<std::int64_t>(b) * r + q], vq, v[b]);
       __syncwarp();
     }
-    for (int a = r - 1; a >= 0; --a) {  // R (upper): s_a = v_a / R[a][a]; v_b -= R[b][a] s_a
-      const double sa = v[a] / A[static_cast<std::int64_t>(a) * r + a];
+    for (int q = r - 1; q >= 0; --q) {  // R (upper): s_q = v_q / R[q][q]; v_b -= R[b][q] s_q
+      const double sq = v[q] / A[static_cast<std::int64_t>(q) * r + q];
       __syncwarp();
-      if (lane == 0) v[a] = sa;
-      for (int b = lane; b < a; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(b) * r + a], sa, v[b]);
+      if (lane == 0) v[q] = sq;
+      for (int b = lane; b < q; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(b) * r + q], sq, v[b]);
       __syncwarp();
     }
   } else {
-    for (int a = 0; a < r; ++a) {  // R^T (lower): w_a = v_a / R[a][a]; v_b -= R[a][b] w_a
-      const double wa = v[a] / A[static_cast<std::int64_t>(a) * r + a];
+    for (int q = 0; q < r; ++q) {  // R^T (lower): w_q = v_q / R[q][q]; v_b -= R[q][b] w_q
+      const double wq = v[q] / A[static_cast<std::int64_t>(q) * r + q];
       __syncwarp();
-      if (lane == 0) v[a] = wa;
-      for (int b = a + 1 + lane; b < r; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(a) * r + b], wa, v[b]);
+      if (lane == 0) v[q] = wq;
+      for (int b = q + 1 + lane; b < r; b += 32)
+        v[b] = fma(-A[static_cast<std::int64_t>(q) * r + b], wq, v[b]);
       __syncwarp();
     }
-    for (int a = r - 1; a >= 0; --a) {  // L^T (unit upper): v_b -= L[a][b] v_a
-      const double va = v[a];
+    for (int q = r - 1; q >= 0; --q) {  // L^T (unit upper): v_b -= L[q][b] v_q
+      const double vq = v[q];
       __syncwarp();
-      for (int b = lane; b < a; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(a) * r + b], va, v[b]);
+      for (int b = lane; b < q; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(q) * r + b], vq, v[b]);
       __syncwarp();
     }
   }
-  for (int a = lane; a < r; a += 32) Sg[a] = v[a];
+  for (int q = lane; q < r; q += 32) Sg[q] = v[q];
 }
 
-// One CTA per leaf tile, rows in passes of 32 (8 warps x 4 rows).
-template <int K, bool STORED>
-__global__ void __launch_bounds__(kThreads) phase2_kernel(const Phase2Args a) {
+// ---- phase 2, compute part --------------------------------------------------
+enum RangeKind : int { kRangeSelf = 0, kRangePoints = 1, kRangeProxy = 2 };
+
+// Walk sources [j0, j1) of one range for this lane group: lane -> (row, group);
+// each group takes every G-th source, all lanes of a group read the same
+// source (broadcast). R rows per lane (1 or 2).
+template <int K, int R, bool SELF>
+__device__ __forceinline__ void walk(const double (&tx)[R], const double (&ty)[R],
+                                     const double (&tz)[R], const int (&ti)[R], double (&acc)[R],
+                                     const double* __restrict__ sx, const double* __restrict__ sy,
+                                     const double* __restrict__ sz, const double* __restrict__ sw,
+                                     int j0, int j1, int G, double diag) {
+  int j = j0;
+  for (; j + G < j1; j += 2 * G) {
+    const double x0 = __ldg(sx + j), y0 = __ldg(sy + j), z0 = __ldg(sz + j), w0 = __ldg(sw + j);
+    const double x1 = __ldg(sx + j + G), y1 = __ldg(sy + j + G), z1 = __ldg(sz + j + G),
+                 w1 = __ldg(sw + j + G);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double k0 = kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
+      double k1 = kernel_r2_fast<K>(sq3(tx[r] - x1, ty[r] - y1, tz[r] - z1));
+      if (SELF) {
+        k0 = ti[r] == j ? diag : k0;
+        k1 = ti[r] == j + G ? diag : k1;
+      }
+      acc[r] = fma(k0, w0, acc[r]);
+      acc[r] = fma(k1, w1, acc[r]);
+    }
+  }
+  if (j < j1) {
+    const double x0 = __ldg(sx + j), y0 = __ldg(sy + j), z0 = __ldg(sz + j), w0 = __ldg(sw + j);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double k0 = kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
+      if (SELF) k0 = ti[r] == j ? diag : k0;
+      acc[r] = fma(k0, w0, acc[r]);
+    }
+  }
+}
+
+struct TileRanges {
+  std::int64_t start[kMaxRanges];  // first index in its array (points / S space)
+  int pre[kMaxRanges + 1];         // prefix of lengths
+  unsigned char kind[kMaxRanges];
+  int n;
+};
+
+template <int K, int R>
+__device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, std::int64_t xb, int r0,
+                             int m, int mp, double* cpart) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::int64_t X = a.leaf0 + blockIdx.x;
-  const std::int64_t xb = a.leaf_off[X];
-  const int mrows = static_cast<int>(a.leaf_off[X + 1] - xb);
-  if (mrows == 0) return;
+  const int G = 32 / mp;  // source groups per warp (R == 2 -> mp == 32, G == 1)
+  const int grp = lane / mp, row = lane % mp;
+  double tx[R], ty[R], tz[R], acc[R];
+  int ti[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = row + 32 * r;
+    const bool ok = i < m;
+    const std::int64_t gi = xb + r0 + i;
+    tx[r] = ok ? a.px[gi] : kFar;
+    ty[r] = ok ? a.py[gi] : kFar;
+    tz[r] = ok ? a.pz[gi] : kFar;
+    ti[r] = ok ? r0 + i : -1;  // local index within the leaf (self range)
+    acc[r] = 0.0;
+  }
+  // this warp's contiguous slice of the tile's virtual source stream
+  const int T = tr.pre[tr.n];
+  const int v0 = static_cast<int>(static_cast<long long>(T) * warp / kWarps);
+  const int v1 = static_cast<int>(static_cast<long long>(T) * (warp + 1) / kWarps);
+  int ri = 0;
+  while (ri < tr.n && tr.pre[ri + 1] <= v0) ++ri;
+  for (int v = v0; v < v1 && ri < tr.n; ++ri) {
+    const int rbeg = tr.pre[ri], rend = min(tr.pre[ri + 1], v1);
+    const int j0 = v - rbeg + grp, j1 = rend - rbeg;
+    const std::int64_t st = tr.start[ri];
+    switch (tr.kind[ri]) {
+      case kRangeSelf:
+        walk<K, R, true>(tx, ty, tz, ti, acc, a.px + st, a.py + st, a.pz + st, a.xp + st, j0, j1,
+                         G, a.diag);
+        break;
+      case kRangePoints:
+        walk<K, R, false>(tx, ty, tz, ti, acc, a.px + st, a.py + st, a.pz + st, a.xp + st, j0, j1,
+                          G, a.diag);
+        break;
+      default:
+        walk<K, R, false>(tx, ty, tz, ti, acc, a.qx + st, a.qy + st, a.qz + st, a.S + st, j0, j1,
+                          G, a.diag);
+        break;
+    }
+    v = rend;
+  }
+  // combine the G source groups of each row (fixed butterfly order)
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    for (int o = mp; o < 32; o <<= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
+    if (grp == 0 && row + 32 * r < m) cpart[warp * 64 + row + 32 * r] = acc[r];
+  }
+}
+
+// One tile (leaf) at a time per CTA, persistent over the owned leaves.
+template <int K, bool STORED>
+__global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Args a) {
+  __shared__ TileRanges tr;
+  __shared__ double cpart[kWarps * 64];
   const int L = a.depth;
-  const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
-
-  for (int r0 = 0; r0 < mrows; r0 += kWarps * kRows) {
-    double tx[kRows], ty[kRows], tz[kRows], acc[kRows];
-    int ti[kRows];
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int i = r0 + warp * kRows + r;
-      const bool ok = i < mrows;
-      tx[r] = ok ? a.px[xb + i] : kFar;
-      ty[r] = ok ? a.py[xb + i] : kFar;
-      tz[r] = ok ? a.pz[xb + i] : kFar;
-      ti[r] = ok ? i : -1;
-      acc[r] = 0.0;
-    }
-
-    // ---- near field (self, edge, face) + directly evaluated leaf partners
-    if (STORED) {
-      std::int64_t ntot = 0;
-      for (std::int32_t e = nb; e < ne; ++e) {
-        const std::int32_t Y = a.near_ids[e];
-        ntot += a.leaf_off[Y + 1] - a.leaf_off[Y];
-      }
-      const double* nf = a.NF + a.nf_off[X];
-      std::int64_t coff = 0;
-      for (std::int32_t e = nb; e < ne; ++e) {
+  for (std::int64_t t = blockIdx.x; t < a.nleaves; t += gridDim.x) {
+    const std::int64_t X = a.leaf0 + t;
+    const std::int64_t xb = a.leaf_off[X];
+    const int mrows = static_cast<int>(a.leaf_off[X + 1] - xb);
+    if (mrows == 0) continue;
+    __syncthreads();  // tr / cpart reuse
+    if (threadIdx.x == 0) {
+      // source ranges: self, neighbours (stored: only the direct partners),
+      // then the proxy ranges of the ancestors at proxy levels
+      int n = 0, pre = 0;
+      const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
+      const std::int32_t nd = STORED ? a.near_dense[X] : 0;  // dense entries of the list
+      for (std::int32_t e = nb; e < ne && n < kMaxRanges; ++e) {
+        if (STORED && e - nb < nd) continue;
         const std::int32_t Y = a.near_ids[e];
         const std::int64_t yb = a.leaf_off[Y];
-        const int n = static_cast<int>(a.leaf_off[Y + 1] - yb);
-#pragma unroll
-        for (int r = 0; r < kRows; ++r) {
-          if (ti[r] < 0) continue;
-          const double* row = nf + static_cast<std::int64_t>(ti[r]) * ntot + coff;
-          for (int j = lane; j < n; j += 32) acc[r] = fma(ld_stream1(row + j), a.xp[yb + j], acc[r]);
+        const int len = static_cast<int>(a.leaf_off[Y + 1] - yb);
+        tr.start[n] = yb;
+        tr.kind[n] = Y == X ? kRangeSelf : kRangePoints;
+        tr.pre[n] = pre;
+        pre += len;
+        ++n;
+      }
+      for (int l = 1; l <= L && n < kMaxRanges; ++l) {
+        if (a.mode[l] != 1) continue;
+        const std::int64_t g = a.lbase[l] + (X >> (3 * (L - l)));
+        const int R = a.nt.rpad[g];
+        if (R == 0) continue;
+        tr.start[n] = a.nt.soff[g];
+        tr.kind[n] = kRangeProxy;
+        tr.pre[n] = pre;
+        pre += R;
+        ++n;
+      }
+      tr.pre[n] = pre;
+      tr.n = n;
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < mrows; r0 += 64) {
+      const int m = min(64, mrows - r0);
+      int mp = 1;
+      while (mp < m && mp < 32) mp <<= 1;
+      if (m > 32) compute_rows<K, 2>(a, tr, xb, r0, m, 32, cpart);
+      else compute_rows<K, 1>(a, tr, xb, r0, m, mp, cpart);
+      __syncthreads();
+      if (threadIdx.x < m) {
+        const int i = threadIdx.x;
+        double v = 0.0;
+        if (STORED) {  // stored dense near blocks, column-major per leaf
+          const std::int32_t nb = a.near_off[X];
+          const std::int32_t nd = a.near_dense[X];
+          const double* nf = a.NF + a.nf_off[X];
+          int c = 0;
+          for (std::int32_t e = nb; e < nb + nd; ++e) {
+            const std::int32_t Y = a.near_ids[e];
+            const std::int64_t yb = a.leaf_off[Y];
+            const int len = static_cast<int>(a.leaf_off[Y + 1] - yb);
+            for (int j = 0; j < len; ++j, ++c)
+              v = fma(nf[static_cast<std::int64_t>(c) * mrows + r0 + i], a.xp[yb + j], v);
+          }
         }
-        coff += n;
-      }
-    } else {
-      for (std::int32_t e = nb; e < ne; ++e) {
-        const std::int32_t Y = a.near_ids[e];
-        const std::int64_t yb = a.leaf_off[Y];
-        const int n = static_cast<int>(a.leaf_off[Y + 1] - yb);
-        if (Y == X)
-          p2p_rows_self<K, kRows>(tx, ty, tz, ti, acc, a.px + yb, a.py + yb, a.pz + yb, a.xp + yb, n,
-                                  lane, a.diag);
-        else
-          p2p_rows<K, kRows>(tx, ty, tz, acc, a.px + yb, a.py + yb, a.pz + yb, a.xp + yb, n, lane);
-      }
-    }
-
-    // ---- low-rank levels 1..L
-    for (int l = 1; l <= L; ++l) {
-      const std::int64_t g = a.lbase[l] + (X >> (3 * (L - l)));
-      const int R = a.nt.rpad[g];
-      if (R == 0) continue;
-      const std::int64_t so = a.nt.soff[g];
-      if (a.mode[l] == 1) {  // proxy: K(X, P_A) s_A
-        p2p_rows<K, kRows>(tx, ty, tz, acc, a.qx + so, a.qy + so, a.qz + so, a.S + so, R, lane);
-        continue;
-      }
-      const std::int64_t rowoff = xb + r0 + warp * kRows - a.nt.rowbeg[g];
-      const double* Wg = a.W + a.nt.woff[g] + rowoff * R;
-      const double2* S2 = reinterpret_cast<const double2*>(a.S + so);
-      const int R2 = R >> 1;
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) {
-        if (ti[r] < 0) continue;
-        const double2* row = reinterpret_cast<const double2*>(Wg + static_cast<std::int64_t>(r) * R);
-        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < kWarps; ++w) v += cpart[w * 64 + i];
+        if (a.spart) a.cpart_out[xb + r0 + i] = v;
+        else a.b[a.perm[xb + r0 + i]] = v;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- phase 2, stream part: rows of W_A . S_A over the stream levels
+__global__ void __launch_bounds__(kThreads, 2) p2_stream_kernel(const Phase2Args a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int L = a.depth;
+  for (std::int64_t t = blockIdx.x; t < a.nleaves; t += gridDim.x) {
+    const std::int64_t X = a.leaf0 + t;
+    const std::int64_t xb = a.leaf_off[X];
+    const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
+    for (int i = warp; i < m; i += kWarps) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int l = 1; l <= L; ++l) {
+        if (a.mode[l] != 0) continue;
+        const std::int64_t g = a.lbase[l] + (X >> (3 * (L - l)));
+        const int R = a.nt.rpad[g];
+        if (R == 0) continue;
+        const double2* row = reinterpret_cast<const double2*>(
+            a.W + a.nt.woff[g] + (xb + i - a.nt.rowbeg[g]) * R);
+        const double2* S2 = reinterpret_cast<const double2*>(a.S + a.nt.soff[g]);
+        const int R2 = R >> 1;
         int c = lane;
-        for (; c + 96 < R2; c += 128) {
-          const double2 w0 = ld_stream(row + c), w1 = ld_stream(row + c + 32);
-          const double2 w2 = ld_stream(row + c + 64), w3 = ld_stream(row + c + 96);
-          const double2 q0 = __ldg(S2 + c), q1 = __ldg(S2 + c + 32);
-          const double2 q2 = __ldg(S2 + c + 64), q3 = __ldg(S2 + c + 96);
-          s0 = fma(w0.x, q0.x, s0);
-          s1 = fma(w0.y, q0.y, s1);
-          s0 = fma(w1.x, q1.x, s0);
-          s1 = fma(w1.y, q1.y, s1);
-          s0 = fma(w2.x, q2.x, s0);
-          s1 = fma(w2.y, q2.y, s1);
-          s0 = fma(w3.x, q3.x, s0);
-          s1 = fma(w3.y, q3.y, s1);
+        for (; c + 224 < R2; c += 256) {
+          double2 w[8], q[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) w[u] = ld_stream(row + c + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) q[u] = __ldg(S2 + c + 32 * u);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            s0 = fma(w[u].x, q[u].x, s0);
+            s1 = fma(w[u].y, q[u].y, s1);
+          }
         }
         for (; c < R2; c += 32) {
           const double2 w0 = ld_stream(row + c);
@@ -384,21 +460,24 @@ __global__ void __launch_bounds__(kThreads) phase2_kernel(const Phase2Args a) {
           s0 = fma(w0.x, q0.x, s0);
           s1 = fma(w0.y, q0.y, s1);
         }
-        acc[r] += s0 + s1;
       }
-    }
-
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const double v = warp_sum(acc[r]);
-      if (lane == 0 && ti[r] >= 0) a.b[a.perm[xb + ti[r]]] = v;
+      const double v = warp_sum(s0 + s1);
+      if (lane == 0) a.spart[xb + i] = v;
     }
   }
 }
 
-// Build-time pass over every near-field pair: the reference forms all dense
-// leaf blocks during initialize (hmatrix.cpp:124-147), so coincident points
-// raise DegenerateGeometryError there; optionally stores the blocks.
+__global__ void combine_kernel(const double* __restrict__ cpart, const double* __restrict__ spart,
+                               const std::int32_t* __restrict__ perm, std::int64_t row0,
+                               std::int64_t row1, double* __restrict__ b) {
+  const std::int64_t p = row0 + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (p < row1) b[perm[p]] = cpart[p] + spart[p];
+}
+
+// Build-time pass over every dense near-field pair: the reference forms all
+// dense leaf blocks during initialize (hmatrix.cpp:124-147), so coincident
+// points raise DegenerateGeometryError there; optionally stores the blocks
+// (column-major per leaf: NF[nf_off[X] + c * m + i]).
 template <int K>
 __global__ void __launch_bounds__(kThreads) near_scan_kernel(const Phase2Args a,
                                                              double* __restrict__ NF,
@@ -407,20 +486,16 @@ __global__ void __launch_bounds__(kThreads) near_scan_kernel(const Phase2Args a,
   const std::int64_t xb = a.leaf_off[X];
   const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
   if (m == 0) return;
-  const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
-  std::int64_t ntot = 0;
-  for (std::int32_t e = nb; e < ne; ++e) {
-    const std::int32_t Y = a.near_ids[e];
-    ntot += a.leaf_off[Y + 1] - a.leaf_off[Y];
-  }
+  const std::int32_t nb = a.near_off[X];
+  const std::int32_t nd = a.near_dense[X];
   unsigned f = 0;
   std::int64_t coff = 0;
-  for (std::int32_t e = nb; e < ne; ++e) {
+  for (std::int32_t e = nb; e < nb + nd; ++e) {
     const std::int32_t Y = a.near_ids[e];
     const std::int64_t yb = a.leaf_off[Y];
     const int n = static_cast<int>(a.leaf_off[Y + 1] - yb);
     for (int q = threadIdx.x; q < m * n; q += blockDim.x) {
-      const int i = q / n, j = q % n;
+      const int j = q / m, i = q % m;
       const std::int64_t gi = xb + i, gj = yb + j;
       double v;
       if (gi == gj) {
@@ -430,11 +505,19 @@ __global__ void __launch_bounds__(kThreads) near_scan_kernel(const Phase2Args a,
         if (r2 < kCoincidentTol2) f |= kFlagDegenGeom;
         v = kernel_r2_fast<K>(r2);
       }
-      if (NF) NF[a.nf_off[X] + static_cast<std::int64_t>(i) * ntot + coff + j] = v;
+      if (NF) NF[a.nf_off[X] + (coff + j) * m + i] = v;
     }
     coff += n;
   }
   if (f) atomicOr(flags, f);
+}
+
+template <class F>
+int grid_for(F kernel, int sms, int per_sm, std::int64_t work) {
+  int nb = 0;
+  H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, 0));
+  const std::int64_t g = static_cast<std::int64_t>(sms) * std::max(1, std::min(nb, per_sm));
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, work)));
 }
 
 }  // namespace
@@ -445,17 +528,31 @@ void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, do
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_phase1(const P1Item* items, std::int64_t nitems, NodeTable nt, const double* W,
-                   const double* xp, const std::int32_t* spos, double* S, double* P,
-                   const double* px, const double* py, const double* pz, const double* qx,
-                   const double* qy, const double* qz, int kernel, cudaStream_t s) {
-  if (nitems == 0) return;
-  const P1Args a{items, nt, W, xp, spos, S, P, px, py, pz, qx, qy, qz};
-  const unsigned grid = static_cast<unsigned>(nitems);
+void launch_p1_stream(const P1Args& a, int sms, int per_sm, cudaStream_t s) {
+  if (a.nitems == 0) return;
+  const int grid = grid_for(p1_stream_kernel, sms, per_sm, a.nitems);
+  p1_stream_kernel<<<grid, kThreads, 0, s>>>(a);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_p1_proxy(const P1Args& a, int kernel, int sms, int per_sm, cudaStream_t s) {
+  if (a.nitems == 0) return;
   switch (kernel) {
-    case kLaplace: phase1_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a); break;
-    case kR4: phase1_kernel<kR4><<<grid, kThreads, 0, s>>>(a); break;
-    default: phase1_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a); break;
+    case kLaplace: {
+      const int grid = grid_for(p1_proxy_kernel<kLaplace>, sms, per_sm, a.nitems);
+      p1_proxy_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+    case kR4: {
+      const int grid = grid_for(p1_proxy_kernel<kR4>, sms, per_sm, a.nitems);
+      p1_proxy_kernel<kR4><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+    default: {
+      const int grid = grid_for(p1_proxy_kernel<kHelmholtz>, sms, per_sm, a.nitems);
+      p1_proxy_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
   }
   H3D_CUDA_CHECK(cudaGetLastError());
 }
@@ -487,23 +584,44 @@ void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* l
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_phase2(const Phase2Args& a, cudaStream_t s) {
-  const unsigned grid = static_cast<unsigned>(a.nleaves);
+void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
+  if (a.nleaves == 0) return;
   const bool stored = a.NF != nullptr;
-#define H3D_P2(KK)                                                              \
-  if (stored) phase2_kernel<KK, true><<<grid, kThreads, 0, s>>>(a);             \
-  else phase2_kernel<KK, false><<<grid, kThreads, 0, s>>>(a);
-  switch (a.kernel) {
-    case kLaplace: H3D_P2(kLaplace); break;
-    case kR4: H3D_P2(kR4); break;
-    default: H3D_P2(kHelmholtz); break;
+#define H3D_P2C(KK)                                                                      \
+  if (stored) {                                                                          \
+    const int grid = grid_for(p2_compute_kernel<KK, true>, sms, per_sm, a.nleaves);      \
+    p2_compute_kernel<KK, true><<<grid, kThreads, 0, s>>>(a);                            \
+  } else {                                                                               \
+    const int grid = grid_for(p2_compute_kernel<KK, false>, sms, per_sm, a.nleaves);     \
+    p2_compute_kernel<KK, false><<<grid, kThreads, 0, s>>>(a);                           \
   }
-#undef H3D_P2
+  switch (a.kernel) {
+    case kLaplace: H3D_P2C(kLaplace); break;
+    case kR4: H3D_P2C(kR4); break;
+    default: H3D_P2C(kHelmholtz); break;
+  }
+#undef H3D_P2C
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
+  if (a.nleaves == 0) return;
+  const int grid = grid_for(p2_stream_kernel, sms, per_sm, a.nleaves);
+  p2_stream_kernel<<<grid, kThreads, 0, s>>>(a);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_combine(const double* cpart, const double* spart, const std::int32_t* perm,
+                    std::int64_t row0, std::int64_t row1, double* b, cudaStream_t s) {
+  if (row1 <= row0) return;
+  combine_kernel<<<static_cast<unsigned>((row1 - row0 + 255) / 256), 256, 0, s>>>(cpart, spart, perm,
+                                                                                 row0, row1, b);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s) {
   const unsigned grid = static_cast<unsigned>(a.nleaves);
+  if (grid == 0) return;
   switch (a.kernel) {
     case kLaplace: near_scan_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
     case kR4: near_scan_kernel<kR4><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;

@@ -311,6 +311,7 @@ void Planner::layout() {
     leaf1 = static_cast<std::int64_t>(oct1_) << (3 * (L_ - 1));
   }
   near_off.assign(nl + 1, 0);
+  near_dense.assign(nl + 1, 0);
   near_ids.clear();
   nf_off.assign(nl + 1, 0);
   nf_total = 0;
@@ -320,13 +321,15 @@ void Planner::layout() {
     nf_off[x] = nf_total;
     const std::int64_t mx = node_size(L_, x);
     if (mx == 0 || x < leaf0 || x >= leaf1) continue;
-    std::int64_t ntot = 0;
+    std::int64_t ndense_pts = 0;
+    std::int32_t nd = 0;
     auto add = [&](std::int64_t y, bool dense) {
       const std::int64_t ny = node_size(L_, y);
       if (ny == 0) return;
       near_ids.push_back(static_cast<std::int32_t>(y));
-      ntot += ny;
       if (dense) {
+        ++nd;
+        ndense_pts += ny;
         ++S.near_blocks;
         S.near_entries += mx * ny;
       } else {
@@ -342,7 +345,8 @@ void Planner::layout() {
         for (std::int32_t e = lists_[L_].off[0][x]; e < lists_[L_].off[0][x + 1]; ++e)
           add(lists_[L_].ids[0][e], false);
     }
-    nf_total += mx * ntot;
+    near_dense[x] = nd;
+    nf_total += mx * ndense_pts;
   }
   near_off[nl] = static_cast<std::int32_t>(near_ids.size());
   nf_off[nl] = nf_total;

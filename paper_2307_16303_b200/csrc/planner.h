@@ -120,6 +120,7 @@ class Planner {
   std::vector<P1Reduce> reds;
   std::int64_t leaf0 = 0, leaf1 = 0;
   std::vector<std::int32_t> near_off, near_ids;
+  std::vector<std::int32_t> near_dense;  // per leaf: leading dense entries (self, edge, face)
   std::vector<std::int64_t> nf_off;  // stored near field offsets (per leaf)
   std::int64_t nf_total = 0;
   std::int64_t row0 = 0, row1 = 0;  // owned permuted rows
