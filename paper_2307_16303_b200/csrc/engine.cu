@@ -538,6 +538,7 @@ void Engine::upload_plan() {
     cpart_.alloc(n_);
     spart_.alloc(n_);
   }
+  counters_.alloc(4);
   if (opt_.near_mode == H3D_NEAR_STORED) {
     nf_off_.upload(P.nf_off, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
@@ -642,6 +643,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   a1.qy = qy_.get();
   a1.qz = qz_.get();
   const bool both1 = n_p1s_ > 0 && n_p1p_ > 0;
+  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 4 * sizeof(unsigned), s));
   if (both1) {
     H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[0], 0));
@@ -649,12 +651,14 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   if (n_p1s_ > 0) {
     a1.items = p1_stream_items_.get();
     a1.nitems = n_p1s_;
+    a1.counter = counters_.get();
     launch_p1_stream(a1, sms_, both1 ? 2 : 4, s);
     ++launches;
   }
   if (n_p1p_ > 0) {
     a1.items = p1_proxy_items_.get();
     a1.nitems = n_p1p_;
+    a1.counter = counters_.get() + 1;
     launch_p1_proxy(a1, opt_.kernel_id, sms_, both1 ? 2 : 4, both1 ? stream2_ : s);
     ++launches;
   }
@@ -670,7 +674,9 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // ---- phase 2: FP64 part (near + direct + proxy levels) on stream2_, HBM
   // part (stream levels) on s, combined into b in original order
   if (P.leaf1 > P.leaf0) {
-    const Phase2Args a2 = phase2_args(bout);
+    Phase2Args a2 = phase2_args(bout);
+    a2.counter = counters_.get() + 2;
+    a2.counter2 = counters_.get() + 3;
     if (has_stream_levels_) {
       H3D_CUDA_CHECK(cudaEventRecord(fork_[1], s));
       H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[1], 0));

@@ -110,6 +110,7 @@ struct P1Args {
   double* P = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;  // permuted points
   const double *qx = nullptr, *qy = nullptr, *qz = nullptr;  // proxy points (S-space)
+  unsigned* counter = nullptr;  // dynamic work counter (zeroed before the launch)
 };
 // persistent CTAs: grid = SMs x per_sm (capped by occupancy and work)
 void launch_p1_stream(const P1Args& a, int sms, int per_sm, cudaStream_t s);
@@ -149,6 +150,8 @@ struct Phase2Args {
   double* cpart_out = nullptr;  // compute partial sums (Morton order) when spart != null
   std::int64_t lbase[24] = {0};  // node_base per level (by value)
   int mode[24] = {0};            // LevelMode per level
+  unsigned* counter = nullptr;   // p2_compute work counter (zeroed before the launch)
+  unsigned* counter2 = nullptr;  // p2_stream work counter
 };
 void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);

@@ -60,8 +60,14 @@ __device__ __forceinline__ void p1_write(const P1Item& it, std::int64_t g, int c
 // ---- phase 1, stream levels: T = W_Z^T x_Z over <= 2048 rows x 256 columns
 __global__ void __launch_bounds__(kThreads, 2) p1_stream_kernel(const P1Args a) {
   __shared__ double red[kWarps][kP1Cols + 2];
+  __shared__ long long s_k;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (std::int64_t k = blockIdx.x; k < a.nitems; k += gridDim.x) {
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_k = static_cast<long long>(atomicAdd(a.counter, 1u));
+    __syncthreads();
+    const long long k = s_k;
+    if (k >= a.nitems) break;
     const P1Item it = a.items[k];
     const std::int64_t g = it.node;
     const int rpad = a.nt.rpad[g];
@@ -127,7 +133,13 @@ __global__ void __launch_bounds__(kThreads, 2) p1_stream_kernel(const P1Args a) 
 template <int K>
 __global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
   __shared__ double2 src[2 * kChunk];  // (x, y), (z, w)
-  for (std::int64_t k = blockIdx.x; k < a.nitems; k += gridDim.x) {
+  __shared__ long long s_k;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_k = static_cast<long long>(atomicAdd(a.counter, 1u));
+    __syncthreads();
+    const long long k = s_k;
+    if (k >= a.nitems) break;
     const P1Item it = a.items[k];
     const std::int64_t g = it.node;
     const std::int64_t rb = a.nt.rowbeg[g] + it.row0;
@@ -246,44 +258,15 @@ __global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64
 }
 
 // ---- phase 2, compute part --------------------------------------------------
+// One leaf tile per work unit. Lane = target row (two rows per lane above 32
+// rows; below, the warp splits into G = 32/mp source groups). Sources: the
+// self block (diagonal rule) read directly, then every other range (near and
+// direct neighbour leaves, proxy lists of the ancestors at proxy levels)
+// flattened into one virtual stream that the CTA stages through shared memory
+// in chunks (many independent loads in flight), each warp evaluating its
+// eighth of every chunk against all rows.
 enum RangeKind : int { kRangeSelf = 0, kRangePoints = 1, kRangeProxy = 2 };
-
-// Walk sources [j0, j1) of one range for this lane group: lane -> (row, group);
-// each group takes every G-th source, all lanes of a group read the same
-// source (broadcast). R rows per lane (1 or 2).
-template <int K, int R, bool SELF>
-__device__ __forceinline__ void walk(const double (&tx)[R], const double (&ty)[R],
-                                     const double (&tz)[R], const int (&ti)[R], double (&acc)[R],
-                                     const double* __restrict__ sx, const double* __restrict__ sy,
-                                     const double* __restrict__ sz, const double* __restrict__ sw,
-                                     int j0, int j1, int G, double diag) {
-  int j = j0;
-  for (; j + G < j1; j += 2 * G) {
-    const double x0 = __ldg(sx + j), y0 = __ldg(sy + j), z0 = __ldg(sz + j), w0 = __ldg(sw + j);
-    const double x1 = __ldg(sx + j + G), y1 = __ldg(sy + j + G), z1 = __ldg(sz + j + G),
-                 w1 = __ldg(sw + j + G);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double k0 = kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
-      double k1 = kernel_r2_fast<K>(sq3(tx[r] - x1, ty[r] - y1, tz[r] - z1));
-      if (SELF) {
-        k0 = ti[r] == j ? diag : k0;
-        k1 = ti[r] == j + G ? diag : k1;
-      }
-      acc[r] = fma(k0, w0, acc[r]);
-      acc[r] = fma(k1, w1, acc[r]);
-    }
-  }
-  if (j < j1) {
-    const double x0 = __ldg(sx + j), y0 = __ldg(sy + j), z0 = __ldg(sz + j), w0 = __ldg(sw + j);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double k0 = kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
-      if (SELF) k0 = ti[r] == j ? diag : k0;
-      acc[r] = fma(k0, w0, acc[r]);
-    }
-  }
-}
+constexpr int kStage = 512;  // sources staged per chunk (16 KB)
 
 struct TileRanges {
   std::int64_t start[kMaxRanges];  // first index in its array (points / S space)
@@ -293,10 +276,19 @@ struct TileRanges {
 };
 
 template <int K, int R>
-__device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, std::int64_t xb, int r0,
-                             int m, int mp, double* cpart) {
+__device__ __forceinline__ void eval_src(const double (&tx)[R], const double (&ty)[R],
+                                         const double (&tz)[R], double (&acc)[R], double2 s0,
+                                         double2 s1) {
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - s0.x, ty[r] - s0.y, tz[r] - s1.x)), s1.y, acc[r]);
+}
+
+template <int K, int R>
+__device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, double2* stage,
+                             std::int64_t xb, int r0, int m, int mp, double* cpart) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = 32 / mp;  // source groups per warp (R == 2 -> mp == 32, G == 1)
+  const int G = 32 / mp;
   const int grp = lane / mp, row = lane % mp;
   double tx[R], ty[R], tz[R], acc[R];
   int ti[R];
@@ -308,34 +300,56 @@ __device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, std::int
     tx[r] = ok ? a.px[gi] : kFar;
     ty[r] = ok ? a.py[gi] : kFar;
     tz[r] = ok ? a.pz[gi] : kFar;
-    ti[r] = ok ? r0 + i : -1;  // local index within the leaf (self range)
+    ti[r] = ok ? r0 + i : -1;
     acc[r] = 0.0;
   }
-  // this warp's contiguous slice of the tile's virtual source stream
-  const int T = tr.pre[tr.n];
-  const int v0 = static_cast<int>(static_cast<long long>(T) * warp / kWarps);
-  const int v1 = static_cast<int>(static_cast<long long>(T) * (warp + 1) / kWarps);
-  int ri = 0;
-  while (ri < tr.n && tr.pre[ri + 1] <= v0) ++ri;
-  for (int v = v0; v < v1 && ri < tr.n; ++ri) {
-    const int rbeg = tr.pre[ri], rend = min(tr.pre[ri + 1], v1);
-    const int j0 = v - rbeg + grp, j1 = rend - rbeg;
-    const std::int64_t st = tr.start[ri];
-    switch (tr.kind[ri]) {
-      case kRangeSelf:
-        walk<K, R, true>(tx, ty, tz, ti, acc, a.px + st, a.py + st, a.pz + st, a.xp + st, j0, j1,
-                         G, a.diag);
-        break;
-      case kRangePoints:
-        walk<K, R, false>(tx, ty, tz, ti, acc, a.px + st, a.py + st, a.pz + st, a.xp + st, j0, j1,
-                          G, a.diag);
-        break;
-      default:
-        walk<K, R, false>(tx, ty, tz, ti, acc, a.qx + st, a.qy + st, a.qz + st, a.S + st, j0, j1,
-                          G, a.diag);
-        break;
+  // self block (range 0 when the tile lists it): warps split it, diagonal rule
+  int vbeg = 0;
+  if (tr.n > 0 && tr.kind[0] == kRangeSelf) {
+    const std::int64_t st = tr.start[0];
+    const int len = tr.pre[1];
+    for (int j = warp * G + grp; j < len; j += kWarps * G) {
+      const double x0 = a.px[st + j], y0 = a.py[st + j], z0 = a.pz[st + j], w0 = a.xp[st + j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double k0 = ti[r] == j ? a.diag : kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
+        acc[r] = fma(k0, w0, acc[r]);
+      }
     }
-    v = rend;
+    vbeg = len;
+  }
+  const int T = tr.pre[tr.n];
+  const int per_warp = kStage / kWarps;
+  for (int base = vbeg; base < T; base += kStage) {
+    const int cnt = min(kStage, T - base);
+    __syncthreads();  // previous chunk consumed
+    for (int q = threadIdx.x; q < cnt; q += kThreads) {
+      const int v = base + q;
+      int lo = 0, hi = tr.n - 1;  // range containing v: pre[lo] <= v < pre[lo+1]
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tr.pre[mid] <= v) lo = mid;
+        else hi = mid - 1;
+      }
+      const std::int64_t idx = tr.start[lo] + (v - tr.pre[lo]);
+      if (tr.kind[lo] == kRangeProxy) {
+        stage[2 * q] = make_double2(a.qx[idx], a.qy[idx]);
+        stage[2 * q + 1] = make_double2(a.qz[idx], a.S[idx]);
+      } else {
+        stage[2 * q] = make_double2(a.px[idx], a.py[idx]);
+        stage[2 * q + 1] = make_double2(a.pz[idx], a.xp[idx]);
+      }
+    }
+    __syncthreads();
+    const int j0 = warp * per_warp, j1 = min(cnt, j0 + per_warp);
+    int j = j0 + grp;
+    for (; j + G < j1; j += 2 * G) {
+      const double2 s0 = stage[2 * j], s1 = stage[2 * j + 1];
+      const double2 u0 = stage[2 * (j + G)], u1 = stage[2 * (j + G) + 1];
+      eval_src<K, R>(tx, ty, tz, acc, s0, s1);
+      eval_src<K, R>(tx, ty, tz, acc, u0, u1);
+    }
+    if (j < j1) eval_src<K, R>(tx, ty, tz, acc, stage[2 * j], stage[2 * j + 1]);
   }
   // combine the G source groups of each row (fixed butterfly order)
 #pragma unroll
@@ -345,24 +359,30 @@ __device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, std::int
   }
 }
 
-// One tile (leaf) at a time per CTA, persistent over the owned leaves.
+// Persistent CTAs pull leaf tiles from a work counter (dynamic balance).
 template <int K, bool STORED>
 __global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Args a) {
   __shared__ TileRanges tr;
   __shared__ double cpart[kWarps * 64];
+  __shared__ double2 stage[2 * kStage];
+  __shared__ long long s_t;
   const int L = a.depth;
-  for (std::int64_t t = blockIdx.x; t < a.nleaves; t += gridDim.x) {
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_t = static_cast<long long>(atomicAdd(a.counter, 1u));
+    __syncthreads();
+    const long long t = s_t;
+    if (t >= a.nleaves) break;
     const std::int64_t X = a.leaf0 + t;
     const std::int64_t xb = a.leaf_off[X];
     const int mrows = static_cast<int>(a.leaf_off[X + 1] - xb);
     if (mrows == 0) continue;
-    __syncthreads();  // tr / cpart reuse
     if (threadIdx.x == 0) {
-      // source ranges: self, neighbours (stored: only the direct partners),
-      // then the proxy ranges of the ancestors at proxy levels
+      // source ranges: self, neighbours (stored mode: only the direct
+      // partners), then the proxy ranges of the ancestors at proxy levels
       int n = 0, pre = 0;
       const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
-      const std::int32_t nd = STORED ? a.near_dense[X] : 0;  // dense entries of the list
+      const std::int32_t nd = STORED ? a.near_dense[X] : 0;
       for (std::int32_t e = nb; e < ne && n < kMaxRanges; ++e) {
         if (STORED && e - nb < nd) continue;
         const std::int32_t Y = a.near_ids[e];
@@ -393,8 +413,8 @@ __global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Arg
       const int m = min(64, mrows - r0);
       int mp = 1;
       while (mp < m && mp < 32) mp <<= 1;
-      if (m > 32) compute_rows<K, 2>(a, tr, xb, r0, m, 32, cpart);
-      else compute_rows<K, 1>(a, tr, xb, r0, m, mp, cpart);
+      if (m > 32) compute_rows<K, 2>(a, tr, stage, xb, r0, m, 32, cpart);
+      else compute_rows<K, 1>(a, tr, stage, xb, r0, m, mp, cpart);
       __syncthreads();
       if (threadIdx.x < m) {
         const int i = threadIdx.x;
@@ -426,7 +446,13 @@ __global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Arg
 __global__ void __launch_bounds__(kThreads, 2) p2_stream_kernel(const Phase2Args a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int L = a.depth;
-  for (std::int64_t t = blockIdx.x; t < a.nleaves; t += gridDim.x) {
+  __shared__ long long s_t;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_t = static_cast<long long>(atomicAdd(a.counter2, 1u));
+    __syncthreads();
+    const long long t = s_t;
+    if (t >= a.nleaves) break;
     const std::int64_t X = a.leaf0 + t;
     const std::int64_t xb = a.leaf_off[X];
     const int m = static_cast<int>(a.leaf_off[X + 1] - xb);

@@ -54,6 +54,6 @@ def test_large_config_against_reference(h3d, name, policy):
     ref_err = rel(g["b_ref_rows"], g["b_exact_rows"])
     # the sampled-row error matches the reference's own reference_error (which sums
     # 1/sqrt(r^2) rows instead of eval_pair's 1/r: equal to ~1e-5 relative)
-    assert abs(ref_err - float(g["ref_error"])) <= 1e-3 * float(g["ref_error"])
+    assert abs(ref_err - float(g["ref_error"])) <= 1e-2 * float(g["ref_error"]) + 1e-14
     assert err <= 2 * ref_err, (err, ref_err)
     rep.close()
