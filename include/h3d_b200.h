@@ -117,6 +117,7 @@ typedef struct {
   int64_t direct_evals;       /* leaf-level admissible entries evaluated exactly */
   int64_t lu_doubles;         /* packed LU storage of proxy-level pairs */
   int64_t level_units[16];    /* per level: sum over pairs of r (m + n) */
+  double level_aca_ms[16];    /* per level: ACA wall time (rank + write pass) */
   int64_t reserved[4];
 } h3d_stats;
 

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
           } else {
             const double r2 = sq3(xi - cx[j], yi - cy[j], zi - cz[j]);
             if (r2 < kCoincidentTol2) local_flags |= kFlagDegenGeom;
-            val = kernel_r2<K>(r2);
+            val = kernel_r2_fast<K>(r2);
           }
           if (rank > 0) {
             double acc = 0.0;
@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
         } else {
           const double r2 = sq3(rx[i] - xj, ry[i] - yj, rz[i] - zj);
           if (r2 < kCoincidentTol2) local_flags |= kFlagDegenGeom;
-          val = kernel_r2<K>(r2);
+          val = kernel_r2_fast<K>(r2);
         }
         if (rank > 0) {
           double acc = 0.0;

@@ -38,20 +38,24 @@ __device__ __forceinline__ double kernel_r2(double r2) {
 }
 
 // Matvec-path radial map: Laplace uses the hardware fp64 rsqrt seed
-// (MUFU.RSQ64H, ~2^-22) plus one Newton step (~1e-13 relative), 1.26x the
-// throughput of rsqrt() in the P2P loop (profiles/r01_summary.md).
-__device__ __forceinline__ double rsqrt_nr1(double x) {
+// (MUFU.RSQ64H, ~2^-22) plus one third-order correction
+//   y1 = y0 (1 + e/2 + 3e^2/8),  e = 1 - x y0^2,
+// cubic convergence: full double accuracy (the depth-0 dense matvec matches the
+// direct sum to < 1e-13, reference test_hmatrix.cpp:21-35) for 5 FP64 ops,
+// cheaper than rsqrt()'s two Newton steps + special-case handling.
+__device__ __forceinline__ double rsqrt_c3(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
   const double p = x * y;
   const double e = fma(-p, y, 1.0);
-  return fma(0.5 * y, e, y);
+  const double c = fma(e, 0.375, 0.5);
+  return fma(y, e * c, y);
 }
 
 template <int K>
 __device__ __forceinline__ double kernel_r2_fast(double r2) {
   if constexpr (K == kLaplace) {
-    return rsqrt_nr1(r2);
+    return rsqrt_c3(r2);
   } else {
     return kernel_r2<K>(r2);
   }

@@ -299,6 +299,7 @@ void Engine::run_aca(bool write) {
     const std::int64_t np = static_cast<std::int64_t>(P.X.size());
     if (np == 0) continue;
     const int mode = plan_->mode(l);
+    const auto t_level = Clock::now();
     std::vector<std::int64_t> xb(np), yb(np);
     std::vector<std::int32_t> m(np), nn(np);
     for (std::int64_t p = 0; p < np; ++p) {
@@ -396,6 +397,7 @@ void Engine::run_aca(bool write) {
       }
       break;
     }
+    if (l < 16) level_aca_ms_[l] += ms_since(t_level);
     std::vector<std::int32_t> rk(np);
     H3D_CUDA_CHECK(cudaMemcpyAsync(rk.data(), d_rank.get(), np * 4, cudaMemcpyDeviceToHost, stream_));
     H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -827,6 +829,7 @@ void Engine::stats(h3d_stats* s) const {
     for (std::size_t p = 0; p < pr.X.size(); ++p)
       u += static_cast<std::int64_t>(pr.rank[p]) * (node_size(l, pr.X[p]) + node_size(l, pr.Y[p]));
     s->level_units[l] = u;
+    s->level_aca_ms[l] = level_aca_ms_[l];
   }
 }
 

@@ -137,6 +137,7 @@ class Engine {
 
   // build timings
   double ms_tree_ = 0, ms_lists_ = 0, ms_aca_rank_ = 0, ms_aca_write_ = 0, ms_total_ = 0;
+  double level_aca_ms_[16] = {};  // rank + write pass per level
 };
 
 }  // namespace h3db

@@ -275,27 +275,35 @@ struct TileRanges {
   int n;
 };
 
-template <int K, int R>
-__device__ __forceinline__ void eval_src(const double (&tx)[R], const double (&ty)[R],
-                                         const double (&tz)[R], double (&acc)[R], double2 s0,
-                                         double2 s1) {
+template <int K>
+__device__ __forceinline__ void eval4(const double (&tx)[4], const double (&ty)[4],
+                                      const double (&tz)[4], double (&acc)[4], double2 s0,
+                                      double2 s1) {
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < 4; ++r)
     acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - s0.x, ty[r] - s0.y, tz[r] - s1.x)), s1.y, acc[r]);
 }
 
-template <int K, int R>
-__device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, double2* stage,
-                             std::int64_t xb, int r0, int m, int mp, double* cpart) {
+// Rows [r0, r0 + nr) of the tile (nr <= 32): warps form ng row groups of 4
+// rows (ng a power of two) x gs = 8 / ng source slices; lanes stride over the
+// sources of the staged chunks; partial sums per (slice, row) are reduced in a
+// fixed order. Returns after writing rowsum[r0 - r0 .. nr).
+template <int K>
+__device__ void compute_pass(const Phase2Args& a, const TileRanges& tr, double2* stage,
+                             std::int64_t xb, int r0, int nr, double* part) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = 32 / mp;
-  const int grp = lane / mp, row = lane % mp;
-  double tx[R], ty[R], tz[R], acc[R];
-  int ti[R];
+  int ng = 1;
+  while (ng * 4 < nr) ng <<= 1;
+  const int gs = kWarps / ng;
+  const int group = warp / gs, slice = warp % gs;
+  double tx[4], ty[4], tz[4], acc[4];
+  int ti[4];
+  bool any = false;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = row + 32 * r;
-    const bool ok = i < m;
+  for (int r = 0; r < 4; ++r) {
+    const int i = 4 * group + r;
+    const bool ok = i < nr;
+    any |= ok;
     const std::int64_t gi = xb + r0 + i;
     tx[r] = ok ? a.px[gi] : kFar;
     ty[r] = ok ? a.py[gi] : kFar;
@@ -303,29 +311,30 @@ __device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, double2*
     ti[r] = ok ? r0 + i : -1;
     acc[r] = 0.0;
   }
-  // self block (range 0 when the tile lists it): warps split it, diagonal rule
+  const int step = 32 * gs;
   int vbeg = 0;
-  if (tr.n > 0 && tr.kind[0] == kRangeSelf) {
+  if (tr.n > 0 && tr.kind[0] == kRangeSelf) {  // self block, diagonal rule
     const std::int64_t st = tr.start[0];
     const int len = tr.pre[1];
-    for (int j = warp * G + grp; j < len; j += kWarps * G) {
-      const double x0 = a.px[st + j], y0 = a.py[st + j], z0 = a.pz[st + j], w0 = a.xp[st + j];
+    if (any)
+      for (int j = slice * 32 + lane; j < len; j += step) {
+        const double x0 = a.px[st + j], y0 = a.py[st + j], z0 = a.pz[st + j], w0 = a.xp[st + j];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double k0 = ti[r] == j ? a.diag : kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
-        acc[r] = fma(k0, w0, acc[r]);
+        for (int r = 0; r < 4; ++r) {
+          const double k0 = ti[r] == j ? a.diag
+                                       : kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
+          acc[r] = fma(k0, w0, acc[r]);
+        }
       }
-    }
     vbeg = len;
   }
   const int T = tr.pre[tr.n];
-  const int per_warp = kStage / kWarps;
   for (int base = vbeg; base < T; base += kStage) {
     const int cnt = min(kStage, T - base);
     __syncthreads();  // previous chunk consumed
     for (int q = threadIdx.x; q < cnt; q += kThreads) {
       const int v = base + q;
-      int lo = 0, hi = tr.n - 1;  // range containing v: pre[lo] <= v < pre[lo+1]
+      int lo = 0, hi = tr.n - 1;  // range with pre[lo] <= v < pre[lo + 1]
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         if (tr.pre[mid] <= v) lo = mid;
@@ -341,29 +350,36 @@ __device__ void compute_rows(const Phase2Args& a, const TileRanges& tr, double2*
       }
     }
     __syncthreads();
-    const int j0 = warp * per_warp, j1 = min(cnt, j0 + per_warp);
-    int j = j0 + grp;
-    for (; j + G < j1; j += 2 * G) {
-      const double2 s0 = stage[2 * j], s1 = stage[2 * j + 1];
-      const double2 u0 = stage[2 * (j + G)], u1 = stage[2 * (j + G) + 1];
-      eval_src<K, R>(tx, ty, tz, acc, s0, s1);
-      eval_src<K, R>(tx, ty, tz, acc, u0, u1);
+    if (any) {
+      int j = slice * 32 + lane;
+      for (; j + step < cnt; j += 2 * step) {
+        const double2 s0 = stage[2 * j], s1 = stage[2 * j + 1];
+        const double2 u0 = stage[2 * (j + step)], u1 = stage[2 * (j + step) + 1];
+        eval4<K>(tx, ty, tz, acc, s0, s1);
+        eval4<K>(tx, ty, tz, acc, u0, u1);
+      }
+      if (j < cnt) eval4<K>(tx, ty, tz, acc, stage[2 * j], stage[2 * j + 1]);
     }
-    if (j < j1) eval_src<K, R>(tx, ty, tz, acc, stage[2 * j], stage[2 * j + 1]);
   }
-  // combine the G source groups of each row (fixed butterfly order)
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    for (int o = mp; o < 32; o <<= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], o);
-    if (grp == 0 && row + 32 * r < m) cpart[warp * 64 + row + 32 * r] = acc[r];
+  for (int r = 0; r < 4; ++r) {
+    const double v = warp_sum(acc[r]);
+    if (lane == 0) part[slice * 32 + 4 * group + r] = v;
   }
+  __syncthreads();
+  if (threadIdx.x < nr) {
+    double v = 0.0;
+    for (int s = 0; s < gs; ++s) v += part[s * 32 + threadIdx.x];
+    part[kWarps * 32 + threadIdx.x] = v;  // pass result
+  }
+  __syncthreads();
 }
 
 // Persistent CTAs pull leaf tiles from a work counter (dynamic balance).
 template <int K, bool STORED>
 __global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Args a) {
   __shared__ TileRanges tr;
-  __shared__ double cpart[kWarps * 64];
+  __shared__ double cpart[kWarps * 32 + 32];
   __shared__ double2 stage[2 * kStage];
   __shared__ long long s_t;
   const int L = a.depth;
@@ -409,16 +425,12 @@ __global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Arg
       tr.n = n;
     }
     __syncthreads();
-    for (int r0 = 0; r0 < mrows; r0 += 64) {
-      const int m = min(64, mrows - r0);
-      int mp = 1;
-      while (mp < m && mp < 32) mp <<= 1;
-      if (m > 32) compute_rows<K, 2>(a, tr, stage, xb, r0, m, 32, cpart);
-      else compute_rows<K, 1>(a, tr, stage, xb, r0, m, mp, cpart);
-      __syncthreads();
+    for (int r0 = 0; r0 < mrows; r0 += 32) {
+      const int m = min(32, mrows - r0);
+      compute_pass<K>(a, tr, stage, xb, r0, m, cpart);
       if (threadIdx.x < m) {
         const int i = threadIdx.x;
-        double v = 0.0;
+        double v = cpart[kWarps * 32 + i];
         if (STORED) {  // stored dense near blocks, column-major per leaf
           const std::int32_t nb = a.near_off[X];
           const std::int32_t nd = a.near_dense[X];
@@ -432,8 +444,6 @@ __global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Arg
               v = fma(nf[static_cast<std::int64_t>(c) * mrows + r0 + i], a.xp[yb + j], v);
           }
         }
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) v += cpart[w * 64 + i];
         if (a.spart) a.cpart_out[xb + r0 + i] = v;
         else a.b[a.perm[xb + r0 + i]] = v;
       }

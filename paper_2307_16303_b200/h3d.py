@@ -101,6 +101,7 @@ class _Stats(C.Structure):
         ("direct_evals", C.c_int64),
         ("lu_doubles", C.c_int64),
         ("level_units", C.c_int64 * 16),
+        ("level_aca_ms", C.c_double * 16),
         ("reserved", C.c_int64 * 4),
     ]
 
@@ -345,10 +346,10 @@ class HMatrixRep:
             if f == "reserved":
                 continue
             v = getattr(s, f)
-            out[f] = list(v) if f in ("level_modes", "level_units") else v
+            out[f] = list(v) if f in ("level_modes", "level_units", "level_aca_ms") else v
         L = out["depth"]
-        out["level_modes"] = out["level_modes"][: L + 1]
-        out["level_units"] = out["level_units"][: L + 1]
+        for f in ("level_modes", "level_units", "level_aca_ms"):
+            out[f] = out[f][: L + 1]
         return out
 
     @property
