@@ -1,6 +1,9 @@
-// Batched partially pivoted ACA on the device: one CTA per admissible pair,
-// persistent CTAs pulling pairs from an atomic counter, u_k / v_k columns in
-// a per-CTA global workspace slot (L1/L2 resident for leaf and mid levels).
+// Batched partially pivoted ACA on the device. One pair per CTA (persistent
+// CTAs pulling pairs from an atomic counter) or, for the few huge blocks of
+// the top levels, one pair per thread-block cluster of up to 16 CTAs that
+// split the rows/columns and reduce through distributed shared memory.
+// u_k / v_k columns live in a per-slot global workspace (L1/L2 resident for
+// leaf and mid levels).
 //
 // Algorithm (pivot rules, stop rules, running Frobenius estimate) follows
 // reference proj/src/lowrank.cpp:157-289 (aca_compress) step for step:
@@ -11,72 +14,133 @@
 //   * residual column, v = row / delta; stop if |u||v| <= 1e-12 |S|_F, or on
 //     the second consecutive |u||v| <= eps |S|_F (candidate dropped);
 //   * |S|_F^2 += |u|^2 |v|^2 + 2 (U^T u).(V^T v); next row = argmax |u|.
-// Reductions are fixed-order (warp butterflies + ordered per-warp combine) so
-// a given launch configuration is bitwise deterministic; the rank pass and
-// the write pass therefore produce identical factors.
+// Reductions are fixed-order (warp butterflies, ordered per-warp and per-CTA
+// combines) so a launch configuration (CTA size, cluster size) is bitwise
+// deterministic; the rank pass and the write pass use the same configuration
+// and therefore produce identical factors.
 //
 // Output (write pass): U = [u_1..u_r] (m x r) and V = [v_1..v_r] (n x r) with
 // U V^T ~= K(X,Y), written row-major into the node-major factor pool W at the
-// pair's column offsets (see engine.cu: W layout). Optionally the reference's
-// own representation (pivots + packed LU, lowrank.cpp:277-287).
+// pair's column offsets (stream levels), or the reference's own
+// representation, pivots + packed LU (lowrank.cpp:277-287; proxy levels).
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace h3db {
 
 namespace {
 
-template <int NT>
-struct Reduce {
+template <int NT, bool CLU>
+struct Ctx {
   static constexpr int NW = NT / 32;
-  double* v;     // [NW]
-  long long* i;  // [NW]
+  double* rv;        // [NW] per-warp scratch
+  long long* ri;     // [NW]
+  double* cv;        // [1] cluster slot
+  long long* ci;     // [1]
+  int CL;
 
-  __device__ __forceinline__ double sum(double x) {
+  __device__ __forceinline__ void bar() {
+    if constexpr (CLU) cg::this_cluster().sync();
+    else __syncthreads();
+  }
+  template <class T>
+  __device__ __forceinline__ T remote(T* p, int rank) {
+    if constexpr (CLU) return *cg::this_cluster().map_shared_rank(p, rank);
+    else return *p;
+  }
+
+  __device__ double local_sum(double x) {
     x = warp_sum(x);
-    if (NW == 1) return x;
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) v[w] = x;
-    __syncthreads();
-    double t = 0.0;
+    if (NW > 1) {
+      if ((threadIdx.x & 31) == 0) rv[threadIdx.x >> 5] = x;
+      __syncthreads();
+      x = 0.0;
 #pragma unroll
-    for (int k = 0; k < NW; ++k) t += v[k];
-    __syncthreads();
-    return t;
-  }
-
-  __device__ __forceinline__ void argmax(double& x, long long& j) {
-    warp_argmax(x, j);
-    if (NW == 1) return;
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) {
-      v[w] = x;
-      i[w] = j;
+      for (int k = 0; k < NW; ++k) x += rv[k];
+      __syncthreads();
     }
-    __syncthreads();
-    x = -1.0;
-    j = -1;
-#pragma unroll
-    for (int k = 0; k < NW; ++k) argmax_combine(x, j, v[k], i[k]);
-    __syncthreads();
+    return x;
   }
 
-  __device__ __forceinline__ long long min_ll(long long x) {
-    x = warp_min_ll(x);
-    if (NW == 1) return x;
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) i[w] = x;
-    __syncthreads();
-    long long t = i[0];
+  __device__ double sum(double x) {
+    x = warp_sum(x);
+    if (NW > 1) {
+      if ((threadIdx.x & 31) == 0) rv[threadIdx.x >> 5] = x;
+      __syncthreads();
+      x = 0.0;
 #pragma unroll
-    for (int k = 1; k < NW; ++k) t = i[k] < t ? i[k] : t;
-    __syncthreads();
-    return t;
+      for (int k = 0; k < NW; ++k) x += rv[k];
+      __syncthreads();
+    }
+    if constexpr (CLU) {
+      if (threadIdx.x == 0) cv[0] = x;
+      bar();
+      double t = 0.0;
+      for (int c = 0; c < CL; ++c) t += remote(cv, c);
+      bar();
+      return t;
+    }
+    return x;
+  }
+
+  __device__ void argmax(double& x, long long& j) {
+    warp_argmax(x, j);
+    if (NW > 1) {
+      if ((threadIdx.x & 31) == 0) {
+        rv[threadIdx.x >> 5] = x;
+        ri[threadIdx.x >> 5] = j;
+      }
+      __syncthreads();
+      x = -1.0;
+      j = -1;
+#pragma unroll
+      for (int k = 0; k < NW; ++k) argmax_combine(x, j, rv[k], ri[k]);
+      __syncthreads();
+    }
+    if constexpr (CLU) {
+      if (threadIdx.x == 0) {
+        cv[0] = x;
+        ci[0] = j;
+      }
+      bar();
+      x = -1.0;
+      j = -1;
+      for (int c = 0; c < CL; ++c) argmax_combine(x, j, remote(cv, c), remote(ci, c));
+      bar();
+    }
+  }
+
+  __device__ long long min_ll(long long x) {
+    x = warp_min_ll(x);
+    if (NW > 1) {
+      if ((threadIdx.x & 31) == 0) ri[threadIdx.x >> 5] = x;
+      __syncthreads();
+      x = ri[0];
+#pragma unroll
+      for (int k = 1; k < NW; ++k) x = ri[k] < x ? ri[k] : x;
+      __syncthreads();
+    }
+    if constexpr (CLU) {
+      if (threadIdx.x == 0) ci[0] = x;
+      bar();
+      long long t = remote(ci, 0);
+      for (int c = 1; c < CL; ++c) {
+        const long long v = remote(ci, c);
+        t = v < t ? v : t;
+      }
+      bar();
+      return t;
+    }
+    return x;
   }
 };
 
 template <int NT>
-__device__ __forceinline__ void bar() {
+__device__ __forceinline__ void tbar() {
   if (NT == 32) __syncwarp();
   else __syncthreads();
 }
@@ -91,62 +155,74 @@ __device__ void write_rows(const double* __restrict__ src, int ld, int rows, int
   for (int i0 = 0; i0 < rows; i0 += 32) {
     for (int a0 = 0; a0 < r; a0 += 32) {
       for (int al = w; al < 32; al += NW) {
-        const int a = a0 + al, i = i0 + lane;
-        tile[al * 33 + lane] = (a < r && i < rows) ? src[static_cast<std::int64_t>(a) * ld + i] : 0.0;
+        const int q = a0 + al, i = i0 + lane;
+        tile[al * 33 + lane] = (q < r && i < rows) ? src[static_cast<std::int64_t>(q) * ld + i] : 0.0;
       }
-      bar<NT>();
+      tbar<NT>();
       for (int il = w; il < 32; il += NW) {
-        const int i = i0 + il, a = a0 + lane;
-        if (i < rows && a < r) dst[static_cast<std::int64_t>(i) * rs + a] = tile[lane * 33 + il];
+        const int i = i0 + il, q = a0 + lane;
+        if (i < rows && q < r) dst[static_cast<std::int64_t>(i) * rs + q] = tile[lane * 33 + il];
       }
-      bar<NT>();
+      tbar<NT>();
     }
   }
 }
 
-template <int NT, int K>
+template <int NT, int K, bool CLU>
 __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
   constexpr int NW = NT / 32;
   extern __shared__ double smem[];
   const int cw = a.cap_ws;
   double* s_vec = smem;            // gathered U(i,:) / V(pj,:)   [cw]
-  double* s_cu = s_vec + cw;       // U^T u                       [cw]
-  double* s_cv = s_cu + cw;        // V^T v                       [cw]
+  double* s_cu = s_vec + cw;       // U^T u (this CTA's rows)     [cw]
+  double* s_cv = s_cu + cw;        // V^T v (this CTA's columns)  [cw]
   double* s_delta = s_cv + cw;     //                             [cw]
   double* s_tile = s_delta + cw;   // 32 x 33
   int* s_prow = reinterpret_cast<int*>(s_tile + 32 * 33);  // [cw]
   int* s_pcol = s_prow + cw;                               // [cw]
   __shared__ double s_rv[NW];
   __shared__ long long s_ri[NW];
+  __shared__ double s_c1;
+  __shared__ long long s_c2;
   __shared__ long long s_pair;
-  Reduce<NT> red{s_rv, s_ri};
+  int CL = 1, crank = 0;
+  if constexpr (CLU) {
+    CL = static_cast<int>(cg::this_cluster().num_blocks());
+    crank = static_cast<int>(cg::this_cluster().block_rank());
+  }
+  Ctx<NT, CLU> cx{s_rv, s_ri, &s_c1, &s_c2, CL};
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* U = a.ws + static_cast<std::int64_t>(blockIdx.x) * a.slot_doubles;
+  const std::int64_t slot = blockIdx.x / CL;
+  double* U = a.ws + slot * a.slot_doubles;
   double* V = U + static_cast<std::int64_t>(cw + 1) * a.ms;
   unsigned char* row_used = reinterpret_cast<unsigned char*>(V + static_cast<std::int64_t>(cw + 1) * a.ns);
   unsigned char* col_used = row_used + a.ms;
 
   for (;;) {
-    __syncthreads();
-    if (tid == 0) s_pair = static_cast<long long>(atomicAdd(a.counter, 1ULL));
-    __syncthreads();
-    const long long p = s_pair;
+    cx.bar();
+    if (crank == 0 && tid == 0) s_pair = static_cast<long long>(atomicAdd(a.counter, 1ULL));
+    cx.bar();
+    const long long p = cx.remote(&s_pair, 0);
     if (p >= a.npairs) break;
 
     const std::int64_t xb = a.xb[p], yb = a.yb[p];
     const int m = a.m[p], n = a.n[p];
+    const int r0 = static_cast<int>(static_cast<long long>(m) * crank / CL);
+    const int r1 = static_cast<int>(static_cast<long long>(m) * (crank + 1) / CL);
+    const int c0 = static_cast<int>(static_cast<long long>(n) * crank / CL);
+    const int c1 = static_cast<int>(static_cast<long long>(n) * (crank + 1) / CL);
     int cap = m < n ? m : n;
     if (a.max_rank > 0 && a.max_rank < cap) cap = static_cast<int>(a.max_rank);
     const double* __restrict__ rx = a.px + xb;
     const double* __restrict__ ry = a.py + xb;
     const double* __restrict__ rz = a.pz + xb;
-    const double* __restrict__ cx = a.px + yb;
-    const double* __restrict__ cy = a.py + yb;
-    const double* __restrict__ cz = a.pz + yb;
-    for (int i = tid; i < m; i += NT) row_used[i] = 0;
-    for (int j = tid; j < n; j += NT) col_used[j] = 0;
-    __syncthreads();
+    const double* __restrict__ cx_ = a.px + yb;
+    const double* __restrict__ cy_ = a.py + yb;
+    const double* __restrict__ cz_ = a.pz + yb;
+    for (int i = r0 + tid; i < r1; i += NT) row_used[i] = 0;
+    for (int j = c0 + tid; j < c1; j += NT) col_used[j] = 0;
+    cx.bar();
 
     int rank = 0, hits = 0;
     long long suggested = 0;
@@ -164,12 +240,12 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
           i = suggested;
         } else {
           long long first = 0x7fffffffffffffffLL;
-          for (int t = tid; t < m; t += NT)
+          for (int t = r0 + tid; t < r1; t += NT)
             if (!row_used[t]) {
               first = t;
               break;
             }
-          first = red.min_ll(first);
+          first = cx.min_ll(first);
           i = first == 0x7fffffffffffffffLL ? -1 : first;
         }
         if (i < 0) break;
@@ -178,12 +254,12 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
         const double xi = rx[i], yi = ry[i], zi = rz[i];
         double best = -1.0;
         long long bestj = -1;
-        for (int j = tid; j < n; j += NT) {
+        for (int j = c0 + tid; j < c1; j += NT) {
           double val;
           if (xb + i == yb + j) {
             val = a.diag;
           } else {
-            const double r2 = sq3(xi - cx[j], yi - cy[j], zi - cz[j]);
+            const double r2 = sq3(xi - cx_[j], yi - cy_[j], zi - cz_[j]);
             if (r2 < kCoincidentTol2) local_flags |= kFlagDegenGeom;
             val = kernel_r2_fast<K>(r2);
           }
@@ -196,13 +272,13 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
           Vc[j] = val;
           if (!col_used[j]) argmax_combine(best, bestj, fabs(val), j);
         }
-        red.argmax(best, bestj);
+        cx.argmax(best, bestj);
         if (bestj < 0) break;
         if (best < 1e-30) {  // AcaOptions::pivot_floor (lowrank.hpp:99)
-          __syncthreads();
-          if (tid == 0) row_used[i] = 1;
+          cx.bar();
+          if (crank == 0 && tid == 0) row_used[i] = 1;
           suggested = -1;
-          __syncthreads();
+          cx.bar();
           continue;
         }
         pi = i;
@@ -210,13 +286,13 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
         break;
       }
       if (pi < 0) break;
-      __syncthreads();  // Vc visible to all threads
+      cx.bar();  // Vc complete across the cluster
       const double delta = Vc[pj];
       for (int q = tid; q < rank; q += NT) s_vec[q] = V[static_cast<std::int64_t>(q) * a.ns + pj];
       __syncthreads();
-      const double xj = cx[pj], yj = cy[pj], zj = cz[pj];
+      const double xj = cx_[pj], yj = cy_[pj], zj = cz_[pj];
       double u2 = 0.0, v2 = 0.0;
-      for (int i = tid; i < m; i += NT) {
+      for (int i = r0 + tid; i < r1; i += NT) {
         double val;
         if (xb + i == yb + pj) {
           val = a.diag;
@@ -235,13 +311,13 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
         u2 = fma(val, val, u2);
       }
       const double inv = 1.0 / delta;
-      for (int j = tid; j < n; j += NT) {
+      for (int j = c0 + tid; j < c1; j += NT) {
         const double v = Vc[j] * inv;
         Vc[j] = v;
         v2 = fma(v, v, v2);
       }
-      u2 = red.sum(u2);
-      v2 = red.sum(v2);
+      u2 = cx.sum(u2);
+      v2 = cx.sum(v2);
       const double uv = sqrt(u2 * v2);
       if (rank > 0) {  // two-hit stop rule (lowrank.cpp:225-239)
         const double ns = sqrt(fro2 > 0.0 ? fro2 : 0.0);
@@ -258,13 +334,13 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
       }
       double cross = 0.0;
       if (rank > 0) {
-        __syncthreads();  // Uc / Vc complete
+        __syncthreads();  // Uc / Vc of this CTA complete
         for (int q = warp; q < rank; q += NW) {
           const double* uq = U + static_cast<std::int64_t>(q) * a.ms;
           const double* vq = V + static_cast<std::int64_t>(q) * a.ns;
           double su = 0.0, sv = 0.0;
-          for (int i = lane; i < m; i += 32) su = fma(uq[i], Uc[i], su);
-          for (int j = lane; j < n; j += 32) sv = fma(vq[j], Vc[j], sv);
+          for (int i = r0 + lane; i < r1; i += 32) su = fma(uq[i], Uc[i], su);
+          for (int j = c0 + lane; j < c1; j += 32) sv = fma(vq[j], Vc[j], sv);
           su = warp_sum(su);
           sv = warp_sum(sv);
           if (lane == 0) {
@@ -272,44 +348,59 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
             s_cv[q] = sv;
           }
         }
-        __syncthreads();
-        for (int q = 0; q < rank; ++q) cross = fma(s_cu[q], s_cv[q], cross);
+        cx.bar();
+        // combine the per-CTA partial vectors in rank order, then the dot
+        // (block-local fixed-order reduction: identical in every CTA)
+        double part = 0.0;
+        for (int q = tid; q < rank; q += NT) {
+          double fu = 0.0, fv = 0.0;
+          for (int c = 0; c < CL; ++c) {
+            fu += cx.remote(s_cu + q, c);
+            fv += cx.remote(s_cv + q, c);
+          }
+          part = fma(fu, fv, part);
+        }
+        cross = cx.local_sum(part);
       }
       fro2 += u2 * v2 + 2.0 * cross;
-      __syncthreads();
+      cx.bar();
       if (tid == 0) {
         s_delta[rank] = delta;
         s_prow[rank] = static_cast<int>(pi);
         s_pcol[rank] = static_cast<int>(pj);
-        row_used[pi] = 1;
-        col_used[pj] = 1;
+        if (crank == 0) {
+          row_used[pi] = 1;
+          col_used[pj] = 1;
+        }
       }
       ++rank;
-      __syncthreads();
+      cx.bar();
       // next row pivot: argmax |u| over unused rows (lowrank.cpp:260-270)
       double best = -1.0;
       long long bi = -1;
-      for (int i = tid; i < m; i += NT)
+      for (int i = r0 + tid; i < r1; i += NT)
         if (!row_used[i]) argmax_combine(best, bi, fabs(Uc[i]), i);
-      red.argmax(best, bi);
+      cx.argmax(best, bi);
       suggested = bi;
     }
 
     if (local_flags) atomicOr(a.flags, local_flags);
     if (overflow) {
-      if (tid == 0) {
+      if (crank == 0 && tid == 0) {
         a.rank_out[p] = -1;
         atomicOr(a.flags, kFlagAcaOverflow);
       }
       continue;
     }
-    if (tid == 0) a.rank_out[p] = rank;
-    __syncthreads();
+    if (crank == 0 && tid == 0) a.rank_out[p] = rank;
+    cx.bar();
     if (a.W != nullptr && rank > 0) {
-      write_rows<NT>(U, a.ms, m, rank, a.W + a.wx[p], a.rx[p], s_tile);
-      write_rows<NT>(V, a.ns, n, rank, a.W + a.wy[p], a.ry[p], s_tile);
+      write_rows<NT>(U + r0, a.ms, r1 - r0, rank, a.W + a.wx[p] + static_cast<std::int64_t>(r0) * a.rx[p],
+                     a.rx[p], s_tile);
+      write_rows<NT>(V + c0, a.ns, c1 - c0, rank, a.W + a.wy[p] + static_cast<std::int64_t>(c0) * a.ry[p],
+                     a.ry[p], s_tile);
     }
-    if (a.lu != nullptr && rank > 0) {
+    if (a.lu != nullptr && rank > 0 && crank == 0) {
       // packed LU (lowrank.cpp:277-287): strict lower u_a(i_b)/delta_a,
       // upper delta_a * v_a(j_b); row-major r x r.
       const std::int64_t po = a.piv_off[p], lo = a.lu_off[p];
@@ -328,27 +419,23 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
   }
 }
 
-template <int NT>
-void launch_nt(const AcaArgs& a, int grid, cudaStream_t s) {
-  const std::size_t smem = aca_smem_bytes(NT, a.cap_ws);
-  switch (a.kernel) {
-    case kLaplace:
-      H3D_CUDA_CHECK(cudaFuncSetAttribute(aca_kernel<NT, kLaplace>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      aca_kernel<NT, kLaplace><<<grid, NT, smem, s>>>(a);
-      break;
-    case kR4:
-      H3D_CUDA_CHECK(cudaFuncSetAttribute(aca_kernel<NT, kR4>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      aca_kernel<NT, kR4><<<grid, NT, smem, s>>>(a);
-      break;
-    default:
-      H3D_CUDA_CHECK(cudaFuncSetAttribute(aca_kernel<NT, kHelmholtz>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      aca_kernel<NT, kHelmholtz><<<grid, NT, smem, s>>>(a);
-      break;
+template <int NT, bool CLU>
+const void* kernel_ptr(int kernel) {
+  switch (kernel) {
+    case kLaplace: return reinterpret_cast<const void*>(aca_kernel<NT, kLaplace, CLU>);
+    case kR4: return reinterpret_cast<const void*>(aca_kernel<NT, kR4, CLU>);
+    default: return reinterpret_cast<const void*>(aca_kernel<NT, kHelmholtz, CLU>);
   }
-  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+const void* kernel_for(int threads, int kernel, bool cluster) {
+  if (cluster) return threads >= 512 ? kernel_ptr<512, true>(kernel) : kernel_ptr<256, true>(kernel);
+  switch (threads) {
+    case 32: return kernel_ptr<32, false>(kernel);
+    case 128: return kernel_ptr<128, false>(kernel);
+    case 256: return kernel_ptr<256, false>(kernel);
+    default: return kernel_ptr<512, false>(kernel);
+  }
 }
 
 }  // namespace
@@ -360,18 +447,7 @@ std::size_t aca_smem_bytes(int /*threads*/, int cap_ws) {
 
 int aca_blocks_per_sm(int threads, int kernel, std::size_t smem) {
   int nb = 0;
-  const void* f = nullptr;
-#define H3D_F(NT)                                                                   \
-  f = kernel == kLaplace ? reinterpret_cast<const void*>(aca_kernel<NT, kLaplace>)  \
-      : kernel == kR4    ? reinterpret_cast<const void*>(aca_kernel<NT, kR4>)       \
-                         : reinterpret_cast<const void*>(aca_kernel<NT, kHelmholtz>);
-  switch (threads) {
-    case 32: H3D_F(32); break;
-    case 128: H3D_F(128); break;
-    case 256: H3D_F(256); break;
-    default: H3D_F(512); break;
-  }
-#undef H3D_F
+  const void* f = kernel_for(threads, kernel, false);
   H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
   H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, threads, smem));
@@ -379,12 +455,57 @@ int aca_blocks_per_sm(int threads, int kernel, std::size_t smem) {
 }
 
 void launch_aca(const AcaArgs& a, int threads, int grid, cudaStream_t s) {
-  switch (threads) {
-    case 32: launch_nt<32>(a, grid, s); break;
-    case 128: launch_nt<128>(a, grid, s); break;
-    case 256: launch_nt<256>(a, grid, s); break;
-    default: launch_nt<512>(a, grid, s); break;
-  }
+  const std::size_t smem = aca_smem_bytes(threads, a.cap_ws);
+  const void* f = kernel_for(threads, a.kernel, false);
+  H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+  void* args[] = {const_cast<AcaArgs*>(&a)};
+  H3D_CUDA_CHECK(cudaLaunchKernel(f, dim3(grid), dim3(threads), args, smem, s));
+}
+
+int aca_max_clusters(int threads, int kernel, int cluster, std::size_t smem) {
+  const void* f = kernel_for(threads, kernel, true);
+  H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+  if (cluster > 8)
+    H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster);
+  cfg.blockDim = dim3(threads >= 512 ? 512 : 256);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  H3D_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, f, &cfg));
+  return n;
+}
+
+void launch_aca_cluster(const AcaArgs& a, int threads, int cluster, int nclusters, cudaStream_t s) {
+  const std::size_t smem = aca_smem_bytes(threads, a.cap_ws);
+  const void* f = kernel_for(threads, a.kernel, true);
+  H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+  if (cluster > 8)
+    H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster * nclusters);
+  cfg.blockDim = dim3(threads >= 512 ? 512 : 256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = cluster;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  void* args[] = {const_cast<AcaArgs*>(&a)};
+  H3D_CUDA_CHECK(cudaLaunchKernelExC(&cfg, f, args));
 }
 
 }  // namespace h3db

@@ -147,9 +147,13 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   t = Clock::now();
   run_aca(true);
   ms_aca_write_ = ms_since(t);
-  if (n_segs_all_ > 0)
+  if (n_segs_all_ > 0) {
     launch_proxy_gather(segs_all_.get(), n_segs_all_, piv_.get(), px_.get(), py_.get(), pz_.get(),
                         qx_.get(), qy_.get(), qz_.get(), stream_);
+    int max_r = 0;
+    for (const auto& sg : plan_->proxy_segs) max_r = std::max(max_r, sg.r);
+    launch_lu_invert(segs_all_.get(), n_segs_all_, lu_.get(), max_r, stream_);
+  }
   near_scan();
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   ms_total_ = ms_since(t0);
@@ -341,10 +345,24 @@ void Engine::run_aca(bool write) {
       const std::int64_t slot_doubles =
           static_cast<std::int64_t>(cap_ws + 1) * (ms + ns) + (ms + ns + 7) / 8 + 2;
       const std::size_t smem = aca_smem_bytes(P.threads, cap_ws);
-      const int bps = aca_blocks_per_sm(P.threads, opt_.kernel_id, smem);
+      // few huge blocks (top levels): one thread-block cluster per pair so the
+      // whole GPU works on them; fixed per level for rank/write determinism
+      if (P.cluster == 0) {
+        int cl = 1;
+        if (P.threads >= 256 && np * 4 <= sms_) {
+          cl = 2;
+          while (cl < 16 && np * cl * 2 <= sms_) cl <<= 1;
+        }
+        P.cluster = cl;
+      }
+      const int bps = P.cluster > 1 ? 1 : aca_blocks_per_sm(P.threads, opt_.kernel_id, smem);
       const std::int64_t budget = std::max<std::int64_t>(
           std::min<std::int64_t>(static_cast<std::int64_t>(free_b / 4), 24LL << 30), 256LL << 20);
-      std::int64_t slots = std::min<std::int64_t>(np, static_cast<std::int64_t>(bps) * sms_);
+      std::int64_t slots =
+          P.cluster > 1
+              ? std::min<std::int64_t>(np, std::max(1, aca_max_clusters(P.threads, opt_.kernel_id,
+                                                                        P.cluster, smem)))
+              : std::min<std::int64_t>(np, static_cast<std::int64_t>(bps) * sms_);
       slots = std::min<std::int64_t>(slots, std::max<std::int64_t>(1, budget / (slot_doubles * 8)));
       DevBuf<double> ws;
       ws.alloc(static_cast<std::size_t>(slots * slot_doubles));
@@ -384,7 +402,10 @@ void Engine::run_aca(bool write) {
       }
       a.flags = flags_.get();
       a.counter = counter.get();
-      launch_aca(a, P.threads, static_cast<int>(slots), stream_);
+      if (P.cluster > 1)
+        launch_aca_cluster(a, P.threads, P.cluster, static_cast<int>(slots), stream_);
+      else
+        launch_aca(a, P.threads, static_cast<int>(slots), stream_);
       unsigned f = 0;
       H3D_CUDA_CHECK(cudaMemcpyAsync(&f, flags_.get(), 4, cudaMemcpyDeviceToHost, stream_));
       H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));

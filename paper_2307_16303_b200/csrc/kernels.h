@@ -86,6 +86,9 @@ struct AcaArgs {
 void launch_aca(const AcaArgs& a, int threads, int grid, cudaStream_t s);
 std::size_t aca_smem_bytes(int threads, int cap_ws);
 int aca_blocks_per_sm(int threads, int kernel, std::size_t smem);
+// cluster tier (one pair per cluster of `cluster` CTAs, DSMEM reductions)
+int aca_max_clusters(int threads, int kernel, int cluster, std::size_t smem);
+void launch_aca_cluster(const AcaArgs& a, int threads, int cluster, int nclusters, cudaStream_t s);
 
 // -------------------------------------------------------------- matvec.cu
 void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp,
@@ -123,6 +126,9 @@ void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int
                          double* qy, double* qz, cudaStream_t s);
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, double* S,
                         cudaStream_t s);
+// build time: replace every pair's packed LU by G = (L R)^-1 (row-major)
+void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, int max_r,
+                      cudaStream_t s);
 
 struct Phase2Args {
   int depth = 0;

@@ -206,10 +206,44 @@ __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int6
   }
 }
 
-// In-place triangular solves on S segments, one warp per ordered proxy block:
-//   side 0 (target = row side X):  s = R^-1 L^-1 v        (lowrank.cpp:310-320)
-//   side 1 (target = col side Y):  s = L^-T R^-T v        (the transposed block)
-// LU packed row-major: strict lower = unit-lower L, upper incl. diagonal = R.
+// Explicit inverse of the packed pivot LU, G = (L R)^-1 = R^-1 L^-1, in place
+// (build time; one thread per column, LU entries read as broadcasts). The
+// matvec then applies the reference's two triangular solves
+// (lowrank.cpp:310-320) as one coalesced GEMV per ordered block.
+__global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
+                                 double* __restrict__ lu, double* __restrict__ scratch,
+                                 int max_r) {
+  const std::int64_t s = blockIdx.x;
+  if (s >= nseg) return;
+  const ProxySeg sg = segs[s];
+  if (sg.side != 0) return;  // each pair appears once with side 0 per owning shard
+  const int r = sg.r;
+  double* A = lu + sg.lu_off;
+  double* Gs = scratch + static_cast<std::int64_t>(blockIdx.x) * max_r * max_r;  // column-major
+  for (int c = threadIdx.x; c < r; c += blockDim.x) {
+    double* g = Gs + static_cast<std::int64_t>(c) * max_r;
+    // L y = e_c (unit lower): y_a = [a == c] - sum_{b<a} L[a][b] y_b
+    for (int q = 0; q < r; ++q) {
+      double acc = q == c ? 1.0 : 0.0;
+      for (int b = c; b < q; ++b) acc = fma(-A[static_cast<std::int64_t>(q) * r + b], g[b], acc);
+      g[q] = q < c ? 0.0 : acc;
+    }
+    // R g = y (upper): g_a = (y_a - sum_{b>a} R[a][b] g_b) / R[a][a]
+    for (int q = r - 1; q >= 0; --q) {
+      double acc = g[q];
+      for (int b = q + 1; b < r; ++b) acc = fma(-A[static_cast<std::int64_t>(q) * r + b], g[b], acc);
+      g[q] = acc / A[static_cast<std::int64_t>(q) * r + q];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // row-major G over the LU slot
+    const int row = e / r, col = e % r;
+    A[e] = Gs[static_cast<std::int64_t>(col) * max_r + row];
+  }
+}
+
+// Per ordered proxy block (one warp): s = G v (target is the pair's row side,
+// = R^-1 L^-1 v) or s = G^T v (column side, = L^-T R^-T v), in place on S.
 __global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
                                    const double* __restrict__ lu, double* __restrict__ S) {
   extern __shared__ double sh[];
@@ -222,39 +256,34 @@ __global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64
   double* Sg = S + sg.so;
   for (int q = lane; q < r; q += 32) v[q] = Sg[q];
   __syncwarp();
-  const double* A = lu + sg.lu_off;
+  const double* G = lu + sg.lu_off;
   if (sg.side == 0) {
-    for (int q = 0; q < r; ++q) {  // L (unit lower): v_b -= L[b][q] v_q
-      const double vq = v[q];
-      __syncwarp();
-      for (int b = q + 1 + lane; b < r; b += 32)
-        v[b] = fma(-A[static_cast<std::int64_t>(b) * r + q], vq, v[b]);
-      __syncwarp();
-    }
-    for (int q = r - 1; q >= 0; --q) {  // R (upper): s_q = v_q / R[q][q]; v_b -= R[b][q] s_q
-      const double sq = v[q] / A[static_cast<std::int64_t>(q) * r + q];
-      __syncwarp();
-      if (lane == 0) v[q] = sq;
-      for (int b = lane; b < q; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(b) * r + q], sq, v[b]);
-      __syncwarp();
+    for (int q = 0; q < r; ++q) {  // row q of G, lanes over columns
+      const double* row = G + static_cast<std::int64_t>(q) * r;
+      double acc = 0.0;
+      for (int b = lane; b < r; b += 32) acc = fma(row[b], v[b], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) Sg[q] = acc;
     }
   } else {
-    for (int q = 0; q < r; ++q) {  // R^T (lower): w_q = v_q / R[q][q]; v_b -= R[q][b] w_q
-      const double wq = v[q] / A[static_cast<std::int64_t>(q) * r + q];
-      __syncwarp();
-      if (lane == 0) v[q] = wq;
-      for (int b = q + 1 + lane; b < r; b += 32)
-        v[b] = fma(-A[static_cast<std::int64_t>(q) * r + b], wq, v[b]);
-      __syncwarp();
+    double acc[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) acc[k] = 0.0;
+    for (int b = 0; b < r; ++b) {  // row b of G scaled by v_b, lanes over columns
+      const double vb = v[b];
+      const double* row = G + static_cast<std::int64_t>(b) * r;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const int q = lane + 32 * k;
+        if (q < r) acc[k] = fma(row[q], vb, acc[k]);
+      }
     }
-    for (int q = r - 1; q >= 0; --q) {  // L^T (unit upper): v_b -= L[q][b] v_q
-      const double vq = v[q];
-      __syncwarp();
-      for (int b = lane; b < q; b += 32) v[b] = fma(-A[static_cast<std::int64_t>(q) * r + b], vq, v[b]);
-      __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const int q = lane + 32 * k;
+      if (q < r) Sg[q] = acc[k];
     }
   }
-  for (int q = lane; q < r; q += 32) Sg[q] = v[q];
 }
 
 // ---- phase 2, compute part --------------------------------------------------
@@ -352,13 +381,8 @@ __device__ void compute_pass(const Phase2Args& a, const TileRanges& tr, double2*
     __syncthreads();
     if (any) {
       int j = slice * 32 + lane;
-      for (; j + step < cnt; j += 2 * step) {
-        const double2 s0 = stage[2 * j], s1 = stage[2 * j + 1];
-        const double2 u0 = stage[2 * (j + step)], u1 = stage[2 * (j + step) + 1];
-        eval4<K>(tx, ty, tz, acc, s0, s1);
-        eval4<K>(tx, ty, tz, acc, u0, u1);
-      }
-      if (j < cnt) eval4<K>(tx, ty, tz, acc, stage[2 * j], stage[2 * j + 1]);
+#pragma unroll 1
+      for (; j < cnt; j += step) eval4<K>(tx, ty, tz, acc, stage[2 * j], stage[2 * j + 1]);
     }
   }
 #pragma unroll
@@ -377,7 +401,7 @@ __device__ void compute_pass(const Phase2Args& a, const TileRanges& tr, double2*
 
 // Persistent CTAs pull leaf tiles from a work counter (dynamic balance).
 template <int K, bool STORED>
-__global__ void __launch_bounds__(kThreads, 2) p2_compute_kernel(const Phase2Args a) {
+__global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Args a) {
   __shared__ TileRanges tr;
   __shared__ double cpart[kWarps * 32 + 32];
   __shared__ double2 stage[2 * kStage];
@@ -609,6 +633,22 @@ void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int
   proxy_gather_kernel<<<static_cast<unsigned>((nseg + 7) / 8), block, 0, s>>>(segs, nseg, piv, px, py,
                                                                             pz, qx, qy, qz);
   H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, int max_r,
+                      cudaStream_t s) {
+  if (nseg == 0 || max_r == 0) return;
+  // scratch for a batch of column-major inverses
+  const std::int64_t batch = std::max<std::int64_t>(1, std::min<std::int64_t>(
+      nseg, (std::int64_t(1) << 29) / (static_cast<std::int64_t>(max_r) * max_r * 8)));
+  double* scratch = nullptr;
+  H3D_CUDA_CHECK(cudaMallocAsync(&scratch, batch * max_r * max_r * 8, s));
+  for (std::int64_t b0 = 0; b0 < nseg; b0 += batch) {
+    const std::int64_t nb = std::min(batch, nseg - b0);
+    lu_invert_kernel<<<static_cast<unsigned>(nb), 128, 0, s>>>(segs + b0, nb, lu, scratch, max_r);
+    H3D_CUDA_CHECK(cudaGetLastError());
+  }
+  H3D_CUDA_CHECK(cudaFreeAsync(scratch, s));
 }
 
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, double* S,

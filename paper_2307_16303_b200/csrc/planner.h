@@ -32,6 +32,7 @@ struct LevelPairs {
   std::vector<std::int32_t> rank;
   std::vector<std::int32_t> eX, eY;  // inter-list entry of Y in X's list / X in Y's list
   int threads = 32;                  // ACA CTA size (fixed per level: determinism)
+  int cluster = 0;                   // ACA CTAs per pair (0 = not chosen yet)
   int max_m = 0, max_n = 0, max_mn = 0;
 };
 
