@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
     if (crank == 0 && tid == 0) s_pair = static_cast<long long>(atomicAdd(a.counter, 1ULL));
     cx.bar();
     const long long p = cx.remote(&s_pair, 0);
+    cx.bar();  // no CTA may exit while a peer still reads its shared memory
     if (p >= a.npairs) break;
 
     const std::int64_t xb = a.xb[p], yb = a.yb[p];

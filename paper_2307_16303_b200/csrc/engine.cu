@@ -629,7 +629,9 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   const Planner& P = *plan_;
   std::int64_t launches = 0;
   if (ev) cudaEventRecord(ev[0], s);
-  if (world_ == 1) {
+  if (world_ == 1 || nccl_comm_ == nullptr) {
+    // single GPU, or a shard without a communicator: x is replicated (every
+    // rank holds all of it), gather it all locally
     launch_gather(xin, perm_.get(), n_, xp_.get(), s);
     ++launches;
   } else {
@@ -720,8 +722,6 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
 
 void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
-  if (world_ > 1 && nccl_comm_ == nullptr)
-    throw InvalidArgument("matvec: sharded engine needs h3d_dev_attach_nccl first");
   cudaEventRecord(ev_[0], stream_);
   const double* xin = x;
   if (host) {
@@ -753,8 +753,6 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
 
 void Engine::matvec_async(const double* x, double* b, cudaStream_t s) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
-  if (world_ > 1 && nccl_comm_ == nullptr)
-    throw InvalidArgument("matvec: sharded engine needs h3d_dev_attach_nccl first");
   cudaEvent_t* ev = nullptr;
   if (prof_on_) {
     if (prof_used_ >= prof_ev_.size() / 4) throw InvalidArgument("profile ring full; read it first");
