@@ -206,10 +206,12 @@ __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int6
   }
 }
 
-// Explicit inverse of the packed pivot LU, G = (L R)^-1 = R^-1 L^-1, in place
-// (build time; one thread per column, LU entries read as broadcasts). The
-// matvec then applies the reference's two triangular solves
-// (lowrank.cpp:310-320) as one coalesced GEMV per ordered block.
+// Triangular inverses of the packed pivot LU, in place (build time; one thread
+// per column): strict lower <- L^-1 (unit diagonal implied), upper incl.
+// diagonal <- R^-1. Applying L^-1 and R^-1 as two GEMVs is as accurate as the
+// reference's forward/backward substitution (lowrank.cpp:310-320) on these
+// ill-conditioned pivot blocks (cond ~ 1e12 at eps 1e-10), unlike forming
+// (L R)^-1, and turns the sequential solves into coalesced, parallel GEMVs.
 __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
                                  double* __restrict__ lu, double* __restrict__ scratch,
                                  int max_r) {
@@ -222,28 +224,31 @@ __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t
   double* Gs = scratch + static_cast<std::int64_t>(blockIdx.x) * max_r * max_r;  // column-major
   for (int c = threadIdx.x; c < r; c += blockDim.x) {
     double* g = Gs + static_cast<std::int64_t>(c) * max_r;
-    // L y = e_c (unit lower): y_a = [a == c] - sum_{b<a} L[a][b] y_b
-    for (int q = 0; q < r; ++q) {
-      double acc = q == c ? 1.0 : 0.0;
-      for (int b = c; b < q; ++b) acc = fma(-A[static_cast<std::int64_t>(q) * r + b], g[b], acc);
-      g[q] = q < c ? 0.0 : acc;
+    // column c of L^-1 (entries q > c; the diagonal 1 is implicit)
+    for (int q = c + 1; q < r; ++q) {
+      double acc = -A[static_cast<std::int64_t>(q) * r + c];
+      for (int b = c + 1; b < q; ++b) acc = fma(-A[static_cast<std::int64_t>(q) * r + b], g[b], acc);
+      g[q] = acc;
     }
-    // R g = y (upper): g_a = (y_a - sum_{b>a} R[a][b] g_b) / R[a][a]
-    for (int q = r - 1; q >= 0; --q) {
-      double acc = g[q];
-      for (int b = q + 1; b < r; ++b) acc = fma(-A[static_cast<std::int64_t>(q) * r + b], g[b], acc);
+    // column c of R^-1 (entries q <= c)
+    g[c] = 1.0 / A[static_cast<std::int64_t>(c) * r + c];
+    for (int q = c - 1; q >= 0; --q) {
+      double acc = 0.0;
+      for (int b = q + 1; b <= c; ++b) acc = fma(-A[static_cast<std::int64_t>(q) * r + b], g[b], acc);
       g[q] = acc / A[static_cast<std::int64_t>(q) * r + q];
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // row-major G over the LU slot
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // row-major over the LU slot
     const int row = e / r, col = e % r;
     A[e] = Gs[static_cast<std::int64_t>(col) * max_r + row];
   }
 }
 
-// Per ordered proxy block (one warp): s = G v (target is the pair's row side,
-// = R^-1 L^-1 v) or s = G^T v (column side, = L^-T R^-T v), in place on S.
+// Per ordered proxy block (one warp), in place on S, with P the packed
+// inverses (strict lower L^-1, upper R^-1):
+//   side 0 (target = pair's row side X):  s = R^-1 (L^-1 v)       (lowrank.cpp:310-320)
+//   side 1 (target = pair's col side Y):  s = L^-T (R^-T v)       (the transposed block)
 __global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
                                    const double* __restrict__ lu, double* __restrict__ S) {
   extern __shared__ double sh[];
@@ -252,36 +257,60 @@ __global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64
   if (s >= nseg) return;
   const ProxySeg sg = segs[s];
   const int r = sg.r;
-  double* v = sh + warp * 320;  // r <= 320 (enforced on the host)
+  double* v = sh + warp * 640;  // v and w, r <= 320 (enforced on the host)
+  double* w = v + 320;
   double* Sg = S + sg.so;
   for (int q = lane; q < r; q += 32) v[q] = Sg[q];
   __syncwarp();
-  const double* G = lu + sg.lu_off;
+  const double* P = lu + sg.lu_off;
   if (sg.side == 0) {
-    for (int q = 0; q < r; ++q) {  // row q of G, lanes over columns
-      const double* row = G + static_cast<std::int64_t>(q) * r;
+    for (int i = 0; i < r; ++i) {  // w = L^-1 v: w_i = v_i + sum_{j<i} P[i][j] v_j
+      const double* row = P + static_cast<std::int64_t>(i) * r;
       double acc = 0.0;
-      for (int b = lane; b < r; b += 32) acc = fma(row[b], v[b], acc);
+      for (int j = lane; j < i; j += 32) acc = fma(row[j], v[j], acc);
       acc = warp_sum(acc);
-      if (lane == 0) Sg[q] = acc;
+      if (lane == 0) w[i] = v[i] + acc;
+    }
+    __syncwarp();
+    for (int i = 0; i < r; ++i) {  // s = R^-1 w: s_i = sum_{j>=i} P[i][j] w_j
+      const double* row = P + static_cast<std::int64_t>(i) * r;
+      double acc = 0.0;
+      for (int j = i + lane; j < r; j += 32) acc = fma(row[j], w[j], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) Sg[i] = acc;
     }
   } else {
     double acc[10];
 #pragma unroll
     for (int k = 0; k < 10; ++k) acc[k] = 0.0;
-    for (int b = 0; b < r; ++b) {  // row b of G scaled by v_b, lanes over columns
-      const double vb = v[b];
-      const double* row = G + static_cast<std::int64_t>(b) * r;
+    for (int i = 0; i < r; ++i) {  // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i
+      const double vi = v[i];
+      const double* row = P + static_cast<std::int64_t>(i) * r;
 #pragma unroll
       for (int k = 0; k < 10; ++k) {
-        const int q = lane + 32 * k;
-        if (q < r) acc[k] = fma(row[q], vb, acc[k]);
+        const int j = lane + 32 * k;
+        if (j >= i && j < r) acc[k] = fma(row[j], vi, acc[k]);
       }
     }
 #pragma unroll
     for (int k = 0; k < 10; ++k) {
-      const int q = lane + 32 * k;
-      if (q < r) Sg[q] = acc[k];
+      const int j = lane + 32 * k;
+      if (j < r) w[j] = acc[k];
+    }
+    __syncwarp();
+    for (int i = 0; i < r; ++i) {  // s = L^-T u: s_j = u_j + sum_{i>j} P[i][j] u_i
+      const double ui = w[i];
+      const double* row = P + static_cast<std::int64_t>(i) * r;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const int j = lane + 32 * k;
+        if (j < i) acc[k] = fma(row[j], ui, acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const int j = lane + 32 * k;
+      if (j < r) Sg[j] = acc[k];
     }
   }
 }
@@ -656,7 +685,7 @@ void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* l
   if (nseg == 0) return;
   constexpr int warps = 4;
   proxy_solve_kernel<<<static_cast<unsigned>((nseg + warps - 1) / warps), 32 * warps,
-                       warps * 320 * sizeof(double), s>>>(segs, nseg, lu, S);
+                       warps * 640 * sizeof(double), s>>>(segs, nseg, lu, S);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
