@@ -85,6 +85,7 @@ template class DevBuf<unsigned long long>;
 template class DevBuf<P1Item>;
 template class DevBuf<P1Reduce>;
 template class DevBuf<ProxySeg>;
+template class DevBuf<P2Item>;
 
 Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_(opt), n_(n) {
   const auto t0 = Clock::now();
@@ -557,11 +558,17 @@ void Engine::upload_plan() {
   has_stream_levels_ = false;
   for (int l = 1; l <= L_; ++l)
     if (P.mode(l) == kModeStream && !P.pairs(l).X.empty()) has_stream_levels_ = true;
-  if (has_stream_levels_) {
-    cpart_.alloc(n_);
-    spart_.alloc(n_);
+  p2_items_.upload(P.p2_items, stream_);
+  n_p2_ = static_cast<std::int64_t>(P.p2_items.size());
+  n_lvl_ = P.n_proxy_levels;
+  if (has_stream_levels_) spart_.alloc(n_);
+  if (has_stream_levels_ || n_p2_ > 0) cpart_.alloc(n_);
+  if (n_p2_ > 0) {
+    // rows of nodes without partners at a proxy level are never written
+    lvl_part_.alloc(static_cast<std::size_t>(n_lvl_) * n_);
+    H3D_CUDA_CHECK(cudaMemsetAsync(lvl_part_.get(), 0, sizeof(double) * n_lvl_ * n_, stream_));
   }
-  counters_.alloc(4);
+  counters_.alloc(5);
   if (opt_.near_mode == H3D_NEAR_STORED) {
     nf_off_.upload(P.nf_off, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
@@ -600,10 +607,14 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.kernel = opt_.kernel_id;
   a.diag = opt_.diagonal;
   a.b = bout;
-  if (has_stream_levels_) {
-    a.spart = spart_.get();
-    a.cpart_out = cpart_.get();
+  if (has_stream_levels_) a.spart = spart_.get();
+  if (has_stream_levels_ || n_p2_ > 0) a.cpart_out = cpart_.get();
+  if (n_p2_ > 0) {
+    a.p2_items = p2_items_.get();
+    a.n_p2_items = n_p2_;
+    a.lvl_part = lvl_part_.get();
   }
+  a.n_total = n_;
   for (int l = 0; l <= L_ && l < 24; ++l) {
     a.lbase[l] = P.node_base()[l];
     a.mode[l] = P.mode(l);
@@ -668,7 +679,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   a1.qy = qy_.get();
   a1.qz = qz_.get();
   const bool both1 = n_p1s_ > 0 && n_p1p_ > 0;
-  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 4 * sizeof(unsigned), s));
+  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 5 * sizeof(unsigned), s));
   if (both1) {
     H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[0], 0));
@@ -702,17 +713,25 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     Phase2Args a2 = phase2_args(bout);
     a2.counter = counters_.get() + 2;
     a2.counter2 = counters_.get() + 3;
+    a2.counter3 = counters_.get() + 4;
     if (has_stream_levels_) {
       H3D_CUDA_CHECK(cudaEventRecord(fork_[1], s));
       H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[1], 0));
       launch_p2_compute(a2, sms_, 2, stream2_);
+      launch_p2_proxy(a2, sms_, 2, stream2_);
       launch_p2_stream(a2, sms_, 2, s);
       H3D_CUDA_CHECK(cudaEventRecord(join_[1], stream2_));
       H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
-      launch_combine(cpart_.get(), spart_.get(), perm_.get(), P.row0, P.row1, bout, s);
-      launches += 3;
+      launches += 2 + (n_p2_ > 0);
     } else {
       launch_p2_compute(a2, sms_, 4, s);
+      launch_p2_proxy(a2, sms_, 4, s);
+      launches += 1 + (n_p2_ > 0);
+    }
+    if (has_stream_levels_ || n_p2_ > 0) {
+      launch_combine(cpart_.get(), has_stream_levels_ ? spart_.get() : nullptr,
+                     n_p2_ > 0 ? lvl_part_.get() : nullptr, n_p2_ > 0 ? n_lvl_ : 0, n_,
+                     perm_.get(), P.row0, P.row1, bout, s);
       ++launches;
     }
   }

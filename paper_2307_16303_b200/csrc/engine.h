@@ -117,7 +117,11 @@ class Engine {
   bool has_stream_levels_ = false;
   DevBuf<std::int32_t> near_off_, near_ids_, near_dense_;
   DevBuf<double> cpart_, spart_;
-  DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream]
+  DevBuf<P2Item> p2_items_;
+  std::int64_t n_p2_ = 0;
+  int n_lvl_ = 0;
+  DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 proxy partials
+  DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy]
   cudaStream_t stream2_ = nullptr;          // concurrent HBM / FP64 kernels
   cudaEvent_t fork_[2] = {}, join_[2] = {};  // per phase
   DevBuf<std::int64_t> nf_off_;

@@ -158,10 +158,20 @@ struct Phase2Args {
   int mode[24] = {0};            // LevelMode per level
   unsigned* counter = nullptr;   // p2_compute work counter (zeroed before the launch)
   unsigned* counter2 = nullptr;  // p2_stream work counter
+  // node-major proxy pass (thread = target row): when set, p2_compute skips
+  // the proxy ranges and p2_proxy writes one partial per proxy level
+  const P2Item* p2_items = nullptr;
+  std::int64_t n_p2_items = 0;
+  double* lvl_part = nullptr;  // [n_proxy_levels x N] (Morton order)
+  std::int64_t n_total = 0;    // N
+  unsigned* counter3 = nullptr;
 };
 void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
-void launch_combine(const double* cpart, const double* spart, const std::int32_t* perm,
+void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
+// b[perm[p]] = cpart[p] + spart[p] (if any) + sum over proxy levels of lvl_part
+void launch_combine(const double* cpart, const double* spart, const double* lvl_part,
+                    int n_lvl, std::int64_t n_total, const std::int32_t* perm,
                     std::int64_t row0, std::int64_t row1, double* b, cudaStream_t s);
 
 // Build-time near-field scan: coincidence check (and optional store).

@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
         ++n;
       }
       for (int l = 1; l <= L && n < kMaxRanges; ++l) {
-        if (a.mode[l] != 1) continue;
+        if (a.mode[l] != 1 || a.p2_items != nullptr) continue;
         const std::int64_t g = a.lbase[l] + (X >> (3 * (L - l)));
         const int R = a.nt.rpad[g];
         if (R == 0) continue;
@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
               v = fma(nf[static_cast<std::int64_t>(c) * mrows + r0 + i], a.xp[yb + j], v);
           }
         }
-        if (a.spart) a.cpart_out[xb + r0 + i] = v;
+        if (a.cpart_out) a.cpart_out[xb + r0 + i] = v;
         else a.b[a.perm[xb + r0 + i]] = v;
       }
       __syncthreads();
@@ -556,11 +556,64 @@ __global__ void __launch_bounds__(kThreads, 2) p2_stream_kernel(const Phase2Args
   }
 }
 
+// ---- phase 2, proxy levels, node-major: b_X += K(X, P_A) s_A for the rows of
+// node A, thread = target row, proxy sources staged in shared memory (the
+// phase-1 proxy layout, which keeps the FP64 pipe ~80% busy).
+template <int K>
+__global__ void __launch_bounds__(kThreads, 2) p2_proxy_kernel(const Phase2Args a) {
+  __shared__ double2 src[2 * kChunk];
+  __shared__ long long s_k;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_k = static_cast<long long>(atomicAdd(a.counter3, 1u));
+    __syncthreads();
+    const long long k = s_k;
+    if (k >= a.n_p2_items) break;
+    const P2Item it = a.p2_items[k];
+    const std::int64_t g = it.node;
+    const std::int64_t so = a.nt.soff[g];
+    const int R = a.nt.rpad[g];
+    const int i = threadIdx.x;
+    const bool active = i < it.nrows;
+    const std::int64_t p = a.nt.rowbeg[g] + it.row0 + i;
+    const double tx = active ? a.px[p] : kFar, ty = active ? a.py[p] : kFar,
+                 tz = active ? a.pz[p] : kFar;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int j0 = 0; j0 < R; j0 += kChunk) {
+      const int nj = min(kChunk, R - j0);
+      __syncthreads();
+      if (threadIdx.x < nj) {
+        const std::int64_t q = so + j0 + threadIdx.x;
+        src[2 * threadIdx.x] = make_double2(a.qx[q], a.qy[q]);
+        src[2 * threadIdx.x + 1] = make_double2(a.qz[q], a.S[q]);
+      }
+      __syncthreads();
+      int j = 0;
+      for (; j + 1 < nj; j += 2) {
+        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
+        const double2 u0 = src[2 * j + 2], u1 = src[2 * j + 3];
+        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
+        acc1 = fma(kernel_r2_fast<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x)), u1.y, acc1);
+      }
+      if (j < nj) {
+        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
+        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
+      }
+    }
+    if (active) a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + p] = acc0 + acc1;
+  }
+}
+
 __global__ void combine_kernel(const double* __restrict__ cpart, const double* __restrict__ spart,
+                               const double* __restrict__ lvl, int n_lvl, std::int64_t n_total,
                                const std::int32_t* __restrict__ perm, std::int64_t row0,
                                std::int64_t row1, double* __restrict__ b) {
   const std::int64_t p = row0 + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  if (p < row1) b[perm[p]] = cpart[p] + spart[p];
+  if (p >= row1) return;
+  double v = cpart[p];
+  for (int l = 0; l < n_lvl; ++l) v += lvl[static_cast<std::int64_t>(l) * n_total + p];
+  if (spart) v += spart[p];
+  b[perm[p]] = v;
 }
 
 // Build-time pass over every dense near-field pair: the reference forms all
@@ -716,11 +769,34 @@ void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) 
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_combine(const double* cpart, const double* spart, const std::int32_t* perm,
+void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
+  if (a.n_p2_items == 0) return;
+  switch (a.kernel) {
+    case kLaplace: {
+      const int grid = grid_for(p2_proxy_kernel<kLaplace>, sms, per_sm, a.n_p2_items);
+      p2_proxy_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+    case kR4: {
+      const int grid = grid_for(p2_proxy_kernel<kR4>, sms, per_sm, a.n_p2_items);
+      p2_proxy_kernel<kR4><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+    default: {
+      const int grid = grid_for(p2_proxy_kernel<kHelmholtz>, sms, per_sm, a.n_p2_items);
+      p2_proxy_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+  }
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_combine(const double* cpart, const double* spart, const double* lvl_part,
+                    int n_lvl, std::int64_t n_total, const std::int32_t* perm,
                     std::int64_t row0, std::int64_t row1, double* b, cudaStream_t s) {
   if (row1 <= row0) return;
-  combine_kernel<<<static_cast<unsigned>((row1 - row0 + 255) / 256), 256, 0, s>>>(cpart, spart, perm,
-                                                                                 row0, row1, b);
+  combine_kernel<<<static_cast<unsigned>((row1 - row0 + 255) / 256), 256, 0, s>>>(
+      cpart, spart, lvl_part, n_lvl, n_total, perm, row0, row1, b);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -299,6 +299,25 @@ void Planner::layout() {
   }
   S.p_doubles = ptot;
 
+  // phase-2 proxy items (node-major, thread = target row): b_X += K(X, P_A) s_A
+  // for every owned node A of a proxy level, rows in chunks of 256
+  p2_items.clear();
+  n_proxy_levels = 0;
+  for (int l = 1; l <= L_; ++l) {
+    if (mode_[l] != kModeProxy) continue;
+    const int slot = n_proxy_levels++;
+    const std::int64_t cnt = 1LL << (3 * l);
+    for (std::int64_t z = 0; z < cnt; ++z) {
+      const std::int64_t g = gid(l, z);
+      if (rpad[g] == 0 || !owned(l, z)) continue;
+      const std::int64_t nr = node_size(l, z);
+      for (std::int64_t r0 = 0; r0 < nr; r0 += kColChunk)
+        p2_items.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
+                                  static_cast<std::int32_t>(std::min<std::int64_t>(kColChunk, nr - r0)),
+                                  slot});
+    }
+  }
+
   // leaf plan: owned leaves; near lists = self, near_edge, near_face (the
   // reference's dense blocks), plus the leaf-level admissible partners when
   // that level is evaluated directly

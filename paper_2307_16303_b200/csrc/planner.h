@@ -47,6 +47,15 @@ struct P1Item {
   std::int64_t pslot;  // -1: write to S through spos; else partial buffer base
 };
 
+// phase-2 proxy item: targets = rows [row0, row0 + nrows) of node `node`
+// (<= 256), sources = the node's proxy list; output slot = proxy-level index
+struct P2Item {
+  std::int32_t node;
+  std::int32_t row0;
+  std::int32_t nrows;
+  std::int32_t slot;
+};
+
 struct P1Reduce {
   std::int32_t node;
   std::int32_t ncols;
@@ -119,6 +128,8 @@ class Planner {
   std::vector<ProxySeg> proxy_segs;
   std::vector<P1Item> items;
   std::vector<P1Reduce> reds;
+  std::vector<P2Item> p2_items;   // owned nodes of proxy levels, <= 256 rows each
+  int n_proxy_levels = 0;         // output slots of the phase-2 proxy kernel
   std::int64_t leaf0 = 0, leaf1 = 0;
   std::vector<std::int32_t> near_off, near_ids;
   std::vector<std::int32_t> near_dense;  // per leaf: leading dense entries (self, edge, face)
