@@ -146,10 +146,12 @@ __device__ __forceinline__ void tbar() {
 }
 
 // Transpose a column-major (rows x r, column stride ld) workspace matrix into
-// row-major W rows (row stride rs) through a 32 x 33 shared tile.
+// the node's tile-major factor pool (planner.h: kTileRows x kTileCols tiles,
+// nct column tiles per tile row): element (i, q) lands at node row row0 + i,
+// node column col0 + q. Staged through a 32 x 33 shared tile.
 template <int NT>
 __device__ void write_rows(const double* __restrict__ src, int ld, int rows, int r,
-                           double* __restrict__ dst, int rs, double* tile) {
+                           double* __restrict__ Wn, int row0, int col0, int nct, double* tile) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i0 = 0; i0 < rows; i0 += 32) {
@@ -161,7 +163,7 @@ __device__ void write_rows(const double* __restrict__ src, int ld, int rows, int
       tbar<NT>();
       for (int il = w; il < 32; il += NW) {
         const int i = i0 + il, q = a0 + lane;
-        if (i < rows && q < r) dst[static_cast<std::int64_t>(i) * rs + q] = tile[lane * 33 + il];
+        if (i < rows && q < r) Wn[tile_index(row0 + i, col0 + q, nct)] = tile[lane * 33 + il];
       }
       tbar<NT>();
     }
@@ -396,10 +398,8 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
     if (crank == 0 && tid == 0) a.rank_out[p] = rank;
     cx.bar();
     if (a.W != nullptr && rank > 0) {
-      write_rows<NT>(U + r0, a.ms, r1 - r0, rank, a.W + a.wx[p] + static_cast<std::int64_t>(r0) * a.rx[p],
-                     a.rx[p], s_tile);
-      write_rows<NT>(V + c0, a.ns, c1 - c0, rank, a.W + a.wy[p] + static_cast<std::int64_t>(c0) * a.ry[p],
-                     a.ry[p], s_tile);
+      write_rows<NT>(U + r0, a.ms, r1 - r0, rank, a.W + a.wx[p], r0, a.cx[p], a.rx[p], s_tile);
+      write_rows<NT>(V + c0, a.ns, c1 - c0, rank, a.W + a.wy[p], c0, a.cy[p], a.ry[p], s_tile);
     }
     if (a.lu != nullptr && rank > 0 && crank == 0) {
       // packed LU (lowrank.cpp:277-287): strict lower u_a(i_b)/delta_a,

@@ -265,6 +265,10 @@ int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, in
     else if (nm == "pair_wy") put(P.pair_wy.at(level), out, count);
     else if (nm == "pair_rx") put(P.pair_rx.at(level), out, count);
     else if (nm == "pair_ry") put(P.pair_ry.at(level), out, count);
+    else if (nm == "pair_cx") put(P.pair_cx.at(level), out, count);
+    else if (nm == "pair_cy") put(P.pair_cy.at(level), out, count);
+    else if (nm == "p2_items") put(P.p2_items, out, count);
+    else if (nm == "p2s_items") put(P.p2s_items, out, count);
     else if (nm == "pair_piv") put(P.pair_piv.at(level), out, count);
     else if (nm == "pair_lu") put(P.pair_lu.at(level), out, count);
     else if (nm == "proxy_segs") put(P.proxy_segs, out, count);

@@ -52,6 +52,36 @@ __device__ __forceinline__ double rsqrt_c3(double x) {
   return fma(y, e * c, y);
 }
 
+// Admissible-block evaluations (proxy regeneration, direct leaf blocks):
+// one Newton step from the same seed, with the factor -1/2 folded out of the
+// sum:  1/sqrt(x) ~= -0.5 * y0 (x y0^2 - 3)  (relative error ~1e-13, far
+// below any ACA tolerance these blocks are compressed or compared at), i.e.
+// acc += y0 (x y0^2 - 3) w costs 4 FP64 ops after the seed; the caller scales
+// its accumulator by kNewtonScale once.
+constexpr double kNewtonScale = -0.5;
+__device__ __forceinline__ double rsqrt_n1_acc(double x, double w, double acc) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double t = x * y;
+  const double h = fma(t, y, -3.0);
+  return fma(y * h, w, acc);
+}
+
+// acc += K(r2) w on the admissible path (Laplace: Newton form, scaled later
+// by far_scale<K>(); others exact)
+template <int K>
+__device__ __forceinline__ double far_acc(double r2, double w, double acc) {
+  if constexpr (K == kLaplace) {
+    return rsqrt_n1_acc(r2, w, acc);
+  } else {
+    return fma(kernel_r2<K>(r2), w, acc);
+  }
+}
+template <int K>
+__device__ __forceinline__ constexpr double far_scale() {
+  return K == kLaplace ? kNewtonScale : 1.0;
+}
+
 template <int K>
 __device__ __forceinline__ double kernel_r2_fast(double r2) {
   if constexpr (K == kLaplace) {
@@ -113,6 +143,64 @@ __device__ __forceinline__ double ld_stream1(const double* p) {
   double r;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
   return r;
+}
+
+// ---- bulk-copy pipeline primitives (TMA engine, sm_90+ PTX; sm_100a here)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global -> shared bulk copy (16-B aligned, multiple of 16 bytes), completion
+// counted in bytes on the stage's mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 }  // namespace h3db

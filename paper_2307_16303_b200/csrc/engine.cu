@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -34,7 +35,7 @@ constexpr int kMaxProxyRank = 320; // proxy_solve_kernel's per-warp shared buffe
 constexpr double kStreamBW = 6.2e12;  // B/s
 double eval_rate(int kernel) {
   switch (kernel) {
-    case kLaplace: return 1.15e12;
+    case kLaplace: return 1.0e12;  // effective rate of the regenerating kernels (r01)
     case kR4: return 0.8e12;
     default: return 0.25e12;
   }
@@ -86,6 +87,7 @@ template class DevBuf<P1Item>;
 template class DevBuf<P1Reduce>;
 template class DevBuf<ProxySeg>;
 template class DevBuf<P2Item>;
+template class DevBuf<StreamDesc>;
 
 Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_(opt), n_(n) {
   const auto t0 = Clock::now();
@@ -110,10 +112,32 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   cudaDeviceProp prop{};
   H3D_CUDA_CHECK(cudaGetDeviceProperties(&prop, opt.device));
   sms_ = prop.multiProcessorCount;
+  if (const char* t = std::getenv("H3D_TUNE")) {
+    const std::string spec(t);
+    std::size_t pos = 0;
+    while (pos < spec.size()) {
+      std::size_t end = spec.find(',', pos);
+      if (end == std::string::npos) end = spec.size();
+      const std::string kv = spec.substr(pos, end - pos);
+      const std::size_t eq = kv.find('=');
+      if (eq != std::string::npos) {
+        const std::string k = kv.substr(0, eq);
+        const int v = std::atoi(kv.c_str() + eq + 1);
+        if (k == "p1s") tune_.p1s = v;
+        else if (k == "p1p") tune_.p1p = v;
+        else if (k == "p2c") tune_.p2c = v;
+        else if (k == "p2s") tune_.p2s = v;
+        else if (k == "p2p") tune_.p2p = v;
+        else if (k == "at") tune_.at = v;
+      }
+      pos = end + 1;
+    }
+  }
   H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
+  H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream3_, cudaStreamNonBlocking));
   for (auto& e : ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&fork_[k], cudaEventDisableTiming));
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&join_[k], cudaEventDisableTiming));
   }
@@ -153,7 +177,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
                         qx_.get(), qy_.get(), qz_.get(), stream_);
     int max_r = 0;
     for (const auto& sg : plan_->proxy_segs) max_r = std::max(max_r, sg.r);
-    launch_lu_invert(segs_all_.get(), n_segs_all_, lu_.get(), max_r, stream_);
+    launch_lu_invert(segs_all_.get(), n_segs_all_, lu_.get(), lu_total_, max_r, stream_);
   }
   near_scan();
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -166,10 +190,11 @@ Engine::~Engine() {
   if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     if (fork_[k]) cudaEventDestroy(fork_[k]);
     if (join_[k]) cudaEventDestroy(join_[k]);
   }
+  if (stream3_) cudaStreamDestroy(stream3_);
   if (stream2_) cudaStreamDestroy(stream2_);
   if (stream_) cudaStreamDestroy(stream_);
 }
@@ -250,6 +275,8 @@ void Engine::build_tree(const double* xyz) {
   py_.alloc(n_);
   pz_.alloc(n_);
   launch_permute_points(xyz_d.get(), perm_.get(), n_, px_.get(), py_.get(), pz_.get(), stream_);
+  p4_.alloc(4 * n_);
+  launch_pack_points(px_.get(), py_.get(), pz_.get(), n_, p4_.get(), stream_);
   leaf_off_.upload(off_[L_], stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
@@ -314,7 +341,7 @@ void Engine::run_aca(bool write) {
       nn[p] = static_cast<std::int32_t>(node_size(l, P.Y[p]));
     }
     DevBuf<std::int64_t> d_xb, d_yb, d_wx, d_wy, d_po, d_lo;
-    DevBuf<std::int32_t> d_m, d_n, d_rank, d_rx, d_ry;
+    DevBuf<std::int32_t> d_m, d_n, d_rank, d_rx, d_ry, d_cx, d_cy;
     d_xb.upload(xb, stream_);
     d_yb.upload(yb, stream_);
     d_m.upload(m, stream_);
@@ -328,6 +355,8 @@ void Engine::run_aca(bool write) {
         d_wy.upload(plan_->pair_wy[l], stream_);
         d_rx.upload(plan_->pair_rx[l], stream_);
         d_ry.upload(plan_->pair_ry[l], stream_);
+        d_cx.upload(plan_->pair_cx[l], stream_);
+        d_cy.upload(plan_->pair_cy[l], stream_);
       } else {
         d_po.upload(plan_->pair_piv[l], stream_);
         d_lo.upload(plan_->pair_lu[l], stream_);
@@ -394,6 +423,8 @@ void Engine::run_aca(bool write) {
         a.rx = d_rx.get();
         a.wy = d_wy.get();
         a.ry = d_ry.get();
+        a.cx = d_cx.get();
+        a.cy = d_cy.get();
       }
       if (write && mode == kModeProxy) {
         a.piv = piv_.get();
@@ -438,6 +469,15 @@ void Engine::run_aca(bool write) {
 //   max(stream, compute_1) + max(stream, compute_2 + near + direct)
 // subject to the factor pool fitting in free memory.
 void Engine::choose_modes() {
+  if (opt_.mode_policy == 2) {
+    for (int l = 1; l <= L_; ++l) {
+      if (plan_->mode(l) != kModeProxy) continue;
+      const auto& rk = plan_->pairs(l).rank;
+      if (!rk.empty() && *std::max_element(rk.begin(), rk.end()) > kMaxProxyRank)
+        throw InvalidArgument("initialize: level " + std::to_string(l) + " has ranks above " +
+                              std::to_string(kMaxProxyRank) + "; use stream mode there");
+    }
+  }
   if (opt_.mode_policy != 1) return;
   std::vector<int> cand;
   std::vector<double> units(L_ + 1, 0.0), lu(L_ + 1, 0.0);
@@ -493,8 +533,11 @@ void Engine::choose_modes() {
       }
     }
     if (!ok || sbytes > budget) continue;
+    // the streamed and regenerated passes do not overlap in practice (they
+    // compete for issue slots and occupancy; r01 hybrid runs were additive),
+    // so the per-phase cost is the sum of both
     const double ts = sbytes / kStreamBW;
-    const double T = std::max(ts, comp) + std::max(ts, comp + fixed / E) + lub / kStreamBW;
+    const double T = 2.0 * (ts + comp) + fixed / E + lub / kStreamBW;
     if (T < best) {
       best = T;
       best_mask = mask;
@@ -517,12 +560,14 @@ void Engine::upload_plan() {
   rows_.upload(P.rows, stream_);
   W_.alloc(std::max<std::int64_t>(Z.w_doubles, 2));
   H3D_CUDA_CHECK(cudaMemsetAsync(W_.get(), 0, W_.size() * 8, stream_));
-  S_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
+  // + padding: the phase-2 stream consumers prefetch one stage of S ahead
+  S_.alloc(std::max<std::int64_t>(Z.s_doubles, 2) + 4 * kTileCols);
   H3D_CUDA_CHECK(cudaMemsetAsync(S_.get(), 0, S_.size() * 8, stream_));
   spos_.upload(P.spos, stream_);
   P_.alloc(std::max<std::int64_t>(Z.p_doubles, 1));
   piv_.alloc(std::max<std::int64_t>(Z.piv_total, 1));
-  lu_.alloc(std::max<std::int64_t>(Z.lu_total, 1));
+  lu_total_ = Z.lu_total;
+  lu_.alloc(std::max<std::int64_t>(2 * Z.lu_total, 1));  // row-major + column-major inverses
   // proxy coordinates share S's index space; padding slots sit far away
   // (their weights are 0, see matvec.cu)
   qx_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
@@ -547,11 +592,32 @@ void Engine::upload_plan() {
   std::vector<P1Item> si, pi;
   for (const auto& it : P.items) (it.kind == kModeStream ? si : pi).push_back(it);
   p1_stream_items_.upload(si, stream_);
+  {
+    std::vector<StreamDesc> d(si.size());
+    for (std::size_t i = 0; i < si.size(); ++i) {
+      const P1Item& it = si[i];
+      const int nct = P.rpad[it.node] / kTileCols;
+      d[i].wbase = P.woff[it.node] +
+                   (static_cast<std::int64_t>(it.row0 / kTileRows) * nct + it.col0 / kTileCols) * kTileDoubles;
+      d[i].aux = P.rowbeg[it.node] + it.row0;
+      d[i].sbase = 0;
+      d[i].nrt = (it.nrows + kTileRows - 1) / kTileRows;
+      d[i].ncti = (it.ncols + kTileCols - 1) / kTileCols;
+      d[i].nct = nct;
+      d[i].nrows = it.nrows;
+      d[i].ncols = it.ncols;
+      d[i].pad = 0;
+    }
+    p1s_desc_.upload(d, stream_);
+  }
   p1_proxy_items_.upload(pi, stream_);
   n_p1s_ = static_cast<std::int64_t>(si.size());
   n_p1p_ = static_cast<std::int64_t>(pi.size());
   p1_red_.upload(P.reds, stream_);
   n_red_ = static_cast<std::int64_t>(P.reds.size());
+  for (std::size_t x = 0; x + 1 < P.near_off.size(); ++x)
+    if (P.near_off[x + 1] - P.near_off[x] > kMaxNearRanges)
+      throw std::logic_error("planner: leaf near list longer than the near kernel's range table");
   near_off_.upload(P.near_off, stream_);
   near_ids_.upload(P.near_ids.empty() ? std::vector<std::int32_t>{0} : P.near_ids, stream_);
   near_dense_.upload(P.near_dense, stream_);
@@ -560,11 +626,29 @@ void Engine::upload_plan() {
     if (P.mode(l) == kModeStream && !P.pairs(l).X.empty()) has_stream_levels_ = true;
   p2_items_.upload(P.p2_items, stream_);
   n_p2_ = static_cast<std::int64_t>(P.p2_items.size());
+  p2s_items_.upload(P.p2s_items, stream_);
+  {
+    std::vector<StreamDesc> d(P.p2s_items.size());
+    for (std::size_t i = 0; i < d.size(); ++i) {
+      const P2Item& it = P.p2s_items[i];
+      const int nct = P.rpad[it.node] / kTileCols;
+      d[i].wbase = P.woff[it.node] + static_cast<std::int64_t>(it.row0 / kTileRows) * nct * kTileDoubles;
+      d[i].aux = static_cast<std::int64_t>(it.slot) * n_ + P.rowbeg[it.node] + it.row0;
+      d[i].sbase = P.soff[it.node];
+      d[i].nrt = 1;
+      d[i].ncti = nct;
+      d[i].nct = nct;
+      d[i].nrows = it.nrows;
+      d[i].ncols = 0;
+      d[i].pad = 0;
+    }
+    p2s_desc_.upload(d, stream_);
+  }
+  n_p2s_ = static_cast<std::int64_t>(P.p2s_items.size());
   n_lvl_ = P.n_proxy_levels;
-  if (has_stream_levels_) spart_.alloc(n_);
-  if (has_stream_levels_ || n_p2_ > 0) cpart_.alloc(n_);
-  if (n_p2_ > 0) {
-    // rows of nodes without partners at a proxy level are never written
+  if (n_lvl_ > 0) {
+    cpart_.alloc(n_);
+    // rows of nodes without partners at a level are never written
     lvl_part_.alloc(static_cast<std::size_t>(n_lvl_) * n_);
     H3D_CUDA_CHECK(cudaMemsetAsync(lvl_part_.get(), 0, sizeof(double) * n_lvl_ * n_, stream_));
   }
@@ -593,6 +677,7 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.px = px_.get();
   a.py = py_.get();
   a.pz = pz_.get();
+  a.p4 = p4_.get();
   a.qx = qx_.get();
   a.qy = qy_.get();
   a.qz = qz_.get();
@@ -607,8 +692,15 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.kernel = opt_.kernel_id;
   a.diag = opt_.diagonal;
   a.b = bout;
-  if (has_stream_levels_) a.spart = spart_.get();
-  if (has_stream_levels_ || n_p2_ > 0) a.cpart_out = cpart_.get();
+  if (n_lvl_ > 0) {
+    a.cpart_out = cpart_.get();
+    a.lvl_part = lvl_part_.get();
+  }
+  if (n_p2s_ > 0) {
+    a.p2s_items = p2s_items_.get();
+    a.p2s_descs = p2s_desc_.get();
+    a.n_p2s_items = n_p2s_;
+  }
   if (n_p2_ > 0) {
     a.p2_items = p2_items_.get();
     a.n_p2_items = n_p2_;
@@ -643,12 +735,13 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   if (world_ == 1 || nccl_comm_ == nullptr) {
     // single GPU, or a shard without a communicator: x is replicated (every
     // rank holds all of it), gather it all locally
-    launch_gather(xin, perm_.get(), n_, xp_.get(), s);
+    launch_gather(xin, perm_.get(), n_, xp_.get(), p4_.get(), s);
     ++launches;
   } else {
     // own slice of x in Morton order, then the all-gather of x over NVLink
     if (P.row1 > P.row0) {
-      launch_gather(xin, perm_.get() + P.row0, P.row1 - P.row0, xp_.get() + P.row0, s);
+      launch_gather(xin, perm_.get() + P.row0, P.row1 - P.row0, xp_.get() + P.row0,
+                    p4_.get() + 4 * P.row0, s);
       ++launches;
     }
     auto comm = static_cast<ncclComm_t>(nccl_comm_);
@@ -660,10 +753,11 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
                                  static_cast<std::size_t>(c), ncclDouble, r, comm, s));
     }
     NCCL_CHECK(ncclGroupEnd());
+    launch_pack_w(xp_.get(), n_, p4_.get(), s);
+    ++launches;
   }
   if (ev) cudaEventRecord(ev[1], s);
-  // ---- phase 1: HBM-bound stream items on s, FP64-bound proxy items on
-  // stream2_, persistent CTAs sized to co-reside on every SM
+  // ---- phase 1: v = K(P, Z) x (proxy levels) / V^T x (stream levels)
   NodeTable nt{rowbeg_.get(), rows_.get(), woff_.get(), rpad_.get(), soff_.get()};
   P1Args a1;
   a1.nt = nt;
@@ -675,63 +769,82 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   a1.px = px_.get();
   a1.py = py_.get();
   a1.pz = pz_.get();
+  a1.p4 = p4_.get();
   a1.qx = qx_.get();
   a1.qy = qy_.get();
   a1.qz = qz_.get();
+  // Streams: s carries the critical path (phase 1 -> reduce -> solve ->
+  // phase-2 proxy levels -> combine); stream3_ runs the near field + direct
+  // leaf blocks (they need x only) from the start, filling whatever the
+  // phase-1 kernels and the latency-bound solve leave idle; stream2_ runs the
+  // HBM-bound stream-level kernels beside the FP64-bound proxy ones.
   const bool both1 = n_p1s_ > 0 && n_p1p_ > 0;
+  const bool has_p2 = P.leaf1 > P.leaf0;
+  const bool parts = n_lvl_ > 0;  // p2_compute writes partials, combine sums them
   H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 5 * sizeof(unsigned), s));
+  Phase2Args a2 = phase2_args(bout);
+  a2.counter = counters_.get() + 2;
+  a2.counter2 = counters_.get() + 3;
+  a2.counter3 = counters_.get() + 4;
+  auto fork_near = [&]() {
+    if (!has_p2) return;
+    H3D_CUDA_CHECK(cudaEventRecord(fork_[2], s));
+    H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
+    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream3_);
+    else launch_p2_near(a2, sms_, parts ? tune_.p2c : 4, stream3_);
+    ++launches;
+    H3D_CUDA_CHECK(cudaEventRecord(join_[2], stream3_));
+  };
+  if (tune_.at == 0) fork_near();
   if (both1) {
     H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[0], 0));
-  }
-  if (n_p1s_ > 0) {
     a1.items = p1_stream_items_.get();
+    a1.descs = p1s_desc_.get();
     a1.nitems = n_p1s_;
     a1.counter = counters_.get();
-    launch_p1_stream(a1, sms_, both1 ? 2 : 4, s);
+    launch_p1_stream(a1, sms_, tune_.p1s, stream2_);
+    ++launches;
+    H3D_CUDA_CHECK(cudaEventRecord(join_[0], stream2_));
+  } else if (n_p1s_ > 0) {
+    a1.items = p1_stream_items_.get();
+    a1.descs = p1s_desc_.get();
+    a1.nitems = n_p1s_;
+    a1.counter = counters_.get();
+    launch_p1_stream(a1, sms_, 4, s);
     ++launches;
   }
   if (n_p1p_ > 0) {
     a1.items = p1_proxy_items_.get();
     a1.nitems = n_p1p_;
     a1.counter = counters_.get() + 1;
-    launch_p1_proxy(a1, opt_.kernel_id, sms_, both1 ? 2 : 4, both1 ? stream2_ : s);
+    launch_p1_proxy(a1, opt_.kernel_id, sms_, both1 ? tune_.p1p : 4, s);
     ++launches;
   }
-  if (both1) {
-    H3D_CUDA_CHECK(cudaEventRecord(join_[0], stream2_));
-    H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
-  }
+  if (both1) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
   launch_phase1_reduce(p1_red_.get(), n_red_, nt, spos_.get(), P_.get(), S_.get(), s);
   launches += n_red_ > 0;
-  launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), S_.get(), s);
+  if (tune_.at != 0) fork_near();
+  launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), s);
   launches += n_segs_solve_ > 0;
   if (ev) cudaEventRecord(ev[2], s);
-  // ---- phase 2: FP64 part (near + direct + proxy levels) on stream2_, HBM
-  // part (stream levels) on s, combined into b in original order
-  if (P.leaf1 > P.leaf0) {
-    Phase2Args a2 = phase2_args(bout);
-    a2.counter = counters_.get() + 2;
-    a2.counter2 = counters_.get() + 3;
-    a2.counter3 = counters_.get() + 4;
-    if (has_stream_levels_) {
+  // ---- phase 2: stream levels (HBM) on stream2_, proxy levels on s
+  if (has_p2) {
+    if (n_p2s_ > 0) {
       H3D_CUDA_CHECK(cudaEventRecord(fork_[1], s));
       H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[1], 0));
-      launch_p2_compute(a2, sms_, 2, stream2_);
-      launch_p2_proxy(a2, sms_, 2, stream2_);
-      launch_p2_stream(a2, sms_, 2, s);
+      launch_p2_stream(a2, sms_, tune_.p2s, stream2_);
+      ++launches;
       H3D_CUDA_CHECK(cudaEventRecord(join_[1], stream2_));
-      H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
-      launches += 2 + (n_p2_ > 0);
-    } else {
-      launch_p2_compute(a2, sms_, 4, s);
-      launch_p2_proxy(a2, sms_, 4, s);
-      launches += 1 + (n_p2_ > 0);
     }
-    if (has_stream_levels_ || n_p2_ > 0) {
-      launch_combine(cpart_.get(), has_stream_levels_ ? spart_.get() : nullptr,
-                     n_p2_ > 0 ? lvl_part_.get() : nullptr, n_p2_ > 0 ? n_lvl_ : 0, n_,
-                     perm_.get(), P.row0, P.row1, bout, s);
+    if (n_p2_ > 0) {
+      launch_p2_proxy(a2, sms_, n_p2s_ > 0 ? tune_.p2p : 4, s);
+      ++launches;
+    }
+    if (n_p2s_ > 0) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
+    H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[2], 0));
+    if (parts) {
+      launch_combine(cpart_.get(), lvl_part_.get(), n_lvl_, n_, perm_.get(), P.row0, P.row1, bout, s);
       ++launches;
     }
   }

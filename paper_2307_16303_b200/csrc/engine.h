@@ -84,6 +84,12 @@ class Engine {
   std::int64_t n_ = 0;
   int L_ = 0;
   int sms_ = 148;
+  // persistent-CTA residency per SM of the matvec kernels and where the
+  // near-field pass forks (0: with phase 1, 1: after the phase-1 reduce);
+  // overridable for tuning through H3D_TUNE="p1s=2,p1p=2,p2c=2,p2s=2,p2p=4,at=0"
+  struct Tune {
+    int p1s = 2, p1p = 2, p2c = 2, p2s = 2, p2p = 2, at = 0;
+  } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
   cudaEvent_t ev_[8] = {};
@@ -94,6 +100,7 @@ class Engine {
   std::vector<std::int32_t> perm_h_;
   DevBuf<std::int32_t> perm_;
   DevBuf<double> px_, py_, pz_;
+  DevBuf<double> p4_;  // packed (x, y, z, x-value) per permuted point
   DevBuf<std::int64_t> leaf_off_;
   DevBuf<unsigned> flags_;
 
@@ -108,6 +115,7 @@ class Engine {
   DevBuf<std::int32_t> spos_;
   DevBuf<std::int32_t> piv_;
   DevBuf<double> lu_;
+  std::int64_t lu_total_ = 0;
   DevBuf<double> qx_, qy_, qz_;
   DevBuf<ProxySeg> segs_all_, segs_solve_;
   std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
@@ -116,14 +124,16 @@ class Engine {
   std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_ = 0;
   bool has_stream_levels_ = false;
   DevBuf<std::int32_t> near_off_, near_ids_, near_dense_;
-  DevBuf<double> cpart_, spart_;
-  DevBuf<P2Item> p2_items_;
-  std::int64_t n_p2_ = 0;
+  DevBuf<double> cpart_;
+  DevBuf<P2Item> p2_items_, p2s_items_;
+  DevBuf<StreamDesc> p1s_desc_, p2s_desc_;
+  std::int64_t n_p2_ = 0, n_p2s_ = 0;
   int n_lvl_ = 0;
-  DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 proxy partials
+  DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 per-level partials
   DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy]
   cudaStream_t stream2_ = nullptr;          // concurrent HBM / FP64 kernels
-  cudaEvent_t fork_[2] = {}, join_[2] = {};  // per phase
+  cudaStream_t stream3_ = nullptr;          // near field + direct (needs x only)
+  cudaEvent_t fork_[3] = {}, join_[3] = {};
   DevBuf<std::int64_t> nf_off_;
   DevBuf<double> NF_;
 

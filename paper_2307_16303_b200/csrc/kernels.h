@@ -67,11 +67,13 @@ struct AcaArgs {
   int cap_ws = 0;     // rank capacity of a slot
   int ms = 0, ns = 0; // column strides of U (m) and V (n) in a slot
   std::int32_t* rank_out = nullptr;
-  // factor write-back (stream levels, write pass)
+  // factor write-back (stream levels, write pass), tile-major (planner.h)
   double* W = nullptr;
-  const std::int64_t* wx = nullptr;  // W offset of U's (row 0, col 0)
-  const std::int32_t* rx = nullptr;  // U row stride
+  const std::int64_t* wx = nullptr;  // W offset of node X's pool
+  const std::int32_t* cx = nullptr;  // first column of the pair's segment in X's layout
+  const std::int32_t* rx = nullptr;  // column tiles of X's pool
   const std::int64_t* wy = nullptr;
+  const std::int32_t* cy = nullptr;
   const std::int32_t* ry = nullptr;
   // pivot + packed-LU write-back (proxy levels, write pass): row pivots at
   // piv[piv_off[p] + a], column pivots at piv[piv_off[p] + r + a]
@@ -91,8 +93,12 @@ int aca_max_clusters(int threads, int kernel, int cluster, std::size_t smem);
 void launch_aca_cluster(const AcaArgs& a, int threads, int cluster, int nclusters, cudaStream_t s);
 
 // -------------------------------------------------------------- matvec.cu
-void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp,
+// xp[p] = x[perm[p]], and the weight lane of the packed points p4 (x, y, z, w)
+void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp, double* p4,
                    cudaStream_t s);
+void launch_pack_w(const double* xp, std::int64_t n, double* p4, cudaStream_t s);
+void launch_pack_points(const double* px, const double* py, const double* pz, std::int64_t n,
+                        double* p4, cudaStream_t s);
 
 struct NodeTable {
   const std::int64_t* rowbeg = nullptr;  // first permuted row of global node g
@@ -104,6 +110,7 @@ struct NodeTable {
 
 struct P1Args {
   const P1Item* items = nullptr;  // one kind per launch
+  const StreamDesc* descs = nullptr;  // stream kind: per-item descriptors
   std::int64_t nitems = 0;
   NodeTable nt;
   const double* W = nullptr;
@@ -112,6 +119,7 @@ struct P1Args {
   double* S = nullptr;
   double* P = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;  // permuted points
+  const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
   const double *qx = nullptr, *qy = nullptr, *qz = nullptr;  // proxy points (S-space)
   unsigned* counter = nullptr;  // dynamic work counter (zeroed before the launch)
 };
@@ -124,11 +132,13 @@ void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
 void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int32_t* piv,
                          const double* px, const double* py, const double* pz, double* qx,
                          double* qy, double* qz, cudaStream_t s);
-void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, double* S,
-                        cudaStream_t s);
-// build time: replace every pair's packed LU by G = (L R)^-1 (row-major)
-void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, int max_r,
-                      cudaStream_t s);
+// lu holds 2 x lu_total doubles: the packed inverses row-major, then column-major
+void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
+                        std::int64_t lu_total, double* S, cudaStream_t s);
+// build time: replace every pair's packed LU by its triangular inverses
+// (strict lower L^-1, upper R^-1), row-major at lu and column-major at lu + lu_total
+void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::int64_t lu_total,
+                      int max_r, cudaStream_t s);
 
 struct Phase2Args {
   int depth = 0;
@@ -140,6 +150,7 @@ struct Phase2Args {
   const double* S = nullptr;
   const double* xp = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;
+  const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
   const double *qx = nullptr, *qy = nullptr, *qz = nullptr;
   const std::int32_t* perm = nullptr;
   // leaf near lists: self + near_edge + near_face (+ direct partners), CSR
@@ -152,8 +163,7 @@ struct Phase2Args {
   int kernel = 0;
   double diag = 0.0;
   double* b = nullptr;          // output, original order
-  double* spart = nullptr;      // stream-level partial sums (Morton order), or null
-  double* cpart_out = nullptr;  // compute partial sums (Morton order) when spart != null
+  double* cpart_out = nullptr;  // near/direct partial sums (Morton order) when levels add partials
   std::int64_t lbase[24] = {0};  // node_base per level (by value)
   int mode[24] = {0};            // LevelMode per level
   unsigned* counter = nullptr;   // p2_compute work counter (zeroed before the launch)
@@ -162,17 +172,26 @@ struct Phase2Args {
   // the proxy ranges and p2_proxy writes one partial per proxy level
   const P2Item* p2_items = nullptr;
   std::int64_t n_p2_items = 0;
-  double* lvl_part = nullptr;  // [n_proxy_levels x N] (Morton order)
+  // stream levels: one row tile per item, one partial per stream level
+  const P2Item* p2s_items = nullptr;
+  const StreamDesc* p2s_descs = nullptr;
+  std::int64_t n_p2s_items = 0;
+  double* lvl_part = nullptr;  // [levels with phase-2 work x N] (Morton order)
   std::int64_t n_total = 0;    // N
   unsigned* counter3 = nullptr;
 };
 void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
+// matrix-free near field + direct leaf blocks (near_mode on-the-fly); near
+// lists of at most kMaxNearRanges leaves (HODLR3D: 27 dense + <= 189 direct)
+constexpr int kMaxNearRanges = 256;
+// matrix-free near field + direct leaf blocks (near_mode on-the-fly)
+void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
-// b[perm[p]] = cpart[p] + spart[p] (if any) + sum over proxy levels of lvl_part
-void launch_combine(const double* cpart, const double* spart, const double* lvl_part,
-                    int n_lvl, std::int64_t n_total, const std::int32_t* perm,
-                    std::int64_t row0, std::int64_t row1, double* b, cudaStream_t s);
+// b[perm[p]] = cpart[p] + sum over levels (in order) of lvl_part[l][p]
+void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
+                    const std::int32_t* perm, std::int64_t row0, std::int64_t row1, double* b,
+                    cudaStream_t s);
 
 // Build-time near-field scan: coincidence check (and optional store).
 void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s);

@@ -41,10 +41,27 @@ constexpr int kP1Cols = 256;    // phase-1 columns per item
 constexpr int kChunk = 256;     // phase-1 proxy: sources staged per round
 constexpr int kMaxRanges = 256; // phase-2 compute: source ranges per tile
 
+// x in Morton order, into xp and the weight lane of the packed points
 __global__ void gather_kernel(const double* __restrict__ x, const std::int32_t* __restrict__ perm,
-                              std::int64_t n, double* __restrict__ xp) {
+                              std::int64_t n, double* __restrict__ xp, double* __restrict__ p4) {
   const std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  if (p < n) xp[p] = __ldg(x + perm[p]);
+  if (p < n) {
+    const double v = __ldg(x + perm[p]);
+    xp[p] = v;
+    p4[4 * p + 3] = v;
+  }
+}
+
+__global__ void pack_w_kernel(const double* __restrict__ xp, std::int64_t n, double* __restrict__ p4) {
+  const std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (p < n) p4[4 * p + 3] = xp[p];
+}
+
+__global__ void pack_points_kernel(const double* __restrict__ px, const double* __restrict__ py,
+                                   const double* __restrict__ pz, std::int64_t n,
+                                   double4* __restrict__ p4) {
+  const std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (p < n) p4[p] = make_double4(px[p], py[p], pz[p], 0.0);
 }
 
 __device__ __forceinline__ void p1_write(const P1Item& it, std::int64_t g, int c, double v,
@@ -57,74 +74,168 @@ __device__ __forceinline__ void p1_write(const P1Item& it, std::int64_t g, int c
   }
 }
 
-// ---- phase 1, stream levels: T = W_Z^T x_Z over <= 2048 rows x 256 columns
-__global__ void __launch_bounds__(kThreads, 2) p1_stream_kernel(const P1Args a) {
-  __shared__ double red[kWarps][kP1Cols + 2];
-  __shared__ long long s_k;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_k = static_cast<long long>(atomicAdd(a.counter, 1u));
-    __syncthreads();
-    const long long k = s_k;
-    if (k >= a.nitems) break;
-    const P1Item it = a.items[k];
-    const std::int64_t g = it.node;
-    const int rpad = a.nt.rpad[g];
-    const double* __restrict__ Wn =
-        a.W + a.nt.woff[g] + static_cast<std::int64_t>(it.row0) * rpad + it.col0;
-    const double* __restrict__ xn = a.xp + a.nt.rowbeg[g] + it.row0;
-    const int ng = (it.ncols + 63) >> 6;
-    double acc[4][2];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
-    int i = warp;
-    for (; i + kWarps < it.nrows; i += 2 * kWarps) {
-      const double x0 = xn[i], x1 = xn[i + kWarps];
-      const double2* r0 = reinterpret_cast<const double2*>(Wn + static_cast<std::int64_t>(i) * rpad);
-      const double2* r1 =
-          reinterpret_cast<const double2*>(Wn + static_cast<std::int64_t>(i + kWarps) * rpad);
-      double2 w0[4], w1[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool ok = q < ng && (2 * lane + 64 * q) < it.ncols;
-        w0[q] = ok ? ld_stream(r0 + lane + 32 * q) : make_double2(0.0, 0.0);
-        w1[q] = ok ? ld_stream(r1 + lane + 32 * q) : make_double2(0.0, 0.0);
+// ---- stream levels: tile pipeline --------------------------------------------
+// Persistent CTA = one producer warp + kSC consumer warps. The producer
+// claims work items (kBatch per atomic, descriptors prefetched) and streams
+// their factor tiles (planner.h tile-major pools) into a kStages-deep
+// shared-memory ring: one stage = up to kSC consecutive 8 KB tiles of one
+// tile row, contiguous in the pool, moved by ONE cp.async.bulk (TMA engine,
+// L2 evict-first) whose completion is counted in bytes on the stage's "full"
+// mbarrier; consumer warp c takes tile c of every stage and releases the
+// stage on its "empty" mbarrier. Few, large bulk copies keep the single
+// issuing thread off the critical path; with the copies off the SM's load
+// path one CTA (5 warps) per SM holds HBM near peak and leaves the rest of
+// the SM to the FP64-bound kernels running beside it.
+constexpr int kStages = 4;  // 4 x 32 KB in flight per SM (~19 MB device-wide)
+constexpr int kSC = 4;      // consumer warps = tiles per stage
+constexpr int kStreamThreads = 32 * (kSC + 1);
+constexpr unsigned kTileBytes = kTileDoubles * sizeof(double);
+
+struct StageMeta {
+  int k;          // item (< 0: stop)
+  int rt, ct;     // phase 1: tile row in the item; phase 2: first column tile of the stage
+  int n;          // tiles in this stage
+  long long aux;  // phase 1: first x row of the item; phase 2: output index of row 0
+  int nrows;      // rows of the item
+  int last;       // phase 1: column count; phase 2: 1 on the item's last stage
+  long long sb;   // phase 2: S offset of the node's columns
+};
+
+struct StreamSmem {
+  double tile[kStages][kSC * kTileDoubles];
+  unsigned long long full[kStages], empty[kStages];
+  StageMeta meta[kStages];
+  double red[2][kSC][kTileRows];  // phase-2 cross-warp row sums (double-buffered)
+};
+
+__device__ __forceinline__ void stream_init(StreamSmem& sm) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&sm.full[s], 1);
+      mbar_init(&sm.empty[s], kSC);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+}
+
+// Producer step: wait for stage t's slot, publish its metadata, start the
+// copy of ntiles consecutive tiles (src == nullptr: the stop marker).
+__device__ __forceinline__ void stream_put(StreamSmem& sm, unsigned t, const StageMeta& meta,
+                                           const double* src, int ntiles, unsigned long long pol) {
+  const int s = t % kStages;
+  if (t >= kStages) mbar_wait(&sm.empty[s], ((t / kStages) - 1) & 1);
+  sm.meta[s] = meta;
+  if (src) {
+    mbar_arrive_tx(&sm.full[s], kTileBytes * ntiles);
+    bulk_g2s(sm.tile[s], src, kTileBytes * ntiles, &sm.full[s], pol);
+  } else {
+    mbar_arrive(&sm.full[s]);
+  }
+}
+
+__device__ __forceinline__ StreamDesc shfl_desc(const StreamDesc& d, int src) {
+  StreamDesc e;
+  e.wbase = __shfl_sync(0xffffffffu, d.wbase, src);
+  e.aux = __shfl_sync(0xffffffffu, d.aux, src);
+  e.sbase = __shfl_sync(0xffffffffu, d.sbase, src);
+  e.nrt = __shfl_sync(0xffffffffu, d.nrt, src);
+  e.ncti = __shfl_sync(0xffffffffu, d.ncti, src);
+  e.nct = __shfl_sync(0xffffffffu, d.nct, src);
+  e.nrows = __shfl_sync(0xffffffffu, d.nrows, src);
+  e.ncols = __shfl_sync(0xffffffffu, d.ncols, src);
+  e.pad = 0;
+  return e;
+}
+
+// Producer warp: claims kBatch items per atomic; the next claim and the next
+// batch's descriptors are in flight while this batch's stages are issued, so
+// the ring does not drain on a claim. Lane 0 issues the copies.
+constexpr int kBatch = 8;
+template <class Issue>
+__device__ __forceinline__ void stream_producer(StreamSmem& sm, const StreamDesc* __restrict__ descs,
+                                                long long nitems, unsigned* counter, Issue issue) {
+  const int lane = threadIdx.x & 31;
+  unsigned t = 0;
+  long long base = 0;
+  if (lane == 0) base = atomicAdd(counter, static_cast<unsigned>(kBatch));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  StreamDesc d{};
+  if (lane < kBatch && base + lane < nitems) d = descs[base + lane];
+  while (base < nitems) {
+    long long nb = 0;
+    if (lane == 0) nb = atomicAdd(counter, static_cast<unsigned>(kBatch));
+    const int cnt = static_cast<int>(min(static_cast<long long>(kBatch), nitems - base));
+    for (int j = 0; j < cnt; ++j) {
+      const StreamDesc e = shfl_desc(d, j);
+      if (lane == 0) issue(t, static_cast<int>(base + j), e);
+      __syncwarp();
+    }
+    base = __shfl_sync(0xffffffffu, nb, 0);
+    if (lane < kBatch && base + lane < nitems) d = descs[base + lane];
+  }
+  if (lane == 0) stream_put(sm, t, StageMeta{-1, 0, 0, 0, 0, 0, 0, 0}, nullptr, 0, 0);
+}
+
+// ---- phase 1, stream levels: T = W_Z^T x_Z, item = <= 2048 rows x <= 256
+// columns of W_Z; a stage is one tile row of the item (its <= kSC column
+// tiles), consumer warp c owns the item's column tile c, lane = two columns,
+// rows accumulated in order. x rows come from L2 through the read-only path,
+// one row tile ahead.
+__global__ void __launch_bounds__(kStreamThreads, 1) p1_stream_kernel(const P1Args a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  stream_init(sm);
+  if (warp == 0) {
+    const unsigned long long pol = l2_evict_first();
+    stream_producer(sm, a.descs, a.nitems, a.counter, [&](unsigned& t, int k, const StreamDesc& e) {
+      for (int rt = 0; rt < e.nrt; ++rt, ++t)
+        stream_put(sm, t, StageMeta{k, rt, 0, e.ncti, e.aux, e.nrows, e.ncols, 0},
+                   a.W + e.wbase + static_cast<long long>(rt) * e.nct * kTileDoubles, e.ncti, pol);
+    });
+    return;
+  }
+  const int cw = warp - 1;
+  double acc0 = 0.0, acc1 = 0.0;
+  long long pk = -1;
+  int prt = -1;
+  double xpre = 0.0;
+  auto xload = [&](long long aux, int rt, int nrows) {
+    const int r = rt * kTileRows + lane;
+    return (lane < kTileRows && r < nrows) ? __ldg(a.xp + aux + r) : 0.0;
+  };
+  for (unsigned t = 0;; ++t) {
+    const int s = t % kStages;
+    mbar_wait(&sm.full[s], (t / kStages) & 1);
+    const StageMeta m = sm.meta[s];
+    if (m.k < 0) break;
+    if (cw < m.n) {
+      const double xv = (pk == m.k && prt == m.rt) ? xpre : xload(m.aux, m.rt, m.nrows);
+      const int nrt = (m.nrows + kTileRows - 1) / kTileRows;
+      if (m.rt + 1 < nrt) {
+        xpre = xload(m.aux, m.rt + 1, m.nrows);
+        pk = m.k;
+        prt = m.rt + 1;
       }
+      const double2* tl = reinterpret_cast<const double2*>(sm.tile[s] + cw * kTileDoubles);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc[q][0] = fma(w0[q].x, x0, acc[q][0]);
-        acc[q][1] = fma(w0[q].y, x0, acc[q][1]);
-        acc[q][0] = fma(w1[q].x, x1, acc[q][0]);
-        acc[q][1] = fma(w1[q].y, x1, acc[q][1]);
+      for (int i = 0; i < kTileRows; ++i) {
+        const double xi = __shfl_sync(0xffffffffu, xv, i);
+        const double2 w = tl[i * (kTileCols / 2) + lane];
+        acc0 = fma(w.x, xi, acc0);
+        acc1 = fma(w.y, xi, acc1);
+      }
+      if (m.rt == nrt - 1) {
+        const P1Item it = a.items[m.k];
+        const int c = cw * kTileCols + 2 * lane;
+        if (c < m.last) p1_write(it, it.node, c, acc0, a);
+        if (c + 1 < m.last) p1_write(it, it.node, c + 1, acc1, a);
+        acc0 = acc1 = 0.0;
       }
     }
-    for (; i < it.nrows; i += kWarps) {
-      const double x0 = xn[i];
-      const double2* r0 = reinterpret_cast<const double2*>(Wn + static_cast<std::int64_t>(i) * rpad);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q < ng && (2 * lane + 64 * q) < it.ncols) {
-          const double2 w = ld_stream(r0 + lane + 32 * q);
-          acc[q][0] = fma(w.x, x0, acc[q][0]);
-          acc[q][1] = fma(w.y, x0, acc[q][1]);
-        }
-      }
-    }
-    __syncthreads();  // red reuse across items
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      red[warp][2 * lane + 64 * q] = acc[q][0];
-      red[warp][2 * lane + 64 * q + 1] = acc[q][1];
-    }
-    __syncthreads();
-    const int c = threadIdx.x;
-    if (c < it.ncols) {
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) v += red[w][c];
-      p1_write(it, g, c, v, a);
-    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
   }
 }
 
@@ -153,24 +264,24 @@ __global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
       const int nj = min(kChunk, it.nrows - j0);
       __syncthreads();
       if (threadIdx.x < nj) {
-        const std::int64_t p = rb + j0 + threadIdx.x;
-        src[2 * threadIdx.x] = make_double2(a.px[p], a.py[p]);
-        src[2 * threadIdx.x + 1] = make_double2(a.pz[p], a.xp[p]);
+        const double4 q = reinterpret_cast<const double4*>(a.p4)[rb + j0 + threadIdx.x];
+        src[2 * threadIdx.x] = make_double2(q.x, q.y);
+        src[2 * threadIdx.x + 1] = make_double2(q.z, q.w);
       }
       __syncthreads();
       int j = 0;
       for (; j + 1 < nj; j += 2) {
         const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
         const double2 u0 = src[2 * j + 2], u1 = src[2 * j + 3];
-        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
-        acc1 = fma(kernel_r2_fast<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x)), u1.y, acc1);
+        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
+        acc1 = far_acc<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x), u1.y, acc1);
       }
       if (j < nj) {
         const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
+        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
       }
     }
-    if (active) p1_write(it, g, c, acc0 + acc1, a);
+    if (active) p1_write(it, g, c, far_scale<K>() * (acc0 + acc1), a);
   }
 }
 
@@ -208,13 +319,15 @@ __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int6
 
 // Triangular inverses of the packed pivot LU, in place (build time; one thread
 // per column): strict lower <- L^-1 (unit diagonal implied), upper incl.
-// diagonal <- R^-1. Applying L^-1 and R^-1 as two GEMVs is as accurate as the
-// reference's forward/backward substitution (lowrank.cpp:310-320) on these
-// ill-conditioned pivot blocks (cond ~ 1e12 at eps 1e-10), unlike forming
-// (L R)^-1, and turns the sequential solves into coalesced, parallel GEMVs.
+// diagonal <- R^-1, and the same matrix column-major at lu + lu_total (the
+// side-0 solve reads it by columns). Applying L^-1 and R^-1 as two GEMVs is as
+// accurate as the reference's forward/backward substitution
+// (lowrank.cpp:310-320) on these ill-conditioned pivot blocks (cond ~ 1e12 at
+// eps 1e-10), unlike forming (L R)^-1, and turns the sequential solves into
+// coalesced, parallel GEMVs.
 __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
-                                 double* __restrict__ lu, double* __restrict__ scratch,
-                                 int max_r) {
+                                 double* __restrict__ lu, std::int64_t lu_total,
+                                 double* __restrict__ scratch, int max_r) {
   const std::int64_t s = blockIdx.x;
   if (s >= nseg) return;
   const ProxySeg sg = segs[s];
@@ -239,79 +352,125 @@ __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {  // row-major over the LU slot
-    const int row = e / r, col = e % r;
-    A[e] = Gs[static_cast<std::int64_t>(col) * max_r + row];
+  double* AT = A + lu_total;
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) {
+    const int hi = e / r, lo = e % r;
+    A[e] = Gs[static_cast<std::int64_t>(lo) * max_r + hi];   // row-major: (row hi, col lo)
+    AT[e] = Gs[static_cast<std::int64_t>(hi) * max_r + lo];  // column-major: (row lo, col hi)
   }
 }
 
-// Per ordered proxy block (one warp), in place on S, with P the packed
-// inverses (strict lower L^-1, upper R^-1):
+// One ordered proxy block per warp, in place on S; lane owns outputs
+// i = lane + 32 k (k < NK), the loop runs over the other index so every
+// matrix access is a coalesced row (side 1, row-major P) or column (side 0,
+// column-major PT) and the only cross-lane traffic is a shared broadcast.
 //   side 0 (target = pair's row side X):  s = R^-1 (L^-1 v)       (lowrank.cpp:310-320)
 //   side 1 (target = pair's col side Y):  s = L^-T (R^-T v)       (the transposed block)
-__global__ void proxy_solve_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
-                                   const double* __restrict__ lu, double* __restrict__ S) {
-  extern __shared__ double sh[];
+template <int NK>
+__device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __restrict__ P,
+                                          const double* __restrict__ PT, double* v, double* w,
+                                          double* __restrict__ Sg, int lane) {
+  const int r = sg.r;
+  double acc[NK];
+#pragma unroll
+  for (int k = 0; k < NK; ++k) acc[k] = 0.0;
+  if (sg.side == 0) {
+    // w = L^-1 v: w_i = v_i + sum_{j<i} PT[j][i] v_j
+#pragma unroll 8
+    for (int j = 0; j < r; ++j) {
+      const double vj = v[j];
+      const double* col = PT + static_cast<std::int64_t>(j) * r;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int i = lane + 32 * k;
+        if (k >= (j >> 5) && i > j && i < r) acc[k] = fma(col[i], vj, acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const int i = lane + 32 * k;
+      if (i < r) w[i] = v[i] + acc[k];
+      acc[k] = 0.0;
+    }
+    __syncwarp();
+    // s = R^-1 w: s_i = sum_{j>=i} PT[j][i] w_j
+#pragma unroll 8
+    for (int j = 0; j < r; ++j) {
+      const double wj = w[j];
+      const double* col = PT + static_cast<std::int64_t>(j) * r;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int i = lane + 32 * k;
+        if (32 * k <= j && i <= j) acc[k] = fma(col[i], wj, acc[k]);
+      }
+    }
+  } else {
+    // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i
+#pragma unroll 8
+    for (int i = 0; i < r; ++i) {
+      const double vi = v[i];
+      const double* row = P + static_cast<std::int64_t>(i) * r;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int j = lane + 32 * k;
+        if (k >= (i >> 5) && j >= i && j < r) acc[k] = fma(row[j], vi, acc[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const int j = lane + 32 * k;
+      if (j < r) w[j] = acc[k];
+    }
+    __syncwarp();
+    // s = L^-T u: s_j = u_j + sum_{i>j} P[i][j] u_i
+#pragma unroll 8
+    for (int i = 1; i < r; ++i) {
+      const double ui = w[i];
+      const double* row = P + static_cast<std::int64_t>(i) * r;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int j = lane + 32 * k;
+        if (32 * k < i && j < i) acc[k] = fma(row[j], ui, acc[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NK; ++k) {
+    const int i = lane + 32 * k;
+    if (i < r) Sg[i] = acc[k];
+  }
+}
+
+__global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __restrict__ segs,
+                                                          std::int64_t nseg,
+                                                          const double* __restrict__ lu,
+                                                          std::int64_t lu_total,
+                                                          double* __restrict__ S) {
+  __shared__ double sh[4][640];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x >> 5) + warp;
   if (s >= nseg) return;
   const ProxySeg sg = segs[s];
   const int r = sg.r;
-  double* v = sh + warp * 640;  // v and w, r <= 320 (enforced on the host)
+  double* v = sh[warp];  // v and w, r <= 320 (enforced on the host)
   double* w = v + 320;
   double* Sg = S + sg.so;
   for (int q = lane; q < r; q += 32) v[q] = Sg[q];
   __syncwarp();
   const double* P = lu + sg.lu_off;
-  if (sg.side == 0) {
-    for (int i = 0; i < r; ++i) {  // w = L^-1 v: w_i = v_i + sum_{j<i} P[i][j] v_j
-      const double* row = P + static_cast<std::int64_t>(i) * r;
-      double acc = 0.0;
-      for (int j = lane; j < i; j += 32) acc = fma(row[j], v[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) w[i] = v[i] + acc;
-    }
-    __syncwarp();
-    for (int i = 0; i < r; ++i) {  // s = R^-1 w: s_i = sum_{j>=i} P[i][j] w_j
-      const double* row = P + static_cast<std::int64_t>(i) * r;
-      double acc = 0.0;
-      for (int j = i + lane; j < r; j += 32) acc = fma(row[j], w[j], acc);
-      acc = warp_sum(acc);
-      if (lane == 0) Sg[i] = acc;
-    }
-  } else {
-    double acc[10];
-#pragma unroll
-    for (int k = 0; k < 10; ++k) acc[k] = 0.0;
-    for (int i = 0; i < r; ++i) {  // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i
-      const double vi = v[i];
-      const double* row = P + static_cast<std::int64_t>(i) * r;
-#pragma unroll
-      for (int k = 0; k < 10; ++k) {
-        const int j = lane + 32 * k;
-        if (j >= i && j < r) acc[k] = fma(row[j], vi, acc[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 10; ++k) {
-      const int j = lane + 32 * k;
-      if (j < r) w[j] = acc[k];
-    }
-    __syncwarp();
-    for (int i = 0; i < r; ++i) {  // s = L^-T u: s_j = u_j + sum_{i>j} P[i][j] u_i
-      const double ui = w[i];
-      const double* row = P + static_cast<std::int64_t>(i) * r;
-#pragma unroll
-      for (int k = 0; k < 10; ++k) {
-        const int j = lane + 32 * k;
-        if (j < i) acc[k] = fma(row[j], ui, acc[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 10; ++k) {
-      const int j = lane + 32 * k;
-      if (j < r) Sg[j] = acc[k];
-    }
+  const double* PT = P + lu_total;
+  switch ((r + 31) >> 5) {
+    case 0: break;
+    case 1: solve_seg<1>(sg, P, PT, v, w, Sg, lane); break;
+    case 2: solve_seg<2>(sg, P, PT, v, w, Sg, lane); break;
+    case 3: solve_seg<3>(sg, P, PT, v, w, Sg, lane); break;
+    case 4: solve_seg<4>(sg, P, PT, v, w, Sg, lane); break;
+    case 5: solve_seg<5>(sg, P, PT, v, w, Sg, lane); break;
+    case 6: solve_seg<6>(sg, P, PT, v, w, Sg, lane); break;
+    case 7: solve_seg<7>(sg, P, PT, v, w, Sg, lane); break;
+    case 8: solve_seg<8>(sg, P, PT, v, w, Sg, lane); break;
+    case 9: solve_seg<9>(sg, P, PT, v, w, Sg, lane); break;
+    default: solve_seg<10>(sg, P, PT, v, w, Sg, lane); break;
   }
 }
 
@@ -505,54 +664,272 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
   }
 }
 
-// ---- phase 2, stream part: rows of W_A . S_A over the stream levels
-__global__ void __launch_bounds__(kThreads, 2) p2_stream_kernel(const Phase2Args a) {
+// ---- phase 2, near field + direct leaf blocks, matrix-free ------------------
+// One owned leaf X per CTA pass (persistent CTAs, work counter). Sources =
+// X's near list flattened (self, edge and face neighbours: the reference's
+// dense blocks; then the leaf-level admissible partners evaluated directly),
+// moved from the packed (x, y, z, w) points into a double-buffered shared
+// stage by cp.async.bulk, one copy per (range, chunk) piece, completion on the
+// buffer's mbarrier. Warp w owns rows [w RPW, (w + 1) RPW) of the leaf
+// (RPW = ceil(m / 8)), lanes stride over the staged sources, each source is
+// evaluated against the warp's RPW rows (RPW independent FP64 chains per
+// lane). Dense-near sources use the full-accuracy rsqrt (+ the diagonal rule
+// on the self block), admissible ones the Newton form. Rows are owned by one
+// warp: the only reduction is the fixed warp butterfly.
+constexpr int kNearStage = 512;  // sources per staged chunk (16 KB)
+
+constexpr int kMaxNear = kMaxNearRanges;
+
+struct NearSmem {
+  double4 stage[2][kNearStage];
+  unsigned long long full[2];
+  long long rstart[kMaxNear];  // the leaf's source ranges (permuted point index, length)
+  int rlen[kMaxNear];
+  int cnt[2];
+  int base[2];
+  long long leaf;
+  int nrange, ndense;
+};
+
+// One accumulator per row in the admissible (Newton) scale: dense-near terms
+// enter with weight w / far_scale (exact power-of-two scalings), the caller
+// multiplies by far_scale once.
+template <int K, int RPW>
+__device__ __forceinline__ void near_chunk(const double4* __restrict__ st, int base, int cnt,
+                                           int self_end, int dense_end, int row0,
+                                           const double (&tx)[RPW], const double (&ty)[RPW],
+                                           const double (&tz)[RPW], double (&acc)[RPW], double diag,
+                                           int lane) {
+  constexpr double inv = 1.0 / far_scale<K>();
+  // [0, e_self): self block (diagonal rule); [e_self, e_dense): dense near;
+  // [e_dense, cnt): admissible partners
+  const int e_self = max(0, min(cnt, self_end - base));
+  const int e_dense = max(e_self, min(cnt, dense_end - base));
+  for (int j = lane; j < e_self; j += 32) {
+    const double4 q = st[j];
+    const double w = inv * q.w;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const double k = (row0 + r == base + j) ? diag
+                                              : kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
+      acc[r] = fma(k, w, acc[r]);
+    }
+  }
+  for (int j = e_self + lane; j < e_dense; j += 32) {
+    const double4 q = st[j];
+    const double w = inv * q.w;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+      acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z)), w, acc[r]);
+  }
+  for (int j = e_dense + lane; j < cnt; j += 32) {
+    const double4 q = st[j];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) acc[r] = far_acc<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z), q.w, acc[r]);
+  }
+}
+
+// Thread 0: issue the next chunk of the current leaf into buffer b, walking
+// the range cursor (re, roff) over the shared range table.
+__device__ __forceinline__ int near_issue(NearSmem& sm, int b, const Phase2Args& a, int& re, int& roff,
+                                          int vbase) {
+  int filled = 0;
+  while (re < sm.nrange && filled < kNearStage) {
+    const int len = sm.rlen[re];
+    const int take = min(len - roff, kNearStage - filled);
+    if (take > 0) {
+      const unsigned bytes = static_cast<unsigned>(take) * 32u;
+      mbar_expect_tx(&sm.full[b], bytes);
+      bulk_g2s(&sm.stage[b][filled], reinterpret_cast<const double4*>(a.p4) + sm.rstart[re] + roff,
+               bytes, &sm.full[b], 0);
+      filled += take;
+      roff += take;
+    }
+    if (roff >= len) {
+      ++re;
+      roff = 0;
+    }
+  }
+  sm.cnt[b] = filled;
+  sm.base[b] = vbase;
+  mbar_arrive(&sm.full[b]);
+  return filled;
+}
+
+template <int K, int RPW>
+__device__ void near_leaf(NearSmem& sm, const Phase2Args& a, std::int64_t X, int r0, int mr,
+                          unsigned (&uses)[2]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int L = a.depth;
-  __shared__ long long s_t;
+  const std::int64_t xb = a.leaf_off[X];
+  const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
+  int total = 0, dense_end = 0;
+  for (int e = 0; e < sm.nrange; ++e) {  // shared broadcasts
+    total += sm.rlen[e];
+    if (e < sm.ndense) dense_end = total;
+  }
+  const int nchunks = (total + kNearStage - 1) / kNearStage;
+  int re = 0, roff = 0, vb = 0;
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 2 && c < nchunks; ++c) vb += near_issue(sm, c, a, re, roff, vb);
+  }
+  const int row0 = r0 + warp * RPW;
+  const double4* P4 = reinterpret_cast<const double4*>(a.p4);
+  double tx[RPW], ty[RPW], tz[RPW], acc[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const bool ok = row0 + r < r0 + mr;
+    const double4 q = ok ? P4[xb + row0 + r] : make_double4(kFar, kFar, kFar, 0.0);
+    tx[r] = q.x;
+    ty[r] = q.y;
+    tz[r] = q.z;
+    acc[r] = 0.0;
+  }
+  for (int c = 0; c < nchunks; ++c) {
+    const int b = c & 1;
+    mbar_wait(&sm.full[b], uses[b] & 1);
+    ++uses[b];
+    near_chunk<K, RPW>(sm.stage[b], sm.base[b], sm.cnt[b], m, dense_end, row0, tx, ty, tz, acc, a.diag,
+                       lane);
+    __syncthreads();  // buffer b consumed
+    if (threadIdx.x == 0 && c + 2 < nchunks) vb += near_issue(sm, b, a, re, roff, vb);
+  }
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const double v = far_scale<K>() * warp_sum(acc[r]);
+    const int i = row0 + r;
+    if (lane == r && i < r0 + mr) {
+      if (a.cpart_out) a.cpart_out[xb + i] = v;
+      else a.b[a.perm[xb + i]] = v;
+    }
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(kThreads, 2) p2_near_kernel(const Phase2Args a) {
+  __shared__ __align__(128) NearSmem sm;
+  if (threadIdx.x == 0) {
+    mbar_init(&sm.full[0], 1);
+    mbar_init(&sm.full[1], 1);
+    mbar_fence_init();
+  }
+  unsigned uses[2] = {0u, 0u};
   for (;;) {
     __syncthreads();
-    if (threadIdx.x == 0) s_t = static_cast<long long>(atomicAdd(a.counter2, 1u));
+    if (threadIdx.x == 0) sm.leaf = static_cast<long long>(atomicAdd(a.counter, 1u));
     __syncthreads();
-    const long long t = s_t;
+    const long long t = sm.leaf;
     if (t >= a.nleaves) break;
     const std::int64_t X = a.leaf0 + t;
-    const std::int64_t xb = a.leaf_off[X];
-    const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
-    for (int i = warp; i < m; i += kWarps) {
-      double s0 = 0.0, s1 = 0.0;
-      for (int l = 1; l <= L; ++l) {
-        if (a.mode[l] != 0) continue;
-        const std::int64_t g = a.lbase[l] + (X >> (3 * (L - l)));
-        const int R = a.nt.rpad[g];
-        if (R == 0) continue;
-        const double2* row = reinterpret_cast<const double2*>(
-            a.W + a.nt.woff[g] + (xb + i - a.nt.rowbeg[g]) * R);
-        const double2* S2 = reinterpret_cast<const double2*>(a.S + a.nt.soff[g]);
-        const int R2 = R >> 1;
-        int c = lane;
-        for (; c + 224 < R2; c += 256) {
-          double2 w[8], q[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) w[u] = ld_stream(row + c + 32 * u);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) q[u] = __ldg(S2 + c + 32 * u);
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            s0 = fma(w[u].x, q[u].x, s0);
-            s1 = fma(w[u].y, q[u].y, s1);
-          }
-        }
-        for (; c < R2; c += 32) {
-          const double2 w0 = ld_stream(row + c);
-          const double2 q0 = __ldg(S2 + c);
-          s0 = fma(w0.x, q0.x, s0);
-          s1 = fma(w0.y, q0.y, s1);
-        }
+    {
+      // range table: self, edge + face neighbours (dense), direct partners
+      const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
+      for (int e = threadIdx.x; e < ne - nb; e += kThreads) {
+        const std::int32_t Y = a.near_ids[nb + e];
+        const std::int64_t yb = a.leaf_off[Y];
+        sm.rstart[e] = yb;
+        sm.rlen[e] = static_cast<int>(a.leaf_off[Y + 1] - yb);
       }
-      const double v = warp_sum(s0 + s1);
-      if (lane == 0) a.spart[xb + i] = v;
+      if (threadIdx.x == 0) {
+        sm.nrange = ne - nb;
+        sm.ndense = a.near_dense[X];
+      }
+      __syncthreads();
     }
+    const int m = static_cast<int>(a.leaf_off[X + 1] - a.leaf_off[X]);
+    for (int r0 = 0; r0 < m; r0 += 8 * kWarps) {
+      const int mr = min(8 * kWarps, m - r0);
+      switch ((mr + kWarps - 1) / kWarps) {
+        case 1: near_leaf<K, 1>(sm, a, X, r0, mr, uses); break;
+        case 2: near_leaf<K, 2>(sm, a, X, r0, mr, uses); break;
+        case 3: near_leaf<K, 3>(sm, a, X, r0, mr, uses); break;
+        case 4: near_leaf<K, 4>(sm, a, X, r0, mr, uses); break;
+        case 5: near_leaf<K, 5>(sm, a, X, r0, mr, uses); break;
+        case 6: near_leaf<K, 6>(sm, a, X, r0, mr, uses); break;
+        case 7: near_leaf<K, 7>(sm, a, X, r0, mr, uses); break;
+        default: near_leaf<K, 8>(sm, a, X, r0, mr, uses); break;
+      }
+    }
+  }
+}
+
+// ---- phase 2, stream levels: rows of W_A . S_A, item = one row tile of an
+// owned node A (all its column tiles, kSC per stage); consumer warp c owns
+// column tiles c, c + kSC, ..., lane = two columns, sixteen row accumulators;
+// S columns come through the read-only path one stage ahead. At the item's
+// last stage the warps reduce (fixed butterfly, then warp order) and write
+// the level's partial (combined in level order by combine_kernel).
+__global__ void __launch_bounds__(kStreamThreads, 1) p2_stream_kernel(const Phase2Args a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  stream_init(sm);
+  if (warp == 0) {
+    const unsigned long long pol = l2_evict_first();
+    stream_producer(sm, a.p2s_descs, a.n_p2s_items, a.counter2,
+                    [&](unsigned& t, int k, const StreamDesc& e) {
+                      for (int c0 = 0; c0 < e.nct; c0 += kSC, ++t) {
+                        const int nt = min(kSC, e.nct - c0);
+                        stream_put(sm, t,
+                                   StageMeta{k, 0, c0, nt, e.aux, e.nrows, c0 + nt == e.nct ? 1 : 0,
+                                             e.sbase},
+                                   a.W + e.wbase + static_cast<long long>(c0) * kTileDoubles, nt, pol);
+                      }
+                    });
+    return;
+  }
+  const int cw = warp - 1;
+  double acc[kTileRows];
+#pragma unroll
+  for (int i = 0; i < kTileRows; ++i) acc[i] = 0.0;
+  int parity = 0;
+  // S columns of this warp's tile, prefetched one stage ahead (S is padded
+  // by kSC * kTileCols doubles, engine.cu)
+  long long pk = -1;
+  int pc = -1;
+  double2 spre = make_double2(0.0, 0.0);
+  auto sload = [&](long long sb, int c) {
+    return __ldg(reinterpret_cast<const double2*>(a.S + sb + static_cast<long long>(c) * kTileCols) + lane);
+  };
+  for (unsigned t = 0;; ++t) {
+    const int s = t % kStages;
+    mbar_wait(&sm.full[s], (t / kStages) & 1);
+    const StageMeta m = sm.meta[s];
+    if (m.k < 0) break;
+    if (cw < m.n) {
+      const int c = m.ct + cw;
+      const double2 sv = (pk == m.k && pc == c) ? spre : sload(m.sb, c);
+      if (!m.last) {
+        spre = sload(m.sb, c + kSC);
+        pk = m.k;
+        pc = c + kSC;
+      }
+      const double2* tl = reinterpret_cast<const double2*>(sm.tile[s] + cw * kTileDoubles);
+#pragma unroll
+      for (int i = 0; i < kTileRows; ++i) {
+        const double2 w = tl[i * (kTileCols / 2) + lane];
+        acc[i] = fma(w.y, sv.y, fma(w.x, sv.x, acc[i]));
+      }
+    }
+    if (m.last) {
+      double mine = 0.0;
+#pragma unroll
+      for (int i = 0; i < kTileRows; ++i) {
+        const double v = warp_sum(acc[i]);
+        if (lane == i) mine = v;
+        acc[i] = 0.0;
+      }
+      if (lane < kTileRows) sm.red[parity][cw][lane] = mine;
+      named_bar(1, 32 * kSC);
+      if (cw == 0 && lane < m.nrows) {
+        double v = sm.red[parity][0][lane];
+#pragma unroll
+        for (int w = 1; w < kSC; ++w) v += sm.red[parity][w][lane];
+        a.lvl_part[m.aux + lane] = v;
+      }
+      parity ^= 1;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
   }
 }
 
@@ -592,27 +969,27 @@ __global__ void __launch_bounds__(kThreads, 2) p2_proxy_kernel(const Phase2Args 
       for (; j + 1 < nj; j += 2) {
         const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
         const double2 u0 = src[2 * j + 2], u1 = src[2 * j + 3];
-        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
-        acc1 = fma(kernel_r2_fast<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x)), u1.y, acc1);
+        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
+        acc1 = far_acc<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x), u1.y, acc1);
       }
       if (j < nj) {
         const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        acc0 = fma(kernel_r2_fast<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x)), s1.y, acc0);
+        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
       }
     }
-    if (active) a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + p] = acc0 + acc1;
+    if (active)
+      a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + p] = far_scale<K>() * (acc0 + acc1);
   }
 }
 
-__global__ void combine_kernel(const double* __restrict__ cpart, const double* __restrict__ spart,
-                               const double* __restrict__ lvl, int n_lvl, std::int64_t n_total,
+__global__ void combine_kernel(const double* __restrict__ cpart, const double* __restrict__ lvl,
+                               int n_lvl, std::int64_t n_total,
                                const std::int32_t* __restrict__ perm, std::int64_t row0,
                                std::int64_t row1, double* __restrict__ b) {
   const std::int64_t p = row0 + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
   if (p >= row1) return;
   double v = cpart[p];
   for (int l = 0; l < n_lvl; ++l) v += lvl[static_cast<std::int64_t>(l) * n_total + p];
-  if (spart) v += spart[p];
   b[perm[p]] = v;
 }
 
@@ -664,16 +1041,70 @@ int grid_for(F kernel, int sms, int per_sm, std::int64_t work) {
 
 }  // namespace
 
-void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp,
+void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp, double* p4,
                    cudaStream_t s) {
-  gather_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, perm, n, xp);
+  if (n <= 0) return;
+  gather_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, perm, n, xp, p4);
   H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pack_w(const double* xp, std::int64_t n, double* p4, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_w_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(xp, n, p4);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pack_points(const double* px, const double* py, const double* pz, std::int64_t n,
+                        double* p4, cudaStream_t s) {
+  if (n <= 0) return;
+  pack_points_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      px, py, pz, n, reinterpret_cast<double4*>(p4));
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
+  if (a.nleaves == 0) return;
+  switch (a.kernel) {
+    case kLaplace: {
+      const int grid = grid_for(p2_near_kernel<kLaplace>, sms, per_sm, a.nleaves);
+      p2_near_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+    case kR4: {
+      const int grid = grid_for(p2_near_kernel<kR4>, sms, per_sm, a.nleaves);
+      p2_near_kernel<kR4><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+    default: {
+      const int grid = grid_for(p2_near_kernel<kHelmholtz>, sms, per_sm, a.nleaves);
+      p2_near_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a);
+      break;
+    }
+  }
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+template <class F>
+int stream_grid(F kernel, int sms, int per_sm, std::int64_t work) {
+  static bool attr = false;  // process-wide, set before the first launch
+  if (!attr) {
+    H3D_CUDA_CHECK(cudaFuncSetAttribute(p1_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(StreamSmem))));
+    H3D_CUDA_CHECK(cudaFuncSetAttribute(p2_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(StreamSmem))));
+    attr = true;
+  }
+  int nb = 0;
+  H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kStreamThreads,
+                                                               sizeof(StreamSmem)));
+  const std::int64_t g = static_cast<std::int64_t>(sms) * std::max(1, std::min(nb, per_sm));
+  return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, work)));
 }
 
 void launch_p1_stream(const P1Args& a, int sms, int per_sm, cudaStream_t s) {
   if (a.nitems == 0) return;
-  const int grid = grid_for(p1_stream_kernel, sms, per_sm, a.nitems);
-  p1_stream_kernel<<<grid, kThreads, 0, s>>>(a);
+  const int grid = stream_grid(p1_stream_kernel, sms, per_sm, a.nitems);
+  p1_stream_kernel<<<grid, kStreamThreads, sizeof(StreamSmem), s>>>(a);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -717,8 +1148,8 @@ void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, int max_r,
-                      cudaStream_t s) {
+void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::int64_t lu_total,
+                      int max_r, cudaStream_t s) {
   if (nseg == 0 || max_r == 0) return;
   // scratch for a batch of column-major inverses
   const std::int64_t batch = std::max<std::int64_t>(1, std::min<std::int64_t>(
@@ -727,18 +1158,19 @@ void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, int m
   H3D_CUDA_CHECK(cudaMallocAsync(&scratch, batch * max_r * max_r * 8, s));
   for (std::int64_t b0 = 0; b0 < nseg; b0 += batch) {
     const std::int64_t nb = std::min(batch, nseg - b0);
-    lu_invert_kernel<<<static_cast<unsigned>(nb), 128, 0, s>>>(segs + b0, nb, lu, scratch, max_r);
+    lu_invert_kernel<<<static_cast<unsigned>(nb), 128, 0, s>>>(segs + b0, nb, lu, lu_total, scratch,
+                                                              max_r);
     H3D_CUDA_CHECK(cudaGetLastError());
   }
   H3D_CUDA_CHECK(cudaFreeAsync(scratch, s));
 }
 
-void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, double* S,
-                        cudaStream_t s) {
+void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
+                        std::int64_t lu_total, double* S, cudaStream_t s) {
   if (nseg == 0) return;
   constexpr int warps = 4;
-  proxy_solve_kernel<<<static_cast<unsigned>((nseg + warps - 1) / warps), 32 * warps,
-                       warps * 640 * sizeof(double), s>>>(segs, nseg, lu, S);
+  proxy_solve_kernel<<<static_cast<unsigned>((nseg + warps - 1) / warps), 32 * warps, 0, s>>>(
+      segs, nseg, lu, lu_total, S);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -763,9 +1195,9 @@ void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s)
 }
 
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
-  if (a.nleaves == 0) return;
-  const int grid = grid_for(p2_stream_kernel, sms, per_sm, a.nleaves);
-  p2_stream_kernel<<<grid, kThreads, 0, s>>>(a);
+  if (a.n_p2s_items == 0) return;
+  const int grid = stream_grid(p2_stream_kernel, sms, per_sm, a.n_p2s_items);
+  p2_stream_kernel<<<grid, kStreamThreads, sizeof(StreamSmem), s>>>(a);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -791,12 +1223,12 @@ void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_combine(const double* cpart, const double* spart, const double* lvl_part,
-                    int n_lvl, std::int64_t n_total, const std::int32_t* perm,
-                    std::int64_t row0, std::int64_t row1, double* b, cudaStream_t s) {
+void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
+                    const std::int32_t* perm, std::int64_t row0, std::int64_t row1, double* b,
+                    cudaStream_t s) {
   if (row1 <= row0) return;
   combine_kernel<<<static_cast<unsigned>((row1 - row0 + 255) / 256), 256, 0, s>>>(
-      cpart, spart, lvl_part, n_lvl, n_total, perm, row0, row1, b);
+      cpart, lvl_part, n_lvl, n_total, perm, row0, row1, b);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -12,6 +12,7 @@ namespace h3db {
 
 namespace {
 constexpr std::int64_t kRowChunk = 2048;  // phase-1 stream: rows per item
+static_assert(kRowChunk % kTileRows == 0, "phase-1 stream items start on a row tile");
 constexpr int kColChunk = 256;            // phase-1: columns (targets) per item
 constexpr std::int64_t kSrcChunk = 2048;  // phase-1 proxy: source points per item
 }  // namespace
@@ -160,6 +161,8 @@ void Planner::layout() {
   pair_wy.assign(L_ + 1, {});
   pair_rx.assign(L_ + 1, {});
   pair_ry.assign(L_ + 1, {});
+  pair_cx.assign(L_ + 1, {});
+  pair_cy.assign(L_ + 1, {});
   pair_piv.assign(L_ + 1, {});
   pair_lu.assign(L_ + 1, {});
   for (int l = 1; l <= L_; ++l) {
@@ -200,13 +203,15 @@ void Planner::layout() {
         any = true;
       }
       const std::int64_t g = gid(l, z);
-      const std::int32_t rp = any ? cols + (cols & 1) : 0;
+      const bool stream = mode_[l] == kModeStream;
+      const std::int32_t rp =
+          !any ? 0 : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols : cols + (cols & 1);
       rpad[g] = rp;
       soff[g] = S.s_doubles;
       S.s_doubles += rp;
-      if (mode_[l] == kModeStream) {
+      if (stream) {
         woff[g] = S.w_doubles;
-        S.w_doubles += node_size(l, z) * rp;
+        S.w_doubles += (node_size(l, z) + kTileRows - 1) / kTileRows * kTileRows * rp;
       }
     }
     if (mode_[l] == kModeStream) {
@@ -214,12 +219,16 @@ void Planner::layout() {
       pair_wy[l].resize(P.X.size());
       pair_rx[l].resize(P.X.size());
       pair_ry[l].resize(P.X.size());
+      pair_cx[l].resize(P.X.size());
+      pair_cy[l].resize(P.X.size());
       for (std::size_t p = 0; p < P.X.size(); ++p) {
         const std::int64_t gx = gid(l, P.X[p]), gy = gid(l, P.Y[p]);
-        pair_wx[l][p] = woff[gx] + ec[P.eX[p]];
-        pair_rx[l][p] = rpad[gx];
-        pair_wy[l][p] = woff[gy] + ec[P.eY[p]];
-        pair_ry[l][p] = rpad[gy];
+        pair_wx[l][p] = woff[gx];
+        pair_cx[l][p] = ec[P.eX[p]];
+        pair_rx[l][p] = rpad[gx] / kTileCols;
+        pair_wy[l][p] = woff[gy];
+        pair_cy[l][p] = ec[P.eY[p]];
+        pair_ry[l][p] = rpad[gy] / kTileCols;
       }
     }
   }
@@ -302,19 +311,23 @@ void Planner::layout() {
   // phase-2 proxy items (node-major, thread = target row): b_X += K(X, P_A) s_A
   // for every owned node A of a proxy level, rows in chunks of 256
   p2_items.clear();
+  p2s_items.clear();
   n_proxy_levels = 0;
   for (int l = 1; l <= L_; ++l) {
-    if (mode_[l] != kModeProxy) continue;
-    const int slot = n_proxy_levels++;
+    if (mode_[l] == kModeDirect) continue;
+    const bool stream = mode_[l] == kModeStream;
     const std::int64_t cnt = 1LL << (3 * l);
+    const std::int64_t step = stream ? kTileRows : kColChunk;
+    auto& dst = stream ? p2s_items : p2_items;
+    int slot = -1;
     for (std::int64_t z = 0; z < cnt; ++z) {
       const std::int64_t g = gid(l, z);
       if (rpad[g] == 0 || !owned(l, z)) continue;
+      if (slot < 0) slot = n_proxy_levels++;
       const std::int64_t nr = node_size(l, z);
-      for (std::int64_t r0 = 0; r0 < nr; r0 += kColChunk)
-        p2_items.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
-                                  static_cast<std::int32_t>(std::min<std::int64_t>(kColChunk, nr - r0)),
-                                  slot});
+      for (std::int64_t r0 = 0; r0 < nr; r0 += step)
+        dst.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
+                             static_cast<std::int32_t>(std::min<std::int64_t>(step, nr - r0)), slot});
     }
   }
 

@@ -13,6 +13,24 @@
 
 namespace h3db {
 
+// Stream-level factor pools are tile-major: W_Z (rows x rpad, rows padded to
+// kTileRows, rpad to kTileCols) is stored as kTileRows x kTileCols row-major
+// tiles, tile (rt, ct) at woff + (rt * rpad / kTileCols + ct) * kTileDoubles,
+// so every tile is one contiguous 8 KB bulk copy (cp.async.bulk) for both the
+// column sums of phase 1 and the row dots of phase 2.
+constexpr int kTileRows = 16;
+constexpr int kTileCols = 64;
+constexpr int kTileDoubles = kTileRows * kTileCols;
+#ifdef __CUDACC__
+#define H3D_HD __host__ __device__
+#else
+#define H3D_HD
+#endif
+H3D_HD inline std::int64_t tile_index(std::int64_t i, std::int64_t c, std::int64_t nct) {
+  return ((i / kTileRows) * nct + c / kTileCols) * kTileDoubles + (i % kTileRows) * kTileCols +
+         c % kTileCols;
+}
+
 // How the admissible blocks of one level are applied in the matvec.
 enum LevelMode : int {
   kModeStream = 0,  // explicit ACA factors streamed from the pool W (2 x 8 r(m+n) B)
@@ -47,13 +65,29 @@ struct P1Item {
   std::int64_t pslot;  // -1: write to S through spos; else partial buffer base
 };
 
-// phase-2 proxy item: targets = rows [row0, row0 + nrows) of node `node`
-// (<= 256), sources = the node's proxy list; output slot = proxy-level index
+// phase-2 item: targets = rows [row0, row0 + nrows) of node `node`; proxy
+// levels: <= 256 rows, sources = the node's proxy list; stream levels: one
+// row tile (<= kTileRows rows) dotted with S_node. slot = output partial
+// (one per level with phase-2 work, summed in level order by combine)
 struct P2Item {
   std::int32_t node;
   std::int32_t row0;
   std::int32_t nrows;
   std::int32_t slot;
+};
+
+// Device descriptor of one stream-level work item (engine.cu, from P1Item /
+// P2Item + the node tables), so the bulk-copy producer needs one load per item.
+struct StreamDesc {
+  std::int64_t wbase;  // W offset of the item's first tile
+  std::int64_t aux;    // phase 1: first x row (permuted); phase 2: slot * N + first row
+  std::int64_t sbase;  // phase 2: S offset of the node's columns
+  std::int32_t nrt;    // row tiles
+  std::int32_t ncti;   // column tiles in the item
+  std::int32_t nct;    // column tiles of the node (tile-row stride)
+  std::int32_t nrows;  // rows
+  std::int32_t ncols;  // phase 1: columns
+  std::int32_t pad;
 };
 
 struct P1Reduce {
@@ -122,14 +156,17 @@ class Planner {
   std::vector<std::int64_t> woff, soff, rowbeg;
   std::vector<std::int32_t> rpad, rows;
   std::vector<std::int32_t> spos;
-  // per level, per pair: W write offsets (stream levels) or pivot/LU offsets (proxy)
+  // per level, per pair: stream levels: W node base (pair_wx/wy), first column
+  // of the pair's segment (pair_cx/cy) and column tiles of the node
+  // (pair_rx/ry = rpad / kTileCols); proxy levels: pivot/LU offsets
   std::vector<std::vector<std::int64_t>> pair_wx, pair_wy, pair_piv, pair_lu;
-  std::vector<std::vector<std::int32_t>> pair_rx, pair_ry;
+  std::vector<std::vector<std::int32_t>> pair_rx, pair_ry, pair_cx, pair_cy;
   std::vector<ProxySeg> proxy_segs;
   std::vector<P1Item> items;
   std::vector<P1Reduce> reds;
   std::vector<P2Item> p2_items;   // owned nodes of proxy levels, <= 256 rows each
-  int n_proxy_levels = 0;         // output slots of the phase-2 proxy kernel
+  std::vector<P2Item> p2s_items;  // owned nodes of stream levels, one row tile each
+  int n_proxy_levels = 0;         // output slots of the phase-2 proxy + stream passes
   std::int64_t leaf0 = 0, leaf1 = 0;
   std::vector<std::int32_t> near_off, near_ids;
   std::vector<std::int32_t> near_dense;  // per leaf: leading dense entries (self, edge, face)

@@ -419,7 +419,7 @@ def stats(rep: HMatrixRep) -> dict:
 _PLAN_DTYPES = {
     "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
     "spos": np.int32, "pair_wx": np.int64, "pair_wy": np.int64, "pair_rx": np.int32,
-    "pair_ry": np.int32, "pair_piv": np.int64, "pair_lu": np.int64, "near_off": np.int32,
+    "pair_ry": np.int32, "pair_cx": np.int32, "pair_cy": np.int32, "pair_piv": np.int64, "pair_lu": np.int64, "near_off": np.int32,
     "near_ids": np.int32, "near_dense": np.int32, "node_base": np.int64, "modes": np.int32, "ranges": np.int64,
     "rank_rows": np.int64, "sizes": np.int64,
     # structs, decoded as int64 fields (see csrc/planner.h)
@@ -431,6 +431,10 @@ _PLAN_DTYPES = {
                        ("pslot", np.int64)]),
     "reds": np.dtype([("node", np.int32), ("ncols", np.int32), ("nchunks", np.int32),
                       ("pad", np.int32), ("pbase", np.int64)]),
+    "p2_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
+                          ("slot", np.int32)]),
+    "p2s_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
+                           ("slot", np.int32)]),
 }
 
 

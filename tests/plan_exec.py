@@ -39,6 +39,21 @@ def oracle_inputs(oracle, n, seed, n_max, eps, kind):
                 ppts=pts[perm])
 
 
+TILE_R, TILE_C = 16, 64  # csrc/planner.h kTileRows / kTileCols
+
+
+def tile_index(i, c, nct):
+    """Offset of element (row i, column c) in a tile-major stream-level pool."""
+    return ((i // TILE_R) * nct + c // TILE_C) * (TILE_R * TILE_C) + (i % TILE_R) * TILE_C + c % TILE_C
+
+
+def node_matrix(W, woff, g, rows, R):
+    """Row-major (rows x R) view of node g's tile-major factor pool."""
+    nrp = -(-rows // TILE_R) * TILE_R
+    t = W[woff: woff + nrp * R].reshape(nrp // TILE_R, R // TILE_C, TILE_R, TILE_C)
+    return t.transpose(0, 2, 1, 3).reshape(nrp, R)[:rows]
+
+
 def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
     """Returns b in Morton order for the plan's owned rows (others zero)."""
     L, off, ppts, pd = inp["L"], inp["offsets"], inp["ppts"], inp["pairs"]
@@ -60,6 +75,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
     lu = np.zeros(max(sizes[4], 1))
     woff, soff, rowbeg = plan.array("woff"), plan.array("soff"), plan.array("rowbeg")
     rpad, spos, nb = plan.array("rpad"), plan.array("spos"), plan.array("node_base")
+    rows = plan.array("rows")
 
     def pts_of(l, z):
         return ppts[off[l][z]:off[l][z + 1]]
@@ -69,6 +85,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         if md[l] == 0:
             wx, wy = plan.array("pair_wx", l), plan.array("pair_wy", l)
             rx, ry = plan.array("pair_rx", l), plan.array("pair_ry", l)
+            cx, cy = plan.array("pair_cx", l), plan.array("pair_cy", l)
         elif md[l] == 1:
             po, lo = plan.array("pair_piv", l), plan.array("pair_lu", l)
         for p, (a, b) in enumerate(zip(X, Y)):
@@ -82,10 +99,10 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             if md[l] == 0:
                 FX = np.linalg.solve(Um.T, kernel_matrix(kind, Xp, Yp[cp]).T).T  # K(X,tau) R^-1
                 FY = np.linalg.solve(Lm, kernel_matrix(kind, Yp, Xp[rp]).T).T    # K(Y,sigma) L^-T
-                for i in range(len(Xp)):
-                    W[wx[p] + i * rx[p]: wx[p] + i * rx[p] + r] = FX[i]
-                for j in range(len(Yp)):
-                    W[wy[p] + j * ry[p]: wy[p] + j * ry[p] + r] = FY[j]
+                I, Q = np.meshgrid(np.arange(len(Xp)), np.arange(r), indexing="ij")
+                W[wx[p] + tile_index(I, cx[p] + Q, rx[p])] = FX
+                J, Q = np.meshgrid(np.arange(len(Yp)), np.arange(r), indexing="ij")
+                W[wy[p] + tile_index(J, cy[p] + Q, ry[p])] = FY
             elif md[l] == 1:
                 piv[po[p]: po[p] + r] = rp
                 piv[po[p] + r: po[p] + 2 * r] = cp
@@ -104,9 +121,9 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         c0, nc = int(it["col0"]), int(it["ncols"])
         xs = xp[rb: rb + it["nrows"]]
         if it["kind"] == 0:
-            R = int(rpad[g])
-            Wn = W[woff[g]: woff[g] + (it["row0"] + it["nrows"]) * R].reshape(-1, R)[it["row0"]:]
-            v = Wn[:, c0: c0 + nc].T @ xs
+            assert it["row0"] % TILE_R == 0 and c0 % TILE_C == 0
+            Wn = node_matrix(W, woff[g], g, int(rows[g]), int(rpad[g]))
+            v = Wn[it["row0"]: it["row0"] + it["nrows"], c0: c0 + nc].T @ xs
         else:
             v = kernel_matrix(kind, Q[soff[g] + c0: soff[g] + c0 + nc], ppts[rb: rb + it["nrows"]]) @ xs
         if it["pslot"] < 0:
@@ -134,36 +151,60 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             S[so: so + r] = np.linalg.solve(Um, np.linalg.solve(Lm, v))
         else:
             S[so: so + r] = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, v))
-    # ---- phase 2
+    # ---- phase 2: near field + direct leaf blocks per owned leaf (cpart),
+    # proxy / stream levels per node row chunk into one partial per level
     leaf0, leaf1, row0, row1 = plan.array("ranges")
     noff, nids = plan.array("near_off"), plan.array("near_ids")
-    b = np.zeros(len(ppts))
+    n = len(ppts)
+    cpart = np.zeros(n)
     for X in range(leaf0, leaf1):
         xb, xe = off[L][X], off[L][X + 1]
         if xe == xb:
             continue
         T = ppts[xb:xe]
-        acc = np.zeros(xe - xb)
         for Y in nids[noff[X]: noff[X + 1]]:
             yb, ye = off[L][Y], off[L][Y + 1]
             K = kernel_matrix(kind, T, ppts[yb:ye])
             if Y == X:
                 np.fill_diagonal(K, diag)
-            acc += K @ xp[yb:ye]
-        for l in range(1, L + 1):
-            A = X >> (3 * (L - l))
-            g = nb[l] + A
-            R = int(rpad[g])
-            if R == 0:
+            cpart[xb:xe] += K @ xp[yb:ye]
+    items2 = plan.array("p2_items")
+    items2s = plan.array("p2s_items")
+    nslots = 1 + max([int(v) for v in items2["slot"]] + [int(v) for v in items2s["slot"]] + [-1])
+    lvl = np.zeros((nslots, n))
+    hits = np.zeros((L + 1, n), np.int64)
+
+    def level_of(g):
+        return int(np.searchsorted(nb, g, side="right")) - 1
+    for it in items2:
+        g = int(it["node"])
+        R, so = int(rpad[g]), int(soff[g])
+        assert it["nrows"] <= 256
+        r0 = rowbeg[g] + it["row0"]
+        lvl[it["slot"], r0: r0 + it["nrows"]] = kernel_matrix(kind, ppts[r0: r0 + it["nrows"]],
+                                                              Q[so: so + R]) @ S[so: so + R]
+        hits[level_of(g), r0: r0 + it["nrows"]] += 1
+    for it in items2s:
+        g = int(it["node"])
+        R, so = int(rpad[g]), int(soff[g])
+        assert it["nrows"] <= TILE_R and it["row0"] % TILE_R == 0
+        Wn = node_matrix(W, woff[g], g, int(rows[g]), R)
+        r0 = rowbeg[g] + it["row0"]
+        lvl[it["slot"], r0: r0 + it["nrows"]] = Wn[it["row0"]: it["row0"] + it["nrows"]] @ S[so: so + R]
+        hits[level_of(g), r0: r0 + it["nrows"]] += 1
+    assert hits.max(initial=0) <= 1, "a row written twice at one level"
+    # every owned row of a node with partners is covered once at its level
+    for l in range(1, L + 1):
+        if md[l] == 2:
+            continue
+        for z in range(1 << (3 * l)):
+            g = nb[l] + z
+            b0, b1 = off[l][z], off[l][z + 1]
+            if rpad[g] == 0 or b1 == b0 or not (row0 <= b0 < row1):
                 continue
-            so = soff[g]
-            if md[l] == 1:
-                acc += kernel_matrix(kind, T, Q[so: so + R]) @ S[so: so + R]
-            else:
-                ro = xb - rowbeg[g]
-                Wr = W[woff[g] + ro * R: woff[g] + (ro + xe - xb) * R].reshape(-1, R)
-                acc += Wr @ S[so: so + R]
-        b[xb:xe] = acc
+            assert hits[l, b0:b1].sum() == b1 - b0, (l, z)
+    b = np.zeros(n)
+    b[row0:row1] = cpart[row0:row1] + lvl[:, row0:row1].sum(axis=0)
     return b, (int(row0), int(row1))
 
 
