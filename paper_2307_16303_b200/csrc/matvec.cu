@@ -30,6 +30,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace h3db {
 
 namespace {
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
     const bool active = c < it.ncols;
     const double tx = active ? a.qx[qi] : kFar, ty = active ? a.qy[qi] : kFar,
                  tz = active ? a.qz[qi] : kFar;
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j0 = 0; j0 < it.nrows; j0 += kChunk) {
       const int nj = min(kChunk, it.nrows - j0);
       __syncthreads();
@@ -270,18 +273,19 @@ __global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
       }
       __syncthreads();
       int j = 0;
-      for (; j + 1 < nj; j += 2) {
-        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        const double2 u0 = src[2 * j + 2], u1 = src[2 * j + 3];
-        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
-        acc1 = far_acc<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x), u1.y, acc1);
+      for (; j + 3 < nj; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
+          acc[u] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[u]);
+        }
       }
-      if (j < nj) {
+      for (; j < nj; ++j) {
         const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
+        acc[0] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[0]);
       }
     }
-    if (active) p1_write(it, g, c, far_scale<K>() * (acc0 + acc1), a);
+    if (active) p1_write(it, g, c, far_scale<K>() * ((acc[0] + acc[1]) + (acc[2] + acc[3])), a);
   }
 }
 
@@ -665,46 +669,55 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
 }
 
 // ---- phase 2, near field + direct leaf blocks, matrix-free ------------------
-// One owned leaf X per CTA pass (persistent CTAs, work counter). Sources =
-// X's near list flattened (self, edge and face neighbours: the reference's
-// dense blocks; then the leaf-level admissible partners evaluated directly),
-// moved from the packed (x, y, z, w) points into a double-buffered shared
-// stage by cp.async.bulk, one copy per (range, chunk) piece, completion on the
-// buffer's mbarrier. Warp w owns rows [w RPW, (w + 1) RPW) of the leaf
-// (RPW = ceil(m / 8)), lanes stride over the staged sources, each source is
-// evaluated against the warp's RPW rows (RPW independent FP64 chains per
-// lane). Dense-near sources use the full-accuracy rsqrt (+ the diagonal rule
-// on the self block), admissible ones the Newton form. Rows are owned by one
-// warp: the only reduction is the fixed warp butterfly.
-constexpr int kNearStage = 512;  // sources per staged chunk (16 KB)
-
+// Warp-specialised persistent CTA: a producer warp claims owned leaves X,
+// builds X's source range table (self, edge and face neighbours = the
+// reference's dense blocks, then the leaf-level admissible partners evaluated
+// directly) and streams the flattened sources from the packed (x, y, z, w)
+// points into a double-buffered shared stage with cp.async.bulk (one copy per
+// range piece, byte-counted on the buffer's "full" mbarrier); seven consumer
+// warps own the leaf's rows (warp w: rows [w RPW, (w + 1) RPW), RPW =
+// ceil(m / 7) <= 8), lanes stride over the staged sources and evaluate each one
+// against the warp's RPW rows (RPW independent FP64 chains per lane), then
+// release the buffer on its "empty" mbarrier - no block-wide barrier on the
+// hot path. Dense-near sources use the full-accuracy rsqrt (+ the diagonal
+// rule on the self block), admissible ones the Newton form. Every row has
+// one owning warp: the only reduction is the fixed warp butterfly.
+constexpr int kNearStage = 512;            // sources per staged chunk (16 KB)
+constexpr int kNearConsumers = kWarps - 1;  // 7 consumer warps + 1 producer = 256 threads
+constexpr int kNearThreads = 32 * (kNearConsumers + 1);
+constexpr int kNearRows = 8 * kNearConsumers;  // rows per pass (leaves above 56 points: 2 passes)
 constexpr int kMaxNear = kMaxNearRanges;
+
+struct NearMeta {
+  long long xb;   // first permuted row of the leaf
+  int r0, mr;     // row pass: rows [r0, r0 + mr) of the leaf (mr <= kNearRows)
+  int base, cnt;  // flattened index of the chunk's first source, sources in the chunk (< 0: stop)
+  int m, dense_end;  // rows of the leaf (= self range length), end of the dense-near sources
+  int last, pad;     // last chunk of this row pass
+};
 
 struct NearSmem {
   double4 stage[2][kNearStage];
-  unsigned long long full[2];
-  long long rstart[kMaxNear];  // the leaf's source ranges (permuted point index, length)
+  unsigned long long full[2], empty[2];
+  NearMeta meta[2];
+  long long rstart[kMaxNear];  // producer's range table (permuted index, length)
   int rlen[kMaxNear];
-  int cnt[2];
-  int base[2];
-  long long leaf;
-  int nrange, ndense;
 };
 
 // One accumulator per row in the admissible (Newton) scale: dense-near terms
 // enter with weight w / far_scale (exact power-of-two scalings), the caller
 // multiplies by far_scale once.
 template <int K, int RPW>
-__device__ __forceinline__ void near_chunk(const double4* __restrict__ st, int base, int cnt,
-                                           int self_end, int dense_end, int row0,
+__device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const NearMeta& mt, int row0,
                                            const double (&tx)[RPW], const double (&ty)[RPW],
                                            const double (&tz)[RPW], double (&acc)[RPW], double diag,
                                            int lane) {
   constexpr double inv = 1.0 / far_scale<K>();
+  const int base = mt.base, cnt = mt.cnt;
   // [0, e_self): self block (diagonal rule); [e_self, e_dense): dense near;
   // [e_dense, cnt): admissible partners
-  const int e_self = max(0, min(cnt, self_end - base));
-  const int e_dense = max(e_self, min(cnt, dense_end - base));
+  const int e_self = max(0, min(cnt, mt.m - base));
+  const int e_dense = max(e_self, min(cnt, mt.dense_end - base));
   for (int j = lane; j < e_self; j += 32) {
     const double4 q = st[j];
     const double w = inv * q.w;
@@ -729,125 +742,150 @@ __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, int b
   }
 }
 
-// Thread 0: issue the next chunk of the current leaf into buffer b, walking
-// the range cursor (re, roff) over the shared range table.
-__device__ __forceinline__ int near_issue(NearSmem& sm, int b, const Phase2Args& a, int& re, int& roff,
-                                          int vbase) {
-  int filled = 0;
-  while (re < sm.nrange && filled < kNearStage) {
-    const int len = sm.rlen[re];
-    const int take = min(len - roff, kNearStage - filled);
-    if (take > 0) {
-      const unsigned bytes = static_cast<unsigned>(take) * 32u;
-      mbar_expect_tx(&sm.full[b], bytes);
-      bulk_g2s(&sm.stage[b][filled], reinterpret_cast<const double4*>(a.p4) + sm.rstart[re] + roff,
-               bytes, &sm.full[b], 0);
-      filled += take;
-      roff += take;
-    }
-    if (roff >= len) {
-      ++re;
-      roff = 0;
-    }
-  }
-  sm.cnt[b] = filled;
-  sm.base[b] = vbase;
-  mbar_arrive(&sm.full[b]);
-  return filled;
-}
-
+// Consumer warp: one row pass of one leaf, starting at the (already waited)
+// stage t; returns the next stage sequence number.
 template <int K, int RPW>
-__device__ void near_leaf(NearSmem& sm, const Phase2Args& a, std::int64_t X, int r0, int mr,
-                          unsigned (&uses)[2]) {
+__device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::int64_t xb = a.leaf_off[X];
-  const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
-  int total = 0, dense_end = 0;
-  for (int e = 0; e < sm.nrange; ++e) {  // shared broadcasts
-    total += sm.rlen[e];
-    if (e < sm.ndense) dense_end = total;
-  }
-  const int nchunks = (total + kNearStage - 1) / kNearStage;
-  int re = 0, roff = 0, vb = 0;
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < 2 && c < nchunks; ++c) vb += near_issue(sm, c, a, re, roff, vb);
-  }
-  const int row0 = r0 + warp * RPW;
+  const NearMeta m0 = sm.meta[t % 2];
+  const int row0 = m0.r0 + warp * RPW;
   const double4* P4 = reinterpret_cast<const double4*>(a.p4);
   double tx[RPW], ty[RPW], tz[RPW], acc[RPW];
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
-    const bool ok = row0 + r < r0 + mr;
-    const double4 q = ok ? P4[xb + row0 + r] : make_double4(kFar, kFar, kFar, 0.0);
+    const bool ok = row0 + r < m0.r0 + m0.mr;
+    const double4 q = ok ? P4[m0.xb + row0 + r] : make_double4(kFar, kFar, kFar, 0.0);
     tx[r] = q.x;
     ty[r] = q.y;
     tz[r] = q.z;
     acc[r] = 0.0;
   }
-  for (int c = 0; c < nchunks; ++c) {
-    const int b = c & 1;
-    mbar_wait(&sm.full[b], uses[b] & 1);
-    ++uses[b];
-    near_chunk<K, RPW>(sm.stage[b], sm.base[b], sm.cnt[b], m, dense_end, row0, tx, ty, tz, acc, a.diag,
-                       lane);
-    __syncthreads();  // buffer b consumed
-    if (threadIdx.x == 0 && c + 2 < nchunks) vb += near_issue(sm, b, a, re, roff, vb);
+  for (;;) {
+    const int s = t % 2;
+    const NearMeta mt = sm.meta[s];
+    near_chunk<K, RPW>(sm.stage[s], mt, row0, tx, ty, tz, acc, a.diag, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[s]);
+    ++t;
+    if (mt.last) break;
+    mbar_wait(&sm.full[t % 2], (t / 2) & 1);
   }
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
     const double v = far_scale<K>() * warp_sum(acc[r]);
     const int i = row0 + r;
-    if (lane == r && i < r0 + mr) {
-      if (a.cpart_out) a.cpart_out[xb + i] = v;
-      else a.b[a.perm[xb + i]] = v;
+    if (lane == r && i < m0.r0 + m0.mr) {
+      if (a.cpart_out) a.cpart_out[m0.xb + i] = v;
+      else a.b[a.perm[m0.xb + i]] = v;
     }
   }
+  return t;
+}
+
+// Producer (lane 0): wait for the stage's slot, publish the chunk's metadata,
+// copy its pieces.
+__device__ __forceinline__ void near_put(NearSmem& sm, unsigned t, NearMeta mt, const double4* p4,
+                                         int& re, int& roff, int nrange) {
+  const int s = t % 2;
+  if (t >= 2) mbar_wait(&sm.empty[s], ((t / 2) - 1) & 1);
+  int filled = 0;
+  if (mt.cnt >= 0) {
+    while (re < nrange && filled < kNearStage) {
+      const int len = sm.rlen[re];
+      const int take = min(len - roff, kNearStage - filled);
+      if (take > 0) {
+        const unsigned bytes = static_cast<unsigned>(take) * 32u;
+        mbar_expect_tx(&sm.full[s], bytes);
+        bulk_g2s(&sm.stage[s][filled], p4 + sm.rstart[re] + roff, bytes, &sm.full[s], 0);
+        filled += take;
+        roff += take;
+      }
+      if (roff >= len) {
+        ++re;
+        roff = 0;
+      }
+    }
+    mt.cnt = filled;
+  }
+  sm.meta[s] = mt;
+  mbar_arrive(&sm.full[s]);
 }
 
 template <int K>
-__global__ void __launch_bounds__(kThreads, 2) p2_near_kernel(const Phase2Args a) {
+__global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Args a) {
   __shared__ __align__(128) NearSmem sm;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(&sm.full[0], 1);
-    mbar_init(&sm.full[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sm.full[b], 1);
+      mbar_init(&sm.empty[b], kNearConsumers);
+    }
     mbar_fence_init();
   }
-  unsigned uses[2] = {0u, 0u};
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) sm.leaf = static_cast<long long>(atomicAdd(a.counter, 1u));
-    __syncthreads();
-    const long long t = sm.leaf;
-    if (t >= a.nleaves) break;
-    const std::int64_t X = a.leaf0 + t;
-    {
-      // range table: self, edge + face neighbours (dense), direct partners
-      const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
-      for (int e = threadIdx.x; e < ne - nb; e += kThreads) {
+  __syncthreads();
+  if (warp == kNearConsumers) {  // producer warp
+    const double4* P4 = reinterpret_cast<const double4*>(a.p4);
+    unsigned t = 0;
+    for (;;) {
+      long long k = 0;
+      if (lane == 0) k = static_cast<long long>(atomicAdd(a.counter, 1u));
+      k = __shfl_sync(0xffffffffu, k, 0);
+      if (k >= a.nleaves) break;
+      const std::int64_t X = a.leaf0 + k;
+      const std::int64_t xb = a.leaf_off[X];
+      const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
+      if (m == 0) continue;
+      const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1], nd = a.near_dense[X];
+      const int nrange = ne - nb;
+      int tot = 0, dense = 0;  // per lane, then warp-reduced (integers: exact)
+      for (int e = lane; e < nrange; e += 32) {
         const std::int32_t Y = a.near_ids[nb + e];
         const std::int64_t yb = a.leaf_off[Y];
+        const int len = static_cast<int>(a.leaf_off[Y + 1] - yb);
         sm.rstart[e] = yb;
-        sm.rlen[e] = static_cast<int>(a.leaf_off[Y + 1] - yb);
+        sm.rlen[e] = len;
+        tot += len;
+        if (e < nd) dense += len;
       }
-      if (threadIdx.x == 0) {
-        sm.nrange = ne - nb;
-        sm.ndense = a.near_dense[X];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        dense += __shfl_xor_sync(0xffffffffu, dense, o);
       }
-      __syncthreads();
+      __syncwarp();
+      if (lane == 0) {
+        const int nchunks = (tot + kNearStage - 1) / kNearStage;
+        for (int r0 = 0; r0 < m; r0 += kNearRows) {
+          const int mr = min(kNearRows, m - r0);
+          int re = 0, roff = 0;
+          for (int c = 0; c < nchunks; ++c, ++t)
+            near_put(sm, t,
+                     NearMeta{xb, r0, mr, c * kNearStage, 0, m, dense, c + 1 == nchunks ? 1 : 0, 0}, P4,
+                     re, roff, nrange);
+        }
+      }
+      __syncwarp();
     }
-    const int m = static_cast<int>(a.leaf_off[X + 1] - a.leaf_off[X]);
-    for (int r0 = 0; r0 < m; r0 += 8 * kWarps) {
-      const int mr = min(8 * kWarps, m - r0);
-      switch ((mr + kWarps - 1) / kWarps) {
-        case 1: near_leaf<K, 1>(sm, a, X, r0, mr, uses); break;
-        case 2: near_leaf<K, 2>(sm, a, X, r0, mr, uses); break;
-        case 3: near_leaf<K, 3>(sm, a, X, r0, mr, uses); break;
-        case 4: near_leaf<K, 4>(sm, a, X, r0, mr, uses); break;
-        case 5: near_leaf<K, 5>(sm, a, X, r0, mr, uses); break;
-        case 6: near_leaf<K, 6>(sm, a, X, r0, mr, uses); break;
-        case 7: near_leaf<K, 7>(sm, a, X, r0, mr, uses); break;
-        default: near_leaf<K, 8>(sm, a, X, r0, mr, uses); break;
-      }
+    if (lane == 0) {
+      int re = 0, roff = 0;
+      near_put(sm, t, NearMeta{0, 0, 0, 0, -1, 0, 0, 1, 0}, P4, re, roff, 0);
+    }
+    return;
+  }
+  unsigned t = 0;
+  for (;;) {
+    mbar_wait(&sm.full[t % 2], (t / 2) & 1);
+    const NearMeta mt = sm.meta[t % 2];
+    if (mt.cnt < 0) break;
+    switch ((mt.mr + kNearConsumers - 1) / kNearConsumers) {
+      case 1: t = near_consume<K, 1>(sm, a, t); break;
+      case 2: t = near_consume<K, 2>(sm, a, t); break;
+      case 3: t = near_consume<K, 3>(sm, a, t); break;
+      case 4: t = near_consume<K, 4>(sm, a, t); break;
+      case 5: t = near_consume<K, 5>(sm, a, t); break;
+      case 6: t = near_consume<K, 6>(sm, a, t); break;
+      case 7: t = near_consume<K, 7>(sm, a, t); break;
+      default: t = near_consume<K, 8>(sm, a, t); break;
     }
   }
 }
@@ -955,7 +993,7 @@ __global__ void __launch_bounds__(kThreads, 2) p2_proxy_kernel(const Phase2Args 
     const std::int64_t p = a.nt.rowbeg[g] + it.row0 + i;
     const double tx = active ? a.px[p] : kFar, ty = active ? a.py[p] : kFar,
                  tz = active ? a.pz[p] : kFar;
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int j0 = 0; j0 < R; j0 += kChunk) {
       const int nj = min(kChunk, R - j0);
       __syncthreads();
@@ -966,19 +1004,21 @@ __global__ void __launch_bounds__(kThreads, 2) p2_proxy_kernel(const Phase2Args 
       }
       __syncthreads();
       int j = 0;
-      for (; j + 1 < nj; j += 2) {
-        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        const double2 u0 = src[2 * j + 2], u1 = src[2 * j + 3];
-        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
-        acc1 = far_acc<K>(sq3(tx - u0.x, ty - u0.y, tz - u1.x), u1.y, acc1);
+      for (; j + 3 < nj; j += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
+          acc[u] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[u]);
+        }
       }
-      if (j < nj) {
+      for (; j < nj; ++j) {
         const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        acc0 = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc0);
+        acc[0] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[0]);
       }
     }
     if (active)
-      a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + p] = far_scale<K>() * (acc0 + acc1);
+      a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + p] =
+          far_scale<K>() * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
   }
 }
 
@@ -1032,9 +1072,15 @@ __global__ void __launch_bounds__(kThreads) near_scan_kernel(const Phase2Args a,
 }
 
 template <class F>
-int grid_for(F kernel, int sms, int per_sm, std::int64_t work) {
+int grid_for(F kernel, int sms, int per_sm, std::int64_t work, int threads = kThreads) {
   int nb = 0;
-  H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kThreads, 0));
+  H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0));
+  if (std::getenv("H3D_DEBUG_GRID")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, kernel);
+    std::fprintf(stderr, "grid_for: threads %d regs %d smem %zu occ %d per_sm %d\n", threads, fa.numRegs,
+                 fa.sharedSizeBytes, nb, per_sm);
+  }
   const std::int64_t g = static_cast<std::int64_t>(sms) * std::max(1, std::min(nb, per_sm));
   return static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(g, work)));
 }
@@ -1064,20 +1110,29 @@ void launch_pack_points(const double* px, const double* py, const double* pz, st
 
 void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   if (a.nleaves == 0) return;
+  static bool carve = false;  // two 36 KB CTAs per SM need the shared-heavy carveout
+  if (!carve) {
+    for (const void* f : {reinterpret_cast<const void*>(p2_near_kernel<kLaplace>),
+                          reinterpret_cast<const void*>(p2_near_kernel<kR4>),
+                          reinterpret_cast<const void*>(p2_near_kernel<kHelmholtz>)})
+      H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+    carve = true;
+  }
   switch (a.kernel) {
     case kLaplace: {
-      const int grid = grid_for(p2_near_kernel<kLaplace>, sms, per_sm, a.nleaves);
-      p2_near_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p2_near_kernel<kLaplace>, sms, per_sm, a.nleaves, kNearThreads);
+      p2_near_kernel<kLaplace><<<grid, kNearThreads, 0, s>>>(a);
       break;
     }
     case kR4: {
-      const int grid = grid_for(p2_near_kernel<kR4>, sms, per_sm, a.nleaves);
-      p2_near_kernel<kR4><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p2_near_kernel<kR4>, sms, per_sm, a.nleaves, kNearThreads);
+      p2_near_kernel<kR4><<<grid, kNearThreads, 0, s>>>(a);
       break;
     }
     default: {
-      const int grid = grid_for(p2_near_kernel<kHelmholtz>, sms, per_sm, a.nleaves);
-      p2_near_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p2_near_kernel<kHelmholtz>, sms, per_sm, a.nleaves, kNearThreads);
+      p2_near_kernel<kHelmholtz><<<grid, kNearThreads, 0, s>>>(a);
       break;
     }
   }
