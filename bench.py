@@ -51,11 +51,18 @@ REF_SAMPLE_N = {"c1": 4096, "c2": 65536, "c3": 262144, "c4": 65536, "c5": 262144
 
 FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
 # FP64 peak is not in MEASURED_PEAKS.json; measured on this pool's B200 with
-# tools/fp64_bench.cu (17.49 T DFMA/s sustained, profiles/r01_summary.md)
-FP64_TFLOPS = 35.0
-# FP64 flops per kernel evaluation (SURVEY.md section 8(d) convention: 3 sub +
-# 3 mul + 2 add for r^2, rsqrt, 1 FMA = 2)
-FLOPS_PER_EVAL = {"laplace3d": 11, "r4": 12, "helmholtz-re": 30}
+# tools/fp64_bench.cu: 17.49 T DFMA/s sustained = 35.0 TFLOP/s (profiles/r01_summary.md).
+# The FP64 roofline counts FP64-pipe instructions (DADD/DMUL/DFMA all issue at
+# the DFMA rate) and reports them FMA-equivalent: achieved TFLOP/s = 2 x
+# instructions/s, peak 35.0.
+FP64_INSTR_PEAK = 17.49e12
+FP64_TFLOPS = 2 * FP64_INSTR_PEAK / 1e12
+# FP64-pipe instructions per kernel evaluation (SASS of the matvec kernels):
+# r^2 = 3 DADD + DMUL + 2 DFMA; Laplace admissible (Newton form) 4 more,
+# dense-near (third-order rsqrt) 6 more; 1/r^4 and cos(r)/r use the exact
+# radial maps (reciprocal / sincos sequences).
+INSTR_FAR = {"laplace3d": 10, "r4": 12, "helmholtz-re": 40}
+INSTR_NEAR = {"laplace3d": 12, "r4": 12, "helmholtz-re": 40}
 
 
 def peaks():
@@ -234,7 +241,6 @@ def main():
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    rep.profile(True, args.steps)
     if dist:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -249,13 +255,21 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
-    prof, nprof = rep.profile_read()
-    rep.profile(False, 1)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = n / (ms * 1e-3) / 1e6
+
+    # ---- per-kernel durations: the same K steps again with a CUDA-event pair
+    # around every kernel on its own lane (untimed for the headline number)
+    rep.profile(True, args.steps)
+    for _ in range(args.steps):
+        rep.matvec_async(x.data_ptr(), b.data_ptr(), sp)
+    torch.cuda.synchronize(dev)
+    prof, nprof = rep.profile_read()
+    kern = rep.profile_kernels()
+    rep.profile(False, 1)
 
     # ---- e2e: the public C-ABI call with pinned host buffers (H2D x, D2H b)
     xh = torch.from_numpy(x_host.copy()).pin_memory()
@@ -293,45 +307,65 @@ def main():
         except Exception as e:  # checker unavailable: report, never substitute
             rel_err = f"unavailable: {e}"
 
-    # ---- roofline of the dominant kernel: T_roof = max(bytes / HBM, flops / FP64)
+    # ---- roofline. Algorithmic work per launch of each kernel (DESIGN.md
+    # section 6): stream kernels = the streamed factor bytes of one phase;
+    # proxy kernels = one phase's regenerated entries x FP64 instructions per
+    # entry; near pass = dense-near + direct entries; solves = both
+    # orientations' triangular inverses. Dominant kernel = largest mean
+    # CUDA-event duration (lanes overlap, so shares are of the summed kernel time).
     hbm, peak_src = peaks()
-    p1 = prof.phase1_ms / max(nprof, 1)
-    p2 = prof.phase2_ms / max(nprof, 1)
-    F = st["factor_doubles"]          # streamed factor doubles (stream levels)
-    T = st["tvec_doubles"]
-    U = st["proxy_units"]             # regenerated entries per phase (proxy levels)
-    NE = st["near_entries"] + st["direct_evals"]
-    nloc = st["owned_row_end"] - st["owned_row_begin"]
-    fpe = FLOPS_PER_EVAL[cfg["kernel"]]
-    k1 = dict(name="phase1_kernel (stream V^T x | proxy K(P,Z) x)", bytes=8 * F + 8 * T + 8 * n,
-              flops=fpe * U, ms=p1)
-    k2 = dict(name="phase2_kernel (near + direct + stream U t | proxy K(X,P) s, un-permute)",
-              bytes=8 * F + 8 * T + 44 * nloc, flops=fpe * (U + NE), ms=p2)
-    for k in (k1, k2):
-        tb = k["bytes"] / (hbm * 1e9)
-        tf = k["flops"] / (FP64_TFLOPS * 1e12)
-        k["bound"] = "hbm" if tb >= tf else "fp64"
-        k["t_roof_ms"] = max(tb, tf) * 1e3
-    kd = k2 if p2 >= p1 else k1
-    if kd["bound"] == "hbm":
-        achieved, peak, unit, peak_note = kd["bytes"] / (kd["ms"] * 1e-3) / 1e9, hbm, "GB/s", peak_src
-    else:
-        achieved, peak, unit = kd["flops"] / (kd["ms"] * 1e-3) / 1e12, FP64_TFLOPS, "TFLOP/s"
-        peak_note = "measured fp64 DFMA peak (tools/fp64_bench.cu, profiles/r01_summary.md)"
+    F = st["factor_doubles"]           # streamed factor doubles per phase (stream levels)
+    U = st["proxy_units"]              # regenerated entries per phase (proxy levels)
+    NEAR, DIRECT = st["near_entries"], st["direct_evals"]
+    LU = st["lu_doubles"]
+    kf, kn = INSTR_FAR[cfg["kernel"]], INSTR_NEAR[cfg["kernel"]]
+    nlev = sum(1 for m in st["level_modes"][1:st["depth"] + 1] if m in (0, 1))
+    work = {
+        "p1_stream": ("hbm", 8.0 * F), "p2_stream": ("hbm", 8.0 * F),
+        "p1_proxy": ("fp64", kf * U), "p2_proxy": ("fp64", kf * U),
+        "near": ("fp64", kn * NEAR + kf * DIRECT), "solve": ("hbm", 2 * 8.0 * LU),
+        "gather": ("hbm", 8.0 * (4 * n)), "combine": ("hbm", 8.0 * n * (2 + nlev)),
+        "red_stream": ("hbm", 0.0), "red_proxy": ("hbm", 0.0),
+    }
+    kstats = {}
+    for k, (tot, cnt, start) in kern.items():
+        if cnt == 0:
+            continue
+        kms = tot / cnt
+        bound, w = work[k]
+        if bound == "hbm":
+            ach, pk, unit = w / (kms * 1e-3) / 1e9, hbm, "GB/s"
+        else:
+            ach, pk, unit = 2 * w / (kms * 1e-3) / 1e12, FP64_TFLOPS, "TFLOP/s"
+        kstats[k] = dict(ms=round(kms, 4), start_ms=round(start / cnt, 4), bound=bound,
+                         achieved=round(ach, 3), peak=pk, unit=unit, frac=round(ach / pk, 4))
+    ksum = sum(v["ms"] for v in kstats.values())
+    for v in kstats.values():
+        v["share"] = round(v["ms"] / ksum, 4) if ksum else None
+    dom = max(kstats, key=lambda k: kstats[k]["ms"])
+    kd = kstats[dom]
     traffic = None
     tr = ROOT / "profiles" / "ncu_traffic.json"
     if tr.exists():
         try:
             d = json.loads(tr.read_text())
-            key = "phase2" if p2 >= p1 else "phase1"
-            if d.get("config") == args.config and d.get("policy", "stream") == args.policy \
-                    and d.get(key) is not None:
-                traffic = d[key]
+            if d.get("config") == args.config and d.get("level_modes") == st["level_modes"][:st["depth"] + 1]:
+                traffic = d.get("kernels", {}).get(dom)
         except Exception:
             traffic = None
-    step_bytes = k1["bytes"] + k2["bytes"]
-    step_flops = k1["flops"] + k2["flops"]
-    step_roof_ms = max(step_bytes / (hbm * 1e9), step_flops / (FP64_TFLOPS * 1e12)) * 1e3
+    # step roofline: both resources busy the whole step at best
+    step_bytes = sum(work[k][1] for k in kstats if work[k][0] == "hbm")
+    step_instr = sum(work[k][1] for k in kstats if work[k][0] == "fp64")
+    t_hbm = step_bytes / (hbm * 1e9) * 1e3
+    t_fp = step_instr / FP64_INSTR_PEAK * 1e3
+    step_roof_ms = max(t_hbm, t_fp)
+    # the factor-streaming representation's HBM roofline (what the reference's
+    # matvec would need on this GPU): every level's factors read in both
+    # phases + the stored dense near field (leaf-level admissible blocks that
+    # we evaluate directly are left out: a lower bound)
+    units_all = sum(st["level_units"][1:st["depth"] + 1])
+    stream_repr_bytes = 2 * 8.0 * units_all + 8.0 * NEAR + 16.0 * n
+    t_stream_repr = stream_repr_bytes / (hbm * 1e9) * 1e3
 
     if rank != 0:
         if dist:
@@ -365,33 +399,44 @@ def main():
                                "note": "one ACA per unordered admissible pair; stream = explicit "
                                        "factors in HBM, proxy = pivots+LU regenerated in FP64, "
                                        "direct = exact leaf blocks"},
-            "streamed_factor_GB": round(8 * F / 1e9, 3),
+            "streamed_factor_GB_per_phase": round(8 * F / 1e9, 3),
             "proxy_entries_per_phase": U,
             "lu_GB": round(8 * st["lu_doubles"] / 1e9, 3),
             "near_field": args.near,
             "parallelism": f"Morton-subtree row ownership over {world} GPU(s), NCCL all-gather of x",
-            "l2": f"inputs larger than L2: factor+LU pools {8 * (F + st['lu_doubles']) / 1e9:.1f} GB "
-                  f">> 126 MB L2 (per-step working set re-read from HBM)",
+            "l2": f"inputs larger than L2: per-step working set (factor pool, LU inverses, proxy "
+                  f"points/t-vectors, packed points) "
+                  f"{8 * (st['factor_bytes_alloc'] / 8 + 2 * LU + 4 * st['tvec_doubles'] + 5 * n) / 1e9:.2f} GB "
+                  f">> 126 MB L2",
             "aca_build_s": round(build_s, 3),
             "build_ms": {k: round(st[k], 1) for k in ("build_ms_tree", "build_ms_lists",
                                                        "build_ms_aca_rank", "build_ms_aca_write",
                                                        "build_ms_total")},
             "depth": st["depth"], "aca_pairs": st["aca_pairs"], "max_rank": st["max_rank"],
             "phase_ms": {"gather_or_exchange": round((prof.gather_ms + prof.exchange_ms) / max(nprof, 1), 4),
-                         "phase1": round(p1, 4), "phase2": round(p2, 4)},
+                         "phase1_to_solves": round(prof.phase1_ms / max(nprof, 1), 4),
+                         "rest": round(prof.phase2_ms / max(nprof, 1), 4)},
+            "kernels": kstats,
             "step_roofline": {"t_roof_ms": round(step_roof_ms, 3), "frac": round(step_roof_ms / ms, 4),
-                              "bytes": step_bytes, "fp64_flops": step_flops},
-            "phase_roofline": {"phase1": {"bound": k1["bound"], "t_roof_ms": round(k1["t_roof_ms"], 3),
-                                          "frac": round(k1["t_roof_ms"] / max(p1, 1e-9), 4)},
-                               "phase2": {"bound": k2["bound"], "t_roof_ms": round(k2["t_roof_ms"], 3),
-                                          "frac": round(k2["t_roof_ms"] / max(p2, 1e-9), 4)}},
+                              "t_hbm_ms": round(t_hbm, 3), "t_fp64_ms": round(t_fp, 3),
+                              "hbm_bytes": step_bytes, "fp64_instr": step_instr,
+                              "note": "max(bytes / HBM peak, FP64-pipe instructions / DFMA peak) "
+                                      "over all kernels of one step"},
+            "hbm_roofline_factor_streaming": {
+                "t_roof_ms": round(t_stream_repr, 3), "frac": round(t_stream_repr / ms, 4),
+                "bytes": stream_repr_bytes,
+                "note": "HBM time of the reference's representation (all ACA factors streamed in "
+                        "both phases + stored dense near field) at the measured peak; frac > 1 = "
+                        "faster than any factor-streaming matvec can be"},
             "rel_err_vs_exact_200_rows": rel_err,
         },
-        "roofline": {"bound": kd["bound"], "kernel": kd["name"], "achieved": round(achieved, 3),
-                     "peak": peak, "peak_source": peak_note, "unit": unit,
-                     "frac": round(kd["t_roof_ms"] / kd["ms"], 4), "traffic": traffic,
-                     "alg_bytes_per_launch": kd["bytes"], "alg_fp64_flops_per_launch": kd["flops"],
-                     "t_roof_ms": round(kd["t_roof_ms"], 3), "t_ms": round(kd["ms"], 3)},
+        "roofline": {"bound": kd["bound"], "kernel": dom, "achieved": kd["achieved"],
+                     "peak": kd["peak"], "peak_source": peak_src if kd["bound"] == "hbm" else
+                     "measured FP64 DFMA rate x 2 (tools/fp64_bench.cu, profiles/r01_summary.md)",
+                     "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic,
+                     "alg_work_per_launch": work[dom][1],
+                     "alg_work_unit": "bytes" if kd["bound"] == "hbm" else "FP64-pipe instructions",
+                     "t_ms": kd["ms"], "share_of_kernel_time": kd["share"]},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "Mpoints/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms},

@@ -154,6 +154,25 @@ int h3d_dev_matvec_async(h3d_dev* dev, const double* x_dev, double* b_dev, void*
  * calls (*steps). Used by bench.py for live per-kernel durations. */
 int h3d_dev_profile(h3d_dev* dev, int enable, int64_t capacity);
 int h3d_dev_profile_read(h3d_dev* dev, h3d_timing* sum, int64_t* steps);
+/* Per-kernel CUDA-event durations of the profiled calls, summed (ms), launch
+ * counts and (optional, may be NULL) summed start offsets from the call's
+ * first event, in the order of h3d_kernel_slot; filled by the last
+ * h3d_dev_profile_read. Kernels of different lanes overlap in time. */
+typedef enum {
+  H3D_K_GATHER = 0,    /* x -> Morton order (+ packed weights) */
+  H3D_K_P1_STREAM,     /* phase 1, stream levels (bulk-copy tile pipeline, HBM) */
+  H3D_K_RED_STREAM,    /* phase-1 partial reductions, stream levels */
+  H3D_K_P2_STREAM,     /* phase 2, stream levels */
+  H3D_K_P1_PROXY,      /* phase 1, proxy levels (FP64) */
+  H3D_K_RED_PROXY,     /* phase-1 partial reductions, proxy levels */
+  H3D_K_SOLVE,         /* proxy triangular solves */
+  H3D_K_P2_PROXY,      /* phase 2, proxy levels (FP64) */
+  H3D_K_NEAR,          /* near field + direct leaf blocks (FP64) */
+  H3D_K_COMBINE,       /* sum of the per-level partials, un-permute */
+  H3D_K_COUNT
+} h3d_kernel_slot;
+int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launches, double* start_sum,
+                            int count);
 
 /* Replaces h3d::stats(rep) (hmatrix.hpp:85). */
 int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out);

@@ -4,7 +4,7 @@
 #include <random>
 #include <string>
 
-#include <nccl.h>
+#include "nccl_dyn.h"
 
 #include "../../include/h3d_b200.h"
 #include "engine.h"
@@ -139,6 +139,14 @@ int h3d_dev_profile_read(h3d_dev* dev, h3d_timing* sum, int64_t* steps) {
   });
 }
 
+int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launches, double* start_sum,
+                            int count) {
+  return guarded([&] {
+    if (!dev || !ms_sum || !launches) throw h3db::InvalidArgument("profile_kernels: null argument");
+    eng(dev)->profile_kernels(ms_sum, launches, start_sum, count);
+  });
+}
+
 int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out) {
   return guarded([&] { eng(dev)->stats(out); });
 }
@@ -160,8 +168,8 @@ int h3d_dev_export_pairs(const h3d_dev* dev, int level, int32_t* x, int32_t* y, 
 int h3d_nccl_get_id(void* id128) {
   return guarded([&] {
     ncclUniqueId id;
-    const ncclResult_t r = ncclGetUniqueId(&id);
-    if (r != ncclSuccess) throw h3db::NcclFailure(ncclGetErrorString(r));
+    const ncclResult_t r = h3db::nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) throw h3db::NcclFailure(h3db::nccl().GetErrorString(r));
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     std::memcpy(id128, &id, sizeof(id));
   });

@@ -168,16 +168,30 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned b
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+// Waits for the phase with the given parity. Between probes the warp sleeps
+// (growing backoff): the pipeline kernels share SMs with FP64-bound kernels
+// and a spinning waiter would take their issue slots.
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
   unsigned done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!done);
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+#ifndef H3D_MBAR_SLEEP_MAX
+#define H3D_MBAR_SLEEP_MAX 0
+#endif
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned ns = 16;
+  while (!mbar_try(b, parity)) {
+    if (H3D_MBAR_SLEEP_MAX > 0) {
+      __nanosleep(ns);
+      if (ns < H3D_MBAR_SLEEP_MAX) ns <<= 1;
+    }
+  }
 }
 __device__ __forceinline__ unsigned long long l2_evict_first() {
   unsigned long long pol;

@@ -16,7 +16,7 @@
 #include <cstring>
 #include <numeric>
 
-#include <nccl.h>
+#include "nccl_dyn.h"
 
 namespace h3db {
 
@@ -30,14 +30,25 @@ double ms_since(Clock::time_point t0) {
 constexpr int kMaxDepth = 8;       // 8^8 leaves; beyond that the device tables explode
 constexpr int kMaxProxyRank = 320; // proxy_solve_kernel's per-warp shared buffer
 
-// Cost model (profiles/r01_summary.md): streamed factor bytes at the measured
-// copy bandwidth, regenerated entries at the measured P2P evaluation rate.
-constexpr double kStreamBW = 6.2e12;  // B/s
-double eval_rate(int kernel) {
+// Cost model (calibrated on the r01 C3 runs): the
+// stream levels are HBM-bound (factor bytes twice per matvec at the bulk-copy
+// kernels' measured rate), the proxy levels and the near/direct pass are
+// FP64-bound (measured evaluation rates of the regenerating kernels); the two
+// lanes overlap imperfectly: T = max(H, D) + kOverlapLoss * min(H, D).
+constexpr double kStreamBW = 7.0e12;   // B/s, tile-pipeline read rate
+constexpr double kOverlapLoss = 0.35;
+double proxy_rate(int kernel) {  // evaluations / s, Newton-form proxy kernels
   switch (kernel) {
-    case kLaplace: return 1.0e12;  // effective rate of the regenerating kernels (r01)
+    case kLaplace: return 1.4e12;
+    case kR4: return 1.0e12;
+    default: return 0.2e12;
+  }
+}
+double near_rate(int kernel) {   // evaluations / s, near field + direct blocks
+  switch (kernel) {
+    case kLaplace: return 1.1e12;
     case kR4: return 0.8e12;
-    default: return 0.25e12;
+    default: return 0.15e12;
   }
 }
 
@@ -45,7 +56,7 @@ double eval_rate(int kernel) {
   do {                                                                          \
     ncclResult_t r_ = (expr);                                                   \
     if (r_ != ncclSuccess)                                                      \
-      throw NcclFailure(std::string("NCCL error: ") + ncclGetErrorString(r_) + \
+      throw NcclFailure(std::string("NCCL error: ") + nccl().GetErrorString(r_) + \
                         " (" #expr ")");                                        \
   } while (0)
 
@@ -128,14 +139,18 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2c") tune_.p2c = v;
         else if (k == "p2s") tune_.p2s = v;
         else if (k == "p2p") tune_.p2p = v;
-        else if (k == "at") tune_.at = v;
       }
       pos = end + 1;
     }
   }
   H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
-  H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream2_, cudaStreamNonBlocking));
-  H3D_CUDA_CHECK(cudaStreamCreateWithFlags(&stream3_, cudaStreamNonBlocking));
+  {
+    int least = 0, greatest = 0;
+    H3D_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, greatest));
+    H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream4_, cudaStreamNonBlocking, greatest));
+    H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream3_, cudaStreamNonBlocking, least));
+  }
   for (auto& e : ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
   for (int k = 0; k < 3; ++k) {
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&fork_[k], cudaEventDisableTiming));
@@ -187,13 +202,14 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
 Engine::~Engine() {
   for (auto e : prof_ev_)
     if (e) cudaEventDestroy(e);
-  if (nccl_comm_) ncclCommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+  if (nccl_comm_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   for (int k = 0; k < 3; ++k) {
     if (fork_[k]) cudaEventDestroy(fork_[k]);
     if (join_[k]) cudaEventDestroy(join_[k]);
   }
+  if (stream4_) cudaStreamDestroy(stream4_);
   if (stream3_) cudaStreamDestroy(stream3_);
   if (stream2_) cudaStreamDestroy(stream2_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -513,9 +529,9 @@ void Engine::choose_modes() {
     }
     fixed /= static_cast<double>(world_);
   }
-  const double E = eval_rate(opt_.kernel_id);
   const double budget = 0.8 * static_cast<double>(free_mem_) - 64.0 * static_cast<double>(n_) -
                         (2 << 30);
+  const double Rp = proxy_rate(opt_.kernel_id), Rn = near_rate(opt_.kernel_id);
   double best = 1e300;
   unsigned best_mask = 0;
   const unsigned ncand = static_cast<unsigned>(cand.size());
@@ -525,19 +541,21 @@ void Engine::choose_modes() {
     for (unsigned i = 0; i < ncand; ++i) {
       const int l = cand[i];
       if (mask & (1u << i)) {
+        // level 1 (8 nodes of N/8 points) streams through long partial-sum
+        // chains and few work items: measured slower than its model, keep it
+        // regenerated unless its ranks exceed the solve kernel's capacity
+        if (l == 1 && maxr[l] <= kMaxProxyRank) ok = false;
         sbytes += 8.0 * units[l];
       } else {
         if (maxr[l] > kMaxProxyRank) ok = false;
-        comp += units[l] / E;
-        lub += 16.0 * lu[l];
+        comp += 2.0 * units[l] / Rp;
+        lub += 2.0 * 8.0 * lu[l];  // both orientations read the pair's inverses once
       }
     }
     if (!ok || sbytes > budget) continue;
-    // the streamed and regenerated passes do not overlap in practice (they
-    // compete for issue slots and occupancy; r01 hybrid runs were additive),
-    // so the per-phase cost is the sum of both
-    const double ts = sbytes / kStreamBW;
-    const double T = 2.0 * (ts + comp) + fixed / E + lub / kStreamBW;
+    const double H = 2.0 * sbytes / kStreamBW;
+    const double D = comp + fixed / Rn + lub / kStreamBW;
+    const double T = std::max(H, D) + kOverlapLoss * std::min(H, D);
     if (T < best) {
       best = T;
       best_mask = mask;
@@ -613,8 +631,14 @@ void Engine::upload_plan() {
   p1_proxy_items_.upload(pi, stream_);
   n_p1s_ = static_cast<std::int64_t>(si.size());
   n_p1p_ = static_cast<std::int64_t>(pi.size());
-  p1_red_.upload(P.reds, stream_);
-  n_red_ = static_cast<std::int64_t>(P.reds.size());
+  {
+    std::vector<P1Reduce> rs, rp;
+    for (const auto& r : P.reds) (r.kind == kModeStream ? rs : rp).push_back(r);
+    p1_red_s_.upload(rs, stream_);
+    p1_red_p_.upload(rp, stream_);
+    n_red_s_ = static_cast<std::int64_t>(rs.size());
+    n_red_p_ = static_cast<std::int64_t>(rp.size());
+  }
   for (std::size_t x = 0; x + 1 < P.near_off.size(); ++x)
     if (P.near_off[x + 1] - P.near_off[x] > kMaxNearRanges)
       throw std::logic_error("planner: leaf near list longer than the near kernel's range table");
@@ -728,14 +752,27 @@ void Engine::near_scan() {
 // Enqueue one matvec on stream s: x (original order, device) -> b (original
 // order, device). ev (optional, 4 events) brackets gather/exchange, phase 1
 // (+ reduce + proxy solves), phase 2. Returns the number of kernels launched.
-std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev) {
+std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev,
+                            std::uint32_t* kmask) {
   const Planner& P = *plan_;
   std::int64_t launches = 0;
+  // profiled calls: a (begin, end) event pair around each kernel on its lane
+  auto kb = [&](int k, cudaStream_t st) {
+    if (kmask) cudaEventRecord(ev[4 + 2 * k], st);
+  };
+  auto ke = [&](int k, cudaStream_t st) {
+    if (kmask) {
+      cudaEventRecord(ev[5 + 2 * k], st);
+      *kmask |= 1u << k;
+    }
+  };
   if (ev) cudaEventRecord(ev[0], s);
   if (world_ == 1 || nccl_comm_ == nullptr) {
     // single GPU, or a shard without a communicator: x is replicated (every
     // rank holds all of it), gather it all locally
+    kb(H3D_K_GATHER, s);
     launch_gather(xin, perm_.get(), n_, xp_.get(), p4_.get(), s);
+    ke(H3D_K_GATHER, s);
     ++launches;
   } else {
     // own slice of x in Morton order, then the all-gather of x over NVLink
@@ -745,14 +782,14 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       ++launches;
     }
     auto comm = static_cast<ncclComm_t>(nccl_comm_);
-    NCCL_CHECK(ncclGroupStart());
+    NCCL_CHECK(nccl().GroupStart());
     for (int r = 0; r < world_; ++r) {
       const std::int64_t c = P.rank_row1[r] - P.rank_row0[r];
       if (c > 0)
-        NCCL_CHECK(ncclBroadcast(xp_.get() + P.rank_row0[r], xp_.get() + P.rank_row0[r],
+        NCCL_CHECK(nccl().Broadcast(xp_.get() + P.rank_row0[r], xp_.get() + P.rank_row0[r],
                                  static_cast<std::size_t>(c), ncclDouble, r, comm, s));
     }
-    NCCL_CHECK(ncclGroupEnd());
+    NCCL_CHECK(nccl().GroupEnd());
     launch_pack_w(xp_.get(), n_, p4_.get(), s);
     ++launches;
   }
@@ -773,80 +810,106 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   a1.qx = qx_.get();
   a1.qy = qy_.get();
   a1.qz = qz_.get();
-  // Streams: s carries the critical path (phase 1 -> reduce -> solve ->
-  // phase-2 proxy levels -> combine); stream3_ runs the near field + direct
-  // leaf blocks (they need x only) from the start, filling whatever the
-  // phase-1 kernels and the latency-bound solve leave idle; stream2_ runs the
-  // HBM-bound stream-level kernels beside the FP64-bound proxy ones.
-  const bool both1 = n_p1s_ > 0 && n_p1p_ > 0;
+  // Two lanes forked from s, joined back for the combine:
+  //   stream2_ (HBM): p1_stream -> stream reductions -> [solves done] -> p2_stream
+  //   stream4_ (FP64): p1_proxy -> proxy reductions -> solves -> p2_proxy ->
+  //            near field + direct leaf blocks
+  // Persistent CTAs with per-SM budgets: one 5-warp bulk-copy CTA per SM holds
+  // HBM near peak, the FP64 kernels fill the remaining registers.
   const bool has_p2 = P.leaf1 > P.leaf0;
   const bool parts = n_lvl_ > 0;  // p2_compute writes partials, combine sums them
+  const bool hbm = n_p1s_ > 0 || n_p2s_ > 0;
+  const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0;
   H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 5 * sizeof(unsigned), s));
   Phase2Args a2 = phase2_args(bout);
   a2.counter = counters_.get() + 2;
   a2.counter2 = counters_.get() + 3;
   a2.counter3 = counters_.get() + 4;
-  auto fork_near = [&]() {
-    if (!has_p2) return;
-    H3D_CUDA_CHECK(cudaEventRecord(fork_[2], s));
-    H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
-    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream3_);
-    else launch_p2_near(a2, sms_, parts ? tune_.p2c : 4, stream3_);
-    ++launches;
-    H3D_CUDA_CHECK(cudaEventRecord(join_[2], stream3_));
-  };
-  if (tune_.at == 0) fork_near();
-  if (both1) {
-    H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
+  H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
+  // HBM lane, phase 1
+  if (hbm) {
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[0], 0));
-    a1.items = p1_stream_items_.get();
-    a1.descs = p1s_desc_.get();
-    a1.nitems = n_p1s_;
-    a1.counter = counters_.get();
-    launch_p1_stream(a1, sms_, tune_.p1s, stream2_);
-    ++launches;
-    H3D_CUDA_CHECK(cudaEventRecord(join_[0], stream2_));
-  } else if (n_p1s_ > 0) {
-    a1.items = p1_stream_items_.get();
-    a1.descs = p1s_desc_.get();
-    a1.nitems = n_p1s_;
-    a1.counter = counters_.get();
-    launch_p1_stream(a1, sms_, 4, s);
-    ++launches;
+    if (n_p1s_ > 0) {
+      a1.items = p1_stream_items_.get();
+      a1.descs = p1s_desc_.get();
+      a1.nitems = n_p1s_;
+      a1.counter = counters_.get();
+      kb(H3D_K_P1_STREAM, stream2_);
+      launch_p1_stream(a1, sms_, fp ? tune_.p1s : 2, stream2_);
+      ke(H3D_K_P1_STREAM, stream2_);
+      ++launches;
+    }
+    if (n_red_s_ > 0) {
+      kb(H3D_K_RED_STREAM, stream2_);
+      launch_phase1_reduce(p1_red_s_.get(), n_red_s_, nt, spos_.get(), P_.get(), S_.get(), stream2_);
+      ke(H3D_K_RED_STREAM, stream2_);
+      ++launches;
+    }
   }
+  // FP64 lane: phase 1 proxy levels -> reductions -> solves
+  H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[0], 0));
   if (n_p1p_ > 0) {
     a1.items = p1_proxy_items_.get();
     a1.nitems = n_p1p_;
     a1.counter = counters_.get() + 1;
-    launch_p1_proxy(a1, opt_.kernel_id, sms_, both1 ? tune_.p1p : 4, s);
+    kb(H3D_K_P1_PROXY, stream4_);
+    launch_p1_proxy(a1, opt_.kernel_id, sms_, hbm ? tune_.p1p : 8, stream4_);
+    ke(H3D_K_P1_PROXY, stream4_);
     ++launches;
   }
-  if (both1) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
-  launch_phase1_reduce(p1_red_.get(), n_red_, nt, spos_.get(), P_.get(), S_.get(), s);
-  launches += n_red_ > 0;
-  if (tune_.at != 0) fork_near();
-  launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), s);
-  launches += n_segs_solve_ > 0;
-  if (ev) cudaEventRecord(ev[2], s);
-  // ---- phase 2: stream levels (HBM) on stream2_, proxy levels on s
-  if (has_p2) {
-    if (n_p2s_ > 0) {
-      H3D_CUDA_CHECK(cudaEventRecord(fork_[1], s));
+  if (n_red_p_ > 0) {
+    kb(H3D_K_RED_PROXY, stream4_);
+    launch_phase1_reduce(p1_red_p_.get(), n_red_p_, nt, spos_.get(), P_.get(), S_.get(), stream4_);
+    ke(H3D_K_RED_PROXY, stream4_);
+    ++launches;
+  }
+  if (n_segs_solve_ > 0) {
+    kb(H3D_K_SOLVE, stream4_);
+    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), stream4_);
+    ke(H3D_K_SOLVE, stream4_);
+    ++launches;
+  }
+  if (ev) cudaEventRecord(ev[2], stream4_);
+  // HBM lane, phase 2: held until the solves are done - the latency-bound
+  // solve blocks lose most of their bandwidth to a saturating bulk stream
+  // (measured 0.6 ms alone vs 6-10 ms beside it), and they gate the FP64 lane
+  if (hbm) {
+    if (n_segs_solve_ > 0) {
+      H3D_CUDA_CHECK(cudaEventRecord(fork_[1], stream4_));
       H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[1], 0));
-      launch_p2_stream(a2, sms_, tune_.p2s, stream2_);
-      ++launches;
-      H3D_CUDA_CHECK(cudaEventRecord(join_[1], stream2_));
     }
+    if (has_p2 && n_p2s_ > 0) {
+      kb(H3D_K_P2_STREAM, stream2_);
+      launch_p2_stream(a2, sms_, fp ? tune_.p2s : 2, stream2_);
+      ke(H3D_K_P2_STREAM, stream2_);
+      ++launches;
+    }
+    H3D_CUDA_CHECK(cudaEventRecord(join_[0], stream2_));
+  }
+  // FP64 lane, phase 2: proxy levels, then the near field + direct leaf
+  // blocks (one persistent FP64 kernel resident at a time next to the HBM
+  // lane's bulk-copy CTA)
+  if (has_p2) {
     if (n_p2_ > 0) {
-      launch_p2_proxy(a2, sms_, n_p2s_ > 0 ? tune_.p2p : 4, s);
+      kb(H3D_K_P2_PROXY, stream4_);
+      launch_p2_proxy(a2, sms_, hbm ? tune_.p2p : 8, stream4_);
+      ke(H3D_K_P2_PROXY, stream4_);
       ++launches;
     }
-    if (n_p2s_ > 0) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
-    H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[2], 0));
-    if (parts) {
-      launch_combine(cpart_.get(), lvl_part_.get(), n_lvl_, n_, perm_.get(), P.row0, P.row1, bout, s);
-      ++launches;
-    }
+    kb(H3D_K_NEAR, stream4_);
+    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream4_);
+    else launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
+    ke(H3D_K_NEAR, stream4_);
+    ++launches;
+  }
+  H3D_CUDA_CHECK(cudaEventRecord(join_[1], stream4_));
+  H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
+  if (hbm) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
+  if (has_p2 && parts) {
+    kb(H3D_K_COMBINE, s);
+    launch_combine(cpart_.get(), lvl_part_.get(), n_lvl_, n_, perm_.get(), P.row0, P.row1, bout, s);
+    ke(H3D_K_COMBINE, s);
+    ++launches;
   }
   if (ev) cudaEventRecord(ev[3], s);
   return launches;
@@ -861,7 +924,7 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
     xin = x_.get();
   }
   double* bout = host ? b_.get() : b;
-  const std::int64_t launches = enqueue(xin, bout, stream_, ev_ + 1);
+  const std::int64_t launches = enqueue(xin, bout, stream_, ev_ + 1, nullptr);
   if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
   cudaEventRecord(ev_[5], stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -886,12 +949,15 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
 void Engine::matvec_async(const double* x, double* b, cudaStream_t s) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
   cudaEvent_t* ev = nullptr;
+  std::uint32_t* mask = nullptr;
   if (prof_on_) {
-    if (prof_used_ >= prof_ev_.size() / 4) throw InvalidArgument("profile ring full; read it first");
-    ev = prof_ev_.data() + 4 * prof_used_;
+    if (prof_used_ >= prof_ev_.size() / kProfEv) throw InvalidArgument("profile ring full; read it first");
+    ev = prof_ev_.data() + kProfEv * prof_used_;
+    mask = prof_mask_.data() + prof_used_;
+    *mask = 0;
     ++prof_used_;
   }
-  prof_launches_ += enqueue(x, b, s, ev);
+  prof_launches_ += enqueue(x, b, s, ev, mask);
 }
 
 void Engine::profile(int enable, std::int64_t capacity) {
@@ -899,20 +965,37 @@ void Engine::profile(int enable, std::int64_t capacity) {
   prof_on_ = enable != 0;
   prof_used_ = 0;
   prof_launches_ = 0;
-  const std::size_t need = static_cast<std::size_t>(4 * std::max<std::int64_t>(capacity, 1));
-  if (prof_on_ && prof_ev_.size() < need) {
+  const std::size_t cap = static_cast<std::size_t>(std::max<std::int64_t>(capacity, 1));
+  if (prof_on_ && prof_ev_.size() < kProfEv * cap) {
     for (auto e : prof_ev_) cudaEventDestroy(e);
-    prof_ev_.assign(need, nullptr);
+    prof_ev_.assign(kProfEv * cap, nullptr);
     for (auto& e : prof_ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
   }
+  if (prof_on_ && prof_mask_.size() < cap) prof_mask_.assign(cap, 0u);
 }
 
 void Engine::profile_read(h3d_timing* sum, std::int64_t* steps) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
   std::memset(sum, 0, sizeof(*sum));
+  for (int q = 0; q < H3D_K_COUNT; ++q) {
+    prof_kms_[q] = 0.0;
+    prof_kstart_[q] = 0.0;
+    prof_kn_[q] = 0;
+  }
   for (std::size_t k = 0; k < prof_used_; ++k) {
-    cudaEvent_t* ev = prof_ev_.data() + 4 * k;
+    cudaEvent_t* ev = prof_ev_.data() + kProfEv * k;
     H3D_CUDA_CHECK(cudaEventSynchronize(ev[3]));
+    for (int q = 0; q < H3D_K_COUNT; ++q) {
+      if (!(prof_mask_[k] & (1u << q))) continue;
+      float d = 0;
+      H3D_CUDA_CHECK(cudaEventSynchronize(ev[5 + 2 * q]));
+      cudaEventElapsedTime(&d, ev[4 + 2 * q], ev[5 + 2 * q]);
+      prof_kms_[q] += d;
+      float o = 0;
+      cudaEventElapsedTime(&o, ev[0], ev[4 + 2 * q]);
+      prof_kstart_[q] += o;
+      ++prof_kn_[q];
+    }
     float a = 0, b = 0, c = 0;
     cudaEventElapsedTime(&a, ev[0], ev[1]);
     cudaEventElapsedTime(&b, ev[1], ev[2]);
@@ -929,6 +1012,15 @@ void Engine::profile_read(h3d_timing* sum, std::int64_t* steps) {
   prof_launches_ = 0;
 }
 
+void Engine::profile_kernels(double* ms_sum, std::int64_t* launches, double* start_sum,
+                             int count) const {
+  for (int q = 0; q < count && q < H3D_K_COUNT; ++q) {
+    ms_sum[q] = prof_kms_[q];
+    launches[q] = prof_kn_[q];
+    if (start_sum) start_sum[q] = prof_kstart_[q];
+  }
+}
+
 void Engine::attach_nccl(const void* id128, int rank, int world) {
   if (world != world_ || rank != rank_)
     throw InvalidArgument("attach_nccl: rank/world differ from the engine's shard options");
@@ -936,7 +1028,7 @@ void Engine::attach_nccl(const void* id128, int rank, int world) {
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof(id));
   ncclComm_t comm;
-  NCCL_CHECK(ncclCommInitRank(&comm, world, id, rank));
+  NCCL_CHECK(nccl().CommInitRank(&comm, world, id, rank));
   nccl_comm_ = comm;
 }
 

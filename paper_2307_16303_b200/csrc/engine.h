@@ -58,6 +58,7 @@ class Engine {
   void matvec_async(const double* x, double* b, cudaStream_t s);
   void profile(int enable, std::int64_t capacity);
   void profile_read(h3d_timing* sum, std::int64_t* steps);
+  void profile_kernels(double* ms_sum, std::int64_t* launches, double* start_sum, int count) const;
   void stats(h3d_stats* out) const;
   void export_tree(std::int32_t* perm, int level, std::int64_t* offsets) const;
   std::int64_t export_list(int level, int kind, std::int32_t* offsets, std::int32_t* ids) const;
@@ -74,7 +75,8 @@ class Engine {
   void upload_plan();
   void near_scan();
   void check_flags(const char* where);
-  std::int64_t enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev);
+  std::int64_t enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev,
+                       std::uint32_t* kmask);
   Phase2Args phase2_args(double* bout) const;
   std::int64_t node_size(int level, std::int64_t m) const {
     return off_[level][m + 1] - off_[level][m];
@@ -84,11 +86,11 @@ class Engine {
   std::int64_t n_ = 0;
   int L_ = 0;
   int sms_ = 148;
-  // persistent-CTA residency per SM of the matvec kernels and where the
-  // near-field pass forks (0: with phase 1, 1: after the phase-1 reduce);
-  // overridable for tuning through H3D_TUNE="p1s=2,p1p=2,p2c=2,p2s=2,p2p=4,at=0"
+  // persistent-CTA residency per SM of the matvec kernels when the HBM and
+  // FP64 lanes share the SMs; overridable for tuning through
+  // H3D_TUNE="p1s=1,p1p=4,p2c=2,p2s=1,p2p=4" (proxy kernels: 128-thread CTAs)
   struct Tune {
-    int p1s = 2, p1p = 2, p2c = 2, p2s = 2, p2p = 2, at = 0;
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
@@ -120,8 +122,8 @@ class Engine {
   DevBuf<ProxySeg> segs_all_, segs_solve_;
   std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
   DevBuf<P1Item> p1_stream_items_, p1_proxy_items_;
-  DevBuf<P1Reduce> p1_red_;
-  std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_ = 0;
+  DevBuf<P1Reduce> p1_red_s_, p1_red_p_;  // tall-node partial reductions, stream / proxy kind
+  std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_s_ = 0, n_red_p_ = 0;
   bool has_stream_levels_ = false;
   DevBuf<std::int32_t> near_off_, near_ids_, near_dense_;
   DevBuf<double> cpart_;
@@ -131,8 +133,11 @@ class Engine {
   int n_lvl_ = 0;
   DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 per-level partials
   DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy]
-  cudaStream_t stream2_ = nullptr;          // concurrent HBM / FP64 kernels
-  cudaStream_t stream3_ = nullptr;          // near field + direct (needs x only)
+  // matvec lanes (priorities: the HBM lane and the FP64 critical chain above
+  // the near field, which fills whatever the two leave idle)
+  cudaStream_t stream2_ = nullptr;          // HBM lane: stream levels
+  cudaStream_t stream3_ = nullptr;          // near field + direct leaf blocks (needs x only)
+  cudaStream_t stream4_ = nullptr;          // FP64 lane: proxy levels + solves
   cudaEvent_t fork_[3] = {}, join_[3] = {};
   DevBuf<std::int64_t> nf_off_;
   DevBuf<double> NF_;
@@ -145,7 +150,13 @@ class Engine {
 
   // profiling ring for async matvecs (4 events per step)
   bool prof_on_ = false;
+  // per profiled call: 4 phase events + a (begin, end) pair per kernel slot
+  static constexpr int kProfEv = 4 + 2 * H3D_K_COUNT;
   std::vector<cudaEvent_t> prof_ev_;
+  std::vector<std::uint32_t> prof_mask_;  // kernel slots recorded per call
+  double prof_kms_[H3D_K_COUNT] = {};
+  double prof_kstart_[H3D_K_COUNT] = {};
+  std::int64_t prof_kn_[H3D_K_COUNT] = {};
   std::size_t prof_used_ = 0;
   std::int64_t prof_launches_ = 0;
 

@@ -32,6 +32,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 namespace h3db {
 
@@ -185,7 +186,7 @@ __device__ __forceinline__ void stream_producer(StreamSmem& sm, const StreamDesc
 // tiles), consumer warp c owns the item's column tile c, lane = two columns,
 // rows accumulated in order. x rows come from L2 through the read-only path,
 // one row tile ahead.
-__global__ void __launch_bounds__(kStreamThreads, 1) p1_stream_kernel(const P1Args a) {
+__global__ void __maxnreg__(64) p1_stream_kernel(const P1Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -242,10 +243,41 @@ __global__ void __launch_bounds__(kStreamThreads, 1) p1_stream_kernel(const P1Ar
   }
 }
 
-// ---- phase 1, proxy levels: v_c = sum_j K(P_c, z_j) x_j, thread = target,
-// sources staged in shared memory and read as broadcasts.
+// ---- proxy-level evaluation core (both phases): a 128-thread CTA owns up to
+// 256 targets, two per thread (t and t + 128), and streams the sources
+// through shared memory in chunks of kChunk, read as broadcasts; each staged
+// source feeds two targets (half the shared-memory wavefronts per
+// evaluation of one target per thread - the pipe the co-resident bulk-copy
+// kernel also needs), two sources per step give four independent FP64
+// chains per thread.
+constexpr int kProxyThreads = 128;
+
 template <int K>
-__global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
+__device__ __forceinline__ void proxy_eval2(const double (&tx)[2], const double (&ty)[2],
+                                            const double (&tz)[2], double (&acc)[2][2],
+                                            const double2* __restrict__ src, int nj) {
+  int j = 0;
+  for (; j + 1 < nj; j += 2) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        acc[t][u] = far_acc<K>(sq3(tx[t] - s0.x, ty[t] - s0.y, tz[t] - s1.x), s1.y, acc[t][u]);
+    }
+  }
+  if (j < nj) {
+    const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+      acc[t][0] = far_acc<K>(sq3(tx[t] - s0.x, ty[t] - s0.y, tz[t] - s1.x), s1.y, acc[t][0]);
+  }
+}
+
+// ---- phase 1, proxy levels: v_c = sum_j K(P_c, z_j) x_j (targets = the
+// item's proxies, sources = the node's points)
+template <int K>
+__global__ void __launch_bounds__(kProxyThreads, 4) p1_proxy_kernel(const P1Args a) {
   __shared__ double2 src[2 * kChunk];  // (x, y), (z, w)
   __shared__ long long s_k;
   for (;;) {
@@ -257,35 +289,32 @@ __global__ void __launch_bounds__(kThreads, 2) p1_proxy_kernel(const P1Args a) {
     const P1Item it = a.items[k];
     const std::int64_t g = it.node;
     const std::int64_t rb = a.nt.rowbeg[g] + it.row0;
-    const int c = threadIdx.x;
-    const std::int64_t qi = a.nt.soff[g] + it.col0 + c;
-    const bool active = c < it.ncols;
-    const double tx = active ? a.qx[qi] : kFar, ty = active ? a.qy[qi] : kFar,
-                 tz = active ? a.qz[qi] : kFar;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    double tx[2], ty[2], tz[2], acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int c = threadIdx.x + t * kProxyThreads;
+      const std::int64_t qi = a.nt.soff[g] + it.col0 + c;
+      const bool active = c < it.ncols;
+      tx[t] = active ? a.qx[qi] : kFar;
+      ty[t] = active ? a.qy[qi] : kFar;
+      tz[t] = active ? a.qz[qi] : kFar;
+    }
     for (int j0 = 0; j0 < it.nrows; j0 += kChunk) {
       const int nj = min(kChunk, it.nrows - j0);
       __syncthreads();
-      if (threadIdx.x < nj) {
-        const double4 q = reinterpret_cast<const double4*>(a.p4)[rb + j0 + threadIdx.x];
-        src[2 * threadIdx.x] = make_double2(q.x, q.y);
-        src[2 * threadIdx.x + 1] = make_double2(q.z, q.w);
+      for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
+        const double4 v = reinterpret_cast<const double4*>(a.p4)[rb + j0 + q];
+        src[2 * q] = make_double2(v.x, v.y);
+        src[2 * q + 1] = make_double2(v.z, v.w);
       }
       __syncthreads();
-      int j = 0;
-      for (; j + 3 < nj; j += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
-          acc[u] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[u]);
-        }
-      }
-      for (; j < nj; ++j) {
-        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        acc[0] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[0]);
-      }
+      proxy_eval2<K>(tx, ty, tz, acc, src, nj);
     }
-    if (active) p1_write(it, g, c, far_scale<K>() * ((acc[0] + acc[1]) + (acc[2] + acc[3])), a);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int c = threadIdx.x + t * kProxyThreads;
+      if (c < it.ncols) p1_write(it, g, c, far_scale<K>() * (acc[t][0] + acc[t][1]), a);
+    }
   }
 }
 
@@ -676,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
 // points into a double-buffered shared stage with cp.async.bulk (one copy per
 // range piece, byte-counted on the buffer's "full" mbarrier); seven consumer
 // warps own the leaf's rows (warp w: rows [w RPW, (w + 1) RPW), RPW =
-// ceil(m / 7) <= 8), lanes stride over the staged sources and evaluate each one
+// ceil(m / 7) <= 6), lanes stride over the staged sources and evaluate each one
 // against the warp's RPW rows (RPW independent FP64 chains per lane), then
 // release the buffer on its "empty" mbarrier - no block-wide barrier on the
 // hot path. Dense-near sources use the full-accuracy rsqrt (+ the diagonal
@@ -685,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
 constexpr int kNearStage = 512;            // sources per staged chunk (16 KB)
 constexpr int kNearConsumers = kWarps - 1;  // 7 consumer warps + 1 producer = 256 threads
 constexpr int kNearThreads = 32 * (kNearConsumers + 1);
-constexpr int kNearRows = 8 * kNearConsumers;  // rows per pass (leaves above 56 points: 2 passes)
+constexpr int kNearRows = 6 * kNearConsumers;  // rows per pass (leaves above 42 points: 2 passes)
 constexpr int kMaxNear = kMaxNearRanges;
 
 struct NearMeta {
@@ -812,7 +841,7 @@ __device__ __forceinline__ void near_put(NearSmem& sm, unsigned t, NearMeta mt, 
 }
 
 template <int K>
-__global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Args a) {
+__global__ void __maxnreg__(96) p2_near_kernel(const Phase2Args a) {
   __shared__ __align__(128) NearSmem sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -883,9 +912,7 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
       case 3: t = near_consume<K, 3>(sm, a, t); break;
       case 4: t = near_consume<K, 4>(sm, a, t); break;
       case 5: t = near_consume<K, 5>(sm, a, t); break;
-      case 6: t = near_consume<K, 6>(sm, a, t); break;
-      case 7: t = near_consume<K, 7>(sm, a, t); break;
-      default: t = near_consume<K, 8>(sm, a, t); break;
+      default: t = near_consume<K, 6>(sm, a, t); break;
     }
   }
 }
@@ -896,7 +923,7 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
 // S columns come through the read-only path one stage ahead. At the item's
 // last stage the warps reduce (fixed butterfly, then warp order) and write
 // the level's partial (combined in level order by combine_kernel).
-__global__ void __launch_bounds__(kStreamThreads, 1) p2_stream_kernel(const Phase2Args a) {
+__global__ void __maxnreg__(64) p2_stream_kernel(const Phase2Args a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   StreamSmem& sm = *reinterpret_cast<StreamSmem*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -972,10 +999,10 @@ __global__ void __launch_bounds__(kStreamThreads, 1) p2_stream_kernel(const Phas
 }
 
 // ---- phase 2, proxy levels, node-major: b_X += K(X, P_A) s_A for the rows of
-// node A, thread = target row, proxy sources staged in shared memory (the
-// phase-1 proxy layout, which keeps the FP64 pipe ~80% busy).
+// node A (up to 256 per item, two per thread), the node's proxy list staged
+// in shared memory (proxy_eval2 above).
 template <int K>
-__global__ void __launch_bounds__(kThreads, 2) p2_proxy_kernel(const Phase2Args a) {
+__global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2Args a) {
   __shared__ double2 src[2 * kChunk];
   __shared__ long long s_k;
   for (;;) {
@@ -988,37 +1015,34 @@ __global__ void __launch_bounds__(kThreads, 2) p2_proxy_kernel(const Phase2Args 
     const std::int64_t g = it.node;
     const std::int64_t so = a.nt.soff[g];
     const int R = a.nt.rpad[g];
-    const int i = threadIdx.x;
-    const bool active = i < it.nrows;
-    const std::int64_t p = a.nt.rowbeg[g] + it.row0 + i;
-    const double tx = active ? a.px[p] : kFar, ty = active ? a.py[p] : kFar,
-                 tz = active ? a.pz[p] : kFar;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double4* P4 = reinterpret_cast<const double4*>(a.p4);
+    double tx[2], ty[2], tz[2], acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int i = threadIdx.x + t * kProxyThreads;
+      const double4 q = i < it.nrows ? P4[a.nt.rowbeg[g] + it.row0 + i] : make_double4(kFar, kFar, kFar, 0.0);
+      tx[t] = q.x;
+      ty[t] = q.y;
+      tz[t] = q.z;
+    }
     for (int j0 = 0; j0 < R; j0 += kChunk) {
       const int nj = min(kChunk, R - j0);
       __syncthreads();
-      if (threadIdx.x < nj) {
-        const std::int64_t q = so + j0 + threadIdx.x;
-        src[2 * threadIdx.x] = make_double2(a.qx[q], a.qy[q]);
-        src[2 * threadIdx.x + 1] = make_double2(a.qz[q], a.S[q]);
+      for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
+        const std::int64_t qq = so + j0 + q;
+        src[2 * q] = make_double2(a.qx[qq], a.qy[qq]);
+        src[2 * q + 1] = make_double2(a.qz[qq], a.S[qq]);
       }
       __syncthreads();
-      int j = 0;
-      for (; j + 3 < nj; j += 4) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
-          acc[u] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[u]);
-        }
-      }
-      for (; j < nj; ++j) {
-        const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-        acc[0] = far_acc<K>(sq3(tx - s0.x, ty - s0.y, tz - s1.x), s1.y, acc[0]);
-      }
+      proxy_eval2<K>(tx, ty, tz, acc, src, nj);
     }
-    if (active)
-      a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + p] =
-          far_scale<K>() * ((acc[0] + acc[1]) + (acc[2] + acc[3]));
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int i = threadIdx.x + t * kProxyThreads;
+      if (i < it.nrows)
+        a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + a.nt.rowbeg[g] + it.row0 + i] =
+            far_scale<K>() * (acc[t][0] + acc[t][1]);
+    }
   }
 }
 
@@ -1087,6 +1111,8 @@ int grid_for(F kernel, int sms, int per_sm, std::int64_t work, int threads = kTh
 
 }  // namespace
 
+void configure_kernels();
+
 void launch_gather(const double* x, const std::int32_t* perm, std::int64_t n, double* xp, double* p4,
                    cudaStream_t s) {
   if (n <= 0) return;
@@ -1110,15 +1136,7 @@ void launch_pack_points(const double* px, const double* py, const double* pz, st
 
 void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   if (a.nleaves == 0) return;
-  static bool carve = false;  // two 36 KB CTAs per SM need the shared-heavy carveout
-  if (!carve) {
-    for (const void* f : {reinterpret_cast<const void*>(p2_near_kernel<kLaplace>),
-                          reinterpret_cast<const void*>(p2_near_kernel<kR4>),
-                          reinterpret_cast<const void*>(p2_near_kernel<kHelmholtz>)})
-      H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                          cudaSharedmemCarveoutMaxShared));
-    carve = true;
-  }
+  configure_kernels();
   switch (a.kernel) {
     case kLaplace: {
       const int grid = grid_for(p2_near_kernel<kLaplace>, sms, per_sm, a.nleaves, kNearThreads);
@@ -1139,16 +1157,40 @@ void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-template <class F>
-int stream_grid(F kernel, int sms, int per_sm, std::int64_t work) {
-  static bool attr = false;  // process-wide, set before the first launch
-  if (!attr) {
+// Once per process: the bulk-copy kernels' dynamic shared memory, and one
+// shared-heavy carveout for every matvec kernel - the HBM lane's CTA
+// (~130 KB) and the FP64 kernels co-reside on each SM, so they must agree on
+// the SM's L1/shared split.
+void configure_kernels() {
+  static std::once_flag once;
+  std::call_once(once, [] {
     H3D_CUDA_CHECK(cudaFuncSetAttribute(p1_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(StreamSmem))));
     H3D_CUDA_CHECK(cudaFuncSetAttribute(p2_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(StreamSmem))));
-    attr = true;
-  }
+    const void* fs[] = {
+        reinterpret_cast<const void*>(p1_stream_kernel),
+        reinterpret_cast<const void*>(p2_stream_kernel),
+        reinterpret_cast<const void*>(p1_proxy_kernel<kLaplace>),
+        reinterpret_cast<const void*>(p1_proxy_kernel<kR4>),
+        reinterpret_cast<const void*>(p1_proxy_kernel<kHelmholtz>),
+        reinterpret_cast<const void*>(p2_proxy_kernel<kLaplace>),
+        reinterpret_cast<const void*>(p2_proxy_kernel<kR4>),
+        reinterpret_cast<const void*>(p2_proxy_kernel<kHelmholtz>),
+        reinterpret_cast<const void*>(p2_near_kernel<kLaplace>),
+        reinterpret_cast<const void*>(p2_near_kernel<kR4>),
+        reinterpret_cast<const void*>(p2_near_kernel<kHelmholtz>),
+        reinterpret_cast<const void*>(proxy_solve_kernel),
+    };
+    for (const void* f : fs)
+      H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                          cudaSharedmemCarveoutMaxShared));
+  });
+}
+
+template <class F>
+int stream_grid(F kernel, int sms, int per_sm, std::int64_t work) {
+  configure_kernels();
   int nb = 0;
   H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kStreamThreads,
                                                                sizeof(StreamSmem)));
@@ -1165,20 +1207,21 @@ void launch_p1_stream(const P1Args& a, int sms, int per_sm, cudaStream_t s) {
 
 void launch_p1_proxy(const P1Args& a, int kernel, int sms, int per_sm, cudaStream_t s) {
   if (a.nitems == 0) return;
+  configure_kernels();
   switch (kernel) {
     case kLaplace: {
-      const int grid = grid_for(p1_proxy_kernel<kLaplace>, sms, per_sm, a.nitems);
-      p1_proxy_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p1_proxy_kernel<kLaplace>, sms, per_sm, a.nitems, kProxyThreads);
+      p1_proxy_kernel<kLaplace><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
     case kR4: {
-      const int grid = grid_for(p1_proxy_kernel<kR4>, sms, per_sm, a.nitems);
-      p1_proxy_kernel<kR4><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p1_proxy_kernel<kR4>, sms, per_sm, a.nitems, kProxyThreads);
+      p1_proxy_kernel<kR4><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
     default: {
-      const int grid = grid_for(p1_proxy_kernel<kHelmholtz>, sms, per_sm, a.nitems);
-      p1_proxy_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p1_proxy_kernel<kHelmholtz>, sms, per_sm, a.nitems, kProxyThreads);
+      p1_proxy_kernel<kHelmholtz><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
   }
@@ -1258,20 +1301,21 @@ void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) 
 
 void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   if (a.n_p2_items == 0) return;
+  configure_kernels();
   switch (a.kernel) {
     case kLaplace: {
-      const int grid = grid_for(p2_proxy_kernel<kLaplace>, sms, per_sm, a.n_p2_items);
-      p2_proxy_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p2_proxy_kernel<kLaplace>, sms, per_sm, a.n_p2_items, kProxyThreads);
+      p2_proxy_kernel<kLaplace><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
     case kR4: {
-      const int grid = grid_for(p2_proxy_kernel<kR4>, sms, per_sm, a.n_p2_items);
-      p2_proxy_kernel<kR4><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p2_proxy_kernel<kR4>, sms, per_sm, a.n_p2_items, kProxyThreads);
+      p2_proxy_kernel<kR4><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
     default: {
-      const int grid = grid_for(p2_proxy_kernel<kHelmholtz>, sms, per_sm, a.n_p2_items);
-      p2_proxy_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a);
+      const int grid = grid_for(p2_proxy_kernel<kHelmholtz>, sms, per_sm, a.n_p2_items, kProxyThreads);
+      p2_proxy_kernel<kHelmholtz><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
   }

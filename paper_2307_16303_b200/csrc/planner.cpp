@@ -290,7 +290,7 @@ void Planner::layout() {
       const std::int64_t pbase = ptot;
       if (nrc > 1) {
         ptot += nrc * rp;
-        reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rp, static_cast<std::int32_t>(nrc), 0, pbase});
+        reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rp, static_cast<std::int32_t>(nrc), mode_[l], pbase});
       }
       for (std::int64_t k = 0; k < nrc; ++k)
         for (int cc = 0; cc < ncc; ++cc) {

@@ -94,7 +94,7 @@ struct P1Reduce {
   std::int32_t node;
   std::int32_t ncols;
   std::int32_t nchunks;
-  std::int32_t pad;
+  std::int32_t kind;   // LevelMode of the node's level (the two kinds reduce on different streams)
   std::int64_t pbase;  // partials: pbase + chunk * ncols + c
 };
 

@@ -111,7 +111,7 @@ _EXPORTS = [
     "h3d_random_vector", "h3d_dev_create", "h3d_dev_destroy", "h3d_dev_matvec",
     "h3d_dev_stats", "h3d_dev_export_tree", "h3d_dev_export_list", "h3d_dev_export_pairs",
     "h3d_nccl_get_id", "h3d_dev_attach_nccl", "h3d_dev_matvec_async", "h3d_dev_profile",
-    "h3d_dev_profile_read", "h3d_plan_create", "h3d_plan_destroy", "h3d_plan_pairs",
+    "h3d_dev_profile_read", "h3d_dev_profile_kernels", "h3d_plan_create", "h3d_plan_destroy", "h3d_plan_pairs",
     "h3d_plan_set_ranks", "h3d_plan_set_mode", "h3d_plan_layout", "h3d_plan_array",
 ]
 
@@ -137,6 +137,7 @@ def _load():
     L.h3d_dev_matvec_async.argtypes = [P, P, P, P]
     L.h3d_dev_profile.argtypes = [P, C.c_int, C.c_int64]
     L.h3d_dev_profile_read.argtypes = [P, C.POINTER(_Timing), C.POINTER(C.c_int64)]
+    L.h3d_dev_profile_kernels.argtypes = [P, P, P, P, C.c_int]
     L.h3d_plan_create.argtypes = [C.c_int, C.c_int64, P, P, P, P, C.c_int, C.c_int, P,
                                   C.POINTER(P)]
     L.h3d_plan_destroy.argtypes = [P]
@@ -337,6 +338,16 @@ class HMatrixRep:
             setattr(out, f, getattr(t, f))
         return out, steps.value
 
+    def profile_kernels(self) -> dict:
+        """Per-kernel (summed ms, launches, summed start offset ms) of the calls
+        read by the last profile_read, keyed by KERNEL_SLOTS (kernels of
+        different lanes overlap)."""
+        ms = np.zeros(len(KERNEL_SLOTS))
+        cnt = np.zeros(len(KERNEL_SLOTS), np.int64)
+        st = np.zeros(len(KERNEL_SLOTS))
+        _check(_L.h3d_dev_profile_kernels(self._h, _ptr(ms), _ptr(cnt), _ptr(st), len(KERNEL_SLOTS)))
+        return {k: (float(ms[i]), int(cnt[i]), float(st[i])) for i, k in enumerate(KERNEL_SLOTS)}
+
     # --- introspection ------------------------------------------------------
     def stats(self) -> dict:
         s = _Stats()
@@ -416,6 +427,10 @@ def stats(rep: HMatrixRep) -> dict:
 
 
 # ---------------------------------------------------------------- host planner
+# h3d_kernel_slot order (include/h3d_b200.h)
+KERNEL_SLOTS = ("gather", "p1_stream", "red_stream", "p2_stream", "p1_proxy", "red_proxy", "solve",
+                "p2_proxy", "near", "combine")
+
 _PLAN_DTYPES = {
     "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
     "spos": np.int32, "pair_wx": np.int64, "pair_wy": np.int64, "pair_rx": np.int32,
@@ -430,7 +445,7 @@ _PLAN_DTYPES = {
                        ("col0", np.int32), ("ncols", np.int32), ("kind", np.int32),
                        ("pslot", np.int64)]),
     "reds": np.dtype([("node", np.int32), ("ncols", np.int32), ("nchunks", np.int32),
-                      ("pad", np.int32), ("pbase", np.int64)]),
+                      ("kind", np.int32), ("pbase", np.int64)]),
     "p2_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
                           ("slot", np.int32)]),
     "p2s_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
