@@ -69,23 +69,40 @@ __device__ __forceinline__ double rsqrt_n1_acc(double x, double w, double acc) {
 
 // acc += K(r2) w on the admissible path (Laplace: Newton form, scaled later
 // by far_scale<K>(); others exact)
+// 1/r^4 = (1/r)^4 from the same Newton form: g = y0 (x y0^2 - 3) = -2/r,
+// so g^4 = 16 / r^4 (scale 1/16), no division.
+__device__ __forceinline__ double rsqrt4_n1_acc(double x, double w, double acc) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double t = x * y;
+  const double g = y * fma(t, y, -3.0);
+  const double g2 = g * g;
+  return fma(g2 * g2, w, acc);
+}
+
 template <int K>
 __device__ __forceinline__ double far_acc(double r2, double w, double acc) {
   if constexpr (K == kLaplace) {
     return rsqrt_n1_acc(r2, w, acc);
+  } else if constexpr (K == kR4) {
+    return rsqrt4_n1_acc(r2, w, acc);
   } else {
     return fma(kernel_r2<K>(r2), w, acc);
   }
 }
 template <int K>
 __device__ __forceinline__ constexpr double far_scale() {
-  return K == kLaplace ? kNewtonScale : 1.0;
+  return K == kLaplace ? kNewtonScale : K == kR4 ? 1.0 / 16.0 : 1.0;
 }
 
 template <int K>
 __device__ __forceinline__ double kernel_r2_fast(double r2) {
   if constexpr (K == kLaplace) {
     return rsqrt_c3(r2);
+  } else if constexpr (K == kR4) {
+    const double y = rsqrt_c3(r2);
+    const double y2 = y * y;
+    return y2 * y2;
   } else {
     return kernel_r2<K>(r2);
   }

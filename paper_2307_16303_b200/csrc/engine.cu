@@ -139,6 +139,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2c") tune_.p2c = v;
         else if (k == "p2s") tune_.p2s = v;
         else if (k == "p2p") tune_.p2p = v;
+        else if (k == "skip") tune_.skip = v;
       }
       pos = end + 1;
     }
@@ -189,7 +190,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   ms_aca_write_ = ms_since(t);
   if (n_segs_all_ > 0) {
     launch_proxy_gather(segs_all_.get(), n_segs_all_, piv_.get(), px_.get(), py_.get(), pz_.get(),
-                        qx_.get(), qy_.get(), qz_.get(), stream_);
+                        q4_.get(), stream_);
     int max_r = 0;
     for (const auto& sg : plan_->proxy_segs) max_r = std::max(max_r, sg.r);
     launch_lu_invert(segs_all_.get(), n_segs_all_, lu_.get(), lu_total_, max_r, stream_);
@@ -586,18 +587,10 @@ void Engine::upload_plan() {
   piv_.alloc(std::max<std::int64_t>(Z.piv_total, 1));
   lu_total_ = Z.lu_total;
   lu_.alloc(std::max<std::int64_t>(2 * Z.lu_total, 1));  // row-major + column-major inverses
-  // proxy coordinates share S's index space; padding slots sit far away
-  // (their weights are 0, see matvec.cu)
-  qx_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
-  qy_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
-  qz_.alloc(std::max<std::int64_t>(Z.s_doubles, 2));
-  {
-    std::vector<double> far(qx_.size(), 1e100);
-    H3D_CUDA_CHECK(cudaMemcpyAsync(qx_.get(), far.data(), far.size() * 8, cudaMemcpyHostToDevice, stream_));
-    H3D_CUDA_CHECK(cudaMemcpyAsync(qy_.get(), far.data(), far.size() * 8, cudaMemcpyHostToDevice, stream_));
-    H3D_CUDA_CHECK(cudaMemcpyAsync(qz_.get(), far.data(), far.size() * 8, cudaMemcpyHostToDevice, stream_));
-    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
-  }
+  // proxy records share S's index space; padding slots sit far away with
+  // weight 0 (see matvec.cu)
+  q4_.alloc(4 * std::max<std::int64_t>(Z.s_doubles, 2));
+  launch_fill_far(q4_.get(), std::max<std::int64_t>(Z.s_doubles, 2), stream_);
   std::vector<ProxySeg> solve;
   for (const auto& s : P.proxy_segs)
     if (s.solve) solve.push_back(s);
@@ -677,6 +670,9 @@ void Engine::upload_plan() {
     H3D_CUDA_CHECK(cudaMemsetAsync(lvl_part_.get(), 0, sizeof(double) * n_lvl_ * n_, stream_));
   }
   counters_.alloc(5);
+  sync_flag_.alloc(1);
+  H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), stream_));
+  epoch_ = 0;
   if (opt_.near_mode == H3D_NEAR_STORED) {
     nf_off_.upload(P.nf_off, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
@@ -702,9 +698,7 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.py = py_.get();
   a.pz = pz_.get();
   a.p4 = p4_.get();
-  a.qx = qx_.get();
-  a.qy = qy_.get();
-  a.qz = qz_.get();
+  a.q4 = q4_.get();
   a.perm = perm_.get();
   a.near_off = near_off_.get();
   a.near_ids = near_ids_.get();
@@ -760,6 +754,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   auto kb = [&](int k, cudaStream_t st) {
     if (kmask) cudaEventRecord(ev[4 + 2 * k], st);
   };
+  auto run = [&](int k) { return !(tune_.skip & (1 << k)); };
   auto ke = [&](int k, cudaStream_t st) {
     if (kmask) {
       cudaEventRecord(ev[5 + 2 * k], st);
@@ -807,9 +802,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   a1.py = py_.get();
   a1.pz = pz_.get();
   a1.p4 = p4_.get();
-  a1.qx = qx_.get();
-  a1.qy = qy_.get();
-  a1.qz = qz_.get();
+  a1.q4 = q4_.get();
   // Two lanes forked from s, joined back for the combine:
   //   stream2_ (HBM): p1_stream -> stream reductions -> [solves done] -> p2_stream
   //   stream4_ (FP64): p1_proxy -> proxy reductions -> solves -> p2_proxy ->
@@ -835,7 +828,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       a1.nitems = n_p1s_;
       a1.counter = counters_.get();
       kb(H3D_K_P1_STREAM, stream2_);
-      launch_p1_stream(a1, sms_, fp ? tune_.p1s : 2, stream2_);
+      if (run(H3D_K_P1_STREAM)) launch_p1_stream(a1, sms_, fp ? tune_.p1s : 2, stream2_);
       ke(H3D_K_P1_STREAM, stream2_);
       ++launches;
     }
@@ -853,7 +846,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     a1.nitems = n_p1p_;
     a1.counter = counters_.get() + 1;
     kb(H3D_K_P1_PROXY, stream4_);
-    launch_p1_proxy(a1, opt_.kernel_id, sms_, hbm ? tune_.p1p : 8, stream4_);
+    if (run(H3D_K_P1_PROXY)) launch_p1_proxy(a1, opt_.kernel_id, sms_, hbm ? tune_.p1p : 8, stream4_);
     ke(H3D_K_P1_PROXY, stream4_);
     ++launches;
   }
@@ -865,22 +858,29 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   }
   if (n_segs_solve_ > 0) {
     kb(H3D_K_SOLVE, stream4_);
-    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), stream4_);
+    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), q4_.get(),
+                       stream4_);
     ke(H3D_K_SOLVE, stream4_);
     ++launches;
   }
   if (ev) cudaEventRecord(ev[2], stream4_);
-  // HBM lane, phase 2: held until the solves are done - the latency-bound
-  // solve blocks lose most of their bandwidth to a saturating bulk stream
-  // (measured 0.6 ms alone vs 6-10 ms beside it), and they gate the FP64 lane
+  // HBM lane, phase 2: launched right behind phase 1 so its CTAs take the
+  // SM slots p1_stream leaves (a persistent FP64 kernel launched first would
+  // crowd them out for its whole run), but its producer holds the first copy
+  // until the FP64 lane flags the solves done: the latency-bound solve
+  // blocks lose most of their bandwidth beside a saturating bulk stream
+  // (0.5 ms alone vs 6-10 ms beside it), and they gate the FP64 lane.
   if (hbm) {
-    if (n_segs_solve_ > 0) {
-      H3D_CUDA_CHECK(cudaEventRecord(fork_[1], stream4_));
-      H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[1], 0));
+    if (n_segs_solve_ > 0 && has_p2 && n_p2s_ > 0) {
+      ++epoch_;
+      launch_set_flag(sync_flag_.get(), epoch_, stream4_);
+      ++launches;
+      a2.wait_flag = sync_flag_.get();
+      a2.wait_value = epoch_;
     }
     if (has_p2 && n_p2s_ > 0) {
       kb(H3D_K_P2_STREAM, stream2_);
-      launch_p2_stream(a2, sms_, fp ? tune_.p2s : 2, stream2_);
+      if (run(H3D_K_P2_STREAM)) launch_p2_stream(a2, sms_, fp ? tune_.p2s : 2, stream2_);
       ke(H3D_K_P2_STREAM, stream2_);
       ++launches;
     }
@@ -892,13 +892,13 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   if (has_p2) {
     if (n_p2_ > 0) {
       kb(H3D_K_P2_PROXY, stream4_);
-      launch_p2_proxy(a2, sms_, hbm ? tune_.p2p : 8, stream4_);
+      if (run(H3D_K_P2_PROXY)) launch_p2_proxy(a2, sms_, hbm ? tune_.p2p : 8, stream4_);
       ke(H3D_K_P2_PROXY, stream4_);
       ++launches;
     }
     kb(H3D_K_NEAR, stream4_);
     if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream4_);
-    else launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
+    else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
     ke(H3D_K_NEAR, stream4_);
     ++launches;
   }

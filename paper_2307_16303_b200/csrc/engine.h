@@ -89,8 +89,10 @@ class Engine {
   // persistent-CTA residency per SM of the matvec kernels when the HBM and
   // FP64 lanes share the SMs; overridable for tuning through
   // H3D_TUNE="p1s=1,p1p=4,p2c=2,p2s=1,p2p=4" (proxy kernels: 128-thread CTAs)
+  // ("skip=<mask of h3d_kernel_slot>" drops kernels: timing experiments only,
+  // results are wrong)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4;
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
@@ -118,7 +120,7 @@ class Engine {
   DevBuf<std::int32_t> piv_;
   DevBuf<double> lu_;
   std::int64_t lu_total_ = 0;
-  DevBuf<double> qx_, qy_, qz_;
+  DevBuf<double> q4_;  // proxy records (x, y, z, solved t-vector) in S index space
   DevBuf<ProxySeg> segs_all_, segs_solve_;
   std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
   DevBuf<P1Item> p1_stream_items_, p1_proxy_items_;
@@ -132,6 +134,8 @@ class Engine {
   std::int64_t n_p2_ = 0, n_p2s_ = 0;
   int n_lvl_ = 0;
   DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 per-level partials
+  DevBuf<unsigned> sync_flag_;  // solves-done epoch (FP64 lane -> HBM lane)
+  unsigned epoch_ = 0;
   DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy]
   // matvec lanes (priorities: the HBM lane and the FP64 critical chain above
   // the near field, which fills whatever the two leave idle)

@@ -120,7 +120,7 @@ struct P1Args {
   double* P = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;  // permuted points
   const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
-  const double *qx = nullptr, *qy = nullptr, *qz = nullptr;  // proxy points (S-space)
+  const double* q4 = nullptr;  // proxy records (x, y, z, solved t-vector), S index space
   unsigned* counter = nullptr;  // dynamic work counter (zeroed before the launch)
 };
 // persistent CTAs: grid = SMs x per_sm (capped by occupancy and work)
@@ -129,12 +129,16 @@ void launch_p1_proxy(const P1Args& a, int kernel, int sms, int per_sm, cudaStrea
 void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
                           const std::int32_t* spos, const double* P, double* S,
                           cudaStream_t s);
+// q4[i] = (far, far, far, 0) for i < n (padding records, build)
+void launch_fill_far(double* q4, std::int64_t n, cudaStream_t s);
+// q4[so + a] = (x, y, z, .) of the proxy points of every segment (build)
 void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int32_t* piv,
-                         const double* px, const double* py, const double* pz, double* qx,
-                         double* qy, double* qz, cudaStream_t s);
+                         const double* px, const double* py, const double* pz, double* q4,
+                         cudaStream_t s);
 // lu holds 2 x lu_total doubles: the packed inverses row-major, then column-major
+// reads v from S, writes the solved t-vector into the w lane of q4
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
-                        std::int64_t lu_total, double* S, cudaStream_t s);
+                        std::int64_t lu_total, const double* S, double* q4, cudaStream_t s);
 // build time: replace every pair's packed LU by its triangular inverses
 // (strict lower L^-1, upper R^-1), row-major at lu and column-major at lu + lu_total
 void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::int64_t lu_total,
@@ -151,7 +155,7 @@ struct Phase2Args {
   const double* xp = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;
   const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
-  const double *qx = nullptr, *qy = nullptr, *qz = nullptr;
+  const double* q4 = nullptr;  // proxy records (x, y, z, solved t-vector), S index space
   const std::int32_t* perm = nullptr;
   // leaf near lists: self + near_edge + near_face (+ direct partners), CSR
   const std::int32_t* near_off = nullptr;
@@ -177,6 +181,11 @@ struct Phase2Args {
   const StreamDesc* p2s_descs = nullptr;
   std::int64_t n_p2s_items = 0;
   double* lvl_part = nullptr;  // [levels with phase-2 work x N] (Morton order)
+  // p2_stream: its producer holds the first copy until *wait_flag reaches
+  // wait_value (set on the FP64 lane after the solves), so the HBM lane's
+  // CTAs can be resident early without competing with the solves
+  const unsigned* wait_flag = nullptr;
+  unsigned wait_value = 0;
   std::int64_t n_total = 0;    // N
   unsigned* counter3 = nullptr;
 };
@@ -188,6 +197,8 @@ constexpr int kMaxNearRanges = 256;
 void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
+// *flag = value (release, device scope), stream-ordered
+void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s);
 // b[perm[p]] = cpart[p] + sum over levels (in order) of lvl_part[l][p]
 void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
                     const std::int32_t* perm, std::int64_t row0, std::int64_t row1, double* b,

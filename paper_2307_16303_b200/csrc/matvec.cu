@@ -252,8 +252,8 @@ __global__ void __maxnreg__(64) p1_stream_kernel(const P1Args a) {
 // chains per thread.
 constexpr int kProxyThreads = 128;
 
-template <int K>
-__device__ __forceinline__ void proxy_eval2(const double (&tx)[2], const double (&ty)[2],
+template <int K, int NT>
+__device__ __forceinline__ void proxy_evalT(const double (&tx)[2], const double (&ty)[2],
                                             const double (&tz)[2], double (&acc)[2][2],
                                             const double2* __restrict__ src, int nj) {
   int j = 0;
@@ -262,23 +262,41 @@ __device__ __forceinline__ void proxy_eval2(const double (&tx)[2], const double 
     for (int u = 0; u < 2; ++u) {
       const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
 #pragma unroll
-      for (int t = 0; t < 2; ++t)
+      for (int t = 0; t < NT; ++t)
         acc[t][u] = far_acc<K>(sq3(tx[t] - s0.x, ty[t] - s0.y, tz[t] - s1.x), s1.y, acc[t][u]);
     }
   }
   if (j < nj) {
     const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
 #pragma unroll
-    for (int t = 0; t < 2; ++t)
+    for (int t = 0; t < NT; ++t)
       acc[t][0] = far_acc<K>(sq3(tx[t] - s0.x, ty[t] - s0.y, tz[t] - s1.x), s1.y, acc[t][0]);
   }
 }
 
+// nt = targets of this warp that exist (warp-uniform: 0, 1 or 2 per thread);
+// warps without targets skip straight to the next barrier
+template <int K>
+__device__ __forceinline__ void proxy_eval2(const double (&tx)[2], const double (&ty)[2],
+                                            const double (&tz)[2], double (&acc)[2][2],
+                                            const double2* __restrict__ src, int nj, int nt) {
+  if (nt == 2) proxy_evalT<K, 2>(tx, ty, tz, acc, src, nj);
+  else if (nt == 1) proxy_evalT<K, 1>(tx, ty, tz, acc, src, nj);
+}
+
+__device__ __forceinline__ int warp_targets(int loc, int tpg, int n) {
+  if (__any_sync(0xffffffffu, loc + tpg < n)) return 2;
+  if (__any_sync(0xffffffffu, loc < n)) return 1;
+  return 0;
+}
+
 // ---- phase 1, proxy levels: v_c = sum_j K(P_c, z_j) x_j (targets = the
-// item's proxies, sources = the node's points)
+// item's proxies, sources = the node's points); items with <= 128 / <= 64
+// proxies split the sources over 2 / 4 thread groups as in p2_proxy_kernel.
 template <int K>
 __global__ void __launch_bounds__(kProxyThreads, 4) p1_proxy_kernel(const P1Args a) {
   __shared__ double2 src[2 * kChunk];  // (x, y), (z, w)
+  __shared__ double red[2 * kProxyThreads];
   __shared__ long long s_k;
   for (;;) {
     __syncthreads();
@@ -289,15 +307,20 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p1_proxy_kernel(const P1Args
     const P1Item it = a.items[k];
     const std::int64_t g = it.node;
     const std::int64_t rb = a.nt.rowbeg[g] + it.row0;
+    const int G = it.ncols <= 64 ? 4 : it.ncols <= 128 ? 2 : 1;
+    const int tpg = kProxyThreads / G;
+    const int grp = threadIdx.x / tpg, loc = threadIdx.x % tpg;
+    const int nt = warp_targets(loc, tpg, it.ncols);
     double tx[2], ty[2], tz[2], acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      const int c = threadIdx.x + t * kProxyThreads;
+      const int c = loc + t * tpg;
       const std::int64_t qi = a.nt.soff[g] + it.col0 + c;
-      const bool active = c < it.ncols;
-      tx[t] = active ? a.qx[qi] : kFar;
-      ty[t] = active ? a.qy[qi] : kFar;
-      tz[t] = active ? a.qz[qi] : kFar;
+      const double4 q = c < it.ncols ? reinterpret_cast<const double4*>(a.q4)[qi]
+                                     : make_double4(kFar, kFar, kFar, 0.0);
+      tx[t] = q.x;
+      ty[t] = q.y;
+      tz[t] = q.z;
     }
     for (int j0 = 0; j0 < it.nrows; j0 += kChunk) {
       const int nj = min(kChunk, it.nrows - j0);
@@ -308,12 +331,18 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p1_proxy_kernel(const P1Args
         src[2 * q + 1] = make_double2(v.z, v.w);
       }
       __syncthreads();
-      proxy_eval2<K>(tx, ty, tz, acc, src, nj);
+      const int sub = (nj + G - 1) / G;
+      const int lo = min(nj, grp * sub), hi = min(nj, lo + sub);
+      proxy_eval2<K>(tx, ty, tz, acc, src + 2 * lo, hi - lo, nt);
     }
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int c = threadIdx.x + t * kProxyThreads;
-      if (c < it.ncols) p1_write(it, g, c, far_scale<K>() * (acc[t][0] + acc[t][1]), a);
+    for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = acc[t][0] + acc[t][1];
+    __syncthreads();
+    for (int c = threadIdx.x; c < it.ncols; c += kProxyThreads) {
+      const int per = 2 * tpg;
+      double v = 0.0;
+      for (int q = 0; q < G; ++q) v += red[q * per + c];
+      p1_write(it, g, c, far_scale<K>() * v, a);
     }
   }
 }
@@ -335,8 +364,7 @@ __global__ void phase1_reduce_kernel(const P1Reduce* __restrict__ red, NodeTable
 __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
                                     const std::int32_t* __restrict__ piv,
                                     const double* __restrict__ px, const double* __restrict__ py,
-                                    const double* __restrict__ pz, double* __restrict__ qx,
-                                    double* __restrict__ qy, double* __restrict__ qz) {
+                                    const double* __restrict__ pz, double4* __restrict__ q4) {
   const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.y) + threadIdx.y;
   if (s >= nseg) return;
   const ProxySeg sg = segs[s];
@@ -344,9 +372,7 @@ __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int6
     // side 0: Z = X, proxies = column pivots tau (in Y = k); side 1: row pivots sigma
     const std::int32_t loc = piv[sg.piv_off + (sg.side == 0 ? sg.r : 0) + q];
     const std::int64_t idx = sg.base + loc;
-    qx[sg.so + q] = px[idx];
-    qy[sg.so + q] = py[idx];
-    qz[sg.so + q] = pz[idx];
+    q4[sg.so + q] = make_double4(px[idx], py[idx], pz[idx], 0.0);
   }
 }
 
@@ -402,7 +428,7 @@ __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t
 template <int NK>
 __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __restrict__ P,
                                           const double* __restrict__ PT, double* v, double* w,
-                                          double* __restrict__ Sg, int lane) {
+                                          double* __restrict__ out, int lane) {
   const int r = sg.r;
   double acc[NK];
 #pragma unroll
@@ -470,7 +496,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
     const int i = lane + 32 * k;
-    if (i < r) Sg[i] = acc[k];
+    if (i < r) out[4 * i] = acc[k];  // w lane of the proxy records
   }
 }
 
@@ -478,7 +504,8 @@ __global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __rest
                                                           std::int64_t nseg,
                                                           const double* __restrict__ lu,
                                                           std::int64_t lu_total,
-                                                          double* __restrict__ S) {
+                                                          const double* __restrict__ S,
+                                                          double* __restrict__ q4) {
   __shared__ double sh[4][640];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x >> 5) + warp;
@@ -487,23 +514,24 @@ __global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __rest
   const int r = sg.r;
   double* v = sh[warp];  // v and w, r <= 320 (enforced on the host)
   double* w = v + 320;
-  double* Sg = S + sg.so;
+  const double* Sg = S + sg.so;
+  double* out = q4 + 4 * sg.so + 3;
   for (int q = lane; q < r; q += 32) v[q] = Sg[q];
   __syncwarp();
   const double* P = lu + sg.lu_off;
   const double* PT = P + lu_total;
   switch ((r + 31) >> 5) {
     case 0: break;
-    case 1: solve_seg<1>(sg, P, PT, v, w, Sg, lane); break;
-    case 2: solve_seg<2>(sg, P, PT, v, w, Sg, lane); break;
-    case 3: solve_seg<3>(sg, P, PT, v, w, Sg, lane); break;
-    case 4: solve_seg<4>(sg, P, PT, v, w, Sg, lane); break;
-    case 5: solve_seg<5>(sg, P, PT, v, w, Sg, lane); break;
-    case 6: solve_seg<6>(sg, P, PT, v, w, Sg, lane); break;
-    case 7: solve_seg<7>(sg, P, PT, v, w, Sg, lane); break;
-    case 8: solve_seg<8>(sg, P, PT, v, w, Sg, lane); break;
-    case 9: solve_seg<9>(sg, P, PT, v, w, Sg, lane); break;
-    default: solve_seg<10>(sg, P, PT, v, w, Sg, lane); break;
+    case 1: solve_seg<1>(sg, P, PT, v, w, out, lane); break;
+    case 2: solve_seg<2>(sg, P, PT, v, w, out, lane); break;
+    case 3: solve_seg<3>(sg, P, PT, v, w, out, lane); break;
+    case 4: solve_seg<4>(sg, P, PT, v, w, out, lane); break;
+    case 5: solve_seg<5>(sg, P, PT, v, w, out, lane); break;
+    case 6: solve_seg<6>(sg, P, PT, v, w, out, lane); break;
+    case 7: solve_seg<7>(sg, P, PT, v, w, out, lane); break;
+    case 8: solve_seg<8>(sg, P, PT, v, w, out, lane); break;
+    case 9: solve_seg<9>(sg, P, PT, v, w, out, lane); break;
+    default: solve_seg<10>(sg, P, PT, v, w, out, lane); break;
   }
 }
 
@@ -592,8 +620,9 @@ __device__ void compute_pass(const Phase2Args& a, const TileRanges& tr, double2*
       }
       const std::int64_t idx = tr.start[lo] + (v - tr.pre[lo]);
       if (tr.kind[lo] == kRangeProxy) {
-        stage[2 * q] = make_double2(a.qx[idx], a.qy[idx]);
-        stage[2 * q + 1] = make_double2(a.qz[idx], a.S[idx]);
+        const double4 r = reinterpret_cast<const double4*>(a.q4)[idx];
+        stage[2 * q] = make_double2(r.x, r.y);
+        stage[2 * q + 1] = make_double2(r.z, r.w);
       } else {
         stage[2 * q] = make_double2(a.px[idx], a.py[idx]);
         stage[2 * q + 1] = make_double2(a.pz[idx], a.xp[idx]);
@@ -736,19 +765,33 @@ struct NearSmem {
 // One accumulator per row in the admissible (Newton) scale: dense-near terms
 // enter with weight w / far_scale (exact power-of-two scalings), the caller
 // multiplies by far_scale once.
+// Staged sources are 32-byte (x, y, z, w) records read one per lane: two
+// 16-byte loads per lane, the half order swizzled by lane bit 2 so each
+// group of 8 lanes covers all 32 banks (a plain stride-32 B read is 2-way
+// bank-conflicted).
+__device__ __forceinline__ double4 ld_src(const double4* __restrict__ st, int j, int h) {
+  const double2* p = reinterpret_cast<const double2*>(st + j);
+  const double2 a = p[h], b = p[h ^ 1];
+  return h ? make_double4(b.x, b.y, a.x, a.y) : make_double4(a.x, a.y, b.x, b.y);
+}
+
+// One accumulator per row in the admissible (Newton) scale: dense-near terms
+// enter with weight w / far_scale (exact power-of-two scalings), the caller
+// multiplies by far_scale once.
 template <int K, int RPW>
 __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const NearMeta& mt, int row0,
                                            const double (&tx)[RPW], const double (&ty)[RPW],
                                            const double (&tz)[RPW], double (&acc)[RPW], double diag,
                                            int lane) {
   constexpr double inv = 1.0 / far_scale<K>();
+  const int h = (lane >> 2) & 1;
   const int base = mt.base, cnt = mt.cnt;
   // [0, e_self): self block (diagonal rule); [e_self, e_dense): dense near;
   // [e_dense, cnt): admissible partners
   const int e_self = max(0, min(cnt, mt.m - base));
   const int e_dense = max(e_self, min(cnt, mt.dense_end - base));
   for (int j = lane; j < e_self; j += 32) {
-    const double4 q = st[j];
+    const double4 q = ld_src(st, j, h);
     const double w = inv * q.w;
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
@@ -758,14 +801,14 @@ __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const
     }
   }
   for (int j = e_self + lane; j < e_dense; j += 32) {
-    const double4 q = st[j];
+    const double4 q = ld_src(st, j, h);
     const double w = inv * q.w;
 #pragma unroll
     for (int r = 0; r < RPW; ++r)
       acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z)), w, acc[r]);
   }
   for (int j = e_dense + lane; j < cnt; j += 32) {
-    const double4 q = st[j];
+    const double4 q = ld_src(st, j, h);
 #pragma unroll
     for (int r = 0; r < RPW; ++r) acc[r] = far_acc<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z), q.w, acc[r]);
   }
@@ -811,21 +854,36 @@ __device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) 
   return t;
 }
 
-// Producer (lane 0): wait for the stage's slot, publish the chunk's metadata,
-// copy its pieces.
+// Producer warp: wait for the stage's slot, copy the chunk's range pieces,
+// publish its metadata: one cp.async.bulk per piece from lane 0, byte-counted
+// on the buffer's mbarrier (H3D_NEAR_LDG: the warp's lanes copy the records
+// with 16-byte loads instead - measured 1.4x slower, the producer then
+// cannot stay a chunk ahead).
 __device__ __forceinline__ void near_put(NearSmem& sm, unsigned t, NearMeta mt, const double4* p4,
-                                         int& re, int& roff, int nrange) {
+                                         int& re, int& roff, int nrange, int lane) {
   const int s = t % 2;
-  if (t >= 2) mbar_wait(&sm.empty[s], ((t / 2) - 1) & 1);
+  if (t >= 2) {
+    if (lane == 0) mbar_wait(&sm.empty[s], ((t / 2) - 1) & 1);
+    __syncwarp();
+  }
   int filled = 0;
   if (mt.cnt >= 0) {
     while (re < nrange && filled < kNearStage) {
       const int len = sm.rlen[re];
       const int take = min(len - roff, kNearStage - filled);
       if (take > 0) {
-        const unsigned bytes = static_cast<unsigned>(take) * 32u;
-        mbar_expect_tx(&sm.full[s], bytes);
-        bulk_g2s(&sm.stage[s][filled], p4 + sm.rstart[re] + roff, bytes, &sm.full[s], 0);
+        const double4* src = p4 + sm.rstart[re] + roff;
+#ifndef H3D_NEAR_LDG
+        if (lane == 0) {
+          const unsigned bytes = static_cast<unsigned>(take) * 32u;
+          mbar_expect_tx(&sm.full[s], bytes);
+          bulk_g2s(&sm.stage[s][filled], src, bytes, &sm.full[s], 0);
+        }
+#else
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+        double2* d2 = reinterpret_cast<double2*>(&sm.stage[s][filled]);
+        for (int i = lane; i < 2 * take; i += 32) d2[i] = __ldg(s2 + i);
+#endif
         filled += take;
         roff += take;
       }
@@ -836,8 +894,11 @@ __device__ __forceinline__ void near_put(NearSmem& sm, unsigned t, NearMeta mt, 
     }
     mt.cnt = filled;
   }
-  sm.meta[s] = mt;
-  mbar_arrive(&sm.full[s]);
+  __syncwarp();
+  if (lane == 0) {
+    sm.meta[s] = mt;
+    mbar_arrive(&sm.full[s]);
+  }
 }
 
 template <int K>
@@ -882,22 +943,20 @@ __global__ void __maxnreg__(96) p2_near_kernel(const Phase2Args a) {
         dense += __shfl_xor_sync(0xffffffffu, dense, o);
       }
       __syncwarp();
-      if (lane == 0) {
-        const int nchunks = (tot + kNearStage - 1) / kNearStage;
-        for (int r0 = 0; r0 < m; r0 += kNearRows) {
-          const int mr = min(kNearRows, m - r0);
-          int re = 0, roff = 0;
-          for (int c = 0; c < nchunks; ++c, ++t)
-            near_put(sm, t,
-                     NearMeta{xb, r0, mr, c * kNearStage, 0, m, dense, c + 1 == nchunks ? 1 : 0, 0}, P4,
-                     re, roff, nrange);
-        }
+      const int nchunks = (tot + kNearStage - 1) / kNearStage;
+      for (int r0 = 0; r0 < m; r0 += kNearRows) {
+        const int mr = min(kNearRows, m - r0);
+        int re = 0, roff = 0;
+        for (int c = 0; c < nchunks; ++c, ++t)
+          near_put(sm, t,
+                   NearMeta{xb, r0, mr, c * kNearStage, 0, m, dense, c + 1 == nchunks ? 1 : 0, 0}, P4, re,
+                   roff, nrange, lane);
       }
       __syncwarp();
     }
-    if (lane == 0) {
+    {
       int re = 0, roff = 0;
-      near_put(sm, t, NearMeta{0, 0, 0, 0, -1, 0, 0, 1, 0}, P4, re, roff, 0);
+      near_put(sm, t, NearMeta{0, 0, 0, 0, -1, 0, 0, 1, 0}, P4, re, roff, 0, lane);
     }
     return;
   }
@@ -930,6 +989,15 @@ __global__ void __maxnreg__(64) p2_stream_kernel(const Phase2Args a) {
   stream_init(sm);
   if (warp == 0) {
     const unsigned long long pol = l2_evict_first();
+    if (a.wait_flag != nullptr && lane == 0) {
+      unsigned v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.wait_flag) : "memory");
+        if (static_cast<int>(v - a.wait_value) >= 0) break;
+        __nanosleep(256);
+      }
+    }
+    __syncwarp();
     stream_producer(sm, a.p2s_descs, a.n_p2s_items, a.counter2,
                     [&](unsigned& t, int k, const StreamDesc& e) {
                       for (int c0 = 0; c0 < e.nct; c0 += kSC, ++t) {
@@ -1000,10 +1068,13 @@ __global__ void __maxnreg__(64) p2_stream_kernel(const Phase2Args a) {
 
 // ---- phase 2, proxy levels, node-major: b_X += K(X, P_A) s_A for the rows of
 // node A (up to 256 per item, two per thread), the node's proxy list staged
-// in shared memory (proxy_eval2 above).
+// in shared memory (proxy_eval2 above). Items of <= 128 / <= 64 rows split
+// the CTA into 2 / 4 groups that take disjoint parts of every staged chunk
+// (all 256 target slots busy on small nodes), partials summed in group order.
 template <int K>
 __global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2Args a) {
   __shared__ double2 src[2 * kChunk];
+  __shared__ double red[2 * kProxyThreads];
   __shared__ long long s_k;
   for (;;) {
     __syncthreads();
@@ -1015,11 +1086,15 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2
     const std::int64_t g = it.node;
     const std::int64_t so = a.nt.soff[g];
     const int R = a.nt.rpad[g];
+    const int G = it.nrows <= 64 ? 4 : it.nrows <= 128 ? 2 : 1;
+    const int tpg = kProxyThreads / G;  // threads per group
+    const int grp = threadIdx.x / tpg, loc = threadIdx.x % tpg;
+    const int nt = warp_targets(loc, tpg, it.nrows);
     const double4* P4 = reinterpret_cast<const double4*>(a.p4);
     double tx[2], ty[2], tz[2], acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
-      const int i = threadIdx.x + t * kProxyThreads;
+      const int i = loc + t * tpg;
       const double4 q = i < it.nrows ? P4[a.nt.rowbeg[g] + it.row0 + i] : make_double4(kFar, kFar, kFar, 0.0);
       tx[t] = q.x;
       ty[t] = q.y;
@@ -1029,19 +1104,24 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2
       const int nj = min(kChunk, R - j0);
       __syncthreads();
       for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
-        const std::int64_t qq = so + j0 + q;
-        src[2 * q] = make_double2(a.qx[qq], a.qy[qq]);
-        src[2 * q + 1] = make_double2(a.qz[qq], a.S[qq]);
+        const double4 r = reinterpret_cast<const double4*>(a.q4)[so + j0 + q];
+        src[2 * q] = make_double2(r.x, r.y);
+        src[2 * q + 1] = make_double2(r.z, r.w);
       }
       __syncthreads();
-      proxy_eval2<K>(tx, ty, tz, acc, src, nj);
+      const int sub = (nj + G - 1) / G;
+      const int lo = min(nj, grp * sub), hi = min(nj, lo + sub);
+      proxy_eval2<K>(tx, ty, tz, acc, src + 2 * lo, hi - lo, nt);
     }
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int i = threadIdx.x + t * kProxyThreads;
-      if (i < it.nrows)
-        a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + a.nt.rowbeg[g] + it.row0 + i] =
-            far_scale<K>() * (acc[t][0] + acc[t][1]);
+    for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = acc[t][0] + acc[t][1];
+    __syncthreads();
+    for (int i = threadIdx.x; i < it.nrows; i += kProxyThreads) {
+      const int per = 2 * tpg;  // targets per group
+      double v = 0.0;
+      for (int q = 0; q < G; ++q) v += red[q * per + i];
+      a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + a.nt.rowbeg[g] + it.row0 + i] =
+          far_scale<K>() * v;
     }
   }
 }
@@ -1236,13 +1316,24 @@ void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
+__global__ void fill_far_kernel(double4* __restrict__ q4, std::int64_t n) {
+  const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) q4[i] = make_double4(kFar, kFar, kFar, 0.0);
+}
+
+void launch_fill_far(double* q4, std::int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  fill_far_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<double4*>(q4), n);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
 void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int32_t* piv,
-                         const double* px, const double* py, const double* pz, double* qx,
-                         double* qy, double* qz, cudaStream_t s) {
+                         const double* px, const double* py, const double* pz, double* q4,
+                         cudaStream_t s) {
   if (nseg == 0) return;
   const dim3 block(32, 8);
   proxy_gather_kernel<<<static_cast<unsigned>((nseg + 7) / 8), block, 0, s>>>(segs, nseg, piv, px, py,
-                                                                            pz, qx, qy, qz);
+                                                                            pz, reinterpret_cast<double4*>(q4));
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1264,11 +1355,11 @@ void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::
 }
 
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
-                        std::int64_t lu_total, double* S, cudaStream_t s) {
+                        std::int64_t lu_total, const double* S, double* q4, cudaStream_t s) {
   if (nseg == 0) return;
   constexpr int warps = 4;
   proxy_solve_kernel<<<static_cast<unsigned>((nseg + warps - 1) / warps), 32 * warps, 0, s>>>(
-      segs, nseg, lu, lu_total, S);
+      segs, nseg, lu, lu_total, S, q4);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1319,6 +1410,15 @@ void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
       break;
     }
   }
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+__global__ void set_flag_kernel(unsigned* flag, unsigned value) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+
+void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s) {
+  set_flag_kernel<<<1, 1, 0, s>>>(flag, value);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

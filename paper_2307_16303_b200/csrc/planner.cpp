@@ -325,9 +325,13 @@ void Planner::layout() {
       if (rpad[g] == 0 || !owned(l, z)) continue;
       if (slot < 0) slot = n_proxy_levels++;
       const std::int64_t nr = node_size(l, z);
-      for (std::int64_t r0 = 0; r0 < nr; r0 += step)
+      // proxy levels: even split into ceil(nr / 256) items (a 256 + small
+      // remainder split leaves most of the second item's target slots idle)
+      const std::int64_t per =
+          stream ? step : (nr + (nr + step - 1) / step - 1) / ((nr + step - 1) / step);
+      for (std::int64_t r0 = 0; r0 < nr; r0 += per)
         dst.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
-                             static_cast<std::int32_t>(std::min<std::int64_t>(step, nr - r0)), slot});
+                             static_cast<std::int32_t>(std::min<std::int64_t>(per, nr - r0)), slot});
     }
   }
 
