@@ -277,6 +277,12 @@ int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, in
     else if (nm == "pair_cy") put(P.pair_cy.at(level), out, count);
     else if (nm == "p2_items") put(P.p2_items, out, count);
     else if (nm == "p2s_items") put(P.p2s_items, out, count);
+    else if (nm == "sym_off") put(P.sym_off, out, count);
+    else if (nm == "sym_ids") put(P.sym_ids, out, count);
+    else if (nm == "sym_cnt") put(P.sym_cnt, out, count);
+    else if (nm == "out_off") put(P.out_off, out, count);
+    else if (nm == "in_off") put(P.in_off, out, count);
+    else if (nm == "in_pos") put(P.in_pos, out, count);
     else if (nm == "pair_piv") put(P.pair_piv.at(level), out, count);
     else if (nm == "pair_lu") put(P.pair_lu.at(level), out, count);
     else if (nm == "proxy_segs") put(P.proxy_segs, out, count);

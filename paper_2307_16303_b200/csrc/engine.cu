@@ -44,11 +44,11 @@ double proxy_rate(int kernel) {  // evaluations / s, Newton-form proxy kernels
     default: return 0.2e12;
   }
 }
-double near_rate(int kernel) {   // evaluations / s, near field + direct blocks
-  switch (kernel) {
-    case kLaplace: return 1.1e12;
-    case kR4: return 0.8e12;
-    default: return 0.15e12;
+double near_rate(int kernel) {   // entries / s, near field + direct blocks (each owned
+  switch (kernel) {              // pair evaluated once: ~2x the per-entry rate)
+    case kLaplace: return 1.9e12;
+    case kR4: return 1.4e12;
+    default: return 0.25e12;
   }
 }
 
@@ -638,6 +638,19 @@ void Engine::upload_plan() {
   near_off_.upload(P.near_off, stream_);
   near_ids_.upload(P.near_ids.empty() ? std::vector<std::int32_t>{0} : P.near_ids, stream_);
   near_dense_.upload(P.near_dense, stream_);
+  sym_near_ = opt_.near_mode != H3D_NEAR_STORED;
+  if (sym_near_) {
+    for (std::size_t x = 0; x + 1 < P.sym_off.size(); ++x)
+      if (P.sym_off[x + 1] - P.sym_off[x] > kMaxNearRanges)
+        throw std::logic_error("planner: leaf near list longer than the near kernel's range table");
+    sym_off_.upload(P.sym_off, stream_);
+    sym_ids_.upload(P.sym_ids.empty() ? std::vector<std::int32_t>{0} : P.sym_ids, stream_);
+    sym_cnt_.upload(P.sym_cnt.empty() ? std::vector<std::int32_t>{0} : P.sym_cnt, stream_);
+    out_off_.upload(P.out_off, stream_);
+    in_off_.upload(P.in_off, stream_);
+    in_pos_.upload(P.in_pos.empty() ? std::vector<std::int64_t>{0} : P.in_pos, stream_);
+    pairbuf_.alloc(std::max<std::int64_t>(P.out_off.back(), 1));
+  }
   has_stream_levels_ = false;
   for (int l = 1; l <= L_; ++l)
     if (P.mode(l) == kModeStream && !P.pairs(l).X.empty()) has_stream_levels_ = true;
@@ -663,7 +676,7 @@ void Engine::upload_plan() {
   }
   n_p2s_ = static_cast<std::int64_t>(P.p2s_items.size());
   n_lvl_ = P.n_proxy_levels;
-  if (n_lvl_ > 0) {
+  if (n_lvl_ > 0 || sym_near_) {
     cpart_.alloc(n_);
     // rows of nodes without partners at a level are never written
     lvl_part_.alloc(static_cast<std::size_t>(n_lvl_) * n_);
@@ -710,9 +723,16 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.kernel = opt_.kernel_id;
   a.diag = opt_.diagonal;
   a.b = bout;
-  if (n_lvl_ > 0) {
+  if (n_lvl_ > 0 || sym_near_) {
     a.cpart_out = cpart_.get();
     a.lvl_part = lvl_part_.get();
+  }
+  if (sym_near_) {
+    a.sym_off = sym_off_.get();
+    a.sym_ids = sym_ids_.get();
+    a.sym_cnt = sym_cnt_.get();
+    a.out_off = out_off_.get();
+    a.pairbuf = pairbuf_.get();
   }
   if (n_p2s_ > 0) {
     a.p2s_items = p2s_items_.get();
@@ -810,7 +830,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // Persistent CTAs with per-SM budgets: one 5-warp bulk-copy CTA per SM holds
   // HBM near peak, the FP64 kernels fill the remaining registers.
   const bool has_p2 = P.leaf1 > P.leaf0;
-  const bool parts = n_lvl_ > 0;  // p2_compute writes partials, combine sums them
+  const bool parts = n_lvl_ > 0 || sym_near_;  // near pass writes partials, combine sums them
   const bool hbm = n_p1s_ > 0 || n_p2s_ > 0;
   const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0;
   H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 5 * sizeof(unsigned), s));
@@ -907,7 +927,9 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   if (hbm) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
   if (has_p2 && parts) {
     kb(H3D_K_COMBINE, s);
-    launch_combine(cpart_.get(), lvl_part_.get(), n_lvl_, n_, perm_.get(), P.row0, P.row1, bout, s);
+    launch_combine(cpart_.get(), lvl_part_.get(), n_lvl_, n_, leaf_off_.get(), P.leaf0, P.leaf1 - P.leaf0,
+                   sym_near_ ? in_off_.get() : nullptr, sym_near_ ? in_pos_.get() : nullptr,
+                   sym_near_ ? pairbuf_.get() : nullptr, perm_.get(), bout, s);
     ke(H3D_K_COMBINE, s);
     ++launches;
   }

@@ -128,6 +128,10 @@ class Engine {
   std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_s_ = 0, n_red_p_ = 0;
   bool has_stream_levels_ = false;
   DevBuf<std::int32_t> near_off_, near_ids_, near_dense_;
+  DevBuf<std::int32_t> sym_off_, sym_ids_, sym_cnt_, in_off_;
+  DevBuf<std::int64_t> out_off_, in_pos_;
+  DevBuf<double> pairbuf_;  // symmetric near-field column sums (owned pairs)
+  bool sym_near_ = false;   // matrix-free near field with pair symmetry
   DevBuf<double> cpart_;
   DevBuf<P2Item> p2_items_, p2s_items_;
   DevBuf<StreamDesc> p1s_desc_, p2s_desc_;

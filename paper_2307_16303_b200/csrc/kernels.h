@@ -161,6 +161,13 @@ struct Phase2Args {
   const std::int32_t* near_off = nullptr;
   const std::int32_t* near_ids = nullptr;
   const std::int32_t* near_dense = nullptr;  // per leaf: leading dense entries (self/edge/face)
+  // matrix-free symmetric lists (planner.h): per leaf [self | dense one-way |
+  // direct one-way | dense sym | direct sym], category counts, pair-buffer runs
+  const std::int32_t* sym_off = nullptr;
+  const std::int32_t* sym_ids = nullptr;
+  const std::int32_t* sym_cnt = nullptr;
+  const std::int64_t* out_off = nullptr;
+  double* pairbuf = nullptr;
   // stored near field (near_mode 0): per leaf a column-major m x (sum n) block
   const std::int64_t* nf_off = nullptr;
   const double* NF = nullptr;
@@ -199,10 +206,13 @@ void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 // *flag = value (release, device scope), stream-ordered
 void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s);
-// b[perm[p]] = cpart[p] + sum over levels (in order) of lvl_part[l][p]
+// b[perm[p]] = cpart[p] + incoming pair-buffer runs of p's leaf (ascending
+// partner, may be null) + sum over levels (in order) of lvl_part[l][p];
+// one warp per owned leaf
 void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
-                    const std::int32_t* perm, std::int64_t row0, std::int64_t row1, double* b,
-                    cudaStream_t s);
+                    const std::int64_t* leaf_off, std::int64_t leaf0, std::int64_t nleaves,
+                    const std::int32_t* in_off, const std::int64_t* in_pos, const double* pairbuf,
+                    const std::int32_t* perm, double* b, cudaStream_t s);
 
 // Build-time near-field scan: coincidence check (and optional store).
 void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s);

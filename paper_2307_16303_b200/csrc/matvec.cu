@@ -728,43 +728,45 @@ __global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Arg
 
 // ---- phase 2, near field + direct leaf blocks, matrix-free ------------------
 // Warp-specialised persistent CTA: a producer warp claims owned leaves X,
-// builds X's source range table (self, edge and face neighbours = the
-// reference's dense blocks, then the leaf-level admissible partners evaluated
-// directly) and streams the flattened sources from the packed (x, y, z, w)
-// points into a double-buffered shared stage with cp.async.bulk (one copy per
-// range piece, byte-counted on the buffer's "full" mbarrier); seven consumer
-// warps own the leaf's rows (warp w: rows [w RPW, (w + 1) RPW), RPW =
-// ceil(m / 7) <= 6), lanes stride over the staged sources and evaluate each one
-// against the warp's RPW rows (RPW independent FP64 chains per lane), then
-// release the buffer on its "empty" mbarrier - no block-wide barrier on the
-// hot path. Dense-near sources use the full-accuracy rsqrt (+ the diagonal
-// rule on the self block), admissible ones the Newton form. Every row has
-// one owning warp: the only reduction is the fixed warp butterfly.
-constexpr int kNearStage = 512;            // sources per staged chunk (16 KB)
+// builds X's source range table (planner.h sym lists: self | dense one-way |
+// direct one-way | dense sym | direct sym) and streams the flattened sources
+// from the packed (x, y, z, w) points into a double-buffered shared stage
+// with cp.async.bulk (one copy per range piece, byte-counted on the buffer's
+// "full" mbarrier); seven consumer warps own the leaf's rows (warp w: rows
+// [w RPW, (w + 1) RPW), RPW = ceil(m / 7) <= 7), lanes stride over the staged
+// sources and evaluate each one against the warp's RPW rows (RPW independent
+// FP64 chains per lane). Dense-near sources use the full-accuracy rsqrt (+ the
+// diagonal rule on the self block), admissible ones the Newton form.
+// Symmetry: an owned pair (X, Y), Y > X, is evaluated once - each entry feeds
+// X's row sums and a column sum for Y's point (sum over the warp's rows, then
+// over the warps through shared memory in warp order), written to the pair
+// buffer; combine adds Y's incoming runs. Every output has one writer and a
+// fixed order: bitwise reproducible.
+constexpr int kNearStage = 256;            // sources per staged chunk (8 KB)
 constexpr int kNearConsumers = kWarps - 1;  // 7 consumer warps + 1 producer = 256 threads
 constexpr int kNearThreads = 32 * (kNearConsumers + 1);
-constexpr int kNearRows = 6 * kNearConsumers;  // rows per pass (leaves above 42 points: 2 passes)
+constexpr int kNearRows = kNearPassRows;  // rows per pass (7 per consumer warp; larger leaves: 2+ passes)
+static_assert(kNearRows == 7 * kNearConsumers, "near pass = 7 rows per consumer warp");
 constexpr int kMaxNear = kMaxNearRanges;
 
 struct NearMeta {
-  long long xb;   // first permuted row of the leaf
-  int r0, mr;     // row pass: rows [r0, r0 + mr) of the leaf (mr <= kNearRows)
-  int base, cnt;  // flattened index of the chunk's first source, sources in the chunk (< 0: stop)
-  int m, dense_end;  // rows of the leaf (= self range length), end of the dense-near sources
-  int last, pad;     // last chunk of this row pass
+  long long xb;    // first permuted row of the leaf
+  long long obase; // pair-buffer index of flattened source 0 (sym sources only)
+  int r0, mr;      // row pass: rows [r0, r0 + mr) of the leaf (mr <= kNearRows)
+  int base, cnt;   // flattened index of the chunk's first source, sources in the chunk (< 0: stop)
+  int e0, e1, e2, e3;  // flattened ends: self, dense one-way, direct one-way, dense sym
+  int last, pad;   // last chunk of this row pass
 };
 
 struct NearSmem {
   double4 stage[2][kNearStage];
+  double col[kNearConsumers][kNearStage];  // per-warp column partials of sym sources
   unsigned long long full[2], empty[2];
   NearMeta meta[2];
   long long rstart[kMaxNear];  // producer's range table (permuted index, length)
   int rlen[kMaxNear];
 };
 
-// One accumulator per row in the admissible (Newton) scale: dense-near terms
-// enter with weight w / far_scale (exact power-of-two scalings), the caller
-// multiplies by far_scale once.
 // Staged sources are 32-byte (x, y, z, w) records read one per lane: two
 // 16-byte loads per lane, the half order swizzled by lane bit 2 so each
 // group of 8 lanes covers all 32 banks (a plain stride-32 B read is 2-way
@@ -775,22 +777,59 @@ __device__ __forceinline__ double4 ld_src(const double4* __restrict__ st, int j,
   return h ? make_double4(b.x, b.y, a.x, a.y) : make_double4(a.x, a.y, b.x, b.y);
 }
 
-// One accumulator per row in the admissible (Newton) scale: dense-near terms
-// enter with weight w / far_scale (exact power-of-two scalings), the caller
-// multiplies by far_scale once.
+// One row accumulator per row in the admissible (Newton) scale: dense-near
+// terms enter with weight w / far_scale (exact power-of-two scalings), the
+// caller multiplies by far_scale once; column partials likewise.
+template <int K, int RPW, bool DENSE, bool SYM>
+__device__ __forceinline__ void near_seg(const double4* __restrict__ st, int lo, int hi,
+                                         const double (&tx)[RPW], const double (&ty)[RPW],
+                                         const double (&tz)[RPW], const double (&tw)[RPW],
+                                         double (&acc)[RPW], double* __restrict__ col, int lane) {
+  constexpr double inv = 1.0 / far_scale<K>();
+  const int h = (lane >> 2) & 1;
+  for (int j = lo + lane; j < hi; j += 32) {
+    const double4 q = ld_src(st, j, h);
+    double cp = 0.0;
+    if constexpr (DENSE) {
+      const double w = inv * q.w;
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const double k = kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
+        acc[r] = fma(k, w, acc[r]);
+        if constexpr (SYM) cp = fma(k, tw[r], cp);
+      }
+      if constexpr (SYM) col[j] = inv * cp;
+    } else {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const double r2 = sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z);
+        if constexpr (SYM) {
+          // the Newton-form value once, for both sums
+          const double g = far_acc<K>(r2, 1.0, 0.0);
+          acc[r] = fma(g, q.w, acc[r]);
+          cp = fma(g, tw[r], cp);
+        } else {
+          acc[r] = far_acc<K>(r2, q.w, acc[r]);
+        }
+      }
+      if constexpr (SYM) col[j] = cp;
+    }
+  }
+}
+
 template <int K, int RPW>
 __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const NearMeta& mt, int row0,
                                            const double (&tx)[RPW], const double (&ty)[RPW],
-                                           const double (&tz)[RPW], double (&acc)[RPW], double diag,
+                                           const double (&tz)[RPW], const double (&tw)[RPW],
+                                           double (&acc)[RPW], double* __restrict__ col, double diag,
                                            int lane) {
   constexpr double inv = 1.0 / far_scale<K>();
   const int h = (lane >> 2) & 1;
   const int base = mt.base, cnt = mt.cnt;
-  // [0, e_self): self block (diagonal rule); [e_self, e_dense): dense near;
-  // [e_dense, cnt): admissible partners
-  const int e_self = max(0, min(cnt, mt.m - base));
-  const int e_dense = max(e_self, min(cnt, mt.dense_end - base));
-  for (int j = lane; j < e_self; j += 32) {
+  auto cut = [&](int e) { return max(0, min(cnt, e - base)); };
+  const int c0 = cut(mt.e0), c1 = cut(mt.e1), c2 = cut(mt.e2), c3 = cut(mt.e3);
+  // self block, diagonal rule
+  for (int j = lane; j < c0; j += 32) {
     const double4 q = ld_src(st, j, h);
     const double w = inv * q.w;
 #pragma unroll
@@ -800,18 +839,10 @@ __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const
       acc[r] = fma(k, w, acc[r]);
     }
   }
-  for (int j = e_self + lane; j < e_dense; j += 32) {
-    const double4 q = ld_src(st, j, h);
-    const double w = inv * q.w;
-#pragma unroll
-    for (int r = 0; r < RPW; ++r)
-      acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z)), w, acc[r]);
-  }
-  for (int j = e_dense + lane; j < cnt; j += 32) {
-    const double4 q = ld_src(st, j, h);
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) acc[r] = far_acc<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z), q.w, acc[r]);
-  }
+  near_seg<K, RPW, true, false>(st, c0, c1, tx, ty, tz, tw, acc, col, lane);
+  near_seg<K, RPW, false, false>(st, c1, c2, tx, ty, tz, tw, acc, col, lane);
+  near_seg<K, RPW, true, true>(st, c2, c3, tx, ty, tz, tw, acc, col, lane);
+  near_seg<K, RPW, false, true>(st, c3, cnt, tx, ty, tz, tw, acc, col, lane);
 }
 
 // Consumer warp: one row pass of one leaf, starting at the (already waited)
@@ -822,7 +853,7 @@ __device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) 
   const NearMeta m0 = sm.meta[t % 2];
   const int row0 = m0.r0 + warp * RPW;
   const double4* P4 = reinterpret_cast<const double4*>(a.p4);
-  double tx[RPW], ty[RPW], tz[RPW], acc[RPW];
+  double tx[RPW], ty[RPW], tz[RPW], tw[RPW], acc[RPW];
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
     const bool ok = row0 + r < m0.r0 + m0.mr;
@@ -830,14 +861,26 @@ __device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) 
     tx[r] = q.x;
     ty[r] = q.y;
     tz[r] = q.z;
+    tw[r] = q.w;
     acc[r] = 0.0;
   }
   for (;;) {
     const int s = t % 2;
     const NearMeta mt = sm.meta[s];
-    near_chunk<K, RPW>(sm.stage[s], mt, row0, tx, ty, tz, acc, a.diag, lane);
+    near_chunk<K, RPW>(sm.stage[s], mt, row0, tx, ty, tz, tw, acc, sm.col[warp], a.diag, lane);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);
+    if (mt.base + mt.cnt > mt.e2) {  // chunk holds sym sources: column sums in warp order
+      named_bar(1, 32 * kNearConsumers);
+      const int lo = max(0, mt.e2 - mt.base);
+      for (int j = lo + threadIdx.x; j < mt.cnt; j += 32 * kNearConsumers) {
+        double v = sm.col[0][j];
+#pragma unroll
+        for (int w = 1; w < kNearConsumers; ++w) v += sm.col[w][j];
+        a.pairbuf[mt.obase + mt.base + j] = far_scale<K>() * v;
+      }
+      named_bar(1, 32 * kNearConsumers);
+    }
     ++t;
     if (mt.last) break;
     mbar_wait(&sm.full[t % 2], (t / 2) & 1);
@@ -902,7 +945,7 @@ __device__ __forceinline__ void near_put(NearSmem& sm, unsigned t, NearMeta mt, 
 }
 
 template <int K>
-__global__ void __maxnreg__(96) p2_near_kernel(const Phase2Args a) {
+__global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Args a) {
   __shared__ __align__(128) NearSmem sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -925,38 +968,49 @@ __global__ void __maxnreg__(96) p2_near_kernel(const Phase2Args a) {
       const std::int64_t xb = a.leaf_off[X];
       const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
       if (m == 0) continue;
-      const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1], nd = a.near_dense[X];
+      const std::int32_t nb = a.sym_off[X], ne = a.sym_off[X + 1];
       const int nrange = ne - nb;
-      int tot = 0, dense = 0;  // per lane, then warp-reduced (integers: exact)
+      // range-count boundaries of the four categories after self
+      const int b1 = 1 + a.sym_cnt[4 * X], b2 = b1 + a.sym_cnt[4 * X + 1];
+      const int b3 = b2 + a.sym_cnt[4 * X + 2];
+      int tot = 0, e1 = 0, e2 = 0, e3 = 0;  // per lane, then warp-reduced (integers: exact)
       for (int e = lane; e < nrange; e += 32) {
-        const std::int32_t Y = a.near_ids[nb + e];
+        const std::int32_t Y = a.sym_ids[nb + e];
         const std::int64_t yb = a.leaf_off[Y];
         const int len = static_cast<int>(a.leaf_off[Y + 1] - yb);
         sm.rstart[e] = yb;
         sm.rlen[e] = len;
         tot += len;
-        if (e < nd) dense += len;
+        if (e < b1) e1 += len;
+        if (e < b2) e2 += len;
+        if (e < b3) e3 += len;
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        dense += __shfl_xor_sync(0xffffffffu, dense, o);
+        e1 += __shfl_xor_sync(0xffffffffu, e1, o);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        e3 += __shfl_xor_sync(0xffffffffu, e3, o);
       }
       __syncwarp();
+      const long long obase = a.out_off[X] - e2;
       const int nchunks = (tot + kNearStage - 1) / kNearStage;
       for (int r0 = 0; r0 < m; r0 += kNearRows) {
         const int mr = min(kNearRows, m - r0);
+        // leaves above one pass have no sym partners (planner.cpp), so the
+        // column sums of a sym source are always complete after one sweep
         int re = 0, roff = 0;
         for (int c = 0; c < nchunks; ++c, ++t)
           near_put(sm, t,
-                   NearMeta{xb, r0, mr, c * kNearStage, 0, m, dense, c + 1 == nchunks ? 1 : 0, 0}, P4, re,
-                   roff, nrange, lane);
+                   NearMeta{xb, obase, r0, mr, c * kNearStage, 0, m, e1, e2, e3,
+                            c + 1 == nchunks ? 1 : 0, 0},
+                   P4, re, roff, nrange, lane);
       }
       __syncwarp();
     }
     {
       int re = 0, roff = 0;
-      near_put(sm, t, NearMeta{0, 0, 0, 0, -1, 0, 0, 1, 0}, P4, re, roff, 0, lane);
+      near_put(sm, t, NearMeta{0, 0, 0, 0, 0, -1, 0, 0, 0, 0, 1, 0}, P4, re, roff, 0, lane);
     }
     return;
   }
@@ -971,7 +1025,8 @@ __global__ void __maxnreg__(96) p2_near_kernel(const Phase2Args a) {
       case 3: t = near_consume<K, 3>(sm, a, t); break;
       case 4: t = near_consume<K, 4>(sm, a, t); break;
       case 5: t = near_consume<K, 5>(sm, a, t); break;
-      default: t = near_consume<K, 6>(sm, a, t); break;
+      case 6: t = near_consume<K, 6>(sm, a, t); break;
+      default: t = near_consume<K, 7>(sm, a, t); break;
     }
   }
 }
@@ -1127,14 +1182,26 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2
 }
 
 __global__ void combine_kernel(const double* __restrict__ cpart, const double* __restrict__ lvl,
-                               int n_lvl, std::int64_t n_total,
-                               const std::int32_t* __restrict__ perm, std::int64_t row0,
-                               std::int64_t row1, double* __restrict__ b) {
-  const std::int64_t p = row0 + blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  if (p >= row1) return;
-  double v = cpart[p];
-  for (int l = 0; l < n_lvl; ++l) v += lvl[static_cast<std::int64_t>(l) * n_total + p];
-  b[perm[p]] = v;
+                               int n_lvl, std::int64_t n_total, const std::int64_t* __restrict__ leaf_off,
+                               std::int64_t leaf0, std::int64_t nleaves,
+                               const std::int32_t* __restrict__ in_off,
+                               const std::int64_t* __restrict__ in_pos,
+                               const double* __restrict__ pairbuf,
+                               const std::int32_t* __restrict__ perm, double* __restrict__ b) {
+  const std::int64_t t = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= nleaves) return;
+  const std::int64_t X = leaf0 + t;
+  const std::int64_t xb = leaf_off[X];
+  const int m = static_cast<int>(leaf_off[X + 1] - xb);
+  const int i0 = in_off ? in_off[X] : 0, i1 = in_off ? in_off[X + 1] : 0;
+  for (int i = lane; i < m; i += 32) {
+    const std::int64_t p = xb + i;
+    double v = cpart[p];
+    for (int e = i0; e < i1; ++e) v += pairbuf[in_pos[e] + i];
+    for (int l = 0; l < n_lvl; ++l) v += lvl[static_cast<std::int64_t>(l) * n_total + p];
+    b[perm[p]] = v;
+  }
 }
 
 // Build-time pass over every dense near-field pair: the reference forms all
@@ -1423,11 +1490,13 @@ void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s) {
 }
 
 void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
-                    const std::int32_t* perm, std::int64_t row0, std::int64_t row1, double* b,
-                    cudaStream_t s) {
-  if (row1 <= row0) return;
-  combine_kernel<<<static_cast<unsigned>((row1 - row0 + 255) / 256), 256, 0, s>>>(
-      cpart, lvl_part, n_lvl, n_total, perm, row0, row1, b);
+                    const std::int64_t* leaf_off, std::int64_t leaf0, std::int64_t nleaves,
+                    const std::int32_t* in_off, const std::int64_t* in_pos, const double* pairbuf,
+                    const std::int32_t* perm, double* b, cudaStream_t s) {
+  if (nleaves <= 0) return;
+  const std::int64_t threads = nleaves * 32;
+  combine_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
+      cpart, lvl_part, n_lvl, n_total, leaf_off, leaf0, nleaves, in_off, in_pos, pairbuf, perm, b);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

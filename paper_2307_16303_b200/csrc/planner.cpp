@@ -386,6 +386,58 @@ void Planner::layout() {
   }
   near_off[nl] = static_cast<std::int32_t>(near_ids.size());
   nf_off[nl] = nf_total;
+
+  // symmetric matrix-free lists (see planner.h)
+  sym_off.assign(nl + 1, 0);
+  sym_ids.clear();
+  sym_cnt.assign(4 * nl, 0);
+  out_off.assign(nl + 1, 0);
+  std::vector<std::vector<std::int64_t>> incoming(nl);
+  std::int64_t otot = 0;
+  auto own = [&](std::int64_t y) { return y >= leaf0 && y < leaf1; };
+  // a pair is evaluated once iff both leaves are owned and fit one pass of
+  // the near kernel (their column sums are then complete after one sweep)
+  auto sym = [&](std::int64_t u) { return own(u) && node_size(L_, u) <= kNearPassRows; };
+  for (std::int64_t x = 0; x < nl; ++x) {
+    sym_off[x] = static_cast<std::int32_t>(sym_ids.size());
+    out_off[x] = otot;
+    if (node_size(L_, x) == 0 || !own(x)) continue;
+    std::vector<std::int32_t> cat[4];  // dense one-way, direct one-way, dense sym, direct sym
+    auto put = [&](std::int64_t y, bool dense) {
+      if (node_size(L_, y) == 0) return;
+      const bool pair = sym(x) && sym(y);
+      if (pair && y < x) return;  // supplied by y's pass
+      cat[(pair ? 2 : 0) + (dense ? 0 : 1)].push_back(static_cast<std::int32_t>(y));
+    };
+    if (L_ > 0) {
+      for (int k = 1; k <= 2; ++k)
+        for (std::int32_t e = lists_[L_].off[k][x]; e < lists_[L_].off[k][x + 1]; ++e)
+          put(lists_[L_].ids[k][e], true);
+      if (mode_[L_] == kModeDirect)
+        for (std::int32_t e = lists_[L_].off[0][x]; e < lists_[L_].off[0][x + 1]; ++e)
+          put(lists_[L_].ids[0][e], false);
+    }
+    sym_ids.push_back(static_cast<std::int32_t>(x));
+    for (int c = 0; c < 4; ++c) {
+      sym_cnt[4 * x + c] = static_cast<std::int32_t>(cat[c].size());
+      for (std::int32_t y : cat[c]) {
+        sym_ids.push_back(y);
+        if (c >= 2) {
+          incoming[y].push_back(otot);
+          otot += node_size(L_, y);
+        }
+      }
+    }
+  }
+  sym_off[nl] = static_cast<std::int32_t>(sym_ids.size());
+  out_off[nl] = otot;
+  in_off.assign(nl + 1, 0);
+  in_pos.clear();
+  for (std::int64_t y = 0; y < nl; ++y) {
+    in_off[y] = static_cast<std::int32_t>(in_pos.size());
+    in_pos.insert(in_pos.end(), incoming[y].begin(), incoming[y].end());
+  }
+  in_off[nl] = static_cast<std::int32_t>(in_pos.size());
 }
 
 }  // namespace h3db

@@ -18,6 +18,9 @@ namespace h3db {
 // tiles, tile (rt, ct) at woff + (rt * rpad / kTileCols + ct) * kTileDoubles,
 // so every tile is one contiguous 8 KB bulk copy (cp.async.bulk) for both the
 // column sums of phase 1 and the row dots of phase 2.
+// rows per pass of the matrix-free near kernel (7 consumer warps x 7 rows);
+// only leaves within one pass take part in the symmetric pair evaluation
+constexpr int kNearPassRows = 49;
 constexpr int kTileRows = 16;
 constexpr int kTileCols = 64;
 constexpr int kTileDoubles = kTileRows * kTileCols;
@@ -170,6 +173,18 @@ class Planner {
   std::int64_t leaf0 = 0, leaf1 = 0;
   std::vector<std::int32_t> near_off, near_ids;
   std::vector<std::int32_t> near_dense;  // per leaf: leading dense entries (self, edge, face)
+  // matrix-free near field with the symmetry used once per owned pair: per
+  // owned leaf X the list [self | dense one-way | direct one-way | dense sym |
+  // direct sym] (sym_cnt: the four counts); "sym" = owned partner Y > X, its
+  // entries evaluated once for X's rows and (column sums) Y's rows, Y's part
+  // written to the pair buffer at out_off[X] + (flattened index - sym start);
+  // partners Y < X owned are omitted (their pass supplies X's part, in_off /
+  // in_pos = X's incoming pair-buffer runs, ascending Y); "one-way" = Y owned
+  // by another shard.
+  std::vector<std::int32_t> sym_off, sym_ids, sym_cnt;
+  std::vector<std::int64_t> out_off;  // nl + 1
+  std::vector<std::int32_t> in_off;   // nl + 1
+  std::vector<std::int64_t> in_pos;
   std::vector<std::int64_t> nf_off;  // stored near field offsets (per leaf)
   std::int64_t nf_total = 0;
   std::int64_t row0 = 0, row1 = 0;  // owned permuted rows

@@ -435,7 +435,8 @@ _PLAN_DTYPES = {
     "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
     "spos": np.int32, "pair_wx": np.int64, "pair_wy": np.int64, "pair_rx": np.int32,
     "pair_ry": np.int32, "pair_cx": np.int32, "pair_cy": np.int32, "pair_piv": np.int64, "pair_lu": np.int64, "near_off": np.int32,
-    "near_ids": np.int32, "near_dense": np.int32, "node_base": np.int64, "modes": np.int32, "ranges": np.int64,
+    "near_ids": np.int32, "near_dense": np.int32, "sym_off": np.int32, "sym_ids": np.int32,
+    "sym_cnt": np.int32, "out_off": np.int64, "in_off": np.int32, "in_pos": np.int64, "node_base": np.int64, "modes": np.int32, "ranges": np.int64,
     "rank_rows": np.int64, "sizes": np.int64,
     # structs, decoded as int64 fields (see csrc/planner.h)
     "proxy_segs": np.dtype([("so", np.int64), ("base", np.int64), ("piv_off", np.int64),

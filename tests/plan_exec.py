@@ -168,6 +168,37 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             if Y == X:
                 np.fill_diagonal(K, diag)
             cpart[xb:xe] += K @ xp[yb:ye]
+    # the symmetric matrix-free lists must give the same near field: each
+    # owned pair once, the partner's part through the pair buffer
+    y_off, y_ids, y_cnt = plan.array("sym_off"), plan.array("sym_ids"), plan.array("sym_cnt")
+    ooff, ioff, ipos = plan.array("out_off"), plan.array("in_off"), plan.array("in_pos")
+    pairbuf = np.zeros(max(int(ooff[-1]), 1))
+    csym = np.zeros(n)
+    for X in range(leaf0, leaf1):
+        xb, xe = off[L][X], off[L][X + 1]
+        if xe == xb:
+            continue
+        ids = [int(v) for v in y_ids[y_off[X]: y_off[X + 1]]]
+        assert ids[0] == X
+        nsym_from = 1 + int(y_cnt[4 * X]) + int(y_cnt[4 * X + 1])
+        T = ppts[xb:xe]
+        pos = int(ooff[X])
+        for e, Y in enumerate(ids):
+            yb, ye = off[L][Y], off[L][Y + 1]
+            K = kernel_matrix(kind, T, ppts[yb:ye])
+            if Y == X:
+                np.fill_diagonal(K, diag)
+            csym[xb:xe] += K @ xp[yb:ye]
+            if e >= nsym_from:
+                assert row0 <= yb < row1 and Y > X
+                pairbuf[pos: pos + ye - yb] = K.T @ xp[xb:xe]
+                pos += ye - yb
+    for Y in range(leaf0, leaf1):
+        yb, ye = off[L][Y], off[L][Y + 1]
+        for q in ipos[ioff[Y]: ioff[Y + 1]]:
+            csym[yb:ye] += pairbuf[int(q): int(q) + ye - yb]
+    np.testing.assert_allclose(csym[row0:row1], cpart[row0:row1], rtol=1e-12,
+                               atol=1e-12 * (np.abs(cpart).max() + 1))
     items2 = plan.array("p2_items")
     items2s = plan.array("p2s_items")
     nslots = 1 + max([int(v) for v in items2["slot"]] + [int(v) for v in items2s["slot"]] + [-1])
