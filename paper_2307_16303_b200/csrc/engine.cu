@@ -190,7 +190,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   ms_aca_write_ = ms_since(t);
   if (n_segs_all_ > 0) {
     launch_proxy_gather(segs_all_.get(), n_segs_all_, piv_.get(), px_.get(), py_.get(), pz_.get(),
-                        q4_.get(), stream_);
+                        center_.get(), q4_.get(), q4c_.get(), stream_);
     int max_r = 0;
     for (const auto& sg : plan_->proxy_segs) max_r = std::max(max_r, sg.r);
     launch_lu_invert(segs_all_.get(), n_segs_all_, lu_.get(), lu_total_, max_r, stream_);
@@ -590,7 +590,11 @@ void Engine::upload_plan() {
   // proxy records share S's index space; padding slots sit far away with
   // weight 0 (see matvec.cu)
   q4_.alloc(4 * std::max<std::int64_t>(Z.s_doubles, 2));
-  launch_fill_far(q4_.get(), std::max<std::int64_t>(Z.s_doubles, 2), stream_);
+  launch_fill_far(q4_.get(), std::max<std::int64_t>(Z.s_doubles, 2), false, stream_);
+  q4c_.alloc(4 * std::max<std::int64_t>(Z.s_doubles, 2));
+  launch_fill_far(q4c_.get(), std::max<std::int64_t>(Z.s_doubles, 2), true, stream_);
+  center_.upload(P.center, stream_);
+  vcols_.upload(P.vcols, stream_);
   std::vector<ProxySeg> solve;
   for (const auto& s : P.proxy_segs)
     if (s.solve) solve.push_back(s);
@@ -712,6 +716,9 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.pz = pz_.get();
   a.p4 = p4_.get();
   a.q4 = q4_.get();
+  a.q4c = q4c_.get();
+  a.cen = center_.get();
+  a.vcols = vcols_.get();
   a.perm = perm_.get();
   a.near_off = near_off_.get();
   a.near_ids = near_ids_.get();
@@ -823,6 +830,9 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   a1.pz = pz_.get();
   a1.p4 = p4_.get();
   a1.q4 = q4_.get();
+  a1.q4c = q4c_.get();
+  a1.cen = center_.get();
+  a1.vcols = vcols_.get();
   // Two lanes forked from s, joined back for the combine:
   //   stream2_ (HBM): p1_stream -> stream reductions -> [solves done] -> p2_stream
   //   stream4_ (FP64): p1_proxy -> proxy reductions -> solves -> p2_proxy ->

@@ -121,6 +121,9 @@ class Engine {
   DevBuf<double> lu_;
   std::int64_t lu_total_ = 0;
   DevBuf<double> q4_;  // proxy records (x, y, z, solved t-vector) in S index space
+  DevBuf<double> q4c_;  // the same points centred on their node's box (x', y', z', |.|^2)
+  DevBuf<double> center_;  // box centre per global node
+  DevBuf<std::int32_t> vcols_;  // leading vertex-partner columns per node
   DevBuf<ProxySeg> segs_all_, segs_solve_;
   std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
   DevBuf<P1Item> p1_stream_items_, p1_proxy_items_;

@@ -121,6 +121,9 @@ struct P1Args {
   const double *px = nullptr, *py = nullptr, *pz = nullptr;  // permuted points
   const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
   const double* q4 = nullptr;  // proxy records (x, y, z, solved t-vector), S index space
+  const double* q4c = nullptr;  // proxy records centred on their node's box (x', y', z', |.|^2)
+  const double* cen = nullptr;  // box centre per global node (4 doubles)
+  const std::int32_t* vcols = nullptr;  // per node: leading vertex-partner columns
   unsigned* counter = nullptr;  // dynamic work counter (zeroed before the launch)
 };
 // persistent CTAs: grid = SMs x per_sm (capped by occupancy and work)
@@ -129,12 +132,14 @@ void launch_p1_proxy(const P1Args& a, int kernel, int sms, int per_sm, cudaStrea
 void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
                           const std::int32_t* spos, const double* P, double* S,
                           cudaStream_t s);
-// q4[i] = (far, far, far, 0) for i < n (padding records, build)
-void launch_fill_far(double* q4, std::int64_t n, cudaStream_t s);
+// q4[i] = (far, far, far, 0) (centred: (far, far, far, 3 far^2)) for i < n
+// (padding records, build)
+void launch_fill_far(double* q4, std::int64_t n, bool centred, cudaStream_t s);
 // q4[so + a] = (x, y, z, .) of the proxy points of every segment (build)
+// (and q4c[so + a] = (x - c, y - c, z - c, |.|^2) centred on the segment node's box)
 void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int32_t* piv,
-                         const double* px, const double* py, const double* pz, double* q4,
-                         cudaStream_t s);
+                         const double* px, const double* py, const double* pz, const double* cen,
+                         double* q4, double* q4c, cudaStream_t s);
 // lu holds 2 x lu_total doubles: the packed inverses row-major, then column-major
 // reads v from S, writes the solved t-vector into the w lane of q4
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
@@ -156,6 +161,9 @@ struct Phase2Args {
   const double *px = nullptr, *py = nullptr, *pz = nullptr;
   const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
   const double* q4 = nullptr;  // proxy records (x, y, z, solved t-vector), S index space
+  const double* q4c = nullptr;  // centred proxy records (x', y', z', |.|^2)
+  const double* cen = nullptr;  // box centre per global node (4 doubles)
+  const std::int32_t* vcols = nullptr;  // per node: leading vertex-partner columns
   const std::int32_t* perm = nullptr;
   // leaf near lists: self + near_edge + near_face (+ direct partners), CSR
   const std::int32_t* near_off = nullptr;

@@ -246,42 +246,58 @@ __global__ void __maxnreg__(64) p1_stream_kernel(const P1Args a) {
 // ---- proxy-level evaluation core (both phases): a 128-thread CTA owns up to
 // 256 targets, two per thread (t and t + 128), and streams the sources
 // through shared memory in chunks of kChunk, read as broadcasts; each staged
-// source feeds two targets (half the shared-memory wavefronts per
-// evaluation of one target per thread - the pipe the co-resident bulk-copy
-// kernel also needs), two sources per step give four independent FP64
-// chains per thread.
+// source feeds two targets, two sources per step give four independent FP64
+// chains per thread. Coordinates are centred on the node's box (planner.h
+// `center`): a target is held as a = -2 t', tt = |t'|^2, a source as
+// (s', ss = |s'|^2, w), and for partners at least one box apart
+// r^2 = tt + ss - 2 t'.s' (1 DADD + 3 DFMA instead of 3 DADD + DMUL + 2 DFMA;
+// rounding ~ eps (tt + ss) / r^2 < 50 eps there). Vertex-adjacent partners
+// (whose points can nearly touch; their columns come first, vcols) use the
+// difference form t' - s' = fma(-0.5, a, -s') exactly.
 constexpr int kProxyThreads = 128;
 
-template <int K, int NT>
-__device__ __forceinline__ void proxy_evalT(const double (&tx)[2], const double (&ty)[2],
-                                            const double (&tz)[2], double (&acc)[2][2],
-                                            const double2* __restrict__ src, int nj) {
-  int j = 0;
-  for (; j + 1 < nj; j += 2) {
+struct Tgt {
+  double ax, ay, az, tt;
+};
+
+template <int K, int NT, bool TRICK>
+__device__ __forceinline__ void proxy_evalT(const Tgt (&tg)[2], double (&acc)[2][2],
+                                            const double2* __restrict__ src, int j, int nj) {
+  auto one = [&](int jj, int u) {
+    const double2 s0 = src[3 * jj], s1 = src[3 * jj + 1], s2 = src[3 * jj + 2];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const double2 s0 = src[2 * (j + u)], s1 = src[2 * (j + u) + 1];
-#pragma unroll
-      for (int t = 0; t < NT; ++t)
-        acc[t][u] = far_acc<K>(sq3(tx[t] - s0.x, ty[t] - s0.y, tz[t] - s1.x), s1.y, acc[t][u]);
+    for (int t = 0; t < NT; ++t) {
+      double r2;
+      if constexpr (TRICK) {
+        r2 = fma(tg[t].ax, s0.x, fma(tg[t].ay, s0.y, fma(tg[t].az, s1.x, tg[t].tt + s1.y)));
+      } else {
+        r2 = sq3(fma(-0.5, tg[t].ax, -s0.x), fma(-0.5, tg[t].ay, -s0.y), fma(-0.5, tg[t].az, -s1.x));
+      }
+      acc[t][u] = far_acc<K>(r2, s2.x, acc[t][u]);
     }
+  };
+  for (; j + 1 < nj; j += 2) {
+    one(j, 0);
+    one(j + 1, 1);
   }
-  if (j < nj) {
-    const double2 s0 = src[2 * j], s1 = src[2 * j + 1];
-#pragma unroll
-    for (int t = 0; t < NT; ++t)
-      acc[t][0] = far_acc<K>(sq3(tx[t] - s0.x, ty[t] - s0.y, tz[t] - s1.x), s1.y, acc[t][0]);
-  }
+  if (j < nj) one(j, 0);
 }
 
-// nt = targets of this warp that exist (warp-uniform: 0, 1 or 2 per thread);
-// warps without targets skip straight to the next barrier
+// nt = targets of this warp that exist (warp-uniform: 0, 1 or 2 per thread;
+// warps without targets skip straight to the next barrier); sources [j0, jv)
+// of the span are vertex-adjacent (difference form), [jv, j1) the rest
 template <int K>
-__device__ __forceinline__ void proxy_eval2(const double (&tx)[2], const double (&ty)[2],
-                                            const double (&tz)[2], double (&acc)[2][2],
-                                            const double2* __restrict__ src, int nj, int nt) {
-  if (nt == 2) proxy_evalT<K, 2>(tx, ty, tz, acc, src, nj);
-  else if (nt == 1) proxy_evalT<K, 1>(tx, ty, tz, acc, src, nj);
+__device__ __forceinline__ void proxy_eval2(const Tgt (&tg)[2], double (&acc)[2][2],
+                                            const double2* __restrict__ src, int j0, int jv, int j1,
+                                            int nt, bool vertex_targets) {
+  if (vertex_targets) jv = j1;  // a warp holding vertex-partner targets: all difference form
+  if (nt == 2) {
+    proxy_evalT<K, 2, false>(tg, acc, src, j0, jv);
+    proxy_evalT<K, 2, true>(tg, acc, src, jv, j1);
+  } else if (nt == 1) {
+    proxy_evalT<K, 1, false>(tg, acc, src, j0, jv);
+    proxy_evalT<K, 1, true>(tg, acc, src, jv, j1);
+  }
 }
 
 __device__ __forceinline__ int warp_targets(int loc, int tpg, int n) {
@@ -290,12 +306,17 @@ __device__ __forceinline__ int warp_targets(int loc, int tpg, int n) {
   return 0;
 }
 
+__device__ __forceinline__ Tgt make_tgt(double x, double y, double z, const double4& c) {
+  const double px = x - c.x, py = y - c.y, pz = z - c.z;
+  return Tgt{-2.0 * px, -2.0 * py, -2.0 * pz, fma(pz, pz, fma(py, py, px * px))};
+}
+
 // ---- phase 1, proxy levels: v_c = sum_j K(P_c, z_j) x_j (targets = the
 // item's proxies, sources = the node's points); items with <= 128 / <= 64
 // proxies split the sources over 2 / 4 thread groups as in p2_proxy_kernel.
 template <int K>
-__global__ void __launch_bounds__(kProxyThreads, 4) p1_proxy_kernel(const P1Args a) {
-  __shared__ double2 src[2 * kChunk];  // (x, y), (z, w)
+__global__ void __launch_bounds__(kProxyThreads, 5) p1_proxy_kernel(const P1Args a) {
+  __shared__ double2 src[3 * kChunk];  // (x', y'), (z', ss), (w, -)
   __shared__ double red[2 * kProxyThreads];
   __shared__ long long s_k;
   for (;;) {
@@ -307,33 +328,37 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p1_proxy_kernel(const P1Args
     const P1Item it = a.items[k];
     const std::int64_t g = it.node;
     const std::int64_t rb = a.nt.rowbeg[g] + it.row0;
+    const double4 cen = reinterpret_cast<const double4*>(a.cen)[g];
     const int G = it.ncols <= 64 ? 4 : it.ncols <= 128 ? 2 : 1;
     const int tpg = kProxyThreads / G;
     const int grp = threadIdx.x / tpg, loc = threadIdx.x % tpg;
     const int nt = warp_targets(loc, tpg, it.ncols);
-    double tx[2], ty[2], tz[2], acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int vc = a.vcols[g] - it.col0;  // target columns < vc: vertex partners
+    const bool vwarp = __any_sync(0xffffffffu, loc < vc);
+    Tgt tg[2];
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const int c = loc + t * tpg;
       const std::int64_t qi = a.nt.soff[g] + it.col0 + c;
       const double4 q = c < it.ncols ? reinterpret_cast<const double4*>(a.q4)[qi]
                                      : make_double4(kFar, kFar, kFar, 0.0);
-      tx[t] = q.x;
-      ty[t] = q.y;
-      tz[t] = q.z;
+      tg[t] = make_tgt(q.x, q.y, q.z, cen);
     }
     for (int j0 = 0; j0 < it.nrows; j0 += kChunk) {
       const int nj = min(kChunk, it.nrows - j0);
       __syncthreads();
       for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
         const double4 v = reinterpret_cast<const double4*>(a.p4)[rb + j0 + q];
-        src[2 * q] = make_double2(v.x, v.y);
-        src[2 * q + 1] = make_double2(v.z, v.w);
+        const double px = v.x - cen.x, py = v.y - cen.y, pz = v.z - cen.z;
+        src[3 * q] = make_double2(px, py);
+        src[3 * q + 1] = make_double2(pz, fma(pz, pz, fma(py, py, px * px)));
+        src[3 * q + 2] = make_double2(v.w, 0.0);
       }
       __syncthreads();
       const int sub = (nj + G - 1) / G;
       const int lo = min(nj, grp * sub), hi = min(nj, lo + sub);
-      proxy_eval2<K>(tx, ty, tz, acc, src + 2 * lo, hi - lo, nt);
+      proxy_eval2<K>(tg, acc, src, lo, lo, hi, nt, vwarp);
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = acc[t][0] + acc[t][1];
@@ -364,15 +389,19 @@ __global__ void phase1_reduce_kernel(const P1Reduce* __restrict__ red, NodeTable
 __global__ void proxy_gather_kernel(const ProxySeg* __restrict__ segs, std::int64_t nseg,
                                     const std::int32_t* __restrict__ piv,
                                     const double* __restrict__ px, const double* __restrict__ py,
-                                    const double* __restrict__ pz, double4* __restrict__ q4) {
+                                    const double* __restrict__ pz, const double4* __restrict__ cen,
+                                    double4* __restrict__ q4, double4* __restrict__ q4c) {
   const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.y) + threadIdx.y;
   if (s >= nseg) return;
   const ProxySeg sg = segs[s];
+  const double4 c = cen[sg.node];
   for (int q = threadIdx.x; q < sg.r; q += blockDim.x) {
     // side 0: Z = X, proxies = column pivots tau (in Y = k); side 1: row pivots sigma
     const std::int32_t loc = piv[sg.piv_off + (sg.side == 0 ? sg.r : 0) + q];
     const std::int64_t idx = sg.base + loc;
     q4[sg.so + q] = make_double4(px[idx], py[idx], pz[idx], 0.0);
+    const double x = px[idx] - c.x, y = py[idx] - c.y, z = pz[idx] - c.z;
+    q4c[sg.so + q] = make_double4(x, y, z, fma(z, z, fma(y, y, x * x)));
   }
 }
 
@@ -1123,12 +1152,13 @@ __global__ void __maxnreg__(64) p2_stream_kernel(const Phase2Args a) {
 
 // ---- phase 2, proxy levels, node-major: b_X += K(X, P_A) s_A for the rows of
 // node A (up to 256 per item, two per thread), the node's proxy list staged
-// in shared memory (proxy_eval2 above). Items of <= 128 / <= 64 rows split
-// the CTA into 2 / 4 groups that take disjoint parts of every staged chunk
-// (all 256 target slots busy on small nodes), partials summed in group order.
+// in shared memory (proxy_eval2 above; the node's first vcols sources are
+// vertex partners). Items of <= 128 / <= 64 rows split the CTA into 2 / 4
+// groups that take disjoint parts of every staged chunk (all 256 target
+// slots busy on small nodes), partials summed in group order.
 template <int K>
-__global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2Args a) {
-  __shared__ double2 src[2 * kChunk];
+__global__ void __launch_bounds__(kProxyThreads, 5) p2_proxy_kernel(const Phase2Args a) {
+  __shared__ double2 src[3 * kChunk];
   __shared__ double red[2 * kProxyThreads];
   __shared__ long long s_k;
   for (;;) {
@@ -1141,32 +1171,35 @@ __global__ void __launch_bounds__(kProxyThreads, 4) p2_proxy_kernel(const Phase2
     const std::int64_t g = it.node;
     const std::int64_t so = a.nt.soff[g];
     const int R = a.nt.rpad[g];
+    const int vc = a.vcols[g];
+    const double4 cen = reinterpret_cast<const double4*>(a.cen)[g];
     const int G = it.nrows <= 64 ? 4 : it.nrows <= 128 ? 2 : 1;
     const int tpg = kProxyThreads / G;  // threads per group
     const int grp = threadIdx.x / tpg, loc = threadIdx.x % tpg;
     const int nt = warp_targets(loc, tpg, it.nrows);
     const double4* P4 = reinterpret_cast<const double4*>(a.p4);
-    double tx[2], ty[2], tz[2], acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    Tgt tg[2];
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const int i = loc + t * tpg;
       const double4 q = i < it.nrows ? P4[a.nt.rowbeg[g] + it.row0 + i] : make_double4(kFar, kFar, kFar, 0.0);
-      tx[t] = q.x;
-      ty[t] = q.y;
-      tz[t] = q.z;
+      tg[t] = make_tgt(q.x, q.y, q.z, cen);
     }
     for (int j0 = 0; j0 < R; j0 += kChunk) {
       const int nj = min(kChunk, R - j0);
       __syncthreads();
       for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
-        const double4 r = reinterpret_cast<const double4*>(a.q4)[so + j0 + q];
-        src[2 * q] = make_double2(r.x, r.y);
-        src[2 * q + 1] = make_double2(r.z, r.w);
+        const double4 c4 = reinterpret_cast<const double4*>(a.q4c)[so + j0 + q];
+        src[3 * q] = make_double2(c4.x, c4.y);
+        src[3 * q + 1] = make_double2(c4.z, c4.w);
+        src[3 * q + 2] = make_double2(a.q4[4 * (so + j0 + q) + 3], 0.0);
       }
       __syncthreads();
       const int sub = (nj + G - 1) / G;
       const int lo = min(nj, grp * sub), hi = min(nj, lo + sub);
-      proxy_eval2<K>(tx, ty, tz, acc, src + 2 * lo, hi - lo, nt);
+      const int jv = max(lo, min(hi, vc - j0));
+      proxy_eval2<K>(tg, acc, src, lo, jv, hi, nt, false);
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = acc[t][0] + acc[t][1];
@@ -1383,24 +1416,28 @@ void launch_phase1_reduce(const P1Reduce* red, std::int64_t nred, NodeTable nt,
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-__global__ void fill_far_kernel(double4* __restrict__ q4, std::int64_t n) {
+__global__ void fill_far_kernel(double4* __restrict__ q4, std::int64_t n, double w) {
   const std::int64_t i = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x;
-  if (i < n) q4[i] = make_double4(kFar, kFar, kFar, 0.0);
+  if (i < n) q4[i] = make_double4(kFar, kFar, kFar, w);
 }
 
-void launch_fill_far(double* q4, std::int64_t n, cudaStream_t s) {
+void launch_fill_far(double* q4, std::int64_t n, bool centred, cudaStream_t s) {
   if (n <= 0) return;
-  fill_far_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(reinterpret_cast<double4*>(q4), n);
+  // centred records carry |s'|^2 in w: a padding slot must keep r^2 > 0 in
+  // the tt + ss - 2 t'.s' form (its weight, in the other array, is 0)
+  fill_far_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(
+      reinterpret_cast<double4*>(q4), n, centred ? 3.0 * kFar * kFar : 0.0);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int32_t* piv,
-                         const double* px, const double* py, const double* pz, double* q4,
-                         cudaStream_t s) {
+                         const double* px, const double* py, const double* pz, const double* cen,
+                         double* q4, double* q4c, cudaStream_t s) {
   if (nseg == 0) return;
   const dim3 block(32, 8);
   proxy_gather_kernel<<<static_cast<unsigned>((nseg + 7) / 8), block, 0, s>>>(segs, nseg, piv, px, py,
-                                                                            pz, reinterpret_cast<double4*>(q4));
+                                                                            pz, reinterpret_cast<const double4*>(cen), reinterpret_cast<double4*>(q4),
+      reinterpret_cast<double4*>(q4c));
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -11,6 +11,20 @@
 namespace h3db {
 
 namespace {
+// Morton ids at one level (bit b of ix / iy / iz -> bit 3b / 3b+1 / 3b+2,
+// reference octree.cpp:30-38): Chebyshev distance 1 between distinct boxes
+bool vertex_adjacent(std::int64_t a, std::int64_t b) {
+  std::int64_t d = 0;
+  for (int dim = 0; dim < 3; ++dim) {
+    std::int64_t ca = 0, cb = 0;
+    for (int bit = 0; bit < 21; ++bit) {
+      ca |= ((a >> (3 * bit + dim)) & 1) << bit;
+      cb |= ((b >> (3 * bit + dim)) & 1) << bit;
+    }
+    d = std::max<std::int64_t>(d, ca > cb ? ca - cb : cb - ca);
+  }
+  return d == 1;
+}
 constexpr std::int64_t kRowChunk = 2048;  // phase-1 stream: rows per item
 static_assert(kRowChunk % kTileRows == 0, "phase-1 stream items start on a row tile");
 constexpr int kColChunk = 256;            // phase-1: columns (targets) per item
@@ -145,6 +159,18 @@ void Planner::layout() {
   rowbeg.assign(T, 0);
   rpad.assign(T, 0);
   rows.assign(T, 0);
+  vcols.assign(T, 0);
+  center.assign(4 * T, 0.0);
+  for (int l = 0; l <= L_; ++l) {
+    const std::int64_t cnt = 1LL << (3 * l);
+    const double w = 2.0 / static_cast<double>(1LL << l);
+    for (std::int64_t z = 0; z < cnt; ++z) {
+      std::int64_t c[3] = {0, 0, 0};
+      for (int b = 0; b < l; ++b)
+        for (int d = 0; d < 3; ++d) c[d] |= ((z >> (3 * b + d)) & 1) << b;
+      for (int d = 0; d < 3; ++d) center[4 * gid(l, z) + d] = -1.0 + (static_cast<double>(c[d]) + 0.5) * w;
+    }
+  }
   for (int l = 0; l <= L_; ++l) {
     const std::int64_t cnt = 1LL << (3 * l);
     for (std::int64_t z = 0; z < cnt; ++z) {
@@ -193,16 +219,22 @@ void Planner::layout() {
     const auto& ep = entry_pair_[l];
     auto& ec = entry_col_[l];
     ec.assign(ep.size(), -1);
+    const auto& lid = lists_[l].ids[0];
     for (std::int64_t z = 0; z < cnt; ++z) {
       std::int32_t cols = 0;
       bool any = false;
-      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
-        if (ep[e] < 0) continue;
-        ec[e] = cols;
-        cols += P.rank[ep[e]];
-        any = true;
-      }
       const std::int64_t g = gid(l, z);
+      // vertex-adjacent partners (Chebyshev distance 1) first
+      for (int pass = 0; pass < 2; ++pass) {
+        for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
+          if (ep[e] < 0) continue;
+          if (vertex_adjacent(z, lid[e]) != (pass == 0)) continue;
+          ec[e] = cols;
+          cols += P.rank[ep[e]];
+          any = true;
+        }
+        if (pass == 0) vcols[g] = cols;
+      }
       const bool stream = mode_[l] == kModeStream;
       const std::int32_t rp =
           !any ? 0 : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols : cols + (cols & 1);
@@ -261,6 +293,7 @@ void Planner::layout() {
           sg.r = r;
           sg.side = (P.X[p] == z) ? 0 : 1;
           sg.solve = owned(l, z) ? 1 : 0;
+          sg.node = static_cast<std::int32_t>(gid(l, z));
           proxy_segs.push_back(sg);
         }
         if (!owned(l, k)) continue;

@@ -111,7 +111,7 @@ struct ProxySeg {
   std::int32_t side;     // 0: Z is the pair's row side X (proxies = col pivots tau in k)
                          // 1: Z is the pair's col side Y (proxies = row pivots sigma in k)
   std::int32_t solve;    // 1 if Z is owned here (its S segment is solved before phase 2)
-  std::int32_t pad;
+  std::int32_t node;     // global node id of Z
 };
 
 struct PlanSizes {
@@ -158,6 +158,12 @@ class Planner {
   // results ----------------------------------------------------------------
   std::vector<std::int64_t> woff, soff, rowbeg;
   std::vector<std::int32_t> rpad, rows;
+  // columns of vertex-adjacent partners come first in every node's layout:
+  // vcols[g] of them. Entries against those partners can be arbitrarily
+  // close; the rest are at least one box apart (the regenerating kernels
+  // use a cancellation-prone r^2 form only there)
+  std::vector<std::int32_t> vcols;
+  std::vector<double> center;  // 4 per global node: box centre (x, y, z, 0)
   std::vector<std::int32_t> spos;
   // per level, per pair: stream levels: W node base (pair_wx/wy), first column
   // of the pair's segment (pair_cx/cy) and column tiles of the node
