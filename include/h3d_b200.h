@@ -169,6 +169,7 @@ typedef enum {
   H3D_K_P2_PROXY,      /* phase 2, proxy levels (FP64) */
   H3D_K_NEAR,          /* near field + direct leaf blocks (FP64) */
   H3D_K_COMBINE,       /* sum of the per-level partials, un-permute */
+  H3D_K_PAIR,          /* pair levels: fused one-read pass + per-node gather (HBM) */
   H3D_K_COUNT
 } h3d_kernel_slot;
 int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launches, double* start_sum,

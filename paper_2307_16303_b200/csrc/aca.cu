@@ -151,7 +151,8 @@ __device__ __forceinline__ void tbar() {
 // node column col0 + q. Staged through a 32 x 33 shared tile.
 template <int NT>
 __device__ void write_rows(const double* __restrict__ src, int ld, int rows, int r,
-                           double* __restrict__ Wn, int row0, int col0, int nct, double* tile) {
+                           double* __restrict__ Wn, int row0, int col0, int nct, double* tile,
+                           bool row_major) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i0 = 0; i0 < rows; i0 += 32) {
@@ -163,7 +164,12 @@ __device__ void write_rows(const double* __restrict__ src, int ld, int rows, int
       tbar<NT>();
       for (int il = w; il < 32; il += NW) {
         const int i = i0 + il, q = a0 + lane;
-        if (i < rows && q < r) Wn[tile_index(row0 + i, col0 + q, nct)] = tile[lane * 33 + il];
+        if (i < rows && q < r) {
+          // row_major (pair pools): nct is the row stride
+          const std::int64_t at = row_major ? static_cast<std::int64_t>(row0 + i) * nct + col0 + q
+                                            : tile_index(row0 + i, col0 + q, nct);
+          Wn[at] = tile[lane * 33 + il];
+        }
       }
       tbar<NT>();
     }
@@ -398,8 +404,10 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
     if (crank == 0 && tid == 0) a.rank_out[p] = rank;
     cx.bar();
     if (a.W != nullptr && rank > 0) {
-      write_rows<NT>(U + r0, a.ms, r1 - r0, rank, a.W + a.wx[p], r0, a.cx[p], a.rx[p], s_tile);
-      write_rows<NT>(V + c0, a.ns, c1 - c0, rank, a.W + a.wy[p], c0, a.cy[p], a.ry[p], s_tile);
+      write_rows<NT>(U + r0, a.ms, r1 - r0, rank, a.W + a.wx[p], r0, a.cx[p], a.rx[p], s_tile,
+                     a.row_major != 0);
+      write_rows<NT>(V + c0, a.ns, c1 - c0, rank, a.W + a.wy[p], c0, a.cy[p], a.ry[p], s_tile,
+                     a.row_major != 0);
     }
     if (a.lu != nullptr && rank > 0 && crank == 0) {
       // packed LU (lowrank.cpp:277-287): strict lower u_a(i_b)/delta_a,

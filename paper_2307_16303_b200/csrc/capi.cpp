@@ -283,6 +283,11 @@ int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, in
     else if (nm == "out_off") put(P.out_off, out, count);
     else if (nm == "in_off") put(P.in_off, out, count);
     else if (nm == "in_pos") put(P.in_pos, out, count);
+    else if (nm == "pair_descs") put(P.pair_descs, out, count);
+    else if (nm == "pd_level") put(P.pd_level, out, count);
+    else if (nm == "pc_off") put(P.pc_off, out, count);
+    else if (nm == "pc_pos") put(P.pc_pos, out, count);
+    else if (nm == "pg_items") put(P.pg_items, out, count);
     else if (nm == "pair_piv") put(P.pair_piv.at(level), out, count);
     else if (nm == "pair_lu") put(P.pair_lu.at(level), out, count);
     else if (nm == "proxy_segs") put(P.proxy_segs, out, count);

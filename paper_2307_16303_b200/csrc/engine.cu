@@ -99,6 +99,7 @@ template class DevBuf<P1Reduce>;
 template class DevBuf<ProxySeg>;
 template class DevBuf<P2Item>;
 template class DevBuf<StreamDesc>;
+template class DevBuf<PairDesc>;
 
 Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_(opt), n_(n) {
   const auto t0 = Clock::now();
@@ -172,7 +173,8 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   if (opt_.mode_policy == 2) {
     for (int l = 1; l <= L_ && l < 16; ++l) {
       const int m = opt_.level_modes[l];
-      if (m < 0 || m > 2) throw InvalidArgument("initialize: level_modes entries must be 0, 1 or 2");
+      if (m < 0 || m > 3)
+        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2 or 3");
       if (m == kModeDirect && l != L_)
         throw InvalidArgument("initialize: direct mode is only valid at the leaf level");
       modes_[l] = m;
@@ -367,7 +369,7 @@ void Engine::run_aca(bool write) {
     int level_max_rank = 0;
     if (write) {
       for (std::int64_t p = 0; p < np; ++p) level_max_rank = std::max(level_max_rank, P.rank[p]);
-      if (mode == kModeStream) {
+      if (mode == kModeStream || mode == kModePair) {
         d_wx.upload(plan_->pair_wx[l], stream_);
         d_wy.upload(plan_->pair_wy[l], stream_);
         d_rx.upload(plan_->pair_rx[l], stream_);
@@ -434,7 +436,8 @@ void Engine::run_aca(bool write) {
       a.ms = ms;
       a.ns = ns;
       a.rank_out = d_rank.get();
-      if (write && mode == kModeStream) {
+      if (write && (mode == kModeStream || mode == kModePair)) {
+        a.row_major = mode == kModePair ? 1 : 0;
         a.W = W_.get();
         a.wx = d_wx.get();
         a.rx = d_rx.get();
@@ -488,6 +491,13 @@ void Engine::run_aca(bool write) {
 void Engine::choose_modes() {
   if (opt_.mode_policy == 2) {
     for (int l = 1; l <= L_; ++l) {
+      if (plan_->mode(l) == kModePair) {
+        const auto& rk = plan_->pairs(l).rank;
+        if (!rk.empty() && *std::max_element(rk.begin(), rk.end()) > kPairMaxRp)
+          throw InvalidArgument("initialize: level " + std::to_string(l) + " has ranks above " +
+                                std::to_string(kPairMaxRp) + "; use stream mode there");
+        continue;
+      }
       if (plan_->mode(l) != kModeProxy) continue;
       const auto& rk = plan_->pairs(l).rank;
       if (!rk.empty() && *std::max_element(rk.begin(), rk.end()) > kMaxProxyRank)
@@ -686,7 +696,15 @@ void Engine::upload_plan() {
     lvl_part_.alloc(static_cast<std::size_t>(n_lvl_) * n_);
     H3D_CUDA_CHECK(cudaMemsetAsync(lvl_part_.get(), 0, sizeof(double) * n_lvl_ * n_, stream_));
   }
-  counters_.alloc(5);
+  // pair levels: descriptors, output runs, gather items, one counter per level
+  pair_descs_.upload(P.pair_descs.empty() ? std::vector<PairDesc>{PairDesc{}} : P.pair_descs, stream_);
+  pd_level_ = P.pd_level;
+  pc_off_.upload(P.pc_off, stream_);
+  pc_pos_.upload(P.pc_pos.empty() ? std::vector<std::int64_t>{0} : P.pc_pos, stream_);
+  pg_items_.upload(P.pg_items.empty() ? std::vector<P2Item>{P2Item{}} : P.pg_items, stream_);
+  n_pg_ = static_cast<std::int64_t>(P.pg_items.size());
+  pair_out_.alloc(std::max<std::int64_t>(P.pair_out_total, 1));
+  counters_.alloc(5 + L_ + 1);
   sync_flag_.alloc(1);
   H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), stream_));
   epoch_ = 0;
@@ -841,17 +859,38 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // HBM near peak, the FP64 kernels fill the remaining registers.
   const bool has_p2 = P.leaf1 > P.leaf0;
   const bool parts = n_lvl_ > 0 || sym_near_;  // near pass writes partials, combine sums them
-  const bool hbm = n_p1s_ > 0 || n_p2s_ > 0;
+  const bool pair_lv = pd_level_.size() > 1 && pd_level_.back() > 0;
+  const bool hbm = n_p1s_ > 0 || n_p2s_ > 0 || pair_lv;
   const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0;
-  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, 5 * sizeof(unsigned), s));
+  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, (5 + L_ + 1) * sizeof(unsigned), s));
   Phase2Args a2 = phase2_args(bout);
   a2.counter = counters_.get() + 2;
   a2.counter2 = counters_.get() + 3;
   a2.counter3 = counters_.get() + 4;
   H3D_CUDA_CHECK(cudaEventRecord(fork_[0], s));
-  // HBM lane, phase 1
+  // HBM lane: pair levels (one fused read per pair, x only), phase 1
   if (hbm) {
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, fork_[0], 0));
+    if (pair_lv && has_p2) {
+      kb(H3D_K_PAIR, stream2_);
+      for (int l = 1; l <= L_; ++l) {
+        const std::int64_t n = pd_level_[l + 1] - pd_level_[l];
+        if (n == 0) continue;
+        PairArgs pa;
+        pa.descs = pair_descs_.get() + pd_level_[l];
+        pa.n = n;
+        pa.W = W_.get();
+        pa.xp = xp_.get();
+        pa.out = pair_out_.get();
+        pa.counter = counters_.get() + 5 + l;
+        launch_pair(pa, sms_, fp ? 1 : 2, stream2_);
+        ++launches;
+      }
+      launch_pair_gather(pg_items_.get(), n_pg_, rowbeg_.get(), pc_off_.get(), pc_pos_.get(),
+                         pair_out_.get(), lvl_part_.get(), n_, stream2_);
+      launches += n_pg_ > 0;
+      ke(H3D_K_PAIR, stream2_);
+    }
     if (n_p1s_ > 0) {
       a1.items = p1_stream_items_.get();
       a1.descs = p1s_desc_.get();

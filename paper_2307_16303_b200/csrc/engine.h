@@ -138,6 +138,13 @@ class Engine {
   DevBuf<double> cpart_;
   DevBuf<P2Item> p2_items_, p2s_items_;
   DevBuf<StreamDesc> p1s_desc_, p2s_desc_;
+  DevBuf<PairDesc> pair_descs_;          // pair levels (kModePair)
+  std::vector<std::int64_t> pd_level_;   // descriptor range per level
+  DevBuf<std::int32_t> pc_off_;
+  DevBuf<std::int64_t> pc_pos_;
+  DevBuf<P2Item> pg_items_;
+  std::int64_t n_pg_ = 0;
+  DevBuf<double> pair_out_;
   std::int64_t n_p2_ = 0, n_p2s_ = 0;
   int n_lvl_ = 0;
   DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 per-level partials

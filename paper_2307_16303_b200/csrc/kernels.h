@@ -75,6 +75,7 @@ struct AcaArgs {
   const std::int64_t* wy = nullptr;
   const std::int32_t* cy = nullptr;
   const std::int32_t* ry = nullptr;
+  int row_major = 0;  // pair pools: U / V row-major with row stride rx / ry
   // pivot + packed-LU write-back (proxy levels, write pass): row pivots at
   // piv[piv_off[p] + a], column pivots at piv[piv_off[p] + r + a]
   std::int32_t* piv = nullptr;
@@ -221,6 +222,23 @@ void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std:
                     const std::int64_t* leaf_off, std::int64_t leaf0, std::int64_t nleaves,
                     const std::int32_t* in_off, const std::int64_t* in_pos, const double* pairbuf,
                     const std::int32_t* perm, double* b, cudaStream_t s);
+
+// ---------------------------------------------------------------- pair.cu
+constexpr int kPairMaxRp = 256;  // pair levels: ranks above this stay two-phase
+struct PairArgs {
+  const PairDesc* descs = nullptr;
+  std::int64_t n = 0;
+  const double* W = nullptr;
+  const double* xp = nullptr;
+  double* out = nullptr;
+  unsigned* counter = nullptr;  // zeroed before the launch
+};
+std::size_t pair_smem_bytes();
+// persistent, per_sm CTAs per SM (one 5-warp CTA is the HBM lane's share)
+void launch_pair(const PairArgs& a, int sms, int per_sm, cudaStream_t s);
+void launch_pair_gather(const P2Item* items, std::int64_t nitems, const std::int64_t* rowbeg,
+                        const std::int32_t* pc_off, const std::int64_t* pc_pos, const double* out,
+                        double* lvl, std::int64_t n_total, cudaStream_t s);
 
 // Build-time near-field scan: coincidence check (and optional store).
 void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s);

@@ -276,11 +276,13 @@ __device__ __forceinline__ void proxy_evalT(const Tgt (&tg)[2], double (&acc)[2]
       acc[t][u] = far_acc<K>(r2, s2.x, acc[t][u]);
     }
   };
-  for (; j + 1 < nj; j += 2) {
+  for (; j + 3 < nj; j += 4) {  // four independent evaluations in flight per target
     one(j, 0);
     one(j + 1, 1);
+    one(j + 2, 0);
+    one(j + 3, 1);
   }
-  if (j < nj) one(j, 0);
+  for (; j < nj; ++j) one(j, j & 1);
 }
 
 // nt = targets of this warp that exist (warp-uniform: 0, 1 or 2 per thread;

@@ -53,7 +53,7 @@ Planner::Planner(int depth, std::int64_t n, std::vector<std::vector<std::int64_t
   if (rank_ < 0 || rank_ >= world_) throw std::invalid_argument("planner: shard_rank out of range");
   if (static_cast<int>(mode_.size()) != L_ + 1) mode_.assign(L_ + 1, kModeStream);
   for (int l = 1; l <= L_; ++l) {
-    if (mode_[l] < 0 || mode_[l] > 2) throw std::invalid_argument("planner: bad level mode");
+    if (mode_[l] < 0 || mode_[l] > kModePair) throw std::invalid_argument("planner: bad level mode");
     if (mode_[l] == kModeDirect && l != L_)
       throw std::invalid_argument("planner: direct mode is only valid at the leaf level");
   }
@@ -198,7 +198,7 @@ void Planner::layout() {
       const std::int64_t r = P.rank[p];
       const std::int64_t units = r * (node_size(l, P.X[p]) + node_size(l, P.Y[p]));
       S.sum_rank += r;
-      if (mode_[l] == kModeStream) S.factor_doubles += units;
+      if (mode_[l] == kModeStream || mode_[l] == kModePair) S.factor_doubles += units;
       else S.proxy_units += units;
       S.max_rank = std::max(S.max_rank, P.rank[p]);
       S.ref_float_count += 2ull * static_cast<std::uint64_t>(r * r);
@@ -236,14 +236,34 @@ void Planner::layout() {
         if (pass == 0) vcols[g] = cols;
       }
       const bool stream = mode_[l] == kModeStream;
-      const std::int32_t rp =
-          !any ? 0 : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols : cols + (cols & 1);
+      const std::int32_t rp = !any || mode_[l] == kModePair
+                                  ? 0
+                                  : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols
+                                           : cols + (cols & 1);
       rpad[g] = rp;
       soff[g] = S.s_doubles;
       S.s_doubles += rp;
       if (stream) {
         woff[g] = S.w_doubles;
         S.w_doubles += (node_size(l, z) + kTileRows - 1) / kTileRows * kTileRows * rp;
+      }
+    }
+    if (mode_[l] == kModePair) {
+      // pair-major pool: F_p = [U_p; V_p], (m + n) x rp row-major
+      pair_wx[l].resize(P.X.size());
+      pair_wy[l].resize(P.X.size());
+      pair_rx[l].resize(P.X.size());
+      pair_ry[l].resize(P.X.size());
+      pair_cx[l].assign(P.X.size(), 0);
+      pair_cy[l].assign(P.X.size(), 0);
+      for (std::size_t p = 0; p < P.X.size(); ++p) {
+        const std::int64_t m = node_size(l, P.X[p]), nn = node_size(l, P.Y[p]);
+        const std::int32_t rp = P.rank[p] + (P.rank[p] & 1);
+        pair_wx[l][p] = S.w_doubles;
+        pair_wy[l][p] = S.w_doubles + m * rp;
+        pair_rx[l][p] = rp;
+        pair_ry[l][p] = rp;
+        S.w_doubles += (m + nn) * rp;
       }
     }
     if (mode_[l] == kModeStream) {
@@ -271,6 +291,7 @@ void Planner::layout() {
   spos.assign(std::max<std::int64_t>(S.s_doubles, 1), -1);
   proxy_segs.clear();
   for (int l = 1; l <= L_; ++l) {
+    if (mode_[l] == kModePair) continue;  // no column layout: t-vectors stay in the fused pass
     const std::int64_t cnt = 1LL << (3 * l);
     const auto& off = lists_[l].off[0];
     const auto& ids = lists_[l].ids[0];
@@ -310,7 +331,7 @@ void Planner::layout() {
   reds.clear();
   std::int64_t ptot = 0;
   for (int l = 1; l <= L_; ++l) {
-    if (mode_[l] == kModeDirect) continue;
+    if (mode_[l] == kModeDirect || mode_[l] == kModePair) continue;
     const std::int64_t cnt = 1LL << (3 * l);
     const std::int64_t chunk = mode_[l] == kModeStream ? kRowChunk : kSrcChunk;
     for (std::int64_t z = 0; z < cnt; ++z) {
@@ -345,9 +366,63 @@ void Planner::layout() {
   // for every owned node A of a proxy level, rows in chunks of 256
   p2_items.clear();
   p2s_items.clear();
+  pg_items.clear();
+  pair_descs.clear();
+  pd_level.assign(L_ + 2, 0);
+  pc_off.assign(T + 1, 0);
+  pc_pos.clear();
+  pair_out_total = 0;
   n_proxy_levels = 0;
+  {
+    // pair levels: descriptors of the pairs with an owned side, output runs
+    std::vector<std::vector<std::int64_t>> runs(T);
+    for (int l = 1; l <= L_; ++l) {
+      pd_level[l] = static_cast<std::int64_t>(pair_descs.size());
+      if (mode_[l] != kModePair) continue;
+      const auto& P = pairs_[l];
+      for (std::size_t p = 0; p < P.X.size(); ++p) {
+        const bool ox = owned(l, P.X[p]), oy = owned(l, P.Y[p]);
+        if (!ox && !oy) continue;
+        PairDesc d{};
+        d.woff = pair_wx[l][p];
+        d.xrow = off_[l][P.X[p]];
+        d.yrow = off_[l][P.Y[p]];
+        d.m = static_cast<std::int32_t>(node_size(l, P.X[p]));
+        d.n = static_cast<std::int32_t>(node_size(l, P.Y[p]));
+        d.rp = pair_rx[l][p];
+        d.own = (ox ? 1 : 0) | (oy ? 2 : 0);
+        d.out = pair_out_total;
+        if (ox) runs[gid(l, P.X[p])].push_back(d.out);
+        if (oy) runs[gid(l, P.Y[p])].push_back(d.out + d.m);
+        pair_out_total += d.m + d.n;
+        pair_descs.push_back(d);
+      }
+    }
+    pd_level[L_ + 1] = static_cast<std::int64_t>(pair_descs.size());
+    for (std::int64_t g = 0; g < T; ++g) {
+      pc_off[g] = static_cast<std::int32_t>(pc_pos.size());
+      pc_pos.insert(pc_pos.end(), runs[g].begin(), runs[g].end());
+    }
+    pc_off[T] = static_cast<std::int32_t>(pc_pos.size());
+  }
   for (int l = 1; l <= L_; ++l) {
     if (mode_[l] == kModeDirect) continue;
+    if (mode_[l] == kModePair) {
+      // gather the pair outputs of every owned node into the level's partial
+      const std::int64_t cnt = 1LL << (3 * l);
+      int slot = -1;
+      for (std::int64_t z = 0; z < cnt; ++z) {
+        const std::int64_t g = gid(l, z);
+        if (pc_off[g + 1] == pc_off[g]) continue;
+        if (slot < 0) slot = n_proxy_levels++;
+        const std::int64_t nr = node_size(l, z);
+        for (std::int64_t r0 = 0; r0 < nr; r0 += kColChunk)
+          pg_items.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
+                                    static_cast<std::int32_t>(std::min<std::int64_t>(kColChunk, nr - r0)),
+                                    slot});
+      }
+      continue;
+    }
     const bool stream = mode_[l] == kModeStream;
     const std::int64_t cnt = 1LL << (3 * l);
     const std::int64_t step = stream ? kTileRows : kColChunk;

@@ -40,6 +40,18 @@ enum LevelMode : int {
   kModeProxy = 1,   // matrix-free: pivots + packed LU (reference lowrank.cpp:291-327),
                     //   2 r(m+n) kernel evaluations + 2 r^2 solve FMAs per pair
   kModeDirect = 2,  // exact dense evaluation (leaf level only): 2 m n evaluations per pair
+  kModePair = 3,    // explicit factors, pair-major: one fused pass per pair reads U and V
+                    //   once (8 r(m+n) B), both products through a per-pair output buffer
+};
+
+// Fused pair pass (kModePair levels): F = [U; V] ((m + n) x rp, row-major,
+// rp = r rounded up to even) at woff; t_U = U^T x_X, t_V = V^T x_Y; outputs
+// U t_V (m rows, for X) and V t_U (n rows, for Y) at out.
+struct PairDesc {
+  std::int64_t woff;
+  std::int64_t xrow, yrow;  // first permuted row of X and of Y
+  std::int64_t out;         // pair-output buffer offset (X's rows, then Y's)
+  std::int32_t m, n, rp, own;  // own: bit 0 = X owned here, bit 1 = Y owned
 };
 
 struct LevelLists {
@@ -136,6 +148,7 @@ class Planner {
   void set_mode(int l, int m) {
     if (mode_[l] == kModeDirect || m == kModeDirect)
       throw std::invalid_argument("planner: direct mode is fixed at construction");
+    if (m < 0 || m > kModePair) throw std::invalid_argument("planner: bad level mode");
     mode_[l] = m;
   }
   bool owned(int level, std::int64_t m) const;
@@ -175,6 +188,16 @@ class Planner {
   std::vector<P1Reduce> reds;
   std::vector<P2Item> p2_items;   // owned nodes of proxy levels, <= 256 rows each
   std::vector<P2Item> p2s_items;  // owned nodes of stream levels, one row tile each
+  // pair levels: one descriptor per pair with an owned side (grouped by level),
+  // pd_level[l] .. pd_level[l + 1]; per owned node the output runs of its
+  // pairs (pc_off over global nodes, pc_pos in pair order), gathered into the
+  // level's partial by pg_items (owned nodes, <= 256 rows each)
+  std::vector<PairDesc> pair_descs;
+  std::vector<std::int64_t> pd_level;
+  std::vector<std::int32_t> pc_off;
+  std::vector<std::int64_t> pc_pos;
+  std::vector<P2Item> pg_items;
+  std::int64_t pair_out_total = 0;
   int n_proxy_levels = 0;         // output slots of the phase-2 proxy + stream passes
   std::int64_t leaf0 = 0, leaf1 = 0;
   std::vector<std::int32_t> near_off, near_ids;

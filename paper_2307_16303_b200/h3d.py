@@ -231,7 +231,8 @@ class HmatOptions:
     max_rank: int = 0
     # B200 extension: "auto" (cost model), "stream"
     # (explicit factors everywhere) or "explicit" (level_modes[l]: 0 stream,
-    # 1 proxy, 2 direct at the leaf level)
+    # 1 proxy, 2 direct at the leaf level, 3 pair = explicit factors applied in
+    # one fused read per pair)
     mode_policy: str = "auto"
     level_modes: tuple = ()
 
@@ -429,7 +430,7 @@ def stats(rep: HMatrixRep) -> dict:
 # ---------------------------------------------------------------- host planner
 # h3d_kernel_slot order (include/h3d_b200.h)
 KERNEL_SLOTS = ("gather", "p1_stream", "red_stream", "p2_stream", "p1_proxy", "red_proxy", "solve",
-                "p2_proxy", "near", "combine")
+                "p2_proxy", "near", "combine", "pair")
 
 _PLAN_DTYPES = {
     "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
@@ -447,6 +448,12 @@ _PLAN_DTYPES = {
                        ("pslot", np.int64)]),
     "reds": np.dtype([("node", np.int32), ("ncols", np.int32), ("nchunks", np.int32),
                       ("kind", np.int32), ("pbase", np.int64)]),
+    "pair_descs": np.dtype([("woff", np.int64), ("xrow", np.int64), ("yrow", np.int64),
+                            ("out", np.int64), ("m", np.int32), ("n", np.int32), ("rp", np.int32),
+                            ("own", np.int32)]),
+    "pd_level": np.int64, "pc_off": np.int32, "pc_pos": np.int64,
+    "pg_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
+                          ("slot", np.int32)]),
     "p2_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
                           ("slot", np.int32)]),
     "p2s_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),

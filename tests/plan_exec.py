@@ -82,7 +82,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
 
     for l in range(1, L + 1):
         X, Y = plan.pairs(l)
-        if md[l] == 0:
+        if md[l] in (0, 3):
             wx, wy = plan.array("pair_wx", l), plan.array("pair_wy", l)
             rx, ry = plan.array("pair_rx", l), plan.array("pair_ry", l)
             cx, cy = plan.array("pair_cx", l), plan.array("pair_cy", l)
@@ -96,13 +96,17 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             Lm = np.tril(LU, -1) + np.eye(r)
             Um = np.triu(LU)
             Xp, Yp = pts_of(l, a), pts_of(l, b)
-            if md[l] == 0:
+            if md[l] in (0, 3):
                 FX = np.linalg.solve(Um.T, kernel_matrix(kind, Xp, Yp[cp]).T).T  # K(X,tau) R^-1
                 FY = np.linalg.solve(Lm, kernel_matrix(kind, Yp, Xp[rp]).T).T    # K(Y,sigma) L^-T
                 I, Q = np.meshgrid(np.arange(len(Xp)), np.arange(r), indexing="ij")
-                W[wx[p] + tile_index(I, cx[p] + Q, rx[p])] = FX
-                J, Q = np.meshgrid(np.arange(len(Yp)), np.arange(r), indexing="ij")
-                W[wy[p] + tile_index(J, cy[p] + Q, ry[p])] = FY
+                J, Qy = np.meshgrid(np.arange(len(Yp)), np.arange(r), indexing="ij")
+                if md[l] == 0:
+                    W[wx[p] + tile_index(I, cx[p] + Q, rx[p])] = FX
+                    W[wy[p] + tile_index(J, cy[p] + Qy, ry[p])] = FY
+                else:  # pair-major: U then V, row-major with stride rp
+                    W[wx[p] + I * rx[p] + Q] = FX
+                    W[wy[p] + J * ry[p] + Qy] = FY
             elif md[l] == 1:
                 piv[po[p]: po[p] + r] = rp
                 piv[po[p] + r: po[p] + 2 * r] = cp
@@ -201,7 +205,9 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
                                atol=1e-12 * (np.abs(cpart).max() + 1))
     items2 = plan.array("p2_items")
     items2s = plan.array("p2s_items")
-    nslots = 1 + max([int(v) for v in items2["slot"]] + [int(v) for v in items2s["slot"]] + [-1])
+    pgit = plan.array("pg_items")
+    nslots = 1 + max([int(v) for v in items2["slot"]] + [int(v) for v in items2s["slot"]] +
+                     [int(v) for v in pgit["slot"]] + [-1])
     lvl = np.zeros((nslots, n))
     hits = np.zeros((L + 1, n), np.int64)
 
@@ -222,6 +228,25 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         Wn = node_matrix(W, woff[g], g, int(rows[g]), R)
         r0 = rowbeg[g] + it["row0"]
         lvl[it["slot"], r0: r0 + it["nrows"]] = Wn[it["row0"]: it["row0"] + it["nrows"]] @ S[so: so + R]
+        hits[level_of(g), r0: r0 + it["nrows"]] += 1
+    # pair levels: one fused pass per pair descriptor, gathered per node
+    pdesc = plan.array("pair_descs")
+    pout = np.zeros(max(int(sum(int(d["m"]) + int(d["n"]) for d in pdesc)), 1))
+    for d in pdesc:
+        m_, n_, rp_ = int(d["m"]), int(d["n"]), int(d["rp"])
+        F = W[d["woff"]: d["woff"] + (m_ + n_) * rp_].reshape(m_ + n_, rp_)
+        tu = F[:m_].T @ xp[d["xrow"]: d["xrow"] + m_]
+        tv = F[m_:].T @ xp[d["yrow"]: d["yrow"] + n_]
+        pout[d["out"]: d["out"] + m_] = F[:m_] @ tv
+        pout[d["out"] + m_: d["out"] + m_ + n_] = F[m_:] @ tu
+    pcoff, pcpos = plan.array("pc_off"), plan.array("pc_pos")
+    for it in pgit:
+        g = int(it["node"])
+        r0 = rowbeg[g] + it["row0"]
+        v = np.zeros(it["nrows"])
+        for q in pcpos[pcoff[g]: pcoff[g + 1]]:
+            v += pout[int(q) + it["row0"]: int(q) + it["row0"] + it["nrows"]]
+        lvl[it["slot"], r0: r0 + it["nrows"]] = v
         hits[level_of(g), r0: r0 + it["nrows"]] += 1
     assert hits.max(initial=0) <= 1, "a row written twice at one level"
     # every owned row of a node with partners is covered once at its level

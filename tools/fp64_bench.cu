@@ -16,6 +16,52 @@ __global__ void dfma_peak(double* out, int iters) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
 }
 
+// MUFU.RSQ64H issue rate: 8 independent seeds per thread per iteration
+__global__ void mufu_peak(double* out, int iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + threadIdx.x + k;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      double y;
+      asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a[k]));
+      a[k] = y + 1.0;  // DADD keeps the chain alive (1 DP op per seed)
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// RSQ64H and DFMA interleaved: NR seeds + NF independent FMAs per iteration
+// (separate pipes: time ~ max of the two; shared: ~ sum)
+template <int NR, int NF>
+__global__ void mix_peak(double* out, int iters) {
+  double a[8], f[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = 1.0 + threadIdx.x + k;
+    f[k] = 2.0 + k;
+  }
+  const double m = 1.0000001, c = 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+      double y;
+      asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a[k & 7]));
+      a[k & 7] = y;
+    }
+#pragma unroll
+    for (int k = 0; k < NF; ++k) f[k & 7] = fma(f[k & 7], m, c);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k] + f[k];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 __device__ __forceinline__ double rsqrt_nr1(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -107,6 +153,47 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     const double fmas = double(blocks) * threads * iters * 8;
     printf("DFMA: %.2f T fma/s = %.1f TFLOP/s (fp64)\n", fmas / ms / 1e9, 2 * fmas / ms / 1e9);
+  }
+  {
+    const int iters = 20000, blocks = 148 * 8, threads = 256;
+    double* o;
+    cudaMalloc(&o, sizeof(double) * blocks * threads);
+    auto run = [&](auto kern, const char* name) {
+      kern<<<blocks, threads>>>(o, 10);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      kern<<<blocks, threads>>>(o, iters);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      printf("%s: %.3f ms\n", name, ms);
+    };
+    run(mix_peak<8, 0>, "8 RSQ64H        ");
+    run(mix_peak<0, 32>, "32 DFMA         ");
+    run(mix_peak<8, 32>, "8 RSQ64H+32 DFMA");
+    cudaFree(o);
+  }
+  {
+    const int iters = 20000, blocks = 148 * 8, threads = 256;
+    double* o;
+    cudaMalloc(&o, sizeof(double) * blocks * threads);
+    mufu_peak<<<blocks, threads>>>(o, 10);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    mufu_peak<<<blocks, threads>>>(o, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double ops = 8.0 * iters * blocks * threads;
+    printf("MUFU.RSQ64H (+1 DADD each): %.3f T seeds/s = %.2f per SM per clock at 1.965 GHz\n",
+           ops / ms / 1e9, ops / (ms * 1e-3) / 148 / 1.965e9);
+    cudaFree(o);
   }
   const int ns = 1 << 16, nt = 1 << 20;
   double *sx, *sy, *sz, *sq, *tx;
