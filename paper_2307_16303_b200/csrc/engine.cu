@@ -141,6 +141,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2s") tune_.p2s = v;
         else if (k == "p2p") tune_.p2p = v;
         else if (k == "skip") tune_.skip = v;
+        else if (k == "nf") tune_.nf = v;
       }
       pos = end + 1;
     }
@@ -919,6 +920,20 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ke(H3D_K_P1_PROXY, stream4_);
     ++launches;
   }
+  // without an HBM lane the solves would leave the SMs idle: the near field
+  // + direct blocks (x only) fork off here at one CTA per SM and fill them,
+  // the solve blocks and then p2_proxy take the remaining slots
+  const bool near_fork = has_p2 && (tune_.nf >= 0 ? tune_.nf != 0 : !hbm);
+  if (near_fork) {
+    H3D_CUDA_CHECK(cudaEventRecord(fork_[2], stream4_));
+    H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
+    kb(H3D_K_NEAR, stream3_);
+    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, 1, stream3_);
+    else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, 1, stream3_);
+    ke(H3D_K_NEAR, stream3_);
+    ++launches;
+    H3D_CUDA_CHECK(cudaEventRecord(join_[2], stream3_));
+  }
   if (n_red_p_ > 0) {
     kb(H3D_K_RED_PROXY, stream4_);
     launch_phase1_reduce(p1_red_p_.get(), n_red_p_, nt, spos_.get(), P_.get(), S_.get(), stream4_);
@@ -965,14 +980,17 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       ke(H3D_K_P2_PROXY, stream4_);
       ++launches;
     }
-    kb(H3D_K_NEAR, stream4_);
-    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream4_);
-    else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
-    ke(H3D_K_NEAR, stream4_);
-    ++launches;
+    if (!near_fork) {
+      kb(H3D_K_NEAR, stream4_);
+      if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream4_);
+      else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
+      ke(H3D_K_NEAR, stream4_);
+      ++launches;
+    }
   }
   H3D_CUDA_CHECK(cudaEventRecord(join_[1], stream4_));
   H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[1], 0));
+  if (near_fork) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[2], 0));
   if (hbm) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, join_[0], 0));
   if (has_p2 && parts) {
     kb(H3D_K_COMBINE, s);

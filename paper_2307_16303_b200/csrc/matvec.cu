@@ -466,7 +466,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
   for (int k = 0; k < NK; ++k) acc[k] = 0.0;
   if (sg.side == 0) {
     // w = L^-1 v: w_i = v_i + sum_{j<i} PT[j][i] v_j
-#pragma unroll 8
+#pragma unroll 16
     for (int j = 0; j < r; ++j) {
       const double vj = v[j];
       const double* col = PT + static_cast<std::int64_t>(j) * r;
@@ -484,7 +484,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
     }
     __syncwarp();
     // s = R^-1 w: s_i = sum_{j>=i} PT[j][i] w_j
-#pragma unroll 8
+#pragma unroll 16
     for (int j = 0; j < r; ++j) {
       const double wj = w[j];
       const double* col = PT + static_cast<std::int64_t>(j) * r;
@@ -496,7 +496,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
     }
   } else {
     // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i
-#pragma unroll 8
+#pragma unroll 16
     for (int i = 0; i < r; ++i) {
       const double vi = v[i];
       const double* row = P + static_cast<std::int64_t>(i) * r;
@@ -513,7 +513,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
     }
     __syncwarp();
     // s = L^-T u: s_j = u_j + sum_{i>j} P[i][j] u_i
-#pragma unroll 8
+#pragma unroll 16
     for (int i = 1; i < r; ++i) {
       const double ui = w[i];
       const double* row = P + static_cast<std::int64_t>(i) * r;
