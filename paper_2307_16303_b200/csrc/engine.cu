@@ -920,10 +920,10 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ke(H3D_K_P1_PROXY, stream4_);
     ++launches;
   }
-  // without an HBM lane the solves would leave the SMs idle: the near field
-  // + direct blocks (x only) fork off here at one CTA per SM and fill them,
-  // the solve blocks and then p2_proxy take the remaining slots
-  const bool near_fork = has_p2 && (tune_.nf >= 0 ? tune_.nf != 0 : !hbm);
+  // optional (H3D_TUNE nf=1): the near field + direct blocks (x only) fork
+  // off here at one CTA per SM beside the solves; measured slower - the
+  // latency-bound solve blocks lose more than the idle SMs gain (2.9 -> 5.6 ms)
+  const bool near_fork = has_p2 && tune_.nf == 1;
   if (near_fork) {
     H3D_CUDA_CHECK(cudaEventRecord(fork_[2], stream4_));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
@@ -942,8 +942,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   }
   if (n_segs_solve_ > 0) {
     kb(H3D_K_SOLVE, stream4_);
-    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), q4_.get(),
-                       stream4_);
+    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), stream4_);
     ke(H3D_K_SOLVE, stream4_);
     ++launches;
   }

@@ -91,8 +91,7 @@ class Engine {
   // H3D_TUNE="p1s=1,p1p=4,p2c=2,p2s=1,p2p=4" (proxy kernels: 128-thread CTAs)
   // ("skip=<mask of h3d_kernel_slot>" drops kernels: timing experiments only,
   // results are wrong)
-  // ("nf=0|1": near field after p2_proxy on the FP64 lane / forked after
-  // p1_proxy; default: forked when there is no HBM lane)
+  // ("nf=1": near field forked after p1_proxy instead of after p2_proxy)
   struct Tune {
     int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1;
   } tune_;
@@ -122,7 +121,7 @@ class Engine {
   DevBuf<std::int32_t> piv_;
   DevBuf<double> lu_;
   std::int64_t lu_total_ = 0;
-  DevBuf<double> q4_;  // proxy records (x, y, z, solved t-vector) in S index space
+  DevBuf<double> q4_;  // proxy points (x, y, z, -) in S index space
   DevBuf<double> q4c_;  // the same points centred on their node's box (x', y', z', |.|^2)
   DevBuf<double> center_;  // box centre per global node
   DevBuf<std::int32_t> vcols_;  // leading vertex-partner columns per node

@@ -121,7 +121,7 @@ struct P1Args {
   double* P = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;  // permuted points
   const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
-  const double* q4 = nullptr;  // proxy records (x, y, z, solved t-vector), S index space
+  const double* q4 = nullptr;  // proxy points (x, y, z, -) in S index space
   const double* q4c = nullptr;  // proxy records centred on their node's box (x', y', z', |.|^2)
   const double* cen = nullptr;  // box centre per global node (4 doubles)
   const std::int32_t* vcols = nullptr;  // per node: leading vertex-partner columns
@@ -142,9 +142,9 @@ void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int
                          const double* px, const double* py, const double* pz, const double* cen,
                          double* q4, double* q4c, cudaStream_t s);
 // lu holds 2 x lu_total doubles: the packed inverses row-major, then column-major
-// reads v from S, writes the solved t-vector into the w lane of q4
+// in place on S: v (phase-1 output) -> the solved t-vector
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
-                        std::int64_t lu_total, const double* S, double* q4, cudaStream_t s);
+                        std::int64_t lu_total, double* S, cudaStream_t s);
 // build time: replace every pair's packed LU by its triangular inverses
 // (strict lower L^-1, upper R^-1), row-major at lu and column-major at lu + lu_total
 void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::int64_t lu_total,
@@ -161,7 +161,7 @@ struct Phase2Args {
   const double* xp = nullptr;
   const double *px = nullptr, *py = nullptr, *pz = nullptr;
   const double* p4 = nullptr;  // packed permuted points (x, y, z, x-value)
-  const double* q4 = nullptr;  // proxy records (x, y, z, solved t-vector), S index space
+  const double* q4 = nullptr;  // proxy points (x, y, z, -) in S index space
   const double* q4c = nullptr;  // centred proxy records (x', y', z', |.|^2)
   const double* cen = nullptr;  // box centre per global node (4 doubles)
   const std::int32_t* vcols = nullptr;  // per node: leading vertex-partner columns

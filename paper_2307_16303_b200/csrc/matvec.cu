@@ -527,7 +527,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
     const int i = lane + 32 * k;
-    if (i < r) out[4 * i] = acc[k];  // w lane of the proxy records
+    if (i < r) out[i] = acc[k];  // in place over v
   }
 }
 
@@ -535,8 +535,7 @@ __global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __rest
                                                           std::int64_t nseg,
                                                           const double* __restrict__ lu,
                                                           std::int64_t lu_total,
-                                                          const double* __restrict__ S,
-                                                          double* __restrict__ q4) {
+                                                          double* __restrict__ S) {
   __shared__ double sh[4][640];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x >> 5) + warp;
@@ -545,8 +544,8 @@ __global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __rest
   const int r = sg.r;
   double* v = sh[warp];  // v and w, r <= 320 (enforced on the host)
   double* w = v + 320;
-  const double* Sg = S + sg.so;
-  double* out = q4 + 4 * sg.so + 3;
+  double* Sg = S + sg.so;
+  double* out = Sg;
   for (int q = lane; q < r; q += 32) v[q] = Sg[q];
   __syncwarp();
   const double* P = lu + sg.lu_off;
@@ -653,7 +652,7 @@ __device__ void compute_pass(const Phase2Args& a, const TileRanges& tr, double2*
       if (tr.kind[lo] == kRangeProxy) {
         const double4 r = reinterpret_cast<const double4*>(a.q4)[idx];
         stage[2 * q] = make_double2(r.x, r.y);
-        stage[2 * q + 1] = make_double2(r.z, r.w);
+        stage[2 * q + 1] = make_double2(r.z, a.S[idx]);
       } else {
         stage[2 * q] = make_double2(a.px[idx], a.py[idx]);
         stage[2 * q + 1] = make_double2(a.pz[idx], a.xp[idx]);
@@ -1195,7 +1194,7 @@ __global__ void __launch_bounds__(kProxyThreads, 5) p2_proxy_kernel(const Phase2
         const double4 c4 = reinterpret_cast<const double4*>(a.q4c)[so + j0 + q];
         src[3 * q] = make_double2(c4.x, c4.y);
         src[3 * q + 1] = make_double2(c4.z, c4.w);
-        src[3 * q + 2] = make_double2(a.q4[4 * (so + j0 + q) + 3], 0.0);
+        src[3 * q + 2] = make_double2(a.S[so + j0 + q], 0.0);
       }
       __syncthreads();
       const int sub = (nj + G - 1) / G;
@@ -1461,11 +1460,11 @@ void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::
 }
 
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
-                        std::int64_t lu_total, const double* S, double* q4, cudaStream_t s) {
+                        std::int64_t lu_total, double* S, cudaStream_t s) {
   if (nseg == 0) return;
   constexpr int warps = 4;
   proxy_solve_kernel<<<static_cast<unsigned>((nseg + warps - 1) / warps), 32 * warps, 0, s>>>(
-      segs, nseg, lu, lu_total, S, q4);
+      segs, nseg, lu, lu_total, S);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
