@@ -175,6 +175,34 @@ typedef enum {
 int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launches, double* start_sum,
                             int count);
 
+/* GMRES on the device (replaces h3d::gmres + IEOperator::apply,
+ * solver.hpp:10-28,39-53; solver.cpp:22-125,199-206): solves
+ * (alpha I + beta A) x = rhs with A this handle's HODLR3D operator
+ * (alpha = 0, beta = 1: the plain matvec; the IE operator uses
+ * alpha = 1 + cell self-integral, beta = cell volume). Arnoldi with modified
+ * Gram-Schmidt and Givens rotations, restart 0 = unrestarted, iterate
+ * returned with converged = 0 when max_iter is exhausted. hist (may be NULL)
+ * receives up to hist_cap relative residuals, one per iteration. rhs / x are
+ * host (where = 0) or device (where = 1) arrays in original point order. */
+typedef struct {
+  int iterations;
+  int converged;
+  int history_len;
+  int reserved;
+  double solve_ms;
+  double final_relres;  /* |rhs - op(x)| / |rhs| of the returned iterate */
+} h3d_gmres_info;
+int h3d_dev_gmres(h3d_dev* dev, const double* rhs, double* x, int where, double alpha, double beta,
+                  double tol, int restart, int max_iter, double* hist, int hist_cap, h3d_gmres_info* info);
+/* Exact dense product b = K x (diagonal rule), O(N^2) on the device: the
+ * reference's dense row sums for manufactured right-hand sides
+ * (solver.cpp:247-258). Single-shard handles only. */
+int h3d_dev_direct_matvec(h3d_dev* dev, const double* x, double* b, int where);
+/* Collocation helpers of the IE driver: the tensor grid (kernel.cpp:96-109)
+ * and the cell self-integral of 1/r (solver.cpp:127-193). */
+int h3d_generate_grid_points(int64_t n, double* xyz);
+double h3d_cell_self_integral(double h);
+
 /* Replaces h3d::stats(rep) (hmatrix.hpp:85). */
 int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out);
 

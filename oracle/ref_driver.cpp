@@ -19,6 +19,7 @@
 
 #include "h3d/hmatrix.hpp"
 #include "h3d/parallel.hpp"
+#include "h3d/solver.hpp"
 
 using namespace h3d;
 
@@ -307,6 +308,27 @@ int h3dref_dense_matvec(const double* xyz, std::int64_t n, int kernel_id, double
       }
       b[i] = acc + k.diagonal * x[i];
     }
+  });
+}
+
+// Solver (solver.hpp): the IE manufactured-solution experiment and the cell
+// constant, for the device GMRES parity tests.
+double h3dref_cell_self_integral(double h) { return cell_self_integral(h); }
+
+int h3dref_ie_experiment(int grid_n, double eps, int n_max, std::uint64_t seed, double tol, int restart,
+                         int max_iter, int* iterations, int* converged, double* forward_error) {
+  return guarded([&] {
+    HmatOptions base;
+    base.n_max = n_max;
+    GmresOptions g;
+    g.tol = tol;
+    g.restart = restart;
+    g.max_iter = max_iter;
+    const IeReport r =
+        ie_experiment(grid_n, make_kernel(KernelId::Laplace3d), eps, Variant::Hodlr3d, seed, base, g);
+    *iterations = r.iterations;
+    *converged = r.converged ? 1 : 0;
+    *forward_error = r.forward_error;
   });
 }
 

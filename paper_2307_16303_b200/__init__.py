@@ -5,11 +5,19 @@ from .h3d import (  # noqa: F401
     DegenerateDistributionError,
     DegenerateGeometryError,
     DeviceError,
+    GmresOptions,
+    GmresResult,
     HMatrixRep,
     HmatOptions,
+    IEOperator,
+    IeReport,
     KernelSpec,
     MatvecTiming,
+    cell_self_integral,
+    discretize_ie,
+    generate_grid_points,
     generate_points,
+    ie_experiment,
     initialize,
     library_path,
     make_kernel,

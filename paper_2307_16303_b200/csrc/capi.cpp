@@ -147,6 +147,32 @@ int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launche
   });
 }
 
+int h3d_dev_gmres(h3d_dev* dev, const double* rhs, double* x, int where, double alpha, double beta,
+                  double tol, int restart, int max_iter, double* hist, int hist_cap, h3d_gmres_info* info) {
+  return guarded([&] {
+    if (!dev || !rhs || !x) throw h3db::InvalidArgument("gmres: null argument");
+    std::lock_guard<std::mutex> lk(eng(dev)->mu);
+    eng(dev)->gmres(rhs, x, where == 0, alpha, beta, tol, restart, max_iter, hist, hist_cap, info);
+  });
+}
+
+int h3d_dev_direct_matvec(h3d_dev* dev, const double* x, double* b, int where) {
+  return guarded([&] {
+    if (!dev || !x || !b) throw h3db::InvalidArgument("direct_matvec: null argument");
+    std::lock_guard<std::mutex> lk(eng(dev)->mu);
+    eng(dev)->direct_matvec(x, b, where == 0);
+  });
+}
+
+int h3d_generate_grid_points(int64_t n, double* xyz) {
+  return guarded([&] {
+    if (n < 1) throw h3db::InvalidArgument("generate_points: N must be >= 1");
+    h3db::tensor_grid_points(n, xyz);
+  });
+}
+
+double h3d_cell_self_integral(double h) { return h3db::cell_self_integral(h); }
+
 int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out) {
   return guarded([&] { eng(dev)->stats(out); });
 }

@@ -202,13 +202,16 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
 #define H3D_MBAR_SLEEP_MAX 0
 #endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+#if H3D_MBAR_SLEEP_MAX > 0
   unsigned ns = 16;
   while (!mbar_try(b, parity)) {
-    if (H3D_MBAR_SLEEP_MAX > 0) {
-      __nanosleep(ns);
-      if (ns < H3D_MBAR_SLEEP_MAX) ns <<= 1;
-    }
+    __nanosleep(ns);
+    if (ns < H3D_MBAR_SLEEP_MAX) ns <<= 1;
   }
+#else
+  while (!mbar_try(b, parity)) {
+  }
+#endif
 }
 __device__ __forceinline__ unsigned long long l2_evict_first() {
   unsigned long long pol;

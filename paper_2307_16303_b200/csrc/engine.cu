@@ -1200,3 +1200,147 @@ std::int64_t Engine::export_pairs(int level, std::int32_t* x, std::int32_t* y,
 }
 
 }  // namespace h3db
+
+namespace h3db {
+
+// ---------------------------------------------------------------- solver
+void Engine::direct_matvec(const double* x, double* b, bool host) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  if (world_ != 1) throw InvalidArgument("direct_matvec: single-shard handles only");
+  const double* xin = x;
+  if (host) {
+    H3D_CUDA_CHECK(cudaMemcpyAsync(x_.get(), x, n_ * 8, cudaMemcpyHostToDevice, stream_));
+    xin = x_.get();
+  }
+  double* bout = host ? b_.get() : b;
+  launch_gather(xin, perm_.get(), n_, xp_.get(), p4_.get(), stream_);
+  launch_direct(p4_.get(), n_, opt_.kernel_id, opt_.diagonal, perm_.get(), bout, stream_);
+  if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
+  H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::gmres(const double* rhs, double* xout, bool host, double alpha, double beta, double tol,
+                   int restart, int max_iter, double* hist, int hist_cap, h3d_gmres_info* info) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  if (!(tol > 0)) throw InvalidArgument("gmres: tol must be positive");
+  if (world_ != 1) throw InvalidArgument("gmres: single-shard handles only (Krylov vectors are not sharded)");
+  const auto t0 = Clock::now();
+  const std::int64_t n = n_;
+  max_iter = std::max(max_iter, 1);
+  restart = restart > 0 ? restart : max_iter;
+  const int mcap = std::min(restart, max_iter);
+  cudaStream_t s = stream_;
+  DevBuf<double> f, x, w, r, basis, scal, scratch;
+  f.alloc(n);
+  x.alloc(n);
+  w.alloc(n);
+  r.alloc(n);
+  basis.alloc(static_cast<std::size_t>(mcap + 1) * n);
+  scal.alloc(mcap + 2);
+  scratch.alloc(dot_scratch_doubles());
+  H3D_CUDA_CHECK(cudaMemcpyAsync(f.get(), rhs, n * 8, host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  H3D_CUDA_CHECK(cudaMemsetAsync(x.get(), 0, n * 8, s));
+  auto op = [&](const double* v, double* out) {  // out = alpha v + beta A v
+    enqueue(v, out, s, nullptr, nullptr);
+    if (!(alpha == 0.0 && beta == 1.0)) launch_affine(out, v, n, alpha, beta, s);
+  };
+  auto norm_host = [&](const double* v) {
+    launch_dot(v, v, n, scratch.get(), scal.get(), true, s);
+    double h = 0;
+    H3D_CUDA_CHECK(cudaMemcpyAsync(&h, scal.get(), 8, cudaMemcpyDeviceToHost, s));
+    H3D_CUDA_CHECK(cudaStreamSynchronize(s));
+    return h;
+  };
+  int hlen = 0, total = 0;
+  bool converged = false;
+  double relres = 1.0;
+  const double rhs_norm = norm_host(f.get());
+  if (rhs_norm == 0.0) {
+    converged = true;
+    relres = 0.0;
+  }
+  std::vector<double> hcol(mcap + 2);
+  while (!converged && total < max_iter) {
+    // residual of the current iterate (the rhs itself on the first pass)
+    if (total == 0) {
+      H3D_CUDA_CHECK(cudaMemcpyAsync(r.get(), f.get(), n * 8, cudaMemcpyDeviceToDevice, s));
+    } else {
+      op(x.get(), w.get());
+      launch_sub(r.get(), f.get(), w.get(), n, s);
+    }
+    const double beta0 = norm_host(r.get());
+    if (beta0 / rhs_norm < tol) {
+      converged = true;
+      relres = beta0 / rhs_norm;
+      break;
+    }
+    const int m = std::min(restart, max_iter - total);
+    H3D_CUDA_CHECK(cudaMemsetAsync(basis.get(), 0, n * 8, s));
+    launch_axpy(basis.get(), r.get(), n, nullptr, 0.0, 1.0 / beta0, s);
+    std::vector<double> H(static_cast<std::size_t>(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1, 0.0);
+    auto Hk = [&](int i, int k) -> double& { return H[static_cast<std::size_t>(i) * m + k]; };
+    g[0] = beta0;
+    int k = 0;
+    bool done = false;
+    for (; k < m && !done; ++k) {
+      double* vk = basis.get() + static_cast<std::int64_t>(k) * n;
+      op(vk, w.get());
+      for (int i = 0; i <= k; ++i) {  // modified Gram-Schmidt
+        const double* vi = basis.get() + static_cast<std::int64_t>(i) * n;
+        launch_dot(w.get(), vi, n, scratch.get(), scal.get() + i, false, s);
+        launch_axpy(w.get(), vi, n, scal.get() + i, -1.0, 0.0, s);
+      }
+      launch_dot(w.get(), w.get(), n, scratch.get(), scal.get() + k + 1, true, s);
+      H3D_CUDA_CHECK(cudaMemcpyAsync(hcol.data(), scal.get(), (k + 2) * 8, cudaMemcpyDeviceToHost, s));
+      H3D_CUDA_CHECK(cudaStreamSynchronize(s));
+      const double h_next = hcol[k + 1];
+      if (h_next > 0.0 && k + 1 <= mcap)
+        launch_scale_div(basis.get() + static_cast<std::int64_t>(k + 1) * n, w.get(), n,
+                         scal.get() + k + 1, s);
+      for (int i = 0; i <= k; ++i) Hk(i, k) = hcol[i];
+      Hk(k + 1, k) = h_next;
+      for (int i = 0; i < k; ++i) {  // previous rotations
+        const double t = cs[i] * Hk(i, k) + sn[i] * Hk(i + 1, k);
+        Hk(i + 1, k) = -sn[i] * Hk(i, k) + cs[i] * Hk(i + 1, k);
+        Hk(i, k) = t;
+      }
+      const double den = std::hypot(Hk(k, k), Hk(k + 1, k));
+      cs[k] = den == 0.0 ? 1.0 : Hk(k, k) / den;
+      sn[k] = den == 0.0 ? 0.0 : Hk(k + 1, k) / den;
+      Hk(k, k) = den;
+      Hk(k + 1, k) = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      ++total;
+      const double rel = std::abs(g[k + 1]) / rhs_norm;
+      if (hist && hlen < hist_cap) hist[hlen] = rel;
+      ++hlen;
+      if (rel < tol || h_next == 0.0) done = true;
+    }
+    // back substitution, iterate update
+    std::vector<double> y(k, 0.0);
+    for (int i = k - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int j = i + 1; j < k; ++j) acc -= Hk(i, j) * y[j];
+      y[i] = acc / Hk(i, i);
+    }
+    for (int j = 0; j < k; ++j)
+      launch_axpy(x.get(), basis.get() + static_cast<std::int64_t>(j) * n, n, nullptr, 0.0, y[j], s);
+    op(x.get(), w.get());
+    launch_sub(r.get(), f.get(), w.get(), n, s);
+    relres = norm_host(r.get()) / rhs_norm;
+    if (relres < tol) converged = true;
+  }
+  H3D_CUDA_CHECK(cudaMemcpyAsync(xout, x.get(), n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  H3D_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (info) {
+    info->iterations = total;
+    info->converged = converged ? 1 : 0;
+    info->history_len = hlen;
+    info->reserved = 0;
+    info->solve_ms = ms_since(t0);
+    info->final_relres = relres;
+  }
+}
+
+}  // namespace h3db

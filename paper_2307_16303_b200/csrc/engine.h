@@ -64,6 +64,11 @@ class Engine {
   std::int64_t export_list(int level, int kind, std::int32_t* offsets, std::int32_t* ids) const;
   std::int64_t export_pairs(int level, std::int32_t* x, std::int32_t* y, std::int32_t* rank) const;
   void attach_nccl(const void* id128, int rank, int world);
+  // exact dense product b = K x (O(N^2), verification / manufactured RHS)
+  void direct_matvec(const double* x, double* b, bool host);
+  // GMRES on (alpha I + beta A) x = rhs, reference solver.cpp:22-125
+  void gmres(const double* rhs, double* x, bool host, double alpha, double beta, double tol, int restart,
+             int max_iter, double* hist, int hist_cap, h3d_gmres_info* info);
 
   std::mutex mu;  // serialises calls per handle (the handle owns stream + scratch)
 

@@ -240,6 +240,27 @@ void launch_pair_gather(const P2Item* items, std::int64_t nitems, const std::int
                         const std::int32_t* pc_off, const std::int64_t* pc_pos, const double* out,
                         double* lvl, std::int64_t n_total, cudaStream_t s);
 
+// --------------------------------------------------------------- gmres.cu
+std::size_t dot_scratch_doubles();
+// *out = a . b (or its square root), fixed-order two-stage reduction
+void launch_dot(const double* a, const double* b, std::int64_t n, double* scratch, double* out, bool sqrt_of,
+                cudaStream_t s);
+// y += c x with c = sign * (*cdev) if cdev else chost
+void launch_axpy(double* y, const double* x, std::int64_t n, const double* cdev, double sign, double chost,
+                 cudaStream_t s);
+void launch_scale_div(double* y, const double* x, std::int64_t n, const double* d, cudaStream_t s);
+void launch_affine(double* w, const double* v, std::int64_t n, double alpha, double beta, cudaStream_t s);
+void launch_sub(double* r, const double* f, const double* w, std::int64_t n, cudaStream_t s);
+// exact dense product (diagonal rule) from the packed Morton-order points,
+// b in original order
+void launch_direct(const double* p4, std::int64_t n, int kernel, double diag, const std::int32_t* perm,
+                   double* b, cudaStream_t s);
+
+// ------------------------------------------------------------------ ie.cpp
+double unit_cell_integral_constant();
+double cell_self_integral(double h);
+void tensor_grid_points(std::int64_t n, double* xyz);
+
 // Build-time near-field scan: coincidence check (and optional store).
 void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cudaStream_t s);
 

@@ -113,7 +113,19 @@ _EXPORTS = [
     "h3d_nccl_get_id", "h3d_dev_attach_nccl", "h3d_dev_matvec_async", "h3d_dev_profile",
     "h3d_dev_profile_read", "h3d_dev_profile_kernels", "h3d_plan_create", "h3d_plan_destroy", "h3d_plan_pairs",
     "h3d_plan_set_ranks", "h3d_plan_set_mode", "h3d_plan_layout", "h3d_plan_array",
+    "h3d_dev_gmres", "h3d_dev_direct_matvec", "h3d_generate_grid_points", "h3d_cell_self_integral",
 ]
+
+
+class _GmresInfo(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int),
+        ("converged", C.c_int),
+        ("history_len", C.c_int),
+        ("reserved", C.c_int),
+        ("solve_ms", C.c_double),
+        ("final_relres", C.c_double),
+    ]
 
 
 def _load():
@@ -148,6 +160,12 @@ def _load():
     L.h3d_plan_array.argtypes = [P, C.c_char_p, C.c_int, P, C.POINTER(C.c_int64)]
     L.h3d_nccl_get_id.argtypes = [P]
     L.h3d_dev_attach_nccl.argtypes = [P, P, C.c_int, C.c_int]
+    L.h3d_dev_gmres.argtypes = [P, P, P, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                C.c_int, P, C.c_int, C.POINTER(_GmresInfo)]
+    L.h3d_dev_direct_matvec.argtypes = [P, P, P, C.c_int]
+    L.h3d_generate_grid_points.argtypes = [C.c_int64, P]
+    L.h3d_cell_self_integral.argtypes = [C.c_double]
+    L.h3d_cell_self_integral.restype = C.c_double
     return L
 
 
@@ -402,6 +420,36 @@ class HMatrixRep:
         _check(_L.h3d_dev_attach_nccl(self._h, C.cast(buf, C.c_void_p), rank, world))
 
 
+    # --- solver -------------------------------------------------------------
+    def gmres(self, rhs, alpha: float = 0.0, beta: float = 1.0,
+              options: Optional["GmresOptions"] = None) -> "GmresResult":
+        """Device GMRES on (alpha I + beta A~) x = rhs (reference solver.cpp:22-125
+        over IEOperator::apply, solver.cpp:199-206). Host vectors, original order."""
+        opt = options or GmresOptions()
+        f = np.ascontiguousarray(rhs, dtype=np.float64)
+        if f.ndim != 1 or len(f) != self.n:
+            raise ValueError("gmres: rhs length != N")
+        x = np.empty(self.n, dtype=np.float64)
+        cap = max(int(opt.max_iter), 1)
+        hist = np.zeros(cap, dtype=np.float64)
+        info = _GmresInfo()
+        _check(_L.h3d_dev_gmres(self._h, _ptr(f), _ptr(x), 0, float(alpha), float(beta),
+                                float(opt.tol), int(opt.restart), int(opt.max_iter), _ptr(hist), cap,
+                                C.byref(info)))
+        return GmresResult(x=x, iterations=info.iterations, converged=bool(info.converged),
+                           residual_history=hist[: min(info.history_len, cap)].copy(),
+                           solve_ms=info.solve_ms, final_relres=info.final_relres)
+
+    def direct_matvec(self, x) -> np.ndarray:
+        """Exact dense b = K x on the device, O(N^2) (reference solver.cpp:247-258)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if x.ndim != 1 or len(x) != self.n:
+            raise ValueError("direct_matvec: vector length != N")
+        b = np.empty(self.n, dtype=np.float64)
+        _check(_L.h3d_dev_direct_matvec(self._h, _ptr(x), _ptr(b), 0))
+        return b
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_char * 128)()
     _check(_L.h3d_nccl_get_id(C.cast(buf, C.c_void_p)))
@@ -425,6 +473,112 @@ def matvec(rep: HMatrixRep, x, timing: Optional[MatvecTiming] = None) -> np.ndar
 
 def stats(rep: HMatrixRep) -> dict:
     return rep.stats()
+
+
+# ---------------------------------------------------------------- IE solver
+@dataclasses.dataclass
+class GmresOptions:
+    """Reference solver.hpp:10-14."""
+
+    tol: float = 1e-10
+    restart: int = 0
+    max_iter: int = 500
+
+
+@dataclasses.dataclass
+class GmresResult:
+    """Reference solver.hpp:16-21 (+ device timing and the true final residual)."""
+
+    x: np.ndarray
+    iterations: int = 0
+    converged: bool = False
+    residual_history: np.ndarray = dataclasses.field(default_factory=lambda: np.zeros(0))
+    solve_ms: float = 0.0
+    final_relres: float = 0.0
+
+
+def generate_grid_points(n: int) -> np.ndarray:
+    """generate_points(TensorGrid, n) (reference kernel.cpp:96-109): cell centres
+    of the side^3 partition of [-1,1]^3 (n must be a perfect cube), z fastest, (n, 3)."""
+    out = np.empty((n, 3), dtype=np.float64)
+    _check(_L.h3d_generate_grid_points(int(n), _ptr(out)))
+    return out
+
+
+def cell_self_integral(h: float) -> float:
+    """Integral of 1/r over a cube of side h about its centre (reference solver.cpp:127-197)."""
+    return float(_L.h3d_cell_self_integral(float(h)))
+
+
+class IEOperator:
+    """d I + w K_offdiag on the grid_n^3 collocation grid (reference solver.hpp:35-53)."""
+
+    def __init__(self, n: int, kernel: KernelSpec, eps: float, variant: str = "hodlr3d",
+                 base: Optional[HmatOptions] = None, device: int = 0):
+        if n < 2:
+            raise ValueError("discretize_ie: n must be >= 2")
+        if kernel.name != "laplace3d":
+            raise ValueError("discretize_ie: unsupported kernel (only laplace3d has the singular "
+                             "cell quadrature wired)")
+        self.grid_n = n
+        self.size = n * n * n
+        h = 2.0 / n
+        self.cell_volume = h * h * h
+        self.diagonal = 1.0 + cell_self_integral(h)
+        self.collocation = generate_grid_points(self.size)
+        opts = dataclasses.replace(base or HmatOptions(), epsilon=eps)
+        self.rep = initialize(self.collocation, kernel, variant, opts, device=device)
+
+    def apply(self, x) -> np.ndarray:
+        """solver.cpp:199-206: d x + w A~ x."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        return self.diagonal * x + self.cell_volume * self.rep.matvec(x)
+
+    def solve(self, f, options: Optional[GmresOptions] = None) -> GmresResult:
+        return self.rep.gmres(f, alpha=self.diagonal, beta=self.cell_volume, options=options)
+
+    def close(self):
+        self.rep.close()
+
+
+def discretize_ie(n: int, kernel: KernelSpec, eps: float, variant: str = "hodlr3d",
+                  base: Optional[HmatOptions] = None, device: int = 0) -> IEOperator:
+    """Reference solver.cpp:218-240."""
+    return IEOperator(n, kernel, eps, variant, base, device)
+
+
+@dataclasses.dataclass
+class IeReport:
+    """Reference solver.hpp:55-65 (solve time in seconds, device-resident GMRES)."""
+
+    variant: str = "hodlr3d"
+    grid_n: int = 0
+    size: int = 0
+    epsilon: float = 0.0
+    iterations: int = 0
+    converged: bool = False
+    solve_seconds: float = 0.0
+    forward_error: float = 0.0
+    seed: int = 0
+
+
+def ie_experiment(n: int, kernel: KernelSpec, eps: float, variant: str = "hodlr3d", seed: int = 0,
+                  base: Optional[HmatOptions] = None,
+                  gmres_opt: Optional[GmresOptions] = None, device: int = 0) -> IeReport:
+    """Manufactured-solution protocol (reference solver.cpp:243-300): sigma from
+    mt19937_64(seed), f = d sigma + w (K sigma) by exact dense row sums on the
+    device, GMRES over the hierarchical operator, relative forward error."""
+    op = discretize_ie(n, kernel, eps, variant, base, device)
+    try:
+        sigma = random_vector(op.size, seed)
+        f = op.diagonal * sigma + op.cell_volume * op.rep.direct_matvec(sigma)
+        sol = op.solve(f, gmres_opt)
+    finally:
+        op.close()
+    err = float(np.sqrt(np.sum((sol.x - sigma) ** 2) / np.sum(sigma * sigma)))
+    return IeReport(variant=variant, grid_n=n, size=op.size, epsilon=eps,
+                    iterations=sol.iterations, converged=sol.converged,
+                    solve_seconds=sol.solve_ms * 1e-3, forward_error=err, seed=seed)
 
 
 # ---------------------------------------------------------------- host planner

@@ -235,6 +235,11 @@ class RefLib:
                                        C.c_int64, _I32, _I32, _D, C.c_int64, C.POINTER(C.c_int)]
         L.h3dref_census.argtypes = [_P, _U64]
         L.h3dref_dense_matvec.argtypes = [_D, C.c_int64, C.c_int, C.c_double, _D, _D]
+        L.h3dref_cell_self_integral.argtypes = [C.c_double]
+        L.h3dref_cell_self_integral.restype = C.c_double
+        L.h3dref_ie_experiment.argtypes = [C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_double,
+                                           C.c_int, C.c_int, C.POINTER(C.c_int),
+                                           C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.h3dref_max_threads.restype = C.c_int
 
     def _check(self, st):
@@ -256,6 +261,17 @@ class RefLib:
         out = np.empty(n, dtype=np.float64)
         self.L.h3dref_random_vector(n, seed, out)
         return out
+
+    def cell_self_integral(self, h: float) -> float:
+        return float(self.L.h3dref_cell_self_integral(float(h)))
+
+    def ie_experiment(self, grid_n: int, eps: float, n_max: int = 216, seed: int = 0,
+                      tol: float = 1e-10, restart: int = 0, max_iter: int = 500) -> dict:
+        """reference solver.cpp:243-300 (HODLR3D, laplace3d)."""
+        it, cv, fe = C.c_int(0), C.c_int(0), C.c_double(0.0)
+        self._check(self.L.h3dref_ie_experiment(grid_n, eps, n_max, seed, tol, restart, max_iter,
+                                                C.byref(it), C.byref(cv), C.byref(fe)))
+        return {"iterations": it.value, "converged": bool(cv.value), "forward_error": fe.value}
 
     def dense_matvec(self, pts, x, kernel="laplace3d", diag=0.0):
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1)
