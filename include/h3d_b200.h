@@ -66,8 +66,9 @@ typedef struct {
    * 1 = auto (default): leaf level evaluated exactly, upper levels split
    *     between streamed factors and matrix-free proxies (pivots + LU, the
    *     reference's own storage, lowrank.cpp:291-327) by a HBM/FP64 cost model;
-   * 2 = explicit per level from level_modes[l] (0 stream, 1 proxy, 2 direct;
-   *     direct only at the leaf level). */
+   * 2 = explicit per level from level_modes[l] (0 stream, 1 proxy, 2 direct,
+   *     3 pair = explicit factors in one fused read per pair; direct only at
+   *     the leaf level, pair ranks <= 256). */
   int mode_policy;
   int level_modes[16];
   int64_t reserved[4];
