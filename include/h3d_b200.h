@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define H3D_B200_ABI_VERSION 1
+#define H3D_B200_ABI_VERSION 2
 
 enum h3d_status {
   H3D_OK = 0,
@@ -42,6 +42,12 @@ enum h3d_status {
 
 /* Kernel ids follow h3d::KernelId (reference kernel.hpp:42). */
 enum h3d_kernel { H3D_LAPLACE3D = 0, H3D_R4 = 1, H3D_HELMHOLTZ_RE = 2 };
+
+/* Block-structure variants, h3d::Variant order (reference octree.hpp:80):
+ * HODLR3D (vertex partners compressed), HODLR (every sibling compressed, weak
+ * admissibility) and H-strong (only well-separated partners compressed; vertex
+ * partners join the dense near field). Lists: octree.cpp:197-260. */
+enum h3d_variant { H3D_HODLR3D = 0, H3D_HODLR = 1, H3D_HSTRONG = 2 };
 
 /* Near-field (dense leaf block) storage; mirrors h3d::DenseMode
  * (reference hmatrix.hpp:12-14): Cached stores the blocks at initialize,
@@ -71,6 +77,7 @@ typedef struct {
    *     the leaf level, pair ranks <= 256). */
   int mode_policy;
   int level_modes[16];
+  int variant;          /* h3d_variant (Variant argument of initialize, hmatrix.hpp:57-58) */
   int64_t reserved[4];
 } h3d_options;
 
@@ -134,9 +141,9 @@ void h3d_default_options(h3d_options* opt);
 int h3d_generate_points(int64_t n, uint64_t seed, double* xyz);
 void h3d_random_vector(int64_t n, uint64_t seed, double* out);
 
-/* Replaces h3d::initialize(PointSet, KernelSpec, Variant::Hodlr3d, HmatOptions)
- * (hmatrix.hpp:57-58 / hmatrix.cpp:52-151): octree + lists + batched ACA on
- * the device. xyz is host AoS (Point3[n]). */
+/* Replaces h3d::initialize(PointSet, KernelSpec, Variant, HmatOptions)
+ * (hmatrix.hpp:57-58 / hmatrix.cpp:52-151): octree + lists (opt->variant) +
+ * batched ACA on the device. xyz is host AoS (Point3[n]). */
 int h3d_dev_create(const double* xyz, int64_t n, const h3d_options* opt, h3d_dev** out);
 void h3d_dev_destroy(h3d_dev* dev);
 
@@ -211,8 +218,8 @@ int h3d_dev_stats(const h3d_dev* dev, h3d_stats* out);
  * perm[n] (permuted position -> original index, Octree::perm, octree.hpp:61);
  * offsets[8^level + 1] (node m = [off[m], off[m+1]), Octree::levels). */
 int h3d_dev_export_tree(const h3d_dev* dev, int32_t* perm, int level, int64_t* offsets);
-/* Interaction list CSR at a level, kind 0 inter / 1 near_edge / 2 near_face
- * (NodeLists, octree.hpp:88-93). ids may be NULL to query *count. */
+/* Interaction list CSR at a level, kind 0 inter / 1 near_edge / 2 near_face /
+ * 3 near_vertex (H-strong only) (NodeLists, octree.hpp:88-93). ids may be NULL to query *count. */
 int h3d_dev_export_list(const h3d_dev* dev, int level, int kind, int32_t* offsets,
                         int32_t* ids, int64_t* count);
 /* Compressed pairs at a level: (X, Y, rank) with X < Y (Morton ids). */
@@ -228,8 +235,8 @@ int h3d_dev_attach_nccl(h3d_dev* dev, const void* id128, int rank, int world);
 /* Host planner (no GPU): the shard ownership, column layout, work items and
  * leaf lists the engine derives from the tree, for CPU verification of the
  * multi-GPU logic. offsets = concat over levels of 8^l + 1 int64; list_off =
- * concat over (level 1..L, kind 0..2) of 8^l + 1 int32; list_ids = concat of
- * the ids; list_counts[3*l + k] = ids per (level, kind); modes = L + 1 ints
+ * concat over (level 1..L, kind 0..3) of 8^l + 1 int32; list_ids = concat of
+ * the ids; list_counts[4*l + k] = ids per (level, kind); modes = L + 1 ints
  * (0 stream, 1 proxy, 2 direct) or NULL. */
 typedef struct h3d_plan h3d_plan;
 int h3d_plan_create(int depth, int64_t n, const int64_t* offsets, const int32_t* list_off,

@@ -468,8 +468,9 @@ struct orc_rep {
   int32_t* perm;
   double *px, *py, *pz;              /* permuted SoA coordinates */
   int64_t* off[ORC_MAX_LEVELS];      /* 8^l + 1 node offsets */
-  int32_t* lst_off[ORC_MAX_LEVELS][3];
-  int32_t* lst_ids[ORC_MAX_LEVELS][3];
+  int variant;                       /* 0 hodlr3d, 1 hodlr, 2 hstrong (octree.hpp:80) */
+  int32_t* lst_off[ORC_MAX_LEVELS][4];  /* kinds: inter, near_edge, near_face, near_vertex */
+  int32_t* lst_ids[ORC_MAX_LEVELS][4];
   lr_level lr[ORC_MAX_LEVELS];
   int32_t *piv_row, *piv_col;
   double* lu;
@@ -568,19 +569,24 @@ static int build_tree(orc_rep* rep, const double* xyz, int64_t n, int n_max, int
   return ORC_OK;
 }
 
-/* build_interaction_lists, variant Hodlr3d (octree.cpp:197-260) */
+/* build_interaction_lists (octree.cpp:197-260). Candidates: the 7 siblings,
+ * plus (hodlr3d / hstrong) the children of the parent's near_edge and
+ * near_face (and near_vertex for hstrong), sorted ascending. hodlr: every
+ * candidate is inter. hodlr3d: ws + vertex -> inter. hstrong: ws -> inter,
+ * vertex -> near_vertex. Edge / face -> near_edge / near_face. */
 static void build_lists(orc_rep* rep) {
   const int L = rep->depth;
-  for (int k = 0; k < 3; ++k) {
+  const int V = rep->variant;
+  for (int k = 0; k < 4; ++k) {
     rep->lst_off[0][k] = (int32_t*)calloc(2, sizeof(int32_t));
     rep->lst_ids[0][k] = (int32_t*)malloc(sizeof(int32_t));
   }
   int32_t cand[8 + 8 * 32];
   for (int l = 1; l <= L; ++l) {
     const int64_t count = nodes_at(l);
-    int64_t cap[3] = {count * 16 + 16, count * 12 + 16, count * 6 + 16};
-    int64_t tot[3] = {0, 0, 0};
-    for (int k = 0; k < 3; ++k) {
+    int64_t cap[4] = {count * 16 + 16, count * 12 + 16, count * 6 + 16, count * 8 + 16};
+    int64_t tot[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 4; ++k) {
       rep->lst_off[l][k] = (int32_t*)malloc(sizeof(int32_t) * (size_t)(count + 1));
       rep->lst_ids[l][k] = (int32_t*)malloc(sizeof(int32_t) * (size_t)cap[k]);
     }
@@ -590,7 +596,8 @@ static void build_lists(orc_rep* rep) {
       for (int64_t s = base; s < base + 8; ++s)
         if (s != m) cand[nc++] = (int32_t)s;
       const int64_t par = m >> 3;
-      for (int k = 1; k <= 2; ++k) { /* parent near_edge, then near_face */
+      const int kmax = V == 1 ? 0 : V == 2 ? 3 : 2;
+      for (int k = 1; k <= kmax; ++k) { /* parent near_edge, near_face[, near_vertex] */
         const int32_t* po = rep->lst_off[l - 1][k];
         const int32_t* pi = rep->lst_ids[l - 1][k];
         for (int32_t e = po[par]; e < po[par + 1]; ++e)
@@ -599,12 +606,15 @@ static void build_lists(orc_rep* rep) {
       qsort(cand, (size_t)nc, sizeof(int32_t), cmp_i32);
       int mx, my, mz;
       morton_decode(m, l, &mx, &my, &mz);
-      for (int k = 0; k < 3; ++k) rep->lst_off[l][k][m] = (int32_t)tot[k];
+      for (int k = 0; k < 4; ++k) rep->lst_off[l][k][m] = (int32_t)tot[k];
       for (int q = 0; q < nc; ++q) {
-        int cx, cy, cz;
-        morton_decode(cand[q], l, &cx, &cy, &cz);
-        const int cls = classify_offset(cx - mx, cy - my, cz - mz);
-        const int k = (cls == 4 || cls == 3) ? 0 : cls == 2 ? 1 : 2; /* self impossible */
+        int k = 0;
+        if (V != 1) {
+          int cx, cy, cz;
+          morton_decode(cand[q], l, &cx, &cy, &cz);
+          const int cls = classify_offset(cx - mx, cy - my, cz - mz); /* self impossible */
+          k = cls == 4 ? 0 : cls == 3 ? (V == 2 ? 3 : 0) : cls == 2 ? 1 : 2;
+        }
         if (tot[k] == cap[k]) {
           cap[k] *= 2;
           rep->lst_ids[l][k] =
@@ -613,7 +623,7 @@ static void build_lists(orc_rep* rep) {
         rep->lst_ids[l][k][tot[k]++] = cand[q];
       }
     }
-    for (int k = 0; k < 3; ++k) rep->lst_off[l][k][count] = (int32_t)tot[k];
+    for (int k = 0; k < 4; ++k) rep->lst_off[l][k][count] = (int32_t)tot[k];
   }
 }
 
@@ -644,7 +654,7 @@ void orc_free(orc_rep* rep) {
   free(rep->pz);
   for (int l = 0; l < ORC_MAX_LEVELS; ++l) {
     free(rep->off[l]);
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < 4; ++k) {
       free(rep->lst_off[l][k]);
       free(rep->lst_ids[l][k]);
     }
@@ -664,7 +674,7 @@ void orc_free(orc_rep* rep) {
 
 /* initialize (hmatrix.cpp:52-151) */
 int orc_initialize(const double* xyz, int64_t n, int kernel_id, double diag, int n_max,
-                   double eps, int depth_cap, int64_t max_rank, orc_rep** out) {
+                   double eps, int depth_cap, int64_t max_rank, int variant, orc_rep** out) {
   *out = NULL;
   if (n == 0) {
     set_err("initialize: empty point set");
@@ -679,6 +689,12 @@ int orc_initialize(const double* xyz, int64_t n, int kernel_id, double diag, int
   rep->diag = diag;
   rep->eps = eps;
   rep->max_rank = max_rank;
+  if (variant < 0 || variant > 2) {
+    orc_free(rep);
+    set_err("unknown variant");
+    return ORC_EINVAL;
+  }
+  rep->variant = variant;
   int st = build_tree(rep, xyz, n, n_max, depth_cap);
   if (st != ORC_OK) {
     orc_free(rep);
@@ -768,7 +784,7 @@ int orc_initialize(const double* xyz, int64_t n, int kernel_id, double diag, int
     free(res);
   }
 
-  /* leaf dense blocks in visit order: self, edge, face (hmatrix.cpp:105-120) */
+  /* leaf dense blocks in visit order: self, edge, face, vertex (hmatrix.cpp:105-120) */
   {
     const int64_t cnt = nodes_at(L);
     const int64_t* off = rep->off[L];
@@ -782,7 +798,7 @@ int orc_initialize(const double* xyz, int64_t n, int kernel_id, double diag, int
           rep->d_source[nd] = (int32_t)m;
         }
         ++nd;
-        for (int k = 1; k <= 2; ++k) {
+        for (int k = 1; k <= 3; ++k) {
           const int32_t* lo = rep->lst_off[L][k];
           const int32_t* li = rep->lst_ids[L][k];
           for (int32_t e = lo[m]; e < lo[m + 1]; ++e) {
@@ -1101,9 +1117,15 @@ void orc_uniform_stream(int64_t n, uint64_t seed, double* out) {
 }
 
 /* Tree and lists only (no ACA): for bit-exact parity at full BASELINE sizes. */
-int orc_tree_lists(const double* xyz, int64_t n, int n_max, int depth_cap, orc_rep** out) {
+int orc_tree_lists(const double* xyz, int64_t n, int n_max, int depth_cap, int variant,
+                   orc_rep** out) {
   *out = NULL;
+  if (variant < 0 || variant > 2) {
+    set_err("unknown variant");
+    return ORC_EINVAL;
+  }
   orc_rep* rep = (orc_rep*)calloc(1, sizeof(orc_rep));
+  rep->variant = variant;
   int st = build_tree(rep, xyz, n, n_max, depth_cap);
   if (st != ORC_OK) {
     orc_free(rep);

@@ -39,9 +39,9 @@ int orc_generate_points(int64_t n, uint64_t seed, double* xyz);
 /* tools/h3d.cpp:135-137: mt19937_64(seed), 2u-1 */
 void orc_random_vector(int64_t n, uint64_t seed, double* out);
 
-/* hmatrix.cpp:52-151 (variant hodlr3d, on-the-fly dense) */
+/* hmatrix.cpp:52-151 (on-the-fly dense); variant 0 hodlr3d, 1 hodlr, 2 hstrong */
 int orc_initialize(const double* xyz, int64_t n, int kernel_id, double diag, int n_max,
-                   double eps, int depth_cap, int64_t max_rank, orc_rep** out);
+                   double eps, int depth_cap, int64_t max_rank, int variant, orc_rep** out);
 void orc_free(orc_rep* rep);
 /* hmatrix.cpp:153-226 */
 int orc_matvec(const orc_rep* rep, const double* x, double* b);
@@ -50,7 +50,7 @@ int orc_depth(const orc_rep* rep);
 void orc_export_perm(const orc_rep* rep, int32_t* perm);
 /* 8^l + 1 offsets: node m covers [off[m], off[m+1]) */
 void orc_export_offsets(const orc_rep* rep, int level, int64_t* off);
-/* kind 0 inter, 1 near_edge, 2 near_face; offsets has 8^l + 1 entries */
+/* kind 0 inter, 1 near_edge, 2 near_face, 3 near_vertex; offsets has 8^l + 1 entries */
 int64_t orc_export_list(const orc_rep* rep, int level, int kind, int32_t* offsets,
                         int32_t* ids);
 int64_t orc_lr_blocks(const orc_rep* rep, int level, int32_t* target, int32_t* source,
@@ -81,7 +81,8 @@ void orc_set_threads(int n);
 /* raw uniform01 stream of mt19937_64(seed) (kernel.hpp:24-26) */
 void orc_uniform_stream(int64_t n, uint64_t seed, double* out);
 /* build_tree + build_interaction_lists only (octree.cpp:76-260), no ACA */
-int orc_tree_lists(const double* xyz, int64_t n, int n_max, int depth_cap, orc_rep** out);
+int orc_tree_lists(const double* xyz, int64_t n, int n_max, int depth_cap, int variant,
+                   orc_rep** out);
 
 #ifdef __cplusplus
 }

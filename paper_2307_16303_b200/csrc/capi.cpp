@@ -241,14 +241,14 @@ int h3d_plan_create(int depth, int64_t n, const int64_t* offsets, const int32_t*
       const int64_t cnt = 1LL << (3 * l);
       off[l].assign(offsets + po, offsets + po + cnt + 1);
       po += cnt + 1;
-      for (int k = 0; k < 3; ++k) {
+      for (int k = 0; k < h3db::kListKinds; ++k) {
         if (l == 0) {
           lists[0].off[k].assign(2, 0);
           continue;
         }
         lists[l].off[k].assign(list_off + lo, list_off + lo + cnt + 1);
         lo += cnt + 1;
-        const int64_t c = list_counts[3 * l + k];
+        const int64_t c = list_counts[h3db::kListKinds * l + k];
         lists[l].ids[k].assign(list_ids + li, list_ids + li + c);
         li += c;
       }

@@ -114,6 +114,8 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   if (n > 0x7fffffffLL) throw InvalidArgument("initialize: N exceeds int32 point indices");
   if (opt.mode_policy < 0 || opt.mode_policy > 2)
     throw InvalidArgument("initialize: mode_policy must be 0, 1 or 2");
+  if (opt.variant < kVariantHodlr3d || opt.variant > kVariantHStrong)
+    throw InvalidArgument("unknown variant (0 hodlr3d, 1 hodlr, 2 hstrong)");
   world_ = opt.shard_world < 1 ? 1 : opt.shard_world;
   rank_ = opt.shard_rank;
   if (!(world_ == 1 || world_ == 2 || world_ == 4 || world_ == 8))
@@ -304,32 +306,34 @@ void Engine::build_tree(const double* xyz) {
 // ---------------------------------------------------------------- lists
 void Engine::build_lists() {
   lists_.assign(L_ + 1, LevelLists{});
-  for (int k = 0; k < 3; ++k) lists_[0].off[k].assign(2, 0);
+  for (int k = 0; k < kListKinds; ++k) lists_[0].off[k].assign(2, 0);
   if (L_ == 0) return;
   const std::int64_t maxcnt = 1LL << (3 * L_);
   const std::size_t tb = scan_temp_bytes(maxcnt);
   DevBuf<unsigned char> tmp;
   tmp.alloc(tb);
   DevBuf<std::int32_t> counts, offs;
-  counts.alloc(3 * (maxcnt + 1));
-  offs.alloc(3 * (maxcnt + 1));
+  counts.alloc(kListKinds * (maxcnt + 1));
+  offs.alloc(kListKinds * (maxcnt + 1));
   for (int l = 1; l <= L_; ++l) {
     const std::int64_t cnt = 1LL << (3 * l);
-    H3D_CUDA_CHECK(cudaMemsetAsync(counts.get(), 0, 3 * (cnt + 1) * 4, stream_));
-    launch_list_counts(l, counts.get(), stream_);
-    for (int k = 0; k < 3; ++k)
+    H3D_CUDA_CHECK(cudaMemsetAsync(counts.get(), 0, kListKinds * (cnt + 1) * 4, stream_));
+    launch_list_counts(l, opt_.variant, counts.get(), stream_);
+    for (int k = 0; k < kListKinds; ++k)
       exclusive_scan_i32(tmp.get(), tb, counts.get() + k * (cnt + 1), offs.get() + k * (cnt + 1), cnt,
                          stream_);
-    std::vector<std::int32_t> hoff(3 * (cnt + 1));
+    std::vector<std::int32_t> hoff(kListKinds * (cnt + 1));
     H3D_CUDA_CHECK(cudaMemcpyAsync(hoff.data(), offs.get(), hoff.size() * 4, cudaMemcpyDeviceToHost, stream_));
     H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    DevBuf<std::int32_t> ids[3];
-    for (int k = 0; k < 3; ++k) {
+    DevBuf<std::int32_t> ids[kListKinds];
+    std::int32_t* idp[kListKinds];
+    for (int k = 0; k < kListKinds; ++k) {
       lists_[l].off[k].assign(hoff.begin() + k * (cnt + 1), hoff.begin() + (k + 1) * (cnt + 1));
       ids[k].alloc(lists_[l].off[k][cnt]);
+      idp[k] = ids[k].get();
     }
-    launch_list_fill(l, offs.get(), ids[0].get(), ids[1].get(), ids[2].get(), stream_);
-    for (int k = 0; k < 3; ++k) {
+    launch_list_fill(l, opt_.variant, offs.get(), idp, stream_);
+    for (int k = 0; k < kListKinds; ++k) {
       lists_[l].ids[k].resize(lists_[l].off[k][cnt]);
       if (!lists_[l].ids[k].empty())
         H3D_CUDA_CHECK(cudaMemcpyAsync(lists_[l].ids[k].data(), ids[k].get(),
@@ -395,6 +399,10 @@ void Engine::run_aca(bool write) {
       const std::int64_t slot_doubles =
           static_cast<std::int64_t>(cap_ws + 1) * (ms + ns) + (ms + ns + 7) / 8 + 2;
       const std::size_t smem = aca_smem_bytes(P.threads, cap_ws);
+      if (smem > 227u * 1024u)
+        throw InvalidArgument("initialize: ACA rank at level " + std::to_string(l) + " exceeds " +
+                              std::to_string(cap_ws / 2) +
+                              " (shared-memory pivot state); raise eps or set max_rank");
       // few huge blocks (top levels): one thread-block cluster per pair so the
       // whole GPU works on them; fixed per level for rank/write determinism
       if (P.cluster == 0) {
@@ -530,7 +538,7 @@ void Engine::choose_modes() {
       if (mx == 0) continue;
       double nsum = mx;
       if (L_ > 0) {
-        for (int k = 1; k <= 2; ++k)
+        for (int k = 1; k < kListKinds; ++k)
           for (std::int32_t e = lst.off[k][x]; e < lst.off[k][x + 1]; ++e)
             nsum += static_cast<double>(node_size(L_, lst.ids[k][e]));
         if (plan_->mode(L_) == kModeDirect)
@@ -1174,7 +1182,7 @@ void Engine::export_tree(std::int32_t* perm, int level, std::int64_t* offsets) c
 
 std::int64_t Engine::export_list(int level, int kind, std::int32_t* offsets,
                                  std::int32_t* ids) const {
-  if (level < 0 || level > L_ || kind < 0 || kind > 2)
+  if (level < 0 || level > L_ || kind < 0 || kind >= kListKinds)
     throw InvalidArgument("export_list: level/kind out of range");
   const auto& o = lists_[level].off[kind];
   const auto& v = lists_[level].ids[kind];

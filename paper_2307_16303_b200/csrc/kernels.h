@@ -39,11 +39,11 @@ void launch_permute_points(const double* xyz, const std::int32_t* perm, std::int
                            double* px, double* py, double* pz, cudaStream_t s);
 
 // --------------------------------------------------------------- lists.cu
-// HODLR3D lists at one level (octree.cpp:197-260): kind 0 inter (vertex +
-// well-separated), 1 near_edge, 2 near_face. counts: 3 x (8^l + 1).
-void launch_list_counts(int level, std::int32_t* counts, cudaStream_t s);
-void launch_list_fill(int level, const std::int32_t* offsets, std::int32_t* ids0,
-                      std::int32_t* ids1, std::int32_t* ids2, cudaStream_t s);
+// Interaction lists at one level (octree.cpp:197-260) for a variant: kind 0
+// inter, 1 near_edge, 2 near_face, 3 near_vertex. counts: kListKinds x (8^l + 1).
+void launch_list_counts(int level, int variant, std::int32_t* counts, cudaStream_t s);
+void launch_list_fill(int level, int variant, const std::int32_t* offsets, std::int32_t* const* ids,
+                      cudaStream_t s);
 // exclusive scan of n int32 into int32 (n+1 outputs, last = total)
 std::size_t scan_temp_bytes(std::int64_t n);
 void exclusive_scan_i32(void* tmp, std::size_t tmp_bytes, const std::int32_t* in,

@@ -2,7 +2,8 @@
 //   build_pairs  <- the per-level ACA job list of initialize (hmatrix.cpp:74-98),
 //                   halved to unordered pairs X < Y (lists swap-symmetric,
 //                   test_octree.cpp:167-181; kernels symmetric, kernel.cpp:7-21)
-//   near lists   <- the dense leaf block list (hmatrix.cpp:105-120): self, edge, face
+//   near lists   <- the dense leaf block list (hmatrix.cpp:105-120): self, edge,
+//                   face, vertex (H-strong)
 //   ownership    <- Morton-subtree analogue of plan_partition (parallel.cpp:34-74)
 #include "planner.h"
 
@@ -482,7 +483,7 @@ void Planner::layout() {
     };
     add(x, true);
     if (L_ > 0) {
-      for (int k = 1; k <= 2; ++k)
+      for (int k = 1; k < kListKinds; ++k)
         for (std::int32_t e = lists_[L_].off[k][x]; e < lists_[L_].off[k][x + 1]; ++e)
           add(lists_[L_].ids[k][e], true);
       if (mode_[L_] == kModeDirect)
@@ -518,7 +519,7 @@ void Planner::layout() {
       cat[(pair ? 2 : 0) + (dense ? 0 : 1)].push_back(static_cast<std::int32_t>(y));
     };
     if (L_ > 0) {
-      for (int k = 1; k <= 2; ++k)
+      for (int k = 1; k < kListKinds; ++k)
         for (std::int32_t e = lists_[L_].off[k][x]; e < lists_[L_].off[k][x + 1]; ++e)
           put(lists_[L_].ids[k][e], true);
       if (mode_[L_] == kModeDirect)

@@ -54,10 +54,18 @@ struct PairDesc {
   std::int32_t m, n, rp, own;  // own: bit 0 = X owned here, bit 1 = Y owned
 };
 
+// Variants, h3d::Variant order (reference octree.hpp:80)
+constexpr int kVariantHodlr3d = 0;
+constexpr int kVariantHodlr = 1;
+constexpr int kVariantHStrong = 2;
+constexpr int kListKinds = 4;
+
 struct LevelLists {
-  // CSR per kind: 0 inter, 1 near_edge, 2 near_face (reference NodeLists)
-  std::vector<std::int32_t> off[3];
-  std::vector<std::int32_t> ids[3];
+  // CSR per kind: 0 inter, 1 near_edge, 2 near_face, 3 near_vertex (reference
+  // NodeLists, octree.hpp:88-93; near_vertex only for H-strong). Kinds 1..3
+  // are the dense leaf blocks (hmatrix.cpp:105-120).
+  std::vector<std::int32_t> off[kListKinds];
+  std::vector<std::int32_t> ids[kListKinds];
 };
 
 struct LevelPairs {

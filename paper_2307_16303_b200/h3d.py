@@ -25,6 +25,7 @@ import numpy as np
 _LIB_PATH = Path(__file__).resolve().parent / "lib" / "libh3d_b200.so"
 
 KERNELS = {"laplace3d": 0, "r4": 1, "helmholtz-re": 2}
+VARIANTS = {"hodlr3d": 0, "hodlr": 1, "hstrong": 2}  # h3d::Variant order (octree.hpp:80)
 NEAR_STORED, NEAR_MATRIX_FREE = 0, 1
 
 
@@ -54,6 +55,7 @@ class _Options(C.Structure):
         ("shard_world", C.c_int),
         ("mode_policy", C.c_int),
         ("level_modes", C.c_int * 16),
+        ("variant", C.c_int),
         ("reserved", C.c_int64 * 4),
     ]
 
@@ -271,7 +273,7 @@ class HMatrixRep:
     """Device-resident HODLR3D representation (reference hmatrix.hpp:37-55)."""
 
     def __init__(self, points, kernel: KernelSpec, options: HmatOptions, device: int = 0,
-                 shard_rank: int = 0, shard_world: int = 1):
+                 shard_rank: int = 0, shard_world: int = 1, variant: str = "hodlr3d"):
         pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
         o = _Options()
         _L.h3d_default_options(C.byref(o))
@@ -294,12 +296,16 @@ class HMatrixRep:
         for l, m in enumerate(options.level_modes):
             if l < 16:
                 o.level_modes[l] = int(m)
+        if variant not in VARIANTS:
+            raise ValueError(f"unknown variant: {variant}")
+        o.variant = VARIANTS[variant]
         h = C.c_void_p()
         self._h = None
         _check(_L.h3d_dev_create(_ptr(pts), len(pts), C.byref(o), C.byref(h)))
         self._h = h
         self.kernel = kernel
         self.options = options
+        self.variant = variant
         self.n = len(pts)
         self.device = device
         self.shard_rank, self.shard_world = shard_rank, shard_world
@@ -397,7 +403,7 @@ class HMatrixRep:
         return o
 
     def list(self, level: int, kind: int):
-        """Interaction list CSR (kind 0 inter, 1 near_edge, 2 near_face)."""
+        """Interaction list CSR (kind 0 inter, 1 near_edge, 2 near_face, 3 near_vertex)."""
         nn = 1 << (3 * level)
         off = np.empty(nn + 1, np.int32)
         cnt = C.c_int64(0)
@@ -459,12 +465,14 @@ def nccl_unique_id() -> bytes:
 def initialize(points, kernel: KernelSpec, variant: str = "hodlr3d",
                options: Optional[HmatOptions] = None, device: int = 0, shard_rank: int = 0,
                shard_world: int = 1) -> HMatrixRep:
-    """Reference hmatrix.hpp:57-58. Only the HODLR3D variant is on the device path."""
-    if variant != "hodlr3d":
-        raise ValueError(f"variant {variant!r} is not on the B200 path (hodlr3d only)")
+    """Reference hmatrix.hpp:57-58; variant "hodlr3d", "hodlr" or "hstrong"
+    (parse_variant, octree.cpp:180-185)."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant: {variant}")
     if len(np.asarray(points).reshape(-1, 3)) == 0:
         raise ValueError("initialize: empty point set")
-    return HMatrixRep(points, kernel, options or HmatOptions(), device, shard_rank, shard_world)
+    return HMatrixRep(points, kernel, options or HmatOptions(), device, shard_rank, shard_world,
+                      variant)
 
 
 def matvec(rep: HMatrixRep, x, timing: Optional[MatvecTiming] = None) -> np.ndarray:
@@ -624,13 +632,16 @@ class Plan:
     def __init__(self, depth, n, offsets, lists, shard_rank=0, shard_world=1, modes=None):
         off = np.ascontiguousarray(np.concatenate([np.asarray(offsets[l], np.int64)
                                                    for l in range(depth + 1)]))
-        lo, li, counts = [], [], np.zeros(3 * (depth + 1), np.int64)
+        lo, li, counts = [], [], np.zeros(4 * (depth + 1), np.int64)
         for l in range(1, depth + 1):
-            for k in range(3):
-                o, ids = lists[l][k]
+            for k in range(4):
+                if k < len(lists[l]):
+                    o, ids = lists[l][k]
+                else:  # no near_vertex kind given: empty (HODLR3D / HODLR)
+                    o, ids = np.zeros((1 << (3 * l)) + 1, np.int32), np.zeros(0, np.int32)
                 lo.append(np.asarray(o, np.int32))
                 li.append(np.asarray(ids, np.int32))
-                counts[3 * l + k] = len(ids)
+                counts[4 * l + k] = len(ids)
         lo = np.ascontiguousarray(np.concatenate(lo) if lo else np.zeros(1, np.int32))
         li = np.ascontiguousarray(np.concatenate(li) if li else np.zeros(1, np.int32))
         md = None if modes is None else np.ascontiguousarray(np.asarray(modes, np.int32))

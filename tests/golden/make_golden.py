@@ -19,8 +19,13 @@ HERE = Path(__file__).resolve().parent
 sys.path.insert(0, str(HERE.parent))
 from oracle_lib import RefLib  # noqa: E402
 
-# name: (N, kernel, n_max, eps, seed)  -- C1 is BASELINE.json configs[0]
+# name: (N, kernel, n_max, eps, seed[, variant])  -- C1 is BASELINE.json configs[0]
 CONFIGS = {
+    # the other two block structures of the reference (octree.cpp:197-260)
+    "hodlr_n3000_laplace_nmax100_eps1e-6": (3000, "laplace3d", 100, 1e-6, 29, "hodlr"),
+    "hodlr_n12000_r4_nmax64_eps1e-8": (12000, "r4", 64, 1e-8, 41, "hodlr"),
+    "hstrong_n3000_helm_nmax100_eps1e-6": (3000, "helmholtz-re", 100, 1e-6, 29, "hstrong"),
+    "hstrong_n20000_laplace_nmax64_eps1e-8": (20000, "laplace3d", 64, 1e-8, 43, "hstrong"),
     "c1_n4096_laplace_nmax64_eps1e-10": (4096, "laplace3d", 64, 1e-10, 1),
     "n3000_r4_nmax100_eps1e-6": (3000, "r4", 100, 1e-6, 29),
     "n3000_helm_nmax100_eps1e-6": (3000, "helmholtz-re", 100, 1e-6, 29),
@@ -29,18 +34,22 @@ CONFIGS = {
 }
 
 
-def main():
+def main(only=()):
     ref = RefLib()
     ref.set_threads(8)
-    for name, (n, kern, n_max, eps, seed) in CONFIGS.items():
+    for name, cfg in CONFIGS.items():
+        if only and name not in only:
+            continue
+        n, kern, n_max, eps, seed = cfg[:5]
+        variant = cfg[5] if len(cfg) > 5 else "hodlr3d"
         pts = ref.generate_points(n, seed)
         x = ref.random_vector(n, seed + 17)
-        rep = ref.initialize(pts, kern, n_max=n_max, eps=eps)
+        rep = ref.initialize(pts, kern, n_max=n_max, eps=eps, variant=variant)
         out = dict(n=n, kernel=kern, n_max=n_max, eps=eps, seed=seed, depth=rep.depth,
-                   perm=rep.perm(), x=x)
+                   perm=rep.perm(), x=x, variant=variant)
         for l in range(rep.depth + 1):
             out[f"off{l}"] = rep.offsets(l)
-            for k, kn in enumerate(["inter", "edge", "face"]):
+            for k, kn in enumerate(["inter", "edge", "face", "vertex"]):
                 o, ids = rep.list(l, k)
                 out[f"{kn}_off{l}"] = o
                 out[f"{kn}_ids{l}"] = ids
@@ -58,4 +67,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]))

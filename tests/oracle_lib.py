@@ -21,6 +21,11 @@ ORACLE_SO = ROOT / "oracle" / "liboracle.so"
 REF_SO = ROOT / "oracle" / "_ref" / "libh3dref.so"
 
 KERNELS = {"laplace3d": 0, "r4": 1, "helmholtz-re": 2}
+VARIANTS = {"hodlr3d": 0, "hodlr": 1, "hstrong": 2}  # h3d::Variant order (octree.hpp:80)
+
+
+def _variant(v) -> int:
+    return VARIANTS[v] if isinstance(v, str) else int(v)
 
 _P = C.c_void_p
 _D = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
@@ -51,7 +56,7 @@ class Oracle:
         L.orc_generate_points.argtypes = [C.c_int64, C.c_uint64, _D]
         L.orc_random_vector.argtypes = [C.c_int64, C.c_uint64, _D]
         L.orc_initialize.argtypes = [_D, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_double,
-                                     C.c_int, C.c_int64, C.POINTER(_P)]
+                                     C.c_int, C.c_int64, C.c_int, C.POINTER(_P)]
         L.orc_free.argtypes = [_P]
         L.orc_matvec.argtypes = [_P, _D, _D]
         L.orc_depth.argtypes = [_P]
@@ -71,7 +76,7 @@ class Oracle:
         L.orc_exact_rows.argtypes = [_D, C.c_int64, C.c_int, C.c_double, _D, _I64, C.c_int64, _D]
         L.orc_set_threads.argtypes = [C.c_int]
         L.orc_uniform_stream.argtypes = [C.c_int64, C.c_uint64, _D]
-        L.orc_tree_lists.argtypes = [_D, C.c_int64, C.c_int, C.c_int, C.POINTER(_P)]
+        L.orc_tree_lists.argtypes = [_D, C.c_int64, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]
 
     def _check(self, st):
         if st != 0:
@@ -82,10 +87,11 @@ class Oracle:
         self.L.orc_uniform_stream(n, seed, out)
         return out
 
-    def tree_lists(self, pts, n_max=216, depth_cap=12) -> "OracleRep":
+    def tree_lists(self, pts, n_max=216, depth_cap=12, variant="hodlr3d") -> "OracleRep":
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1)
         h = _P()
-        self._check(self.L.orc_tree_lists(pts, len(pts) // 3, n_max, depth_cap, C.byref(h)))
+        self._check(self.L.orc_tree_lists(pts, len(pts) // 3, n_max, depth_cap, _variant(variant),
+                                          C.byref(h)))
         return OracleRep(self, h, len(pts) // 3)
 
     def set_threads(self, n: int):
@@ -131,11 +137,11 @@ class Oracle:
         return rp[:k].copy(), cp[:k].copy(), lu[: k * k].reshape(k, k).copy()
 
     def initialize(self, pts, kernel="laplace3d", n_max=216, eps=1e-7, depth_cap=12,
-                   max_rank=0, diag=0.0) -> "OracleRep":
+                   max_rank=0, diag=0.0, variant="hodlr3d") -> "OracleRep":
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1)
         h = _P()
         self._check(self.L.orc_initialize(pts, len(pts) // 3, KERNELS[kernel], diag, n_max, eps,
-                                          depth_cap, max_rank, C.byref(h)))
+                                          depth_cap, max_rank, _variant(variant), C.byref(h)))
         return OracleRep(self, h, len(pts) // 3)
 
 
@@ -298,7 +304,8 @@ class RefLib:
                    max_rank=0, diag=0.0, variant=0, cached=False) -> "RefRep":
         pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1)
         h = _P()
-        self._check(self.L.h3dref_initialize(pts, len(pts) // 3, KERNELS[kernel], diag, variant,
+        self._check(self.L.h3dref_initialize(pts, len(pts) // 3, KERNELS[kernel], diag,
+                                             _variant(variant),
                                              n_max, eps, int(cached), depth_cap, max_rank,
                                              C.byref(h)))
         return RefRep(self, h, len(pts) // 3)

@@ -22,12 +22,12 @@ def kernel_matrix(kind, A, B):
         return np.cos(r) / r
 
 
-def oracle_inputs(oracle, n, seed, n_max, eps, kind):
+def oracle_inputs(oracle, n, seed, n_max, eps, kind, variant="hodlr3d"):
     pts = oracle.generate_points(n, seed)
-    orep = oracle.initialize(pts, kind, n_max=n_max, eps=eps)
+    orep = oracle.initialize(pts, kind, n_max=n_max, eps=eps, variant=variant)
     L = orep.depth
     offsets = [orep.offsets(l) for l in range(L + 1)]
-    lists = [None] + [[orep.list(l, k) for k in range(3)] for l in range(1, L + 1)]
+    lists = [None] + [[orep.list(l, k) for k in range(4)] for l in range(1, L + 1)]
     pairs = {}
     for l in range(1, L + 1):
         t, s, r = orep.lr_blocks(l)
@@ -279,7 +279,7 @@ def symmetric_reference(inp, x, kind, direct_leaf=False, diag=0.0):
             continue
         nbrs = [X]
         if L > 0:
-            for k in (1, 2):
+            for k in (1, 2, 3):
                 o, ids = lists[L][k]
                 nbrs += [int(v) for v in ids[o[X]:o[X + 1]]]
         for Y in nbrs:

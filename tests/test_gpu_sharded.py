@@ -41,3 +41,26 @@ def test_shards_reproduce_single_gpu(h3d, oracle, world, levels):
     assert rows_seen == N and not np.isnan(b).any()
     assert rel(b, b1) <= 1e-12
     assert rel(b, oracle.dense_matvec(pts, x)) <= 10 * opt.epsilon
+
+
+@pytest.mark.parametrize("variant", ["hodlr", "hstrong"])
+@pytest.mark.parametrize("world", [2, 8])
+def test_shards_reproduce_single_gpu_variants(h3d, oracle, world, variant):
+    # test_parallel.cpp:175-187 runs the parallel path on hstrong as well
+    pts = h3d.generate_points(N, SEED)
+    x = h3d.random_vector(N, 9)
+    opt = h3d.HmatOptions(n_max=64, epsilon=1e-7)
+    lap = h3d.make_kernel("laplace3d")
+    ref = h3d.initialize(pts, lap, variant, options=opt)
+    b1 = ref.matvec(x)
+    perm = ref.perm()
+    b = np.full(N, np.nan)
+    for r in range(world):
+        rep = h3d.initialize(pts, lap, variant, options=opt, shard_rank=r, shard_world=world)
+        st = rep.stats()
+        own = perm[st["owned_row_begin"]:st["owned_row_end"]]
+        b[own] = rep.matvec(x)[own]
+        rep.close()
+    assert not np.isnan(b).any()
+    assert rel(b, b1) <= 1e-12
+    assert rel(b, oracle.dense_matvec(pts, x)) <= 10 * opt.epsilon

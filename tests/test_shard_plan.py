@@ -32,12 +32,12 @@ def _free_port():
     return p
 
 
-def _inputs():
+def _inputs(variant="hodlr3d"):
     from oracle_lib import Oracle
     o = Oracle()
     o.set_threads(2)
     from plan_exec import oracle_inputs
-    inp = oracle_inputs(o, N, SEED, NMAX, EPS, KIND)
+    inp = oracle_inputs(o, N, SEED, NMAX, EPS, KIND, variant)
     x = o.random_vector(N, SEED + 17)
     inp["x"] = x
     inp["b_oracle"] = inp["orep"].matvec(x)
@@ -56,14 +56,14 @@ def _run_shard(rank, world, modes, inp, xp_full):
     return simulate(plan, inp, xp_full, KIND)
 
 
-def _worker(rank, world, port, modes, q):
+def _worker(rank, world, port, modes, q, variant="hodlr3d"):
     try:
         import torch
         import torch.distributed as dist
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         dist.init_process_group("gloo", rank=rank, world_size=world)
-        inp = _inputs()
+        inp = _inputs(variant)
         perm = inp["perm"]
         xp = inp["x"][perm]
         from paper_2307_16303_b200.h3d import Plan
@@ -94,11 +94,12 @@ def _worker(rank, world, port, modes, q):
         q.put(("err", traceback.format_exc(), None))
 
 
-def _run_world(world, modes):
+def _run_world(world, modes, variant="hodlr3d"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, modes, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, modes, q, variant))
+             for r in range(world)]
     for p in procs:
         p.start()
     status, payload, sizes = q.get(timeout=600)
@@ -136,6 +137,18 @@ def test_sharded_plan_reproduces_the_oracle(ref_inputs, world, modes_name):
     e_ours = rel(b, ref_inputs["b_exact"])
     e_ref = rel(ref_inputs["b_oracle"], ref_inputs["b_exact"])
     assert e_ours <= 2 * e_ref
+
+
+@pytest.mark.parametrize("variant", ["hodlr", "hstrong"])
+def test_sharded_plan_variants(variant):
+    # the other two block structures (octree.cpp:197-260) through the same
+    # plan: hybrid modes (proxy / stream / direct leaf), world 2 over gloo
+    inp = _inputs(variant)
+    L = inp["L"]
+    assert L == 3
+    b, _ = _run_world(2, [0, 1, 0, 2], variant)
+    assert rel(b, inp["b_sym_direct"]) <= 1e-12
+    assert rel(b, inp["b_oracle"]) <= 10 * EPS
 
 
 def test_shard_ownership_partitions_rows_and_leaves(ref_inputs):
