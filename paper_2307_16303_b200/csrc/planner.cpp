@@ -161,6 +161,9 @@ void Planner::layout() {
   rpad.assign(T, 0);
   rows.assign(T, 0);
   vcols.assign(T, 0);
+  p1a.assign(T, 0);
+  p1b.assign(T, 0);
+  p1c.assign(T, 0);
   center.assign(4 * T, 0.0);
   for (int l = 0; l <= L_; ++l) {
     const std::int64_t cnt = 1LL << (3 * l);
@@ -225,17 +228,30 @@ void Planner::layout() {
       std::int32_t cols = 0;
       bool any = false;
       const std::int64_t g = gid(l, z);
-      // vertex-adjacent partners (Chebyshev distance 1) first
-      for (int pass = 0; pass < 2; ++pass) {
+      // column groups: touching partners (Chebyshev distance 1) first (the
+      // proxy kernels' difference form covers the prefix [0, vcols)); within
+      // each, partners whose phase-1 output is consumed on this shard first.
+      // An owned node's columns against a remote partner feed only phase 2
+      // (that partner's t-vector comes from its ghost pool here), so phase 1
+      // runs over [0, p1a) and [p1b, p1c) only. One shard: one range.
+      const bool oz = owned(l, z);
+      std::int32_t grp_end[4] = {0, 0, 0, 0};
+      for (int pass = 0; pass < 4; ++pass) {
+        const bool want_touch = pass < 2, want_need = (pass & 1) == 0;
         for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
           if (ep[e] < 0) continue;
-          if (vertex_adjacent(z, lid[e]) != (pass == 0)) continue;
+          if (vertex_adjacent(z, lid[e]) != want_touch) continue;
+          if ((!oz || owned(l, lid[e])) != want_need) continue;
           ec[e] = cols;
           cols += P.rank[ep[e]];
           any = true;
         }
-        if (pass == 0) vcols[g] = cols;
+        grp_end[pass] = cols;
       }
+      vcols[g] = grp_end[1];
+      p1a[g] = grp_end[0];
+      p1b[g] = grp_end[1];
+      p1c[g] = grp_end[2];
       const bool stream = mode_[l] == kModeStream;
       const std::int32_t rp = !any || mode_[l] == kModePair
                                   ? 0
@@ -341,24 +357,34 @@ void Planner::layout() {
       if (rp == 0) continue;
       const std::int64_t nr = node_size(l, z);
       const std::int64_t nrc = (nr + chunk - 1) / chunk;
-      const int ncc = (rp + kColChunk - 1) / kColChunk;
       const std::int64_t pbase = ptot;
       if (nrc > 1) {
         ptot += nrc * rp;
         reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rp, static_cast<std::int32_t>(nrc), mode_[l], pbase});
       }
+      // column ranges whose t-vectors are consumed on this shard (see the
+      // column groups above), tile-aligned on stream levels
+      const int al = mode_[l] == kModeStream ? kTileCols : 1;
+      auto down = [&](int v) { return v / al * al; };
+      auto up = [&](int v) { return std::min(rp, (v + al - 1) / al * al); };
+      int rng[2][2] = {{0, up(p1a[g])}, {down(p1b[g]), up(p1c[g])}};
+      if (rng[1][0] <= rng[0][1]) {  // adjacent or overlapping after alignment: merge
+        rng[0][1] = std::max(rng[0][1], rng[1][1]);
+        rng[1][0] = rng[1][1] = 0;
+      }
       for (std::int64_t k = 0; k < nrc; ++k)
-        for (int cc = 0; cc < ncc; ++cc) {
-          P1Item it{};
-          it.node = static_cast<std::int32_t>(g);
-          it.row0 = static_cast<std::int32_t>(k * chunk);
-          it.nrows = static_cast<std::int32_t>(std::min<std::int64_t>(chunk, nr - k * chunk));
-          it.col0 = cc * kColChunk;
-          it.ncols = std::min(kColChunk, rp - cc * kColChunk);
-          it.kind = mode_[l];
-          it.pslot = nrc > 1 ? pbase + k * rp + cc * kColChunk : -1;
-          items.push_back(it);
-        }
+        for (const auto& rg : rng)
+          for (int c0 = rg[0]; c0 < rg[1]; c0 += kColChunk) {
+            P1Item it{};
+            it.node = static_cast<std::int32_t>(g);
+            it.row0 = static_cast<std::int32_t>(k * chunk);
+            it.nrows = static_cast<std::int32_t>(std::min<std::int64_t>(chunk, nr - k * chunk));
+            it.col0 = c0;
+            it.ncols = std::min(kColChunk, rg[1] - c0);
+            it.kind = mode_[l];
+            it.pslot = nrc > 1 ? pbase + k * rp + c0 : -1;
+            items.push_back(it);
+          }
     }
   }
   S.p_doubles = ptot;

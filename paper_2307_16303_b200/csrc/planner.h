@@ -184,6 +184,9 @@ class Planner {
   // close; the rest are at least one box apart (the regenerating kernels
   // use a cancellation-prone r^2 form only there)
   std::vector<std::int32_t> vcols;
+  // phase-1 column ranges per node: [0, p1a) and [p1b, p1c) (columns whose
+  // partner's t-vector is consumed on this shard; all columns on one shard)
+  std::vector<std::int32_t> p1a, p1b, p1c;
   std::vector<double> center;  // 4 per global node: box centre (x, y, z, 0)
   std::vector<std::int32_t> spos;
   // per level, per pair: stream levels: W node base (pair_wx/wy), first column
