@@ -542,6 +542,19 @@ class IEOperator:
         x = np.ascontiguousarray(x, dtype=np.float64)
         return self.diagonal * x + self.cell_volume * self.rep.matvec(x)
 
+    def dense_matrix(self, max_n: int = 24) -> np.ndarray:
+        """Dense assembly for cross-checks, guarded to small grids (reference
+        solver.cpp:208-216; host numpy, not the device path)."""
+        if self.grid_n > max_n:
+            raise ValueError("dense_matrix: grid too large for dense assembly")
+        p = self.collocation
+        d = p[:, None, :] - p[None, :, :]
+        r = np.sqrt(np.einsum("ijk,ijk->ij", d, d))
+        np.fill_diagonal(r, 1.0)
+        a = self.cell_volume / r
+        np.fill_diagonal(a, self.diagonal)
+        return a
+
     def solve(self, f, options: Optional[GmresOptions] = None) -> GmresResult:
         return self.rep.gmres(f, alpha=self.diagonal, beta=self.cell_volume, options=options)
 

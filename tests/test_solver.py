@@ -28,6 +28,14 @@ def test_cell_self_integral_matches_reference_golden():
         assert h3d.cell_self_integral(h) == v, h
 
 
+def test_unit_cell_constant_frozen():
+    # test_solver.cpp:94-102
+    h3d = _pkg()
+    assert abs(h3d.cell_self_integral(1.0) - 2.380077363979) <= 2.380077363979 * 1e-9
+    assert h3d.cell_self_integral(0.5) == pytest.approx(h3d.cell_self_integral(1.0) / 4, rel=1e-15)
+    assert h3d.cell_self_integral(0.125) == pytest.approx(h3d.cell_self_integral(0.25) / 4, rel=1e-15)
+
+
 def test_cell_self_integral_scales_as_h_squared():
     h3d = _pkg()
     c = h3d.cell_self_integral(1.0)
@@ -148,3 +156,76 @@ def test_direct_matvec_vs_oracle(h3d, oracle, kern):
     b = rep.direct_matvec(x)
     want = oracle.dense_matvec(pts, x, kern)
     assert np.linalg.norm(b - want) / np.linalg.norm(want) < 1e-14
+
+
+@pytest.mark.gpu
+def test_gmres_identity_and_diagonal_one_iteration(h3d):
+    # test_solver.cpp:11-35: alpha I (beta = 0) is solved in one iteration
+    pts = h3d.generate_points(500, 3)
+    rep = h3d.initialize(pts, h3d.make_kernel("laplace3d"), options=h3d.HmatOptions(n_max=64))
+    f = h3d.random_vector(500, 4)
+    for alpha in (1.0, 2.5):
+        r = rep.gmres(f, alpha, 0.0)
+        assert r.converged and r.iterations == 1
+        assert np.allclose(r.x, f / alpha, rtol=1e-14, atol=0)
+
+
+@pytest.mark.gpu
+def test_ie_n2_matches_dense_assembly(h3d):
+    # test_solver.cpp:104-133
+    op = h3d.discretize_ie(2, h3d.make_kernel("laplace3d"), 1e-7)
+    try:
+        assert op.size == 8
+        assert op.diagonal == pytest.approx(1.0 + h3d.cell_self_integral(1.0))
+        a = op.dense_matrix()
+        p = op.collocation
+        for i in range(8):
+            for j in range(8):
+                want = op.diagonal if i == j else op.cell_volume / np.linalg.norm(p[i] - p[j])
+                assert a[i, j] == pytest.approx(want, rel=1e-14)
+        x = np.random.default_rng(2).random(8)
+        assert np.allclose(op.apply(x), a @ x, rtol=1e-6)
+    finally:
+        op.close()
+
+
+@pytest.mark.gpu
+def test_ie_hierarchical_apply_vs_dense(h3d):
+    # test_solver.cpp:144-164
+    eps = 1e-7
+    op = h3d.discretize_ie(8, h3d.make_kernel("laplace3d"), eps)
+    try:
+        a = op.dense_matrix()
+        rng = np.random.default_rng(12)
+        for _ in range(3):
+            x = 2 * rng.random(op.size) - 1
+            y, ye = op.apply(x), a @ x
+            assert np.linalg.norm(y - ye) / np.linalg.norm(ye) <= 10 * eps
+    finally:
+        op.close()
+
+
+@pytest.mark.gpu
+def test_ie_manufactured_solution_vs_dense_lu(h3d):
+    # test_solver.cpp:166-190
+    lap = h3d.make_kernel("laplace3d")
+    rep = h3d.ie_experiment(8, lap, 1e-7, seed=99)
+    assert rep.converged and rep.forward_error <= 1e-5
+    op = h3d.discretize_ie(8, lap, 1e-7)
+    try:
+        sigma = h3d.random_vector(op.size, 99)
+        a = op.dense_matrix()
+        sc = np.linalg.solve(a, a @ sigma)
+        dense_err = np.linalg.norm(sc - sigma) / np.linalg.norm(sigma)
+        assert rep.forward_error <= max(10 * dense_err, 1e-5)
+    finally:
+        op.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["hodlr", "hstrong"])
+def test_ie_experiment_other_variants(h3d, variant):
+    # the solver runs over every block structure (solver.cpp:218-240 takes a Variant)
+    r = h3d.ie_experiment(12, h3d.make_kernel("laplace3d"), 1e-7, variant, seed=5,
+                          base=h3d.HmatOptions(n_max=64))
+    assert r.converged and r.forward_error <= 1e-7
