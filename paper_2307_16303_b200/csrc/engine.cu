@@ -144,6 +144,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2p") tune_.p2p = v;
         else if (k == "skip") tune_.skip = v;
         else if (k == "nf") tune_.nf = v;
+        else if (k == "pps") tune_.pps = v;
       }
       pos = end + 1;
     }
@@ -722,7 +723,7 @@ void Engine::upload_plan() {
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
   }
   x_.alloc(n_);
-  xp_.alloc(n_);
+  xp_.alloc(n_ + 2);  // + pad: the pair pass bulk-copies x runs rounded to 16 B
   b_.alloc(n_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
 }
@@ -892,7 +893,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
         pa.xp = xp_.get();
         pa.out = pair_out_.get();
         pa.counter = counters_.get() + 5 + l;
-        launch_pair(pa, sms_, fp ? 1 : 2, stream2_);
+        launch_pair(pa, sms_, tune_.pps > 0 ? tune_.pps : 2, stream2_);
         ++launches;
       }
       launch_pair_gather(pg_items_.get(), n_pg_, rowbeg_.get(), pc_off_.get(), pc_pos_.get(),

@@ -98,7 +98,7 @@ class Engine {
   // results are wrong)
   // ("nf=1": near field forked after p1_proxy instead of after p2_proxy)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1;
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1, pps = 0;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;

@@ -224,7 +224,7 @@ void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std:
                     const std::int32_t* perm, double* b, cudaStream_t s);
 
 // ---------------------------------------------------------------- pair.cu
-constexpr int kPairMaxRp = 256;  // pair levels: ranks above this stay two-phase
+constexpr int kPairMaxRp = 128;  // pair levels: ranks above this stay two-phase
 struct PairArgs {
   const PairDesc* descs = nullptr;
   std::int64_t n = 0;

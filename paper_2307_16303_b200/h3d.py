@@ -22,7 +22,9 @@ from typing import Optional
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libh3d_b200.so"
+# H3D_LIB_PATH: developer override (tuning builds of the same library)
+_LIB_PATH = Path(os.environ.get("H3D_LIB_PATH") or
+                 Path(__file__).resolve().parent / "lib" / "libh3d_b200.so")
 
 KERNELS = {"laplace3d": 0, "r4": 1, "helmholtz-re": 2}
 VARIANTS = {"hodlr3d": 0, "hodlr": 1, "hstrong": 2}  # h3d::Variant order (octree.hpp:80)
