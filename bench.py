@@ -394,7 +394,7 @@ def main():
         "config": {
             "workload": cfg["desc"],
             "representation": {"policy": args.policy,
-                               "level_modes": {str(l): ["stream", "proxy", "direct", "pair"][m]
+                               "level_modes": {str(l): ["stream", "proxy", "direct", "pair", "fused"][m]
                                                for l, m in enumerate(st["level_modes"]) if l > 0},
                                "note": "one ACA per unordered admissible pair; stream = explicit "
                                        "factors in HBM, proxy = pivots+LU regenerated in FP64, "

@@ -73,6 +73,7 @@ typedef struct {
    *     between streamed factors and matrix-free proxies (pivots + LU, the
    *     reference's own storage, lowrank.cpp:291-327) by a HBM/FP64 cost model;
    * 2 = explicit per level from level_modes[l] (0 stream, 1 proxy, 2 direct,
+   *     4 fused proxy pass (pair-major, each regenerated entry evaluated once),
    *     3 pair = explicit factors in one fused read per pair; direct only at
    *     the leaf level, pair ranks <= 256). */
   int mode_policy;
@@ -178,6 +179,7 @@ typedef enum {
   H3D_K_NEAR,          /* near field + direct leaf blocks (FP64) */
   H3D_K_COMBINE,       /* sum of the per-level partials, un-permute */
   H3D_K_PAIR,          /* pair levels: fused one-read pass + per-node gather (HBM) */
+  H3D_K_FUSED,         /* fused levels: one evaluation per entry, both orientations (FP64) */
   H3D_K_COUNT
 } h3d_kernel_slot;
 int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launches, double* start_sum,

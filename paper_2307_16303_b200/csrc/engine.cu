@@ -177,8 +177,8 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   if (opt_.mode_policy == 2) {
     for (int l = 1; l <= L_ && l < 16; ++l) {
       const int m = opt_.level_modes[l];
-      if (m < 0 || m > 3)
-        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2 or 3");
+      if (m < 0 || m > kModeLast)
+        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2, 3 or 4");
       if (m == kModeDirect && l != L_)
         throw InvalidArgument("initialize: direct mode is only valid at the leaf level");
       modes_[l] = m;
@@ -200,6 +200,25 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     int max_r = 0;
     for (const auto& sg : plan_->proxy_segs) max_r = std::max(max_r, sg.r);
     launch_lu_invert(segs_all_.get(), n_segs_all_, lu_.get(), lu_total_, max_r, stream_);
+  }
+  if (!plan_->fused_descs.empty()) {
+    // triangular inverses of the fused pairs' pivot LUs (one side-0 segment each)
+    std::vector<ProxySeg> segs;
+    int max_r = 0;
+    for (const auto& d : plan_->fused_descs) {
+      ProxySeg sg{};
+      sg.lu_off = d.lu_off;
+      sg.piv_off = d.piv_off;
+      sg.r = d.r;
+      sg.side = 0;
+      segs.push_back(sg);
+      max_r = std::max(max_r, d.r);
+    }
+    DevBuf<ProxySeg> d_segs;
+    d_segs.upload(segs, stream_);
+    launch_lu_invert(d_segs.get(), static_cast<std::int64_t>(segs.size()), lu_.get(), lu_total_, max_r,
+                     stream_);
+    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   }
   near_scan();
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -456,7 +475,7 @@ void Engine::run_aca(bool write) {
         a.cx = d_cx.get();
         a.cy = d_cy.get();
       }
-      if (write && mode == kModeProxy) {
+      if (write && (mode == kModeProxy || mode == kModeFused)) {
         a.piv = piv_.get();
         a.lu = lu_.get();
         a.piv_off = d_po.get();
@@ -506,6 +525,20 @@ void Engine::choose_modes() {
         if (!rk.empty() && *std::max_element(rk.begin(), rk.end()) > kPairMaxRp)
           throw InvalidArgument("initialize: level " + std::to_string(l) + " has ranks above " +
                                 std::to_string(kPairMaxRp) + "; use stream mode there");
+        continue;
+      }
+      if (plan_->mode(l) == kModeFused) {
+        const auto& P = plan_->pairs(l);
+        for (std::size_t p = 0; p < P.X.size(); ++p) {
+          if (P.rank[p] > kFusedMaxRank)
+            throw InvalidArgument("initialize: level " + std::to_string(l) + " has ranks above " +
+                                  std::to_string(kFusedMaxRank) + "; use proxy or stream mode there");
+          const std::int64_t m = node_size(l, P.X[p]), n = node_size(l, P.Y[p]);
+          if (std::max(m, n) > fused_max_node())
+            throw InvalidArgument("initialize: level " + std::to_string(l) +
+                                  " has nodes with more points than the fused pass holds (" +
+                                  std::to_string(fused_max_node()) + "); use proxy or stream mode there");
+        }
         continue;
       }
       if (plan_->mode(l) != kModeProxy) continue;
@@ -709,6 +742,12 @@ void Engine::upload_plan() {
   // pair levels: descriptors, output runs, gather items, one counter per level
   pair_descs_.upload(P.pair_descs.empty() ? std::vector<PairDesc>{PairDesc{}} : P.pair_descs, stream_);
   pd_level_ = P.pd_level;
+  fused_descs_.upload(P.fused_descs.empty() ? std::vector<FusedDesc>{FusedDesc{}} : P.fused_descs, stream_);
+  fd_level_ = P.fd_level;
+  pg_level_ = P.pg_level;
+  // gather items per lane: pair levels on the HBM lane, fused levels on the
+  // FP64 lane (each range contiguous: levels of one kind are gathered together
+  // only when they are adjacent; otherwise per level, see enqueue)
   pc_off_.upload(P.pc_off, stream_);
   pc_pos_.upload(P.pc_pos.empty() ? std::vector<std::int64_t>{0} : P.pc_pos, stream_);
   pg_items_.upload(P.pg_items.empty() ? std::vector<P2Item>{P2Item{}} : P.pg_items, stream_);
@@ -871,7 +910,19 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   const bool parts = n_lvl_ > 0 || sym_near_;  // near pass writes partials, combine sums them
   const bool pair_lv = pd_level_.size() > 1 && pd_level_.back() > 0;
   const bool hbm = n_p1s_ > 0 || n_p2s_ > 0 || pair_lv;
-  const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0;
+  const bool fused_lv = fd_level_.size() > 1 && fd_level_.back() > 0;
+  const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0 || fused_lv;
+  // per-level gather of pair-major outputs into the level partials
+  auto gather_levels = [&](int mode, cudaStream_t st) {
+    for (int l = 1; l <= L_; ++l) {
+      if (P.mode(l) != mode) continue;
+      const std::int64_t g0 = pg_level_[l], g1 = pg_level_[l + 1];
+      if (g1 <= g0) continue;
+      launch_pair_gather(pg_items_.get() + g0, g1 - g0, rowbeg_.get(), pc_off_.get(), pc_pos_.get(),
+                         pair_out_.get(), lvl_part_.get(), n_, st);
+      ++launches;
+    }
+  };
   H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, (5 + L_ + 1) * sizeof(unsigned), s));
   Phase2Args a2 = phase2_args(bout);
   a2.counter = counters_.get() + 2;
@@ -896,9 +947,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
         launch_pair(pa, sms_, tune_.pps > 0 ? tune_.pps : 2, stream2_);
         ++launches;
       }
-      launch_pair_gather(pg_items_.get(), n_pg_, rowbeg_.get(), pc_off_.get(), pc_pos_.get(),
-                         pair_out_.get(), lvl_part_.get(), n_, stream2_);
-      launches += n_pg_ > 0;
+      gather_levels(kModePair, stream2_);
       ke(H3D_K_PAIR, stream2_);
     }
     if (n_p1s_ > 0) {
@@ -982,6 +1031,21 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // blocks (one persistent FP64 kernel resident at a time next to the HBM
   // lane's bulk-copy CTA)
   if (has_p2) {
+    if (fused_lv) {
+      kb(H3D_K_FUSED, stream4_);
+      FusedArgs fa;
+      fa.descs = fused_descs_.get();
+      fa.n = fd_level_.back();
+      fa.p4 = p4_.get();
+      fa.piv = piv_.get();
+      fa.lu = lu_.get();
+      fa.lu_total = lu_total_;
+      fa.out = pair_out_.get();
+      if (run(H3D_K_FUSED)) launch_fused(fa, opt_.kernel_id, sms_, stream4_);
+      ++launches;
+      gather_levels(kModeFused, stream4_);
+      ke(H3D_K_FUSED, stream4_);
+    }
     if (n_p2_ > 0) {
       kb(H3D_K_P2_PROXY, stream4_);
       if (run(H3D_K_P2_PROXY)) launch_p2_proxy(a2, sms_, hbm ? tune_.p2p : 8, stream4_);

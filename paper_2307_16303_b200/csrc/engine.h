@@ -146,6 +146,9 @@ class Engine {
   DevBuf<StreamDesc> p1s_desc_, p2s_desc_;
   DevBuf<PairDesc> pair_descs_;          // pair levels (kModePair)
   std::vector<std::int64_t> pd_level_;   // descriptor range per level
+  DevBuf<FusedDesc> fused_descs_;        // fused levels (kModeFused)
+  std::vector<std::int64_t> fd_level_, pg_level_;
+  std::int64_t pg_pair_[2] = {0, 0}, pg_fused_[2] = {0, 0};  // gather item ranges per lane
   DevBuf<std::int32_t> pc_off_;
   DevBuf<std::int64_t> pc_pos_;
   DevBuf<P2Item> pg_items_;

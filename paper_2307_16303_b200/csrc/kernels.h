@@ -240,6 +240,20 @@ void launch_pair_gather(const P2Item* items, std::int64_t nitems, const std::int
                         const std::int32_t* pc_off, const std::int64_t* pc_pos, const double* out,
                         double* lvl, std::int64_t n_total, cudaStream_t s);
 
+// --------------------------------------------------------------- fused.cu
+constexpr int kFusedMaxRank = 128;  // fused levels: ranks above this stay two-phase
+struct FusedArgs {
+  const FusedDesc* descs = nullptr;
+  std::int64_t n = 0;
+  const double* p4 = nullptr;  // permuted (x, y, z, x-value)
+  const std::int32_t* piv = nullptr;
+  const double* lu = nullptr;  // triangular inverses (lu_invert_kernel)
+  std::int64_t lu_total = 0;
+  double* out = nullptr;       // pair-output buffer
+};
+int fused_max_node();  // points per node of a fused pair
+void launch_fused(const FusedArgs& a, int kernel, int sms, cudaStream_t s);
+
 // --------------------------------------------------------------- gmres.cu
 std::size_t dot_scratch_doubles();
 // *out = a . b (or its square root), fixed-order two-stage reduction

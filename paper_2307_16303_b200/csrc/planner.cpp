@@ -54,7 +54,7 @@ Planner::Planner(int depth, std::int64_t n, std::vector<std::vector<std::int64_t
   if (rank_ < 0 || rank_ >= world_) throw std::invalid_argument("planner: shard_rank out of range");
   if (static_cast<int>(mode_.size()) != L_ + 1) mode_.assign(L_ + 1, kModeStream);
   for (int l = 1; l <= L_; ++l) {
-    if (mode_[l] < 0 || mode_[l] > kModePair) throw std::invalid_argument("planner: bad level mode");
+    if (mode_[l] < 0 || mode_[l] > kModeLast) throw std::invalid_argument("planner: bad level mode");
     if (mode_[l] == kModeDirect && l != L_)
       throw std::invalid_argument("planner: direct mode is only valid at the leaf level");
   }
@@ -208,7 +208,7 @@ void Planner::layout() {
       S.ref_float_count += 2ull * static_cast<std::uint64_t>(r * r);
       S.ref_int_count += 4ull * static_cast<std::uint64_t>(r);
     }
-    if (mode_[l] == kModeProxy) {
+    if (mode_[l] == kModeProxy || mode_[l] == kModeFused) {
       pair_piv[l].resize(P.X.size());
       pair_lu[l].resize(P.X.size());
       for (std::size_t p = 0; p < P.X.size(); ++p) {
@@ -216,7 +216,7 @@ void Planner::layout() {
         pair_piv[l][p] = S.piv_total;
         pair_lu[l][p] = S.lu_total;
         S.piv_total += 2 * r;
-        S.lu_total += r * r;
+        S.lu_total += r * r + (r & 1);  // even: 16-B aligned slots (bulk-copied by fused.cu)
       }
     }
     const auto& off = lists_[l].off[0];
@@ -253,7 +253,7 @@ void Planner::layout() {
       p1b[g] = grp_end[1];
       p1c[g] = grp_end[2];
       const bool stream = mode_[l] == kModeStream;
-      const std::int32_t rp = !any || mode_[l] == kModePair
+      const std::int32_t rp = !any || mode_[l] == kModePair || mode_[l] == kModeFused
                                   ? 0
                                   : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols
                                            : cols + (cols & 1);
@@ -308,7 +308,8 @@ void Planner::layout() {
   spos.assign(std::max<std::int64_t>(S.s_doubles, 1), -1);
   proxy_segs.clear();
   for (int l = 1; l <= L_; ++l) {
-    if (mode_[l] == kModePair) continue;  // no column layout: t-vectors stay in the fused pass
+    // no column layout: t-vectors stay inside the pair-major passes
+    if (mode_[l] == kModePair || mode_[l] == kModeFused) continue;
     const std::int64_t cnt = 1LL << (3 * l);
     const auto& off = lists_[l].off[0];
     const auto& ids = lists_[l].ids[0];
@@ -348,7 +349,7 @@ void Planner::layout() {
   reds.clear();
   std::int64_t ptot = 0;
   for (int l = 1; l <= L_; ++l) {
-    if (mode_[l] == kModeDirect || mode_[l] == kModePair) continue;
+    if (mode_[l] == kModeDirect || mode_[l] == kModePair || mode_[l] == kModeFused) continue;
     const std::int64_t cnt = 1LL << (3 * l);
     const std::int64_t chunk = mode_[l] == kModeStream ? kRowChunk : kSrcChunk;
     for (std::int64_t z = 0; z < cnt; ++z) {
@@ -396,6 +397,9 @@ void Planner::layout() {
   pg_items.clear();
   pair_descs.clear();
   pd_level.assign(L_ + 2, 0);
+  fused_descs.clear();
+  fd_level.assign(L_ + 2, 0);
+  pg_level.assign(L_ + 2, 0);
   pc_off.assign(T + 1, 0);
   pc_pos.clear();
   pair_out_total = 0;
@@ -405,6 +409,34 @@ void Planner::layout() {
     std::vector<std::vector<std::int64_t>> runs(T);
     for (int l = 1; l <= L_; ++l) {
       pd_level[l] = static_cast<std::int64_t>(pair_descs.size());
+      fd_level[l] = static_cast<std::int64_t>(fused_descs.size());
+      if (mode_[l] == kModeFused) {
+        const auto& P = pairs_[l];
+        for (std::size_t p = 0; p < P.X.size(); ++p) {
+          const bool ox = owned(l, P.X[p]), oy = owned(l, P.Y[p]);
+          if (!ox && !oy) continue;
+          FusedDesc d{};
+          d.piv_off = pair_piv[l][p];
+          d.lu_off = pair_lu[l][p];
+          d.xrow = off_[l][P.X[p]];
+          d.yrow = off_[l][P.Y[p]];
+          d.m = static_cast<std::int32_t>(node_size(l, P.X[p]));
+          d.n = static_cast<std::int32_t>(node_size(l, P.Y[p]));
+          d.r = P.rank[p];
+          d.own = (ox ? 1 : 0) | (oy ? 2 : 0);
+          d.touch = vertex_adjacent(P.X[p], P.Y[p]) ? 1 : 0;
+          const std::int64_t gx = gid(l, P.X[p]), gy = gid(l, P.Y[p]);
+          d.cx = 0.5 * (center[4 * gx] + center[4 * gy]);
+          d.cy = 0.5 * (center[4 * gx + 1] + center[4 * gy + 1]);
+          d.cz = 0.5 * (center[4 * gx + 2] + center[4 * gy + 2]);
+          d.out = pair_out_total;
+          if (ox) runs[gx].push_back(d.out);
+          if (oy) runs[gy].push_back(d.out + d.m);
+          pair_out_total += d.m + d.n;
+          fused_descs.push_back(d);
+        }
+        continue;
+      }
       if (mode_[l] != kModePair) continue;
       const auto& P = pairs_[l];
       for (std::size_t p = 0; p < P.X.size(); ++p) {
@@ -426,6 +458,7 @@ void Planner::layout() {
       }
     }
     pd_level[L_ + 1] = static_cast<std::int64_t>(pair_descs.size());
+    fd_level[L_ + 1] = static_cast<std::int64_t>(fused_descs.size());
     for (std::int64_t g = 0; g < T; ++g) {
       pc_off[g] = static_cast<std::int32_t>(pc_pos.size());
       pc_pos.insert(pc_pos.end(), runs[g].begin(), runs[g].end());
@@ -433,8 +466,9 @@ void Planner::layout() {
     pc_off[T] = static_cast<std::int32_t>(pc_pos.size());
   }
   for (int l = 1; l <= L_; ++l) {
+    pg_level[l] = static_cast<std::int64_t>(pg_items.size());
     if (mode_[l] == kModeDirect) continue;
-    if (mode_[l] == kModePair) {
+    if (mode_[l] == kModePair || mode_[l] == kModeFused) {
       // gather the pair outputs of every owned node into the level's partial
       const std::int64_t cnt = 1LL << (3 * l);
       int slot = -1;
@@ -469,6 +503,7 @@ void Planner::layout() {
                              static_cast<std::int32_t>(std::min<std::int64_t>(per, nr - r0)), slot});
     }
   }
+  pg_level[L_ + 1] = static_cast<std::int64_t>(pg_items.size());
 
   // leaf plan: owned leaves; near lists = self, near_edge, near_face (the
   // reference's dense blocks), plus the leaf-level admissible partners when

@@ -42,6 +42,23 @@ enum LevelMode : int {
   kModeDirect = 2,  // exact dense evaluation (leaf level only): 2 m n evaluations per pair
   kModePair = 3,    // explicit factors, pair-major: one fused pass per pair reads U and V
                     //   once (8 r(m+n) B), both products through a per-pair output buffer
+  kModeFused = 4,   // matrix-free like kModeProxy, pair-major: r(m+n) kernel evaluations per
+                    //   pair, each entry kept in shared memory for both orientations
+};
+constexpr int kModeLast = kModeFused;
+
+// Fused proxy pass (kModeFused levels, fused.cu): pivots sigma (row, in X) at
+// piv_off, tau (column, in Y) at piv_off + r; inverses at lu_off (row-major)
+// and lu_off + lu_total (column-major); outputs like PairDesc.
+struct FusedDesc {
+  std::int64_t piv_off, lu_off;
+  std::int64_t xrow, yrow;
+  std::int64_t out;
+  std::int32_t m, n, r, own;
+  std::int32_t touch;  // 1: the boxes touch (difference form of r^2)
+  std::int32_t pad;
+  double cx, cy, cz;   // pair centre (midpoint of the two box centres)
+  double pad2;
 };
 
 // Fused pair pass (kModePair levels): F = [U; V] ((m + n) x rp, row-major,
@@ -156,7 +173,7 @@ class Planner {
   void set_mode(int l, int m) {
     if (mode_[l] == kModeDirect || m == kModeDirect)
       throw std::invalid_argument("planner: direct mode is fixed at construction");
-    if (m < 0 || m > kModePair) throw std::invalid_argument("planner: bad level mode");
+    if (m < 0 || m > kModeLast) throw std::invalid_argument("planner: bad level mode");
     mode_[l] = m;
   }
   bool owned(int level, std::int64_t m) const;
@@ -205,6 +222,11 @@ class Planner {
   // level's partial by pg_items (owned nodes, <= 256 rows each)
   std::vector<PairDesc> pair_descs;
   std::vector<std::int64_t> pd_level;
+  // fused levels: one descriptor per pair with an owned side (grouped by
+  // level, fd_level[l] .. fd_level[l + 1]); outputs share pair_out / pc_* /
+  // pg_items; pg_level[l] .. pg_level[l + 1] = the level's gather items
+  std::vector<FusedDesc> fused_descs;
+  std::vector<std::int64_t> fd_level, pg_level;
   std::vector<std::int32_t> pc_off;
   std::vector<std::int64_t> pc_pos;
   std::vector<P2Item> pg_items;

@@ -607,7 +607,7 @@ def ie_experiment(n: int, kernel: KernelSpec, eps: float, variant: str = "hodlr3
 # ---------------------------------------------------------------- host planner
 # h3d_kernel_slot order (include/h3d_b200.h)
 KERNEL_SLOTS = ("gather", "p1_stream", "red_stream", "p2_stream", "p1_proxy", "red_proxy", "solve",
-                "p2_proxy", "near", "combine", "pair")
+                "p2_proxy", "near", "combine", "pair", "fused")
 
 _PLAN_DTYPES = {
     "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
