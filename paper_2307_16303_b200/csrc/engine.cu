@@ -856,9 +856,10 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     }
   };
   if (ev) cudaEventRecord(ev[0], s);
-  if (world_ == 1 || nccl_comm_ == nullptr) {
-    // single GPU, or a shard without a communicator: x is replicated (every
-    // rank holds all of it), gather it all locally
+  if (nccl_comm_ == nullptr) {
+    // no communicator (one GPU, or a shard built on replicated x): gather
+    // all of x locally. With one attached (any world size, including 1 for
+    // tests/test_gpu_sharded.py) the exchange below runs.
     kb(H3D_K_GATHER, s);
     launch_gather(xin, perm_.get(), n_, xp_.get(), p4_.get(), s);
     ke(H3D_K_GATHER, s);
