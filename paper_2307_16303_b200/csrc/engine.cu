@@ -145,6 +145,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "skip") tune_.skip = v;
         else if (k == "nf") tune_.nf = v;
         else if (k == "pps") tune_.pps = v;
+        else if (k == "graphs") tune_.graphs = v;
       }
       pos = end + 1;
     }
@@ -226,6 +227,8 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
 }
 
 Engine::~Engine() {
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   for (auto e : prof_ev_)
     if (e) cudaEventDestroy(e);
   if (nccl_comm_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
@@ -756,7 +759,6 @@ void Engine::upload_plan() {
   counters_.alloc(5 + L_ + 1);
   sync_flag_.alloc(1);
   H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), stream_));
-  epoch_ = 0;
   if (opt_.near_mode == H3D_NEAR_STORED) {
     nf_off_.upload(P.nf_off, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
@@ -925,6 +927,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     }
   };
   H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, (5 + L_ + 1) * sizeof(unsigned), s));
+  H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), s));
   Phase2Args a2 = phase2_args(bout);
   a2.counter = counters_.get() + 2;
   a2.counter2 = counters_.get() + 3;
@@ -1014,11 +1017,10 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // (0.5 ms alone vs 6-10 ms beside it), and they gate the FP64 lane.
   if (hbm) {
     if (n_segs_solve_ > 0 && has_p2 && n_p2s_ > 0) {
-      ++epoch_;
-      launch_set_flag(sync_flag_.get(), epoch_, stream4_);
+      launch_set_flag(sync_flag_.get(), 1u, stream4_);
       ++launches;
       a2.wait_flag = sync_flag_.get();
-      a2.wait_value = epoch_;
+      a2.wait_value = 1u;
     }
     if (has_p2 && n_p2s_ > 0) {
       kb(H3D_K_P2_STREAM, stream2_);
@@ -1086,7 +1088,9 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
     xin = x_.get();
   }
   double* bout = host ? b_.get() : b;
-  const std::int64_t launches = enqueue(xin, bout, stream_, ev_ + 1, nullptr);
+  // with a timing breakdown requested the kernels run eagerly (per-phase
+  // events), else through the graph cache
+  const std::int64_t launches = t ? enqueue(xin, bout, stream_, ev_ + 1, nullptr) : run_graph(xin, bout, stream_);
   if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
   cudaEventRecord(ev_[5], stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -1108,8 +1112,54 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
   }
 }
 
+// Replay of the captured matvec for (x, b): the first call runs eagerly (it
+// also sets the kernels' one-time attributes), the second captures the whole
+// two-lane enqueue on the engine's stream (fork / join through events become
+// graph edges) and every later call is one cudaGraphLaunch on the caller's
+// stream. Not used with a communicator attached, with profiling on, or with
+// H3D_TUNE graphs=0.
+std::int64_t Engine::run_graph(const double* x, double* b, cudaStream_t s) {
+  if (!tune_.graphs || nccl_comm_ != nullptr) return enqueue(x, b, s, nullptr, nullptr);
+  GraphEntry* e = nullptr;
+  for (auto& g : graphs_)
+    if (g.x == x && g.b == b) e = &g;
+  if (e == nullptr) {
+    if (graphs_.size() >= 8) {
+      if (graphs_.front().exec) cudaGraphExecDestroy(graphs_.front().exec);
+      graphs_.erase(graphs_.begin());
+    }
+    graphs_.push_back(GraphEntry{x, b, nullptr, 0, 0});
+    e = &graphs_.back();
+  }
+  if (e->exec == nullptr) {
+    if (e->seen++ == 0) return enqueue(x, b, s, nullptr, nullptr);
+    H3D_CUDA_CHECK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeRelaxed));
+    std::int64_t launches = 0;
+    try {
+      launches = enqueue(x, b, stream_, nullptr, nullptr);
+    } catch (...) {
+      cudaGraph_t g = nullptr;
+      cudaStreamEndCapture(stream_, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    cudaGraph_t g = nullptr;
+    H3D_CUDA_CHECK(cudaStreamEndCapture(stream_, &g));
+    const cudaError_t err = cudaGraphInstantiate(&e->exec, g, 0);
+    cudaGraphDestroy(g);
+    H3D_CUDA_CHECK(err);
+    e->launches = launches;
+  }
+  H3D_CUDA_CHECK(cudaGraphLaunch(e->exec, s));
+  return e->launches;
+}
+
 void Engine::matvec_async(const double* x, double* b, cudaStream_t s) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  if (!prof_on_) {
+    prof_launches_ += run_graph(x, b, s);
+    return;
+  }
   cudaEvent_t* ev = nullptr;
   std::uint32_t* mask = nullptr;
   if (prof_on_) {

@@ -98,7 +98,7 @@ class Engine {
   // results are wrong)
   // ("nf=1": near field forked after p1_proxy instead of after p2_proxy)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1, pps = 0;
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1, pps = 0, graphs = 1;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
@@ -157,8 +157,18 @@ class Engine {
   std::int64_t n_p2_ = 0, n_p2s_ = 0;
   int n_lvl_ = 0;
   DevBuf<double> lvl_part_;  // [n_lvl_ x N] phase-2 per-level partials
-  DevBuf<unsigned> sync_flag_;  // solves-done epoch (FP64 lane -> HBM lane)
-  unsigned epoch_ = 0;
+  DevBuf<unsigned> sync_flag_;  // solves done (FP64 lane -> HBM lane): reset per matvec, set to 1
+  // CUDA graphs of the whole matvec (both lanes, fork/join), one per (x, b)
+  // pair seen twice; replayed on the caller's stream
+  struct GraphEntry {
+    const double* x = nullptr;
+    double* b = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    std::int64_t launches = 0;
+    int seen = 0;
+  };
+  std::vector<GraphEntry> graphs_;
+  std::int64_t run_graph(const double* x, double* b, cudaStream_t s);
   DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy]
   // matvec lanes (priorities: the HBM lane and the FP64 critical chain above
   // the near field, which fills whatever the two leave idle)
