@@ -311,6 +311,9 @@ int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, in
     else if (nm == "in_pos") put(P.in_pos, out, count);
     else if (nm == "pair_descs") put(P.pair_descs, out, count);
     else if (nm == "pd_level") put(P.pd_level, out, count);
+    else if (nm == "fused_descs") put(P.fused_descs, out, count);
+    else if (nm == "fd_level") put(P.fd_level, out, count);
+    else if (nm == "pg_level") put(P.pg_level, out, count);
     else if (nm == "pc_off") put(P.pc_off, out, count);
     else if (nm == "pc_pos") put(P.pc_pos, out, count);
     else if (nm == "pg_items") put(P.pg_items, out, count);

@@ -629,6 +629,12 @@ _PLAN_DTYPES = {
                             ("out", np.int64), ("m", np.int32), ("n", np.int32), ("rp", np.int32),
                             ("own", np.int32)]),
     "pd_level": np.int64, "pc_off": np.int32, "pc_pos": np.int64,
+    "fused_descs": np.dtype([("piv_off", np.int64), ("lu_off", np.int64), ("xrow", np.int64),
+                             ("yrow", np.int64), ("out", np.int64), ("m", np.int32), ("n", np.int32),
+                             ("r", np.int32), ("own", np.int32), ("touch", np.int32), ("pad", np.int32),
+                             ("cx", np.float64), ("cy", np.float64), ("cz", np.float64),
+                             ("pad2", np.float64)]),
+    "fd_level": np.int64, "pg_level": np.int64,
     "pg_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),
                           ("slot", np.int32)]),
     "p2_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32),

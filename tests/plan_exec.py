@@ -86,7 +86,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             wx, wy = plan.array("pair_wx", l), plan.array("pair_wy", l)
             rx, ry = plan.array("pair_rx", l), plan.array("pair_ry", l)
             cx, cy = plan.array("pair_cx", l), plan.array("pair_cy", l)
-        elif md[l] == 1:
+        elif md[l] in (1, 4):
             po, lo = plan.array("pair_piv", l), plan.array("pair_lu", l)
         for p, (a, b) in enumerate(zip(X, Y)):
             rp, cp, LU = pd[(l, int(a), int(b))]
@@ -107,7 +107,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
                 else:  # pair-major: U then V, row-major with stride rp
                     W[wx[p] + I * rx[p] + Q] = FX
                     W[wy[p] + J * ry[p] + Qy] = FY
-            elif md[l] == 1:
+            elif md[l] in (1, 4):
                 piv[po[p]: po[p] + r] = rp
                 piv[po[p] + r: po[p] + 2 * r] = cp
                 lu[lo[p]: lo[p] + r * r] = LU.reshape(-1)
@@ -231,7 +231,9 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         hits[level_of(g), r0: r0 + it["nrows"]] += 1
     # pair levels: one fused pass per pair descriptor, gathered per node
     pdesc = plan.array("pair_descs")
-    pout = np.zeros(max(int(sum(int(d["m"]) + int(d["n"]) for d in pdesc)), 1))
+    fdesc = plan.array("fused_descs")
+    pout = np.zeros(max(int(sum(int(d["m"]) + int(d["n"]) for d in pdesc) +
+                            sum(int(d["m"]) + int(d["n"]) for d in fdesc)), 1))
     for d in pdesc:
         m_, n_, rp_ = int(d["m"]), int(d["n"]), int(d["rp"])
         F = W[d["woff"]: d["woff"] + (m_ + n_) * rp_].reshape(m_ + n_, rp_)
@@ -239,6 +241,26 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         tv = F[m_:].T @ xp[d["yrow"]: d["yrow"] + n_]
         pout[d["out"]: d["out"] + m_] = F[:m_] @ tv
         pout[d["out"] + m_: d["out"] + m_ + n_] = F[m_:] @ tu
+    # fused levels: per pair, E = K(partner pivots, own points) once for both
+    # orientations (fused.cu): b_X += K(X,tau) R^-1 L^-1 K(sigma,Y) x_Y and
+    # b_Y += K(Y,sigma) L^-T R^-T K(tau,X) x_X
+    for d in plan.array("fused_descs"):
+        m_, n_, r = int(d["m"]), int(d["n"]), int(d["r"])
+        if r == 0:
+            continue
+        Xp = ppts[d["xrow"]: d["xrow"] + m_]
+        Yp = ppts[d["yrow"]: d["yrow"] + n_]
+        sig = piv[d["piv_off"]: d["piv_off"] + r]
+        tau = piv[d["piv_off"] + r: d["piv_off"] + 2 * r]
+        LU = lu[d["lu_off"]: d["lu_off"] + r * r].reshape(r, r)
+        Lm = np.tril(LU, -1) + np.eye(r)
+        Um = np.triu(LU)
+        EX = kernel_matrix(kind, Yp[tau], Xp)  # r x m: K(tau, X)
+        EY = kernel_matrix(kind, Xp[sig], Yp)  # r x n: K(sigma, Y)
+        sX = np.linalg.solve(Um, np.linalg.solve(Lm, EY @ xp[d["yrow"]: d["yrow"] + n_]))
+        sY = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, EX @ xp[d["xrow"]: d["xrow"] + m_]))
+        pout[d["out"]: d["out"] + m_] = EX.T @ sX
+        pout[d["out"] + m_: d["out"] + m_ + n_] = EY.T @ sY
     pcoff, pcpos = plan.array("pc_off"), plan.array("pc_pos")
     for it in pgit:
         g = int(it["node"])
