@@ -56,4 +56,20 @@ def test_large_config_against_reference(h3d, name, policy):
     # 1/sqrt(r^2) rows instead of eval_pair's 1/r: equal to ~1e-5 relative)
     assert abs(ref_err - float(g["ref_error"])) <= 1e-2 * float(g["ref_error"]) + 1e-14
     assert err <= 2 * ref_err, (err, ref_err)
+    if policy == "stream":
+        # ACA ranks per level against the reference's census (count, sum and
+        # max of its ordered-block ranks). The reference compresses (X, Y) and
+        # (Y, X) separately (each ACA starts from its own row 0, so the two
+        # orientations' ranks can differ by a few); the device compresses each
+        # unordered pair once, so 2 x its rank sum tracks the census sum.
+        rows_out = []
+        for l, cnt, rsum, rmax in g["ranks"]:
+            _, _, r = rep.pairs(int(l))
+            rows_out.append((int(l), int(cnt), int(rsum), int(rmax), len(r), 2 * int(r.sum()), int(r.max())))
+            print(f"{name} level {l}: ref blocks {cnt} sum {rsum} max {rmax}; "
+                  f"device pairs {len(r)} 2*sum {2 * int(r.sum())} max {int(r.max())}")
+        for l, cnt, rsum, rmax, npair, dsum, dmax in rows_out:
+            assert 2 * npair == cnt
+            assert abs(dsum - rsum) <= (0.05 if cnt < 100 else 0.01) * rsum, l
+            assert abs(dmax - rmax) <= max(2, 0.05 * rmax), l
     rep.close()
