@@ -456,26 +456,48 @@ __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t
 // column-major PT) and the only cross-lane traffic is a shared broadcast.
 //   side 0 (target = pair's row side X):  s = R^-1 (L^-1 v)       (lowrank.cpp:310-320)
 //   side 1 (target = pair's col side Y):  s = L^-T (R^-T v)       (the transposed block)
+// One GEMV sweep of the solve: acc[k] (lane output i = lane + 32 k) +=
+// M[j][i] x[j] over rows j of M with pred(i, j). The loads of B rows are
+// issued unconditionally (clamped indices, distinct registers) before any
+// FMA, so a warp keeps B x NK loads in flight instead of waiting one memory
+// latency per row (the predicated load -> FMA form serialises).
+template <int NK, int B, class Pred>
+__device__ __forceinline__ void tri_sweep(const double* __restrict__ M, int r, int j0, const double* x,
+                                          double (&acc)[NK], int lane, Pred pred) {
+  for (int jb = j0; jb < r; jb += B) {
+    double c[B][NK], xv[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int j = min(jb + u, r - 1);
+      xv[u] = x[j];
+      const double* row = M + static_cast<std::int64_t>(j) * r;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) c[u][k] = row[min(lane + 32 * k, r - 1)];
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int j = jb + u;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int i = lane + 32 * k;
+        if (j < r && i < r && pred(i, j)) acc[k] = fma(c[u][k], xv[u], acc[k]);
+      }
+    }
+  }
+}
+
 template <int NK>
 __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __restrict__ P,
                                           const double* __restrict__ PT, double* v, double* w,
                                           double* __restrict__ out, int lane) {
+  constexpr int B = NK <= 2 ? 8 : NK <= 4 ? 4 : 2;
   const int r = sg.r;
   double acc[NK];
 #pragma unroll
   for (int k = 0; k < NK; ++k) acc[k] = 0.0;
   if (sg.side == 0) {
     // w = L^-1 v: w_i = v_i + sum_{j<i} PT[j][i] v_j
-#pragma unroll 16
-    for (int j = 0; j < r; ++j) {
-      const double vj = v[j];
-      const double* col = PT + static_cast<std::int64_t>(j) * r;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const int i = lane + 32 * k;
-        if (k >= (j >> 5) && i > j && i < r) acc[k] = fma(col[i], vj, acc[k]);
-      }
-    }
+    tri_sweep<NK, B>(PT, r, 0, v, acc, lane, [](int i, int j) { return i > j; });
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
       const int i = lane + 32 * k;
@@ -484,28 +506,10 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
     }
     __syncwarp();
     // s = R^-1 w: s_i = sum_{j>=i} PT[j][i] w_j
-#pragma unroll 16
-    for (int j = 0; j < r; ++j) {
-      const double wj = w[j];
-      const double* col = PT + static_cast<std::int64_t>(j) * r;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const int i = lane + 32 * k;
-        if (32 * k <= j && i <= j) acc[k] = fma(col[i], wj, acc[k]);
-      }
-    }
+    tri_sweep<NK, B>(PT, r, 0, w, acc, lane, [](int i, int j) { return i <= j; });
   } else {
-    // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i
-#pragma unroll 16
-    for (int i = 0; i < r; ++i) {
-      const double vi = v[i];
-      const double* row = P + static_cast<std::int64_t>(i) * r;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const int j = lane + 32 * k;
-        if (k >= (i >> 5) && j >= i && j < r) acc[k] = fma(row[j], vi, acc[k]);
-      }
-    }
+    // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i   (here: lane output j, rows i)
+    tri_sweep<NK, B>(P, r, 0, v, acc, lane, [](int j, int i) { return j >= i; });
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
       const int j = lane + 32 * k;
@@ -513,16 +517,7 @@ __device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __re
     }
     __syncwarp();
     // s = L^-T u: s_j = u_j + sum_{i>j} P[i][j] u_i
-#pragma unroll 16
-    for (int i = 1; i < r; ++i) {
-      const double ui = w[i];
-      const double* row = P + static_cast<std::int64_t>(i) * r;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const int j = lane + 32 * k;
-        if (32 * k < i && j < i) acc[k] = fma(row[j], ui, acc[k]);
-      }
-    }
+    tri_sweep<NK, B>(P, r, 1, w, acc, lane, [](int j, int i) { return j < i; });
   }
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
