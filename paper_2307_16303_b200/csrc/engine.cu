@@ -7,6 +7,8 @@
 //   Engine::enqueue     <- h3d::matvec (hmatrix.cpp:153-226); with shard_world > 1
 //                          <- h3d::parallel_matvec (parallel.cpp:111-306)
 //   Engine::stats       <- h3d::stats (hmatrix.cpp:228-251)
+#include <cstdio>
+
 #include "engine.h"
 #include "common.cuh"
 
@@ -1044,7 +1046,27 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       fa.lu = lu_.get();
       fa.lu_total = lu_total_;
       fa.out = pair_out_.get();
+      // H3D_FUSED_PROF=1 (developer): per-phase cycle shares of the fused
+      // pass, printed to stderr after each matvec
+      static const bool fprof = std::getenv("H3D_FUSED_PROF") != nullptr;
+      DevBuf<unsigned long long> pbuf;
+      if (fprof && !kmask) {
+        pbuf.alloc(4096 * kFusedProfSlots);
+        H3D_CUDA_CHECK(cudaMemsetAsync(pbuf.get(), 0, pbuf.size() * 8, stream4_));
+        fa.prof = pbuf.get();
+      }
       if (run(H3D_K_FUSED)) launch_fused(fa, opt_.kernel_id, sms_, stream4_);
+      if (fa.prof) {
+        std::vector<unsigned long long> h(pbuf.size());
+        H3D_CUDA_CHECK(cudaMemcpyAsync(h.data(), pbuf.get(), h.size() * 8, cudaMemcpyDeviceToHost, stream4_));
+        H3D_CUDA_CHECK(cudaStreamSynchronize(stream4_));
+        double t[kFusedProfSlots] = {};
+        for (std::size_t i = 0; i < h.size(); ++i) t[i % kFusedProfSlots] += static_cast<double>(h[i]);
+        const double cyc = t[0] + t[1] + t[2] + t[3] + t[4];
+        std::fprintf(stderr, "fused pass: %.0f CTA-pairs, %.0f cycles/pair: setup %.0f%% eval %.0f%% exchange %.0f%% "
+                     "solve %.0f%% apply %.0f%%\n", t[5], cyc / std::max(t[5], 1.0), 100 * t[0] / cyc,
+                     100 * t[1] / cyc, 100 * t[2] / cyc, 100 * t[3] / cyc, 100 * t[4] / cyc);
+      }
       ++launches;
       gather_levels(kModeFused, stream4_);
       ke(H3D_K_FUSED, stream4_);

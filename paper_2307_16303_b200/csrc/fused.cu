@@ -228,7 +228,21 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(const FusedArgs a) 
     mbar_fence_init();
   }
   unsigned lu_phase = 0, parity = 0;
+  // optional phase profile (thread 0): cycles from pair start to pivots
+  // staged, evaluation done, v exchanged, solve done, apply done
+  unsigned long long ph[kFusedProfSlots] = {0, 0, 0, 0, 0, 0}, tp = 0;
+  auto mark = [&](int slot) {
+    if (a.prof != nullptr && tid == 0) {
+      const unsigned long long now = clock64();
+      ph[slot] += now - tp;
+      tp = now;
+    }
+  };
   for (long long pk = cl; pk < a.n; pk += ncl, parity ^= 1u) {
+    if (a.prof != nullptr && tid == 0) {
+      tp = clock64();
+      ++ph[5];
+    }
     const FusedDesc d = a.descs[pk];
     const int r = d.r;
     const int m = side == 0 ? d.m : d.n;                  // this node's points
@@ -278,12 +292,14 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(const FusedArgs a) 
       q[3] = 3.0 * kFarCoord * kFarCoord;
     }
     __syncthreads();  // pivots staged
+    mark(0);
     const bool active = warp < wall;  // warp-uniform
     if (active) {
       if (d.touch) eval_pass<K, true>(sm, E, r, kc, stride, tid, warp, lane, q, xq);
       else eval_pass<K, false>(sm, E, r, kc, stride, tid, warp, lane, q, xq);
     }
     __syncthreads();
+    mark(1);
     for (int k = tid; k < r; k += kFThreads) {
       double acc = 0.0;
       for (int w = 0; w < wall; ++w) acc += sm.vw[w][k];
@@ -296,6 +312,7 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(const FusedArgs a) 
       lu_phase ^= 1u;
     }
     __syncthreads();
+    mark(2);
     const double* M = stage ? sm.pool : Mg;
     tri_step<0>(side, r, warp, lane, M, sm.vin, sm.vw);
     __syncthreads();
@@ -315,12 +332,19 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(const FusedArgs a) 
       sm.s[i] = side == 0 ? acc : sm.tmp[i] + acc;  // s = R^-1 w  /  L^-T u
     }
     __syncthreads();
+    mark(3);
     if (active && (d.own & (side == 0 ? 1 : 2))) {
       const double o = d.touch ? apply_pass<K, true>(sm, E, r, kc, stride, tid, q)
                                : apply_pass<K, false>(sm, E, r, kc, stride, tid, q);
       if (tid < m) a.out[d.out + (side == 0 ? 0 : d.m) + tid] = far_scale<K>() * o;
     }
+    if (a.prof != nullptr) {
+      __syncthreads();
+      mark(4);
+    }
   }
+  if (a.prof != nullptr && tid == 0)
+    for (int q = 0; q < kFusedProfSlots; ++q) a.prof[blockIdx.x * kFusedProfSlots + q] = ph[q];
   cluster.sync();  // the partner may still read this CTA's last v
 }
 

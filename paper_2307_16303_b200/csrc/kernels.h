@@ -250,7 +250,9 @@ struct FusedArgs {
   const double* lu = nullptr;  // triangular inverses (lu_invert_kernel)
   std::int64_t lu_total = 0;
   double* out = nullptr;       // pair-output buffer
+  unsigned long long* prof = nullptr;  // optional: per-CTA phase cycle sums (kFusedProfSlots each)
 };
+constexpr int kFusedProfSlots = 6;  // setup, evaluation, v exchange, solve, apply, pairs
 int fused_max_node();  // points per node of a fused pair
 void launch_fused(const FusedArgs& a, int kernel, int sms, cudaStream_t s);
 
