@@ -949,7 +949,6 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
         pa.W = W_.get();
         pa.xp = xp_.get();
         pa.out = pair_out_.get();
-        pa.counter = counters_.get() + 5 + l;
         launch_pair(pa, sms_, tune_.pps > 0 ? tune_.pps : 2, stream2_);
         ++launches;
       }

@@ -231,10 +231,9 @@ struct PairArgs {
   const double* W = nullptr;
   const double* xp = nullptr;
   double* out = nullptr;
-  unsigned* counter = nullptr;  // zeroed before the launch
 };
 std::size_t pair_smem_bytes();
-// persistent, per_sm CTAs per SM (one 5-warp CTA is the HBM lane's share)
+// persistent, per_sm CTAs per SM; pairs interleaved statically over the CTAs
 void launch_pair(const PairArgs& a, int sms, int per_sm, cudaStream_t s);
 void launch_pair_gather(const P2Item* items, std::int64_t nitems, const std::int64_t* rowbeg,
                         const std::int32_t* pc_off, const std::int64_t* pc_pos, const double* out,
