@@ -410,10 +410,6 @@ def main():
                   f"{8 * (st['factor_bytes_alloc'] / 8 + 2 * LU + 4 * st['tvec_doubles'] + 5 * n) / 1e9:.2f} GB "
                   f">> 126 MB L2",
             "aca_build_s": round(build_s, 3),
-            # board power (nvidia-smi, 100 ms samples over the timed region) x
-            # step time: the C3 step runs at the 1000 W limit
-            "energy_j_per_step_est": (round(clk["power_w_median"] * ms / 1e3, 2)
-                                      if clk and "power_w_median" in clk else None),
             "build_ms": {k: round(st[k], 1) for k in ("build_ms_tree", "build_ms_lists",
                                                        "build_ms_aca_rank", "build_ms_aca_write",
                                                        "build_ms_total")},
