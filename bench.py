@@ -158,8 +158,16 @@ def reference_cpu_run(cfg_name: str, steps: int, warmup: int):
         rep.matvec(x)
         ts.append(time.perf_counter() - t1)
     mean = sum(ts) / len(ts)
+    model = "unknown CPU"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
     return dict(value=n / mean / 1e6, unit="Mpoints/s", cores=cores, kind=kind,
-                sample=(f"reference matvec (hmatrix.cpp:153-226, OpenMP {cores} threads) at N={n} "
+                sample=(f"reference matvec (hmatrix.cpp:153-226, OpenMP {cores} threads on {model}) at N={n} "
                         f"(same generator/kernel/tol/n_max as the workload, depth {rep.depth}); "
                         f"mean of {steps} steps after {warmup} warm-up; initialize {init_s:.1f} s "
                         f"untimed. Smaller N than the workload favours the reference "
@@ -256,6 +264,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
+    ms_local = ms
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -279,17 +288,32 @@ def main():
         rep.matvec_ptr(xh.data_ptr(), bh.data_ptr(), host=True)
     if dist:
         dist.barrier()
-    t_e2e = []
+    t_e2e, t_h2d, t_d2h = [], [], []
     tm = h3d.MatvecTiming()
     for _ in range(args.steps):
         rep.matvec_ptr(xh.data_ptr(), bh.data_ptr(), host=True, timing=tm)
         t_e2e.append(tm.total_ms)
+        t_h2d.append(tm.h2d_ms)
+        t_d2h.append(tm.d2h_ms)
     e2e_ms = sum(t_e2e) / len(t_e2e)
     if dist:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = n / (e2e_ms * 1e-3) / 1e6
+
+    # ---- per-rank work (multi-GPU): owned rows, streamed bytes, regenerated
+    # entries and device time of each shard (balance check)
+    per_rank = None
+    if dist:
+        try:
+            mine = {"rank": rank, "owned_rows": int(st["owned_row_end"] - st["owned_row_begin"]),
+                    "streamed_factor_GB_per_phase": round(8 * st["factor_doubles"] / 1e9, 3),
+                    "proxy_entries_per_phase": int(st["proxy_units"]), "ms_per_step": round(ms_local, 4)}
+            per_rank = [None] * world
+            dist.all_gather_object(per_rank, mine)
+        except Exception as e:  # reporting only
+            per_rank = f"unavailable: {e}"
 
     # ---- parity spot check on 200 sampled rows against the exact sum (oracle)
     rel_err = None
@@ -430,6 +454,7 @@ def main():
                         "both phases + stored dense near field) at the measured peak; frac > 1 = "
                         "faster than any factor-streaming matvec can be"},
             "rel_err_vs_exact_200_rows": rel_err,
+            "per_rank": per_rank,
         },
         "roofline": {"bound": kd["bound"], "kernel": dom, "achieved": kd["achieved"],
                      "peak": kd["peak"], "peak_source": peak_src if kd["bound"] == "hbm" else
@@ -440,7 +465,8 @@ def main():
                      "t_ms": kd["ms"], "share_of_kernel_time": kd["share"]},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "Mpoints/s", "h2d_bytes_per_step": 8 * n,
-                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms,
+                "h2d_ms": round(sum(t_h2d) / len(t_h2d), 4), "d2h_ms": round(sum(t_d2h) / len(t_d2h), 4)},
         "gpu_launches": int(prof.launches),
         "cpu_baseline": cpu,
     }
