@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define H3D_B200_ABI_VERSION 2
+#define H3D_B200_ABI_VERSION 3
 
 enum h3d_status {
   H3D_OK = 0,
@@ -95,6 +95,9 @@ typedef struct {
   double phase2_ms;     /* near field + U t, fused un-permute */
   double d2h_ms;        /* device b -> host (host mode only) */
   int64_t launches;     /* kernels launched by this call */
+  double device_ms;     /* device part (gather .. un-permute). A call replayed as one
+                           CUDA graph reports only this, h2d_ms, d2h_ms and total_ms
+                           (the per-phase fields stay 0; H3D_TUNE=graphs=0 splits them) */
 } h3d_timing;
 
 /* Representation statistics; superset of h3d::RepStats (hmatrix.hpp:73-85). */

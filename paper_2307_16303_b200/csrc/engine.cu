@@ -146,6 +146,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2p") tune_.p2p = v;
         else if (k == "skip") tune_.skip = v;
         else if (k == "nf") tune_.nf = v;
+        else if (k == "nfc") tune_.nfc = v;
         else if (k == "pps") tune_.pps = v;
         else if (k == "graphs") tune_.graphs = v;
       }
@@ -158,7 +159,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     H3D_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream2_, cudaStreamNonBlocking, greatest));
     H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream4_, cudaStreamNonBlocking, greatest));
-    H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream3_, cudaStreamNonBlocking, least));
+    H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream3_, cudaStreamNonBlocking, greatest));
   }
   for (auto& e : ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
   for (int k = 0; k < 3; ++k) {
@@ -983,16 +984,17 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ke(H3D_K_P1_PROXY, stream4_);
     ++launches;
   }
-  // optional (H3D_TUNE nf=1): the near field + direct blocks (x only) fork
-  // off here at one CTA per SM beside the solves; measured slower - the
-  // latency-bound solve blocks lose more than the idle SMs gain (2.9 -> 5.6 ms)
-  const bool near_fork = has_p2 && tune_.nf == 1;
+  // the near field + direct leaf blocks (x only) fork off here, beside the
+  // latency-bound solves (H3D_TUNE nf=0: after p2_proxy on the FP64 lane).
+  // Measured with the batched-load solve: C2 / C3 / C4 3.5-5.5 % faster
+  // (before it the solves lost more than the near field gained)
+  const bool near_fork = has_p2 && tune_.nf != 0;
   if (near_fork) {
     H3D_CUDA_CHECK(cudaEventRecord(fork_[2], stream4_));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
     kb(H3D_K_NEAR, stream3_);
-    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, 1, stream3_);
-    else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, 1, stream3_);
+    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, tune_.nfc, stream3_);
+    else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, tune_.nfc, stream3_);
     ke(H3D_K_NEAR, stream3_);
     ++launches;
     H3D_CUDA_CHECK(cudaEventRecord(join_[2], stream3_));
@@ -1109,9 +1111,18 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
     xin = x_.get();
   }
   double* bout = host ? b_.get() : b;
-  // with a timing breakdown requested the kernels run eagerly (per-phase
-  // events), else through the graph cache
-  const std::int64_t launches = t ? enqueue(xin, bout, stream_, ev_ + 1, nullptr) : run_graph(xin, bout, stream_);
+  // through the graph cache (events around it: copies and device time), or
+  // eagerly with per-phase events when graphs are off (H3D_TUNE graphs=0)
+  // or a communicator is attached
+  const bool graphed = tune_.graphs && nccl_comm_ == nullptr;
+  std::int64_t launches = 0;
+  if (graphed) {
+    cudaEventRecord(ev_[1], stream_);
+    launches = run_graph(xin, bout, stream_);
+    cudaEventRecord(ev_[4], stream_);
+  } else {
+    launches = enqueue(xin, bout, stream_, ev_ + 1, nullptr);
+  }
   if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
   cudaEventRecord(ev_[5], stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -1124,11 +1135,16 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
     std::memset(t, 0, sizeof(*t));
     t->total_ms = el(0, 5);
     t->h2d_ms = el(0, 1);
-    if (world_ == 1) t->gather_ms = el(1, 2);
-    else t->exchange_ms = el(1, 2);
-    t->phase1_ms = el(2, 3);
-    t->phase2_ms = el(3, 4);
     t->d2h_ms = el(4, 5);
+    if (graphed) {
+      t->device_ms = el(1, 4);  // one graph: no per-phase split
+    } else {
+      if (world_ == 1) t->gather_ms = el(1, 2);
+      else t->exchange_ms = el(1, 2);
+      t->phase1_ms = el(2, 3);
+      t->phase2_ms = el(3, 4);
+      t->device_ms = el(1, 4);
+    }
     t->launches = launches;
   }
 }
@@ -1238,6 +1254,7 @@ void Engine::profile_read(h3d_timing* sum, std::int64_t* steps) {
     sum->phase1_ms += b;
     sum->phase2_ms += c;
     sum->total_ms += a + b + c;
+    sum->device_ms += a + b + c;
   }
   sum->launches = prof_launches_;
   *steps = static_cast<std::int64_t>(prof_used_);

@@ -72,6 +72,7 @@ class _Timing(C.Structure):
         ("phase2_ms", C.c_double),
         ("d2h_ms", C.c_double),
         ("launches", C.c_int64),
+        ("device_ms", C.c_double),
     ]
 
 
@@ -269,6 +270,7 @@ class MatvecTiming:
     phase2_ms: float = 0.0
     d2h_ms: float = 0.0
     launches: int = 0
+    device_ms: float = 0.0  # graph replay: the device time (no per-phase split)
 
 
 class HMatrixRep:

@@ -4,6 +4,7 @@
 """
 import argparse
 import json
+import os
 import sys
 import time
 from pathlib import Path
@@ -27,6 +28,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--check-rows", type=int, default=0)
     a = ap.parse_args()
+    os.environ.setdefault("H3D_TUNE", "graphs=0")  # eager: keeps the per-phase timing split
     t0 = time.time()
     pts = h3d.generate_points(a.n, a.seed)
     x = h3d.random_vector(a.n, a.seed + 17)

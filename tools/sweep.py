@@ -25,7 +25,8 @@ def main():
     x = h3d.random_vector(a.n, 18)
     for lv in a.levels.split(","):
         for tune in a.tunes.split(";"):
-            os.environ["H3D_TUNE"] = tune
+            # eager launches (graphs=0) keep the per-phase timing split
+            os.environ["H3D_TUNE"] = ",".join(t for t in ("graphs=0", tune) if t)
             pol = dict(mode_policy="auto") if lv in ("auto", "stream") else dict(
                 mode_policy="explicit", level_modes=tuple(int(c) for c in lv))
             if lv == "stream":
