@@ -147,6 +147,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "skip") tune_.skip = v;
         else if (k == "nf") tune_.nf = v;
         else if (k == "nfc") tune_.nfc = v;
+        else if (k == "fw") tune_.fw = v;
         else if (k == "pps") tune_.pps = v;
         else if (k == "graphs") tune_.graphs = v;
       }
@@ -1019,7 +1020,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // blocks lose most of their bandwidth beside a saturating bulk stream
   // (0.5 ms alone vs 6-10 ms beside it), and they gate the FP64 lane.
   if (hbm) {
-    if (n_segs_solve_ > 0 && has_p2 && n_p2s_ > 0) {
+    if (n_segs_solve_ > 0 && has_p2 && n_p2s_ > 0 && tune_.fw) {
       launch_set_flag(sync_flag_.get(), 1u, stream4_);
       ++launches;
       a2.wait_flag = sync_flag_.get();

@@ -97,9 +97,10 @@ class Engine {
   // ("skip=<mask of h3d_kernel_slot>" drops kernels: timing experiments only,
   // results are wrong)
   // ("nf=0": near field after p2_proxy instead of forked beside the solves;
-  // "nfc": CTAs per SM of the forked near kernel)
+  // "nfc": CTAs per SM of the forked near kernel; "fw=0": p2_stream does not
+  // wait for the solves-done flag)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1;
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1, fw = 1;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
