@@ -21,6 +21,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--tunes", default="graphs=0;graphs=1")
     ap.add_argument("--gap-ms", type=float, default=5.0)
+    ap.add_argument("--kernel", default="laplace3d")
+    ap.add_argument("--levels", default="auto", help="comma list of auto / explicit level-mode strings")
     a = ap.parse_args()
     import torch
     pts = h3d.generate_points(a.n, 1)
@@ -28,11 +30,14 @@ def main():
     xd = torch.from_numpy(x).cuda()
     bd = torch.empty_like(xd)
     st = torch.cuda.current_stream()
-    for tune in a.tunes.split(";"):
+    for lv in a.levels.split(","):
+      pol = dict(mode_policy="auto") if lv == "auto" else dict(
+          mode_policy="explicit", level_modes=tuple(int(c) for c in lv))
+      for tune in a.tunes.split(";"):
         os.environ["H3D_TUNE"] = tune
         for b in range(a.builds):
-            rep = h3d.initialize(pts, h3d.make_kernel("laplace3d"), "hodlr3d",
-                                 h3d.HmatOptions(n_max=64, epsilon=a.eps))
+            rep = h3d.initialize(pts, h3d.make_kernel(a.kernel), "hodlr3d",
+                                 h3d.HmatOptions(n_max=64, epsilon=a.eps, **pol))
             for _ in range(3):
                 rep.matvec_async(xd.data_ptr(), bd.data_ptr(), st.cuda_stream)
             torch.cuda.synchronize()
@@ -57,7 +62,7 @@ def main():
                 torch.cuda._sleep(int(a.gap_ms * 1.9e6))
                 torch.cuda.synchronize()
             single.sort()
-            print(f"tune '{tune}' build {b}: back-to-back ms/matvec " + " ".join(f"{p:.3f}" for p in per) +
+            print(f"levels {lv} tune '{tune}' build {b}: back-to-back ms/matvec " + " ".join(f"{p:.3f}" for p in per) +
                   f" | one at a time (gap {a.gap_ms} ms): median {single[len(single) // 2]:.3f} "
                   f"min {single[0]:.3f}", flush=True)
             rep.close()
