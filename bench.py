@@ -11,8 +11,12 @@ Multi-GPU (torchrun, one rank per GPU): Morton-subtree row ownership, the x
 all-gather over NVLink inside the step; the time is the max over ranks.
 
 `--impl reference` times the reference's own CPU implementation
-(oracle/_ref/libh3dref.so, the unmodified sources compiled in place) on the
-box's host cores over a bounded sample of the workload.
+(oracle/_ref/libh3dref.so, the unmodified sources compiled in place) on all
+of the box's host cores on the SAME workload (N, kernel, tol, n_max, inputs):
+initialize once (untimed, reported), then W warm-up and K timed matvecs.
+The `cpu_baseline` of our own arm is a bounded sample (N = 262,144, a few
+matvecs) so the default run stays short; the headline CPU comparison is the
+reference arm.
 """
 from __future__ import annotations
 
@@ -45,8 +49,9 @@ CONFIGS = {
                desc="C5: N=4,194,304 uniform [-1,1]^3, Laplace 1/r (diag 0), fp64, n_max 64, "
                     "ACA tol 1e-6, matrix-free near field"),
 }
-# reference-arm sample size (the CPU reference needs ~6 min per initialize at
-# N=1M on 8 cores), same generator/kernel/tol/n_max
+# cpu_baseline sample size of our own arm (the CPU reference needs ~6 min per
+# initialize at N=1M on 8 cores), same generator /
+# kernel / tol / n_max. The reference arm (--impl reference) runs the full N.
 REF_SAMPLE_N = {"c1": 4096, "c2": 65536, "c3": 262144, "c4": 65536, "c5": 262144}
 
 FALLBACK_HBM = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
@@ -133,8 +138,24 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU baseline
-def reference_cpu_run(cfg_name: str, steps: int, warmup: int):
-    """Time the reference CPU matvec (oracle/_ref) on a bounded sample."""
+def workload_config(cfg_name: str, near: str) -> dict:
+    """The `config` object both arms print (identical, so the driver can pair
+    them); diagnostics go to the line's `detail`."""
+    cfg = CONFIGS[cfg_name]
+    return {"workload": cfg["desc"], "n": cfg["n"], "kernel": cfg["kernel"], "aca_tol": cfg["eps"],
+            "n_max": cfg["n_max"], "variant": "hodlr3d",
+            "near_field": "on-the-fly (DenseMode::OnTheFly, matrix-free)" if near == "matrix-free"
+                          else "cached (DenseMode::Cached, stored)",
+            "inputs": "generate_points(UniformRandom, N, seed=1); x = 2u-1 from mt19937_64(18)",
+            "l2": "no flush: every step streams a working set far larger than the 126 MB L2 "
+                  "(GPU: factor pool + LU + points, tens of GB at C3; CPU: the reference's "
+                  "block list)"}
+
+
+def reference_cpu_run(cfg_name: str, steps: int, warmup: int, n: int | None = None,
+                      near: str = "matrix-free"):
+    """Time the reference CPU matvec (oracle/_ref) on all host cores; n=None:
+    the workload's own N, else a bounded sample of that size."""
     from oracle_lib import RefLib, have_ref
     if not have_ref():
         from oracle_lib import Oracle
@@ -144,11 +165,13 @@ def reference_cpu_run(cfg_name: str, steps: int, warmup: int):
     cores = os.cpu_count() or 1
     lib.set_threads(cores)
     cfg = CONFIGS[cfg_name]
-    n = REF_SAMPLE_N[cfg_name]
+    full = n is None
+    n = cfg["n"] if full else n
     pts = lib.generate_points(n, cfg["seed"])
     x = lib.random_vector(n, cfg["seed"] + 17)
     t0 = time.time()
-    rep = lib.initialize(pts, cfg["kernel"], n_max=cfg["n_max"], eps=cfg["eps"])
+    kw = {"cached": near == "stored"} if kind == "reference" else {}
+    rep = lib.initialize(pts, cfg["kernel"], n_max=cfg["n_max"], eps=cfg["eps"], **kw)
     init_s = time.time() - t0
     for _ in range(warmup):
         rep.matvec(x)
@@ -166,13 +189,14 @@ def reference_cpu_run(cfg_name: str, steps: int, warmup: int):
                 break
     except OSError:
         pass
+    what = ("the full workload" if full else
+            "a bounded sample (smaller N than the workload favours the reference: its per-point "
+            "cost grows with N)")
     return dict(value=n / mean / 1e6, unit="Mpoints/s", cores=cores, kind=kind,
-                sample=(f"reference matvec (hmatrix.cpp:153-226, OpenMP {cores} threads on {model}) at N={n} "
-                        f"(same generator/kernel/tol/n_max as the workload, depth {rep.depth}); "
-                        f"mean of {steps} steps after {warmup} warm-up; initialize {init_s:.1f} s "
-                        f"untimed. Smaller N than the workload favours the reference "
-                        f"(its per-point cost grows with N)"),
-                init_s=init_s, ms_per_step=mean * 1e3, n=n)
+                sample=(f"reference matvec (hmatrix.cpp:153-226, OpenMP {cores} threads on {model}) at N={n}, "
+                        f"{what} (same generator/kernel/tol/n_max, depth {rep.depth}); "
+                        f"mean of {steps} steps after {warmup} warm-up; initialize {init_s:.1f} s untimed"),
+                init_s=init_s, ms_per_step=mean * 1e3, n=n, cpu_model=model, depth=rep.depth)
 
 
 # ------------------------------------------------------------------ main
@@ -197,12 +221,18 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        r = reference_cpu_run(args.config, args.steps, args.warmup)
+        r = reference_cpu_run(args.config, args.steps, args.warmup, near=args.near)
         line = {"metric": METRIC, "value": r["value"], "unit": "Mpoints/s", "impl": "reference",
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cfg["desc"], "sample_n": r["n"]},
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic: generate_points(UniformRandom, N, seed=1) and x = 2u-1 from "
+                        "mt19937_64(18), the reference's own generators",
+                "config": workload_config(args.config, args.near),
+                "detail": {"n": r["n"], "depth": r["depth"], "initialize_s": round(r["init_s"], 2),
+                           "threads": r["cores"], "cpu_model": r["cpu_model"],
+                           "build": "oracle/Makefile: unmodified /root/reference/proj/src compiled "
+                                    "in place (-O3, OpenMP) against the Eigen/doctest API shims"},
                 "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": r["value"], "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -399,7 +429,7 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        r = reference_cpu_run(args.config, steps=3, warmup=1)
+        r = reference_cpu_run(args.config, steps=3, warmup=1, n=REF_SAMPLE_N[args.config])
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     line = {
@@ -416,8 +446,8 @@ def main():
         "dtype": "f64",
         "data": "synthetic: generate_points(UniformRandom, N, seed=1) and x = 2u-1 from "
                 "mt19937_64(18), bit-identical to the reference generators",
-        "config": {
-            "workload": cfg["desc"],
+        "config": workload_config(args.config, args.near),
+        "detail": {
             "representation": {"policy": args.policy,
                                "level_modes": {str(l): ["stream", "proxy", "direct", "pair", "fused"][m]
                                                for l, m in enumerate(st["level_modes"]) if l > 0},
@@ -427,7 +457,6 @@ def main():
             "streamed_factor_GB_per_phase": round(8 * F / 1e9, 3),
             "proxy_entries_per_phase": U,
             "lu_GB": round(8 * st["lu_doubles"] / 1e9, 3),
-            "near_field": args.near,
             "parallelism": f"Morton-subtree row ownership over {world} GPU(s), NCCL all-gather of x",
             "l2": f"inputs larger than L2: per-step working set (factor pool, LU inverses, proxy "
                   f"points/t-vectors, packed points) "

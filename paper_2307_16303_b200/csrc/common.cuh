@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
@@ -198,20 +199,24 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
       : "memory");
   return done != 0;
 }
-#ifndef H3D_MBAR_SLEEP_MAX
-#define H3D_MBAR_SLEEP_MAX 0
+// Every device-side wait is bounded: a wait that outlives H3D_WAIT_LIMIT_NS
+// (a pipeline protocol fault, never a slow copy) traps, so the host sees a
+// launch failure (H3D_ECUDA) instead of a hung stream.
+#ifndef H3D_WAIT_LIMIT_NS
+#define H3D_WAIT_LIMIT_NS 20000000000ULL
 #endif
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-#if H3D_MBAR_SLEEP_MAX > 0
-  unsigned ns = 16;
-  while (!mbar_try(b, parity)) {
-    __nanosleep(ns);
-    if (ns < H3D_MBAR_SLEEP_MAX) ns <<= 1;
+  if (mbar_try(b, parity)) return;
+  const unsigned long long t0 = global_ns();
+  for (unsigned k = 1;; ++k) {
+    if (mbar_try(b, parity)) return;
+    if ((k & 1023u) == 0 && global_ns() - t0 > H3D_WAIT_LIMIT_NS) __trap();
   }
-#else
-  while (!mbar_try(b, parity)) {
-  }
-#endif
 }
 __device__ __forceinline__ unsigned long long l2_evict_first() {
   unsigned long long pol;
@@ -236,6 +241,24 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
+
+// Host: run f() once per (flag, current device). Function attributes
+// (dynamic shared memory, carveout) are per device, and one process may drive
+// engines on several GPUs.
+struct PerDeviceOnce {
+  std::mutex mu;
+  unsigned long long seen = 0;
+  template <class F>
+  void operator()(F&& f) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    std::lock_guard<std::mutex> g(mu);
+    if (seen & bit) return;
+    f();
+    seen |= bit;
+  }
+};
 
 }  // namespace h3db
 

@@ -144,7 +144,9 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2c") tune_.p2c = v;
         else if (k == "p2s") tune_.p2s = v;
         else if (k == "p2p") tune_.p2p = v;
+#ifdef H3D_DEVTOOLS
         else if (k == "skip") tune_.skip = v;
+#endif
         else if (k == "nf") tune_.nf = v;
         else if (k == "nfc") tune_.nfc = v;
         else if (k == "fw") tune_.fw = v;
@@ -163,6 +165,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     H3D_CUDA_CHECK(cudaStreamCreateWithPriority(&stream3_, cudaStreamNonBlocking, greatest));
   }
   for (auto& e : ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
+  H3D_CUDA_CHECK(cudaEventCreateWithFlags(&done_ev_, cudaEventDisableTiming));
   for (int k = 0; k < 3; ++k) {
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&fork_[k], cudaEventDisableTiming));
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&join_[k], cudaEventDisableTiming));
@@ -238,6 +241,7 @@ Engine::~Engine() {
   if (nccl_comm_) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
+  if (done_ev_) cudaEventDestroy(done_ev_);
   for (int k = 0; k < 3; ++k) {
     if (fork_[k]) cudaEventDestroy(fork_[k]);
     if (join_[k]) cudaEventDestroy(join_[k]);
@@ -1048,27 +1052,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       fa.lu = lu_.get();
       fa.lu_total = lu_total_;
       fa.out = pair_out_.get();
-      // H3D_FUSED_PROF=1 (developer): per-phase cycle shares of the fused
-      // pass, printed to stderr after each matvec
-      static const bool fprof = std::getenv("H3D_FUSED_PROF") != nullptr;
-      DevBuf<unsigned long long> pbuf;
-      if (fprof && !kmask) {
-        pbuf.alloc(4096 * kFusedProfSlots);
-        H3D_CUDA_CHECK(cudaMemsetAsync(pbuf.get(), 0, pbuf.size() * 8, stream4_));
-        fa.prof = pbuf.get();
-      }
       if (run(H3D_K_FUSED)) launch_fused(fa, opt_.kernel_id, sms_, stream4_);
-      if (fa.prof) {
-        std::vector<unsigned long long> h(pbuf.size());
-        H3D_CUDA_CHECK(cudaMemcpyAsync(h.data(), pbuf.get(), h.size() * 8, cudaMemcpyDeviceToHost, stream4_));
-        H3D_CUDA_CHECK(cudaStreamSynchronize(stream4_));
-        double t[kFusedProfSlots] = {};
-        for (std::size_t i = 0; i < h.size(); ++i) t[i % kFusedProfSlots] += static_cast<double>(h[i]);
-        const double cyc = t[0] + t[1] + t[2] + t[3] + t[4];
-        std::fprintf(stderr, "fused pass: %.0f CTA-pairs, %.0f cycles/pair: setup %.0f%% eval %.0f%% exchange %.0f%% "
-                     "solve %.0f%% apply %.0f%%\n", t[5], cyc / std::max(t[5], 1.0), 100 * t[0] / cyc,
-                     100 * t[1] / cyc, 100 * t[2] / cyc, 100 * t[3] / cyc, 100 * t[4] / cyc);
-      }
       ++launches;
       gather_levels(kModeFused, stream4_);
       ke(H3D_K_FUSED, stream4_);
@@ -1103,8 +1087,19 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   return launches;
 }
 
+void Engine::begin_call(cudaStream_t s) {
+  if (done_valid_ && s != last_stream_) H3D_CUDA_CHECK(cudaStreamWaitEvent(s, done_ev_, 0));
+}
+
+void Engine::end_call(cudaStream_t s) {
+  H3D_CUDA_CHECK(cudaEventRecord(done_ev_, s));
+  done_valid_ = true;
+  last_stream_ = s;
+}
+
 void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  begin_call(stream_);
   cudaEventRecord(ev_[0], stream_);
   const double* xin = x;
   if (host) {
@@ -1126,6 +1121,7 @@ void Engine::matvec(const double* x, double* b, bool host, h3d_timing* t) {
   }
   if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
   cudaEventRecord(ev_[5], stream_);
+  end_call(stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   if (t) {
     float v = 0;
@@ -1194,8 +1190,10 @@ std::int64_t Engine::run_graph(const double* x, double* b, cudaStream_t s) {
 
 void Engine::matvec_async(const double* x, double* b, cudaStream_t s) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  begin_call(s);
   if (!prof_on_) {
     prof_launches_ += run_graph(x, b, s);
+    end_call(s);
     return;
   }
   cudaEvent_t* ev = nullptr;
@@ -1208,6 +1206,7 @@ void Engine::matvec_async(const double* x, double* b, cudaStream_t s) {
     ++prof_used_;
   }
   prof_launches_ += enqueue(x, b, s, ev, mask);
+  end_call(s);
 }
 
 void Engine::profile(int enable, std::int64_t capacity) {
@@ -1370,6 +1369,7 @@ namespace h3db {
 void Engine::direct_matvec(const double* x, double* b, bool host) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
   if (world_ != 1) throw InvalidArgument("direct_matvec: single-shard handles only");
+  begin_call(stream_);
   const double* xin = x;
   if (host) {
     H3D_CUDA_CHECK(cudaMemcpyAsync(x_.get(), x, n_ * 8, cudaMemcpyHostToDevice, stream_));
@@ -1379,7 +1379,60 @@ void Engine::direct_matvec(const double* x, double* b, bool host) {
   launch_gather(xin, perm_.get(), n_, xp_.get(), p4_.get(), stream_);
   launch_direct(p4_.get(), n_, opt_.kernel_id, opt_.diagonal, perm_.get(), bout, stream_);
   if (host) H3D_CUDA_CHECK(cudaMemcpyAsync(b, b_.get(), n_ * 8, cudaMemcpyDeviceToHost, stream_));
+  end_call(stream_);
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+double Engine::reference_error(const double* x, const double* b, bool host, std::int64_t exact_limit,
+                               std::int64_t sample_rows, std::uint64_t seed) {
+  H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
+  if (exact_limit < 0 || sample_rows < 0) throw InvalidArgument("reference_error: negative row count");
+  // rows are permuted (Morton) positions, drawn exactly as hmatrix.cpp:264-271
+  std::vector<std::int64_t> rows;
+  if (n_ <= exact_limit) {
+    rows.resize(static_cast<std::size_t>(n_));
+    for (std::int64_t i = 0; i < n_; ++i) rows[static_cast<std::size_t>(i)] = i;
+  } else {
+    std::mt19937_64 gen(seed);
+    rows.resize(static_cast<std::size_t>(sample_rows));
+    for (auto& r : rows)
+      r = static_cast<std::int64_t>(static_cast<std::size_t>(static_cast<double>(gen() >> 11) * 0x1.0p-53 *
+                                                             static_cast<double>(n_)));
+  }
+  const std::int64_t nr = static_cast<std::int64_t>(rows.size());
+  std::vector<double> exact(rows.size()), bh;
+  begin_call(stream_);
+  const double* xin = x;
+  if (host) {
+    H3D_CUDA_CHECK(cudaMemcpyAsync(x_.get(), x, n_ * 8, cudaMemcpyHostToDevice, stream_));
+    xin = x_.get();
+  } else {
+    bh.resize(static_cast<std::size_t>(n_));
+    H3D_CUDA_CHECK(cudaMemcpyAsync(bh.data(), b, n_ * 8, cudaMemcpyDeviceToHost, stream_));
+  }
+  launch_gather(xin, perm_.get(), n_, xp_.get(), p4_.get(), stream_);
+  DevBuf<std::int64_t> rows_d;
+  DevBuf<double> out_d;
+  if (nr > 0) {
+    rows_d.upload(rows, stream_);
+    out_d.alloc(static_cast<std::size_t>(nr));
+    H3D_CUDA_CHECK(cudaMemsetAsync(flags_.get(), 0, 4, stream_));
+    launch_exact_rows(p4_.get(), n_, opt_.kernel_id, opt_.diagonal, rows_d.get(), nr, out_d.get(), flags_.get(),
+                      stream_);
+    H3D_CUDA_CHECK(cudaMemcpyAsync(exact.data(), out_d.get(), nr * 8, cudaMemcpyDeviceToHost, stream_));
+  }
+  end_call(stream_);
+  H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  if (nr > 0) check_flags("reference_error");
+  const double* bb = host ? b : bh.data();
+  double err2 = 0.0, ref2 = 0.0;
+  for (std::int64_t k = 0; k < nr; ++k) {
+    const double e = exact[static_cast<std::size_t>(k)];
+    const double a = bb[perm_h_[static_cast<std::size_t>(rows[static_cast<std::size_t>(k)])]];
+    err2 += (a - e) * (a - e);
+    ref2 += e * e;
+  }
+  return std::sqrt(err2 / ref2);
 }
 
 void Engine::gmres(const double* rhs, double* xout, bool host, double alpha, double beta, double tol,
@@ -1393,6 +1446,7 @@ void Engine::gmres(const double* rhs, double* xout, bool host, double alpha, dou
   restart = restart > 0 ? restart : max_iter;
   const int mcap = std::min(restart, max_iter);
   cudaStream_t s = stream_;
+  begin_call(s);
   DevBuf<double> f, x, w, r, basis, scal, scratch;
   f.alloc(n);
   x.alloc(n);
@@ -1495,6 +1549,7 @@ void Engine::gmres(const double* rhs, double* xout, bool host, double alpha, dou
     if (relres < tol) converged = true;
   }
   H3D_CUDA_CHECK(cudaMemcpyAsync(xout, x.get(), n * 8, host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  end_call(s);
   H3D_CUDA_CHECK(cudaStreamSynchronize(s));
   if (info) {
     info->iterations = total;

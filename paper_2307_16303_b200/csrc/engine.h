@@ -66,6 +66,11 @@ class Engine {
   void attach_nccl(const void* id128, int rank, int world);
   // exact dense product b = K x (O(N^2), verification / manufactured RHS)
   void direct_matvec(const double* x, double* b, bool host);
+  // relative 2-norm error of b against exact row sums (reference
+  // hmatrix.cpp:253-291): every row if N <= exact_limit, else sample_rows
+  // Morton positions drawn by mt19937_64(seed)
+  double reference_error(const double* x, const double* b, bool host, std::int64_t exact_limit,
+                         std::int64_t sample_rows, std::uint64_t seed);
   // GMRES on (alpha I + beta A) x = rhs, reference solver.cpp:22-125
   void gmres(const double* rhs, double* x, bool host, double alpha, double beta, double tol, int restart,
              int max_iter, double* hist, int hist_cap, h3d_gmres_info* info);
@@ -82,6 +87,17 @@ class Engine {
   void check_flags(const char* where);
   std::int64_t enqueue(const double* xin, double* bout, cudaStream_t s, cudaEvent_t* ev,
                        std::uint32_t* kmask);
+  // Calls that use the handle's scratch (counters, S pool, partials, x in
+  // Morton order) are ordered on the device: each waits for the previous
+  // call's completion event when it runs on a different stream, and records
+  // its own. Two matvec_async calls on different caller streams are then
+  // serialised exactly like two calls on one stream (reference
+  // hmatrix.hpp:34-36: the representation is shareable).
+  void begin_call(cudaStream_t s);
+  void end_call(cudaStream_t s);
+  cudaEvent_t done_ev_ = nullptr;
+  cudaStream_t last_stream_ = nullptr;
+  bool done_valid_ = false;
   Phase2Args phase2_args(double* bout) const;
   std::int64_t node_size(int level, std::int64_t m) const {
     return off_[level][m + 1] - off_[level][m];
@@ -95,7 +111,7 @@ class Engine {
   // FP64 lanes share the SMs; overridable for tuning through
   // H3D_TUNE="p1s=1,p1p=4,p2c=2,p2s=1,p2p=4" (proxy kernels: 128-thread CTAs)
   // ("skip=<mask of h3d_kernel_slot>" drops kernels: timing experiments only,
-  // results are wrong)
+  // results are wrong; honoured only in a -DH3D_DEVTOOLS build)
   // ("nf=0": near field after p2_proxy instead of forked beside the solves;
   // "nfc": CTAs per SM of the forked near kernel; "fw=0": p2_stream does not
   // wait for the solves-done flag)

@@ -351,12 +351,11 @@ __global__ void __launch_bounds__(kFThreads, 2) fused_kernel(const FusedArgs a) 
 template <int K>
 void launch_fused_t(const FusedArgs& a, cudaStream_t s) {
   const void* f = reinterpret_cast<const void*>(fused_kernel<K>);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr([f] {
     H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(FusedSmem))));
-    attr = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(kFThreads);
   cfg.dynamicSmemBytes = sizeof(FusedSmem);
@@ -368,11 +367,16 @@ void launch_fused_t(const FusedArgs& a, cudaStream_t s) {
   at.val.clusterDim.z = 1;
   cfg.attrs = &at;
   cfg.numAttrs = 1;
-  static int max_cl = 0;
+  // co-resident clusters, per device (the occupancy query is device-specific)
+  static int max_cl_dev[64] = {};
+  int dev = 0;
+  H3D_CUDA_CHECK(cudaGetDevice(&dev));
+  int& max_cl = max_cl_dev[dev & 63];
   if (max_cl == 0) {
     cfg.gridDim = dim3(2);
-    H3D_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&max_cl, f, &cfg));
-    max_cl = std::max(max_cl, 1);
+    int m = 0;
+    H3D_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&m, f, &cfg));
+    max_cl = std::max(m, 1);
   }
   const std::int64_t ncl = std::max<std::int64_t>(1, std::min<std::int64_t>(max_cl, a.n));
   cfg.gridDim = dim3(static_cast<unsigned>(2 * ncl));

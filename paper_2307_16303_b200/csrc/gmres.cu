@@ -109,6 +109,44 @@ __global__ void __launch_bounds__(256) direct_kernel(const double4* __restrict__
   if (i < n) b[perm[i]] = acc0 + acc1;
 }
 
+// ---- exact rows for reference_error (reference hmatrix.cpp:253-291): row
+// p (Morton position) of K times x, every column, the diagonal rule at j == p
+// (KernelBlock with offset 0) and the full-accuracy radial map. One CTA per
+// sampled row; fixed-order tree reduction (deterministic). Coincident
+// distinct points raise kFlagDegenGeom (lowrank.cpp:34-36).
+template <int K>
+__global__ void __launch_bounds__(256) exact_rows_kernel(const double4* __restrict__ p4, std::int64_t n,
+                                                         double diag, const std::int64_t* __restrict__ rows,
+                                                         double* __restrict__ out, unsigned* flags) {
+  __shared__ double red[8];
+  const std::int64_t p = rows[blockIdx.x];
+  const double4 t = p4[p];
+  double acc = 0.0;
+  bool degen = false;
+  for (std::int64_t j = threadIdx.x; j < n; j += 256) {
+    const double4 s = p4[j];
+    double k;
+    if (j == p) {
+      k = diag;
+    } else {
+      const double r2 = sq3(t.x - s.x, t.y - s.y, t.z - s.z);
+      degen |= r2 < kCoincidentTol2;
+      k = kernel_r2<K>(r2);
+    }
+    acc = fma(k, s.w, acc);
+  }
+  if (degen) atomicOr(flags, kFlagDegenGeom);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w];
+    out[blockIdx.x] = v;
+  }
+}
+
 unsigned grid1(std::int64_t n) {
   return static_cast<unsigned>(std::min<std::int64_t>((n + 255) / 256, 148 * 16));
 }
@@ -155,6 +193,20 @@ void launch_direct(const double* p4, std::int64_t n, int kernel, double diag, co
     default: direct_kernel<kHelmholtz><<<grid, 256, 0, s>>>(q, n, diag, perm, b); break;
   }
   H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_exact_rows(const double* p4, std::int64_t n, int kernel, double diag, const std::int64_t* rows,
+                       std::int64_t nrows, double* out, unsigned* flags, cudaStream_t s) {
+  const double4* q = reinterpret_cast<const double4*>(p4);
+  for (std::int64_t r0 = 0; r0 < nrows; r0 += 65535) {
+    const unsigned g = static_cast<unsigned>(std::min<std::int64_t>(65535, nrows - r0));
+    switch (kernel) {
+      case kLaplace: exact_rows_kernel<kLaplace><<<g, 256, 0, s>>>(q, n, diag, rows + r0, out + r0, flags); break;
+      case kR4: exact_rows_kernel<kR4><<<g, 256, 0, s>>>(q, n, diag, rows + r0, out + r0, flags); break;
+      default: exact_rows_kernel<kHelmholtz><<<g, 256, 0, s>>>(q, n, diag, rows + r0, out + r0, flags); break;
+    }
+    H3D_CUDA_CHECK(cudaGetLastError());
+  }
 }
 
 }  // namespace h3db

@@ -199,7 +199,8 @@ struct Phase2Args {
   double* lvl_part = nullptr;  // [levels with phase-2 work x N] (Morton order)
   // p2_stream: its producer holds the first copy until *wait_flag reaches
   // wait_value (set on the FP64 lane after the solves), so the HBM lane's
-  // CTAs can be resident early without competing with the solves
+  // CTAs can be resident early without competing with the solves. A bounded
+  // throttle, not a dependency: it gives up after kFlagWaitLimitNs
   const unsigned* wait_flag = nullptr;
   unsigned wait_value = 0;
   std::int64_t n_total = 0;    // N
@@ -270,6 +271,9 @@ void launch_sub(double* r, const double* f, const double* w, std::int64_t n, cud
 // b in original order
 void launch_direct(const double* p4, std::int64_t n, int kernel, double diag, const std::int32_t* perm,
                    double* b, cudaStream_t s);
+// exact row sums (K x)[p] at Morton positions rows[0..nrows) (reference_error)
+void launch_exact_rows(const double* p4, std::int64_t n, int kernel, double diag, const std::int64_t* rows,
+                       std::int64_t nrows, double* out, unsigned* flags, cudaStream_t s);
 
 // ------------------------------------------------------------------ ie.cpp
 double unit_cell_integral_constant();

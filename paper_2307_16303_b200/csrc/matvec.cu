@@ -44,6 +44,9 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kP1Cols = 256;    // phase-1 columns per item
 constexpr int kChunk = 256;     // phase-1 proxy: sources staged per round
 constexpr int kMaxRanges = 256; // phase-2 compute: source ranges per tile
+// p2_stream's solves-done throttle gives up after this long (the solves take
+// 0.3-2.5 ms; the flag orders nothing the kernel's results depend on)
+constexpr unsigned long long kFlagWaitLimitNs = 20000000ULL;
 
 // x in Morton order, into xp and the weight lane of the packed points
 __global__ void gather_kernel(const double* __restrict__ x, const std::int32_t* __restrict__ perm,
@@ -1069,11 +1072,16 @@ __global__ void __maxnreg__(64) p2_stream_kernel(const Phase2Args a) {
   stream_init(sm);
   if (warp == 0) {
     const unsigned long long pol = l2_evict_first();
+    // a throttle only (stream-level S columns are complete when this kernel
+    // starts, by stream order): bounded, so the kernel never depends on the
+    // FP64 lane being scheduled beside it
     if (a.wait_flag != nullptr && lane == 0) {
-      unsigned v;
+      const unsigned long long t0 = global_ns();
       for (;;) {
+        unsigned v;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.wait_flag) : "memory");
         if (static_cast<int>(v - a.wait_value) >= 0) break;
+        if (global_ns() - t0 > kFlagWaitLimitNs) break;
         __nanosleep(256);
       }
     }
@@ -1338,8 +1346,8 @@ void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
 // (~130 KB) and the FP64 kernels co-reside on each SM, so they must agree on
 // the SM's L1/shared split.
 void configure_kernels() {
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static PerDeviceOnce once;
+  once([] {
     H3D_CUDA_CHECK(cudaFuncSetAttribute(p1_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(StreamSmem))));
     H3D_CUDA_CHECK(cudaFuncSetAttribute(p2_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

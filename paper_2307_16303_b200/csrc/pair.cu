@@ -336,14 +336,13 @@ std::size_t pair_smem_bytes() { return sizeof(PairSmem); }
 
 void launch_pair(const PairArgs& a, int sms, int per_sm, cudaStream_t s) {
   if (a.n == 0) return;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  attr([] {
     H3D_CUDA_CHECK(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(PairSmem))));
     H3D_CUDA_CHECK(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                         cudaSharedmemCarveoutMaxShared));
-    attr = true;
-  }
+  });
   int nb = 0;
   H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, pair_kernel, kPThreads,
                                                                sizeof(PairSmem)));
