@@ -5,8 +5,9 @@
  * free-function API of /root/reference/proj/include/h3d/hmatrix.hpp and
  * parallel.hpp. Each entry point below names the reference interface it
  * replaces. Plain pointers and sizes only; no torch types. The C++ host layer
- * (paper_2307_16303_b200/csrc/h3d_b200.hpp) restores the reference's C++
- * signatures and exception types on top of this header.
+ * (include/h3d_b200.hpp, implemented in paper_2307_16303_b200/csrc/hmatrix_b200.cpp,
+ * built as lib/libh3d_b200pp.so) restores the reference's C++ signatures and
+ * exception types on top of this header.
  *
  * Error convention: every int-returning call returns H3D_OK (0) or a status
  * below; h3d_last_error() returns the thread-local message. Status codes map
@@ -27,7 +28,7 @@
 extern "C" {
 #endif
 
-#define H3D_B200_ABI_VERSION 3
+#define H3D_B200_ABI_VERSION 4
 
 enum h3d_status {
   H3D_OK = 0,
@@ -213,6 +214,16 @@ int h3d_dev_gmres(h3d_dev* dev, const double* rhs, double* x, int where, double 
  * reference's dense row sums for manufactured right-hand sides
  * (solver.cpp:247-258). Single-shard handles only. */
 int h3d_dev_direct_matvec(h3d_dev* dev, const double* x, double* b, int where);
+/* Replaces h3d::reference_error(rep, x, b_approx, exact_limit, sample_rows,
+ * seed) (hmatrix.hpp:87-93, hmatrix.cpp:253-291): relative 2-norm error of
+ * b (original order) against exact row sums of K x, every row when
+ * N <= exact_limit, else sample_rows Morton positions p drawn as
+ * floor(uniform01(mt19937_64(seed)) * N) (duplicates possible), exactly the
+ * reference's rows. The exact sums run on the device (full-accuracy radial
+ * map, diagonal rule); x and b are host (where = 0) or device (where = 1)
+ * arrays of length N. Defaults of the reference: 4096, 2000, 7. */
+int h3d_dev_reference_error(h3d_dev* dev, const double* x, const double* b, int where, int64_t exact_limit,
+                            int64_t sample_rows, uint64_t seed, double* out);
 /* Collocation helpers of the IE driver: the tensor grid (kernel.cpp:96-109)
  * and the cell self-integral of 1/r (solver.cpp:127-193). */
 int h3d_generate_grid_points(int64_t n, double* xyz);

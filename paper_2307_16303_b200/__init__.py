@@ -24,5 +24,6 @@ from .h3d import (  # noqa: F401
     matvec,
     nccl_unique_id,
     random_vector,
+    reference_error,
     stats,
 )

@@ -164,6 +164,15 @@ int h3d_dev_direct_matvec(h3d_dev* dev, const double* x, double* b, int where) {
   });
 }
 
+int h3d_dev_reference_error(h3d_dev* dev, const double* x, const double* b, int where, int64_t exact_limit,
+                            int64_t sample_rows, uint64_t seed, double* out) {
+  return guarded([&] {
+    if (!dev || !x || !b || !out) throw h3db::InvalidArgument("reference_error: null argument");
+    std::lock_guard<std::mutex> lk(eng(dev)->mu);
+    *out = eng(dev)->reference_error(x, b, where == 0, exact_limit, sample_rows, seed);
+  });
+}
+
 int h3d_generate_grid_points(int64_t n, double* xyz) {
   return guarded([&] {
     if (n < 1) throw h3db::InvalidArgument("generate_points: N must be >= 1");

@@ -157,6 +157,14 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   return r;
 }
 
+// The same as a plain (non-volatile) asm: read-only data the compiler may
+// batch and schedule freely (stored near-field values).
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double r;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ double ld_stream1(const double* p) {
   double r;
   asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));

@@ -17,6 +17,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <random>
+#include <cmath>
 
 #include "nccl_dyn.h"
 
@@ -706,7 +708,9 @@ void Engine::upload_plan() {
   near_off_.upload(P.near_off, stream_);
   near_ids_.upload(P.near_ids.empty() ? std::vector<std::int32_t>{0} : P.near_ids, stream_);
   near_dense_.upload(P.near_dense, stream_);
-  sym_near_ = opt_.near_mode != H3D_NEAR_STORED;
+  // the cached near field runs the same symmetric pass as the matrix-free
+  // one, with the stored values (bitwise-equal results, test_hmatrix.cpp:138-152)
+  sym_near_ = true;
   if (sym_near_) {
     for (std::size_t x = 0; x + 1 < P.sym_off.size(); ++x)
       if (P.sym_off[x + 1] - P.sym_off[x] > kMaxNearRanges)
@@ -769,6 +773,7 @@ void Engine::upload_plan() {
   H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), stream_));
   if (opt_.near_mode == H3D_NEAR_STORED) {
     nf_off_.upload(P.nf_off, stream_);
+    nf_cols_.upload(P.nf_cols, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
   }
   x_.alloc(n_);
@@ -802,6 +807,7 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.near_dense = near_dense_.get();
   if (opt_.near_mode == H3D_NEAR_STORED) {
     a.nf_off = nf_off_.get();
+    a.nf_cols = nf_cols_.get();
     a.NF = NF_.get();
   }
   a.kernel = opt_.kernel_id;
@@ -998,8 +1004,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     H3D_CUDA_CHECK(cudaEventRecord(fork_[2], stream4_));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
     kb(H3D_K_NEAR, stream3_);
-    if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, tune_.nfc, stream3_);
-    else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, tune_.nfc, stream3_);
+    if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, tune_.nfc, stream3_);
     ke(H3D_K_NEAR, stream3_);
     ++launches;
     H3D_CUDA_CHECK(cudaEventRecord(join_[2], stream3_));
@@ -1065,8 +1070,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     }
     if (!near_fork) {
       kb(H3D_K_NEAR, stream4_);
-      if (opt_.near_mode == H3D_NEAR_STORED) launch_p2_compute(a2, sms_, parts ? tune_.p2c : 4, stream4_);
-      else if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
+      if (run(H3D_K_NEAR)) launch_p2_near(a2, sms_, hbm ? tune_.p2c : 4, stream4_);
       ke(H3D_K_NEAR, stream4_);
       ++launches;
     }

@@ -158,7 +158,7 @@ class Engine {
   DevBuf<std::int32_t> sym_off_, sym_ids_, sym_cnt_, in_off_;
   DevBuf<std::int64_t> out_off_, in_pos_;
   DevBuf<double> pairbuf_;  // symmetric near-field column sums (owned pairs)
-  bool sym_near_ = false;   // matrix-free near field with pair symmetry
+  bool sym_near_ = false;   // near field with pair symmetry (always on; both near modes)
   DevBuf<double> cpart_;
   DevBuf<P2Item> p2_items_, p2s_items_;
   DevBuf<StreamDesc> p1s_desc_, p2s_desc_;
@@ -195,6 +195,7 @@ class Engine {
   cudaStream_t stream4_ = nullptr;          // FP64 lane: proxy levels + solves
   cudaEvent_t fork_[3] = {}, join_[3] = {};
   DevBuf<std::int64_t> nf_off_;
+  DevBuf<std::int32_t> nf_cols_;
   DevBuf<double> NF_;
 
   // matvec scratch

@@ -177,8 +177,10 @@ struct Phase2Args {
   const std::int32_t* sym_cnt = nullptr;
   const std::int64_t* out_off = nullptr;
   double* pairbuf = nullptr;
-  // stored near field (near_mode 0): per leaf a column-major m x (sum n) block
+  // stored near field (near_mode 0): per owned leaf a row-major
+  // m x nf_cols block of its dense sources in symmetric-list order (planner.h)
   const std::int64_t* nf_off = nullptr;
+  const std::int32_t* nf_cols = nullptr;
   const double* NF = nullptr;
   int kernel = 0;
   double diag = 0.0;
@@ -206,7 +208,6 @@ struct Phase2Args {
   std::int64_t n_total = 0;    // N
   unsigned* counter3 = nullptr;
 };
-void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 // matrix-free near field + direct leaf blocks (near_mode on-the-fly); near
 // lists of at most kMaxNearRanges leaves (HODLR3D: 27 dense + <= 189 direct)
 constexpr int kMaxNearRanges = 256;

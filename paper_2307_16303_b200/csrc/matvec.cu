@@ -20,9 +20,9 @@
 //               partial sums of tall nodes reduced in fixed order;
 //   solve    proxy_solve_kernel: s = (LU)^-1 v or (U^T L^T)^-1 v in place;
 //   phase 2  p2_stream_kernel : rows of W_A(l) . S_A(l) over stream levels (HBM)
-//            p2_compute_kernel: near field + direct leaf blocks + K(X, P_A) s_A
-//                               over proxy levels, one continuous source walk
-//                               per warp, lane = target row (FP64)
+//            p2_near_kernel   : near field (matrix-free, or the cached values)
+//                               + direct leaf blocks, each owned pair once
+//            p2_proxy_kernel  : K(X, P_A) s_A over proxy levels (FP64)
 //            combine_kernel   : b[perm[p]] = compute + stream (fused un-permute).
 //
 // Every output has one writer and a fixed accumulation order (no atomics), so
@@ -563,197 +563,6 @@ __global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __rest
   }
 }
 
-// ---- phase 2, compute part --------------------------------------------------
-// One leaf tile per work unit. Lane = target row (two rows per lane above 32
-// rows; below, the warp splits into G = 32/mp source groups). Sources: the
-// self block (diagonal rule) read directly, then every other range (near and
-// direct neighbour leaves, proxy lists of the ancestors at proxy levels)
-// flattened into one virtual stream that the CTA stages through shared memory
-// in chunks (many independent loads in flight), each warp evaluating its
-// eighth of every chunk against all rows.
-enum RangeKind : int { kRangeSelf = 0, kRangePoints = 1, kRangeProxy = 2 };
-constexpr int kStage = 512;  // sources staged per chunk (16 KB)
-
-struct TileRanges {
-  std::int64_t start[kMaxRanges];  // first index in its array (points / S space)
-  int pre[kMaxRanges + 1];         // prefix of lengths
-  unsigned char kind[kMaxRanges];
-  int n;
-};
-
-template <int K>
-__device__ __forceinline__ void eval4(const double (&tx)[4], const double (&ty)[4],
-                                      const double (&tz)[4], double (&acc)[4], double2 s0,
-                                      double2 s1) {
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-    acc[r] = fma(kernel_r2_fast<K>(sq3(tx[r] - s0.x, ty[r] - s0.y, tz[r] - s1.x)), s1.y, acc[r]);
-}
-
-// Rows [r0, r0 + nr) of the tile (nr <= 32): warps form ng row groups of 4
-// rows (ng a power of two) x gs = 8 / ng source slices; lanes stride over the
-// sources of the staged chunks; partial sums per (slice, row) are reduced in a
-// fixed order. Returns after writing rowsum[r0 - r0 .. nr).
-template <int K>
-__device__ void compute_pass(const Phase2Args& a, const TileRanges& tr, double2* stage,
-                             std::int64_t xb, int r0, int nr, double* part) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int ng = 1;
-  while (ng * 4 < nr) ng <<= 1;
-  const int gs = kWarps / ng;
-  const int group = warp / gs, slice = warp % gs;
-  double tx[4], ty[4], tz[4], acc[4];
-  int ti[4];
-  bool any = false;
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int i = 4 * group + r;
-    const bool ok = i < nr;
-    any |= ok;
-    const std::int64_t gi = xb + r0 + i;
-    tx[r] = ok ? a.px[gi] : kFar;
-    ty[r] = ok ? a.py[gi] : kFar;
-    tz[r] = ok ? a.pz[gi] : kFar;
-    ti[r] = ok ? r0 + i : -1;
-    acc[r] = 0.0;
-  }
-  const int step = 32 * gs;
-  int vbeg = 0;
-  if (tr.n > 0 && tr.kind[0] == kRangeSelf) {  // self block, diagonal rule
-    const std::int64_t st = tr.start[0];
-    const int len = tr.pre[1];
-    if (any)
-      for (int j = slice * 32 + lane; j < len; j += step) {
-        const double x0 = a.px[st + j], y0 = a.py[st + j], z0 = a.pz[st + j], w0 = a.xp[st + j];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const double k0 = ti[r] == j ? a.diag
-                                       : kernel_r2_fast<K>(sq3(tx[r] - x0, ty[r] - y0, tz[r] - z0));
-          acc[r] = fma(k0, w0, acc[r]);
-        }
-      }
-    vbeg = len;
-  }
-  const int T = tr.pre[tr.n];
-  for (int base = vbeg; base < T; base += kStage) {
-    const int cnt = min(kStage, T - base);
-    __syncthreads();  // previous chunk consumed
-    for (int q = threadIdx.x; q < cnt; q += kThreads) {
-      const int v = base + q;
-      int lo = 0, hi = tr.n - 1;  // range with pre[lo] <= v < pre[lo + 1]
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (tr.pre[mid] <= v) lo = mid;
-        else hi = mid - 1;
-      }
-      const std::int64_t idx = tr.start[lo] + (v - tr.pre[lo]);
-      if (tr.kind[lo] == kRangeProxy) {
-        const double4 r = reinterpret_cast<const double4*>(a.q4)[idx];
-        stage[2 * q] = make_double2(r.x, r.y);
-        stage[2 * q + 1] = make_double2(r.z, a.S[idx]);
-      } else {
-        stage[2 * q] = make_double2(a.px[idx], a.py[idx]);
-        stage[2 * q + 1] = make_double2(a.pz[idx], a.xp[idx]);
-      }
-    }
-    __syncthreads();
-    if (any) {
-      int j = slice * 32 + lane;
-#pragma unroll 1
-      for (; j < cnt; j += step) eval4<K>(tx, ty, tz, acc, stage[2 * j], stage[2 * j + 1]);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const double v = warp_sum(acc[r]);
-    if (lane == 0) part[slice * 32 + 4 * group + r] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < nr) {
-    double v = 0.0;
-    for (int s = 0; s < gs; ++s) v += part[s * 32 + threadIdx.x];
-    part[kWarps * 32 + threadIdx.x] = v;  // pass result
-  }
-  __syncthreads();
-}
-
-// Persistent CTAs pull leaf tiles from a work counter (dynamic balance).
-template <int K, bool STORED>
-__global__ void __launch_bounds__(kThreads, 3) p2_compute_kernel(const Phase2Args a) {
-  __shared__ TileRanges tr;
-  __shared__ double cpart[kWarps * 32 + 32];
-  __shared__ double2 stage[2 * kStage];
-  __shared__ long long s_t;
-  const int L = a.depth;
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_t = static_cast<long long>(atomicAdd(a.counter, 1u));
-    __syncthreads();
-    const long long t = s_t;
-    if (t >= a.nleaves) break;
-    const std::int64_t X = a.leaf0 + t;
-    const std::int64_t xb = a.leaf_off[X];
-    const int mrows = static_cast<int>(a.leaf_off[X + 1] - xb);
-    if (mrows == 0) continue;
-    if (threadIdx.x == 0) {
-      // source ranges: self, neighbours (stored mode: only the direct
-      // partners), then the proxy ranges of the ancestors at proxy levels
-      int n = 0, pre = 0;
-      const std::int32_t nb = a.near_off[X], ne = a.near_off[X + 1];
-      const std::int32_t nd = STORED ? a.near_dense[X] : 0;
-      for (std::int32_t e = nb; e < ne && n < kMaxRanges; ++e) {
-        if (STORED && e - nb < nd) continue;
-        const std::int32_t Y = a.near_ids[e];
-        const std::int64_t yb = a.leaf_off[Y];
-        const int len = static_cast<int>(a.leaf_off[Y + 1] - yb);
-        tr.start[n] = yb;
-        tr.kind[n] = Y == X ? kRangeSelf : kRangePoints;
-        tr.pre[n] = pre;
-        pre += len;
-        ++n;
-      }
-      for (int l = 1; l <= L && n < kMaxRanges; ++l) {
-        if (a.mode[l] != 1 || a.p2_items != nullptr) continue;
-        const std::int64_t g = a.lbase[l] + (X >> (3 * (L - l)));
-        const int R = a.nt.rpad[g];
-        if (R == 0) continue;
-        tr.start[n] = a.nt.soff[g];
-        tr.kind[n] = kRangeProxy;
-        tr.pre[n] = pre;
-        pre += R;
-        ++n;
-      }
-      tr.pre[n] = pre;
-      tr.n = n;
-    }
-    __syncthreads();
-    for (int r0 = 0; r0 < mrows; r0 += 32) {
-      const int m = min(32, mrows - r0);
-      compute_pass<K>(a, tr, stage, xb, r0, m, cpart);
-      if (threadIdx.x < m) {
-        const int i = threadIdx.x;
-        double v = cpart[kWarps * 32 + i];
-        if (STORED) {  // stored dense near blocks, column-major per leaf
-          const std::int32_t nb = a.near_off[X];
-          const std::int32_t nd = a.near_dense[X];
-          const double* nf = a.NF + a.nf_off[X];
-          int c = 0;
-          for (std::int32_t e = nb; e < nb + nd; ++e) {
-            const std::int32_t Y = a.near_ids[e];
-            const std::int64_t yb = a.leaf_off[Y];
-            const int len = static_cast<int>(a.leaf_off[Y + 1] - yb);
-            for (int j = 0; j < len; ++j, ++c)
-              v = fma(nf[static_cast<std::int64_t>(c) * mrows + r0 + i], a.xp[yb + j], v);
-          }
-        }
-        if (a.cpart_out) a.cpart_out[xb + r0 + i] = v;
-        else a.b[a.perm[xb + r0 + i]] = v;
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // ---- phase 2, near field + direct leaf blocks, matrix-free ------------------
 // Warp-specialised persistent CTA: a producer warp claims owned leaves X,
 // builds X's source range table (planner.h sym lists: self | dense one-way |
@@ -783,7 +592,9 @@ struct NearMeta {
   int r0, mr;      // row pass: rows [r0, r0 + mr) of the leaf (mr <= kNearRows)
   int base, cnt;   // flattened index of the chunk's first source, sources in the chunk (< 0: stop)
   int e0, e1, e2, e3;  // flattened ends: self, dense one-way, direct one-way, dense sym
-  int last, pad;   // last chunk of this row pass
+  int last;        // last chunk of this row pass
+  int nds;         // stored near field: dense columns of the leaf (row stride)
+  long long nfb;   // stored near field: the leaf's block offset
 };
 
 struct NearSmem {
@@ -808,11 +619,12 @@ __device__ __forceinline__ double4 ld_src(const double4* __restrict__ st, int j,
 // One row accumulator per row in the admissible (Newton) scale: dense-near
 // terms enter with weight w / far_scale (exact power-of-two scalings), the
 // caller multiplies by far_scale once; column partials likewise.
-template <int K, int RPW, bool DENSE, bool SYM>
+template <int K, int RPW, bool DENSE, bool SYM, bool STORED>
 __device__ __forceinline__ void near_seg(const double4* __restrict__ st, int lo, int hi,
                                          const double (&tx)[RPW], const double (&ty)[RPW],
                                          const double (&tz)[RPW], const double (&tw)[RPW],
-                                         double (&acc)[RPW], double* __restrict__ col, int lane) {
+                                         double (&acc)[RPW], double* __restrict__ col, int lane,
+                                         const double* __restrict__ nf0, int nds, int nvalid, int dbias) {
   constexpr double inv = 1.0 / far_scale<K>();
   const int h = (lane >> 2) & 1;
   for (int j = lo + lane; j < hi; j += 32) {
@@ -822,7 +634,9 @@ __device__ __forceinline__ void near_seg(const double4* __restrict__ st, int lo,
       const double w = inv * q.w;
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-        const double k = kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
+        double k;
+        if constexpr (STORED) k = r < nvalid ? ldg_stream(nf0 + r * nds + j + dbias) : 0.0;
+        else k = kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
         acc[r] = fma(k, w, acc[r]);
         if constexpr (SYM) cp = fma(k, tw[r], cp);
       }
@@ -845,12 +659,18 @@ __device__ __forceinline__ void near_seg(const double4* __restrict__ st, int lo,
   }
 }
 
-template <int K, int RPW>
+// The stored near field (STORED) replaces every dense kernel value by the one
+// the build stored for it (near_store_kernel: the same function of the same
+// operands), so cached and matrix-free matvecs agree bit for bit (reference
+// test_hmatrix.cpp:138-152). Row r of the warp reads nfr[r] (null: padding
+// row) at the source's dense column: flattened index f for f < e1, f - (e2 -
+// e1) in the dense sym segment.
+template <int K, int RPW, bool STORED>
 __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const NearMeta& mt, int row0,
                                            const double (&tx)[RPW], const double (&ty)[RPW],
                                            const double (&tz)[RPW], const double (&tw)[RPW],
                                            double (&acc)[RPW], double* __restrict__ col, double diag,
-                                           int lane) {
+                                           int lane, const double* __restrict__ nf0, int nvalid) {
   constexpr double inv = 1.0 / far_scale<K>();
   const int h = (lane >> 2) & 1;
   const int base = mt.base, cnt = mt.cnt;
@@ -862,26 +682,31 @@ __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const
     const double w = inv * q.w;
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
-      const double k = (row0 + r == base + j) ? diag
-                                              : kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
+      double k;
+      if constexpr (STORED) k = r < nvalid ? ldg_stream(nf0 + r * mt.nds + base + j) : 0.0;
+      else k = (row0 + r == base + j) ? diag : kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
       acc[r] = fma(k, w, acc[r]);
     }
   }
-  near_seg<K, RPW, true, false>(st, c0, c1, tx, ty, tz, tw, acc, col, lane);
-  near_seg<K, RPW, false, false>(st, c1, c2, tx, ty, tz, tw, acc, col, lane);
-  near_seg<K, RPW, true, true>(st, c2, c3, tx, ty, tz, tw, acc, col, lane);
-  near_seg<K, RPW, false, true>(st, c3, cnt, tx, ty, tz, tw, acc, col, lane);
+  near_seg<K, RPW, true, false, STORED>(st, c0, c1, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid, base);
+  near_seg<K, RPW, false, false, false>(st, c1, c2, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
+  near_seg<K, RPW, true, true, STORED>(st, c2, c3, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid,
+                                       base - (mt.e2 - mt.e1));
+  near_seg<K, RPW, false, true, false>(st, c3, cnt, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
 }
 
 // Consumer warp: one row pass of one leaf, starting at the (already waited)
 // stage t; returns the next stage sequence number.
-template <int K, int RPW>
+template <int K, int RPW, bool STORED>
 __device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const NearMeta m0 = sm.meta[t % 2];
   const int row0 = m0.r0 + warp * RPW;
   const double4* P4 = reinterpret_cast<const double4*>(a.p4);
   double tx[RPW], ty[RPW], tz[RPW], tw[RPW], acc[RPW];
+  // stored near field: this warp's first row, rows below nvalid are real
+  const int nvalid = STORED ? max(0, min(RPW, m0.r0 + m0.mr - row0)) : 0;
+  const double* nf0 = STORED ? a.NF + m0.nfb + static_cast<long long>(row0) * m0.nds : nullptr;
 #pragma unroll
   for (int r = 0; r < RPW; ++r) {
     const bool ok = row0 + r < m0.r0 + m0.mr;
@@ -895,7 +720,8 @@ __device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) 
   for (;;) {
     const int s = t % 2;
     const NearMeta mt = sm.meta[s];
-    near_chunk<K, RPW>(sm.stage[s], mt, row0, tx, ty, tz, tw, acc, sm.col[warp], a.diag, lane);
+    near_chunk<K, RPW, STORED>(sm.stage[s], mt, row0, tx, ty, tz, tw, acc, sm.col[warp], a.diag, lane, nf0,
+                               nvalid);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);
     if (mt.base + mt.cnt > mt.e2) {  // chunk holds sym sources: column sums in warp order
@@ -972,7 +798,7 @@ __device__ __forceinline__ void near_put(NearSmem& sm, unsigned t, NearMeta mt, 
   }
 }
 
-template <int K>
+template <int K, bool STORED>
 __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Args a) {
   __shared__ __align__(128) NearSmem sm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1023,6 +849,8 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
       __syncwarp();
       const long long obase = a.out_off[X] - e2;
       const int nchunks = (tot + kNearStage - 1) / kNearStage;
+      const long long nfb = STORED ? a.nf_off[X] : 0;
+      const int nds = STORED ? a.nf_cols[X] : 0;
       for (int r0 = 0; r0 < m; r0 += kNearRows) {
         const int mr = min(kNearRows, m - r0);
         // leaves above one pass have no sym partners (planner.cpp), so the
@@ -1031,14 +859,14 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
         for (int c = 0; c < nchunks; ++c, ++t)
           near_put(sm, t,
                    NearMeta{xb, obase, r0, mr, c * kNearStage, 0, m, e1, e2, e3,
-                            c + 1 == nchunks ? 1 : 0, 0},
+                            c + 1 == nchunks ? 1 : 0, nds, nfb},
                    P4, re, roff, nrange, lane);
       }
       __syncwarp();
     }
     {
       int re = 0, roff = 0;
-      near_put(sm, t, NearMeta{0, 0, 0, 0, 0, -1, 0, 0, 0, 0, 1, 0}, P4, re, roff, 0, lane);
+      near_put(sm, t, NearMeta{0, 0, 0, 0, 0, -1, 0, 0, 0, 0, 1, 0, 0}, P4, re, roff, 0, lane);
     }
     return;
   }
@@ -1048,13 +876,13 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
     const NearMeta mt = sm.meta[t % 2];
     if (mt.cnt < 0) break;
     switch ((mt.mr + kNearConsumers - 1) / kNearConsumers) {
-      case 1: t = near_consume<K, 1>(sm, a, t); break;
-      case 2: t = near_consume<K, 2>(sm, a, t); break;
-      case 3: t = near_consume<K, 3>(sm, a, t); break;
-      case 4: t = near_consume<K, 4>(sm, a, t); break;
-      case 5: t = near_consume<K, 5>(sm, a, t); break;
-      case 6: t = near_consume<K, 6>(sm, a, t); break;
-      default: t = near_consume<K, 7>(sm, a, t); break;
+      case 1: t = near_consume<K, 1, STORED>(sm, a, t); break;
+      case 2: t = near_consume<K, 2, STORED>(sm, a, t); break;
+      case 3: t = near_consume<K, 3, STORED>(sm, a, t); break;
+      case 4: t = near_consume<K, 4, STORED>(sm, a, t); break;
+      case 5: t = near_consume<K, 5, STORED>(sm, a, t); break;
+      case 6: t = near_consume<K, 6, STORED>(sm, a, t); break;
+      default: t = near_consume<K, 7, STORED>(sm, a, t); break;
     }
   }
 }
@@ -1241,40 +1069,60 @@ __global__ void combine_kernel(const double* __restrict__ cpart, const double* _
   }
 }
 
-// Build-time pass over every dense near-field pair: the reference forms all
-// dense leaf blocks during initialize (hmatrix.cpp:124-147), so coincident
-// points raise DegenerateGeometryError there; optionally stores the blocks
-// (column-major per leaf: NF[nf_off[X] + c * m + i]).
+// Build-time pass over every owned leaf's dense sources in its symmetric
+// list order (self | dense one-way | dense sym; planner.cpp): the reference
+// forms all dense leaf blocks during initialize (hmatrix.cpp:124-147), so
+// coincident points raise DegenerateGeometryError here. With NF set (cached
+// near field) it stores, row-major per leaf, exactly the value the
+// matrix-free near pass computes for each (row, dense source) from the same
+// packed points: diag on the self block's diagonal, kernel_r2_fast of the
+// same sq3 operands elsewhere.
 template <int K>
-__global__ void __launch_bounds__(kThreads) near_scan_kernel(const Phase2Args a,
-                                                             double* __restrict__ NF,
-                                                             unsigned* flags) {
+__global__ void __launch_bounds__(kThreads) near_store_kernel(const Phase2Args a, double* __restrict__ NF,
+                                                              unsigned* flags) {
+  __shared__ long long rs[kMaxNearRanges];
+  __shared__ int rpre[kMaxNearRanges + 1];
+  __shared__ int nr;
   const std::int64_t X = a.leaf0 + blockIdx.x;
   const std::int64_t xb = a.leaf_off[X];
   const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
   if (m == 0) return;
-  const std::int32_t nb = a.near_off[X];
-  const std::int32_t nd = a.near_dense[X];
+  const std::int32_t nb = a.sym_off[X];
+  if (threadIdx.x == 0) {
+    const int c0 = a.sym_cnt[4 * X], c1 = a.sym_cnt[4 * X + 1], c2 = a.sym_cnt[4 * X + 2];
+    int n = 0, pre = 0;
+    auto add = [&](std::int32_t e) {
+      const std::int32_t Y = a.sym_ids[nb + e];
+      rs[n] = a.leaf_off[Y];
+      rpre[n] = pre;
+      pre += static_cast<int>(a.leaf_off[Y + 1] - a.leaf_off[Y]);
+      ++n;
+    };
+    add(0);                                               // self
+    for (int e = 0; e < c0; ++e) add(1 + e);              // dense one-way
+    for (int e = 0; e < c2; ++e) add(1 + c0 + c1 + e);    // dense sym
+    rpre[n] = pre;
+    nr = n;
+  }
+  __syncthreads();
+  const int nds = rpre[nr];
+  const double4* P4 = reinterpret_cast<const double4*>(a.p4);
   unsigned f = 0;
-  std::int64_t coff = 0;
-  for (std::int32_t e = nb; e < nb + nd; ++e) {
-    const std::int32_t Y = a.near_ids[e];
-    const std::int64_t yb = a.leaf_off[Y];
-    const int n = static_cast<int>(a.leaf_off[Y + 1] - yb);
-    for (int q = threadIdx.x; q < m * n; q += blockDim.x) {
-      const int j = q / m, i = q % m;
-      const std::int64_t gi = xb + i, gj = yb + j;
-      double v;
-      if (gi == gj) {
-        v = a.diag;
-      } else {
-        const double r2 = sq3(a.px[gi] - a.px[gj], a.py[gi] - a.py[gj], a.pz[gi] - a.pz[gj]);
-        if (r2 < kCoincidentTol2) f |= kFlagDegenGeom;
-        v = kernel_r2_fast<K>(r2);
-      }
-      if (NF) NF[a.nf_off[X] + (coff + j) * m + i] = v;
+  for (long long q = threadIdx.x; q < static_cast<long long>(m) * nds; q += blockDim.x) {
+    const int i = static_cast<int>(q / nds), d = static_cast<int>(q % nds);
+    int lo = 0;
+    while (lo + 1 < nr && rpre[lo + 1] <= d) ++lo;
+    const double4 t = P4[xb + i];
+    const double4 sp = P4[rs[lo] + (d - rpre[lo])];
+    double v;
+    if (lo == 0 && d == i) {
+      v = a.diag;
+    } else {
+      const double r2 = sq3(t.x - sp.x, t.y - sp.y, t.z - sp.z);
+      if (r2 < kCoincidentTol2) f |= kFlagDegenGeom;
+      v = kernel_r2_fast<K>(r2);
     }
-    coff += n;
+    if (NF) NF[a.nf_off[X] + q] = v;
   }
   if (f) atomicOr(flags, f);
 }
@@ -1321,23 +1169,21 @@ void launch_pack_points(const double* px, const double* py, const double* pz, st
 void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   if (a.nleaves == 0) return;
   configure_kernels();
-  switch (a.kernel) {
-    case kLaplace: {
-      const int grid = grid_for(p2_near_kernel<kLaplace>, sms, per_sm, a.nleaves, kNearThreads);
-      p2_near_kernel<kLaplace><<<grid, kNearThreads, 0, s>>>(a);
-      break;
-    }
-    case kR4: {
-      const int grid = grid_for(p2_near_kernel<kR4>, sms, per_sm, a.nleaves, kNearThreads);
-      p2_near_kernel<kR4><<<grid, kNearThreads, 0, s>>>(a);
-      break;
-    }
-    default: {
-      const int grid = grid_for(p2_near_kernel<kHelmholtz>, sms, per_sm, a.nleaves, kNearThreads);
-      p2_near_kernel<kHelmholtz><<<grid, kNearThreads, 0, s>>>(a);
-      break;
-    }
+  const bool stored = a.NF != nullptr;
+#define H3D_P2N(KK)                                                                          \
+  if (stored) {                                                                              \
+    const int grid = grid_for(p2_near_kernel<KK, true>, sms, per_sm, a.nleaves, kNearThreads); \
+    p2_near_kernel<KK, true><<<grid, kNearThreads, 0, s>>>(a);                              \
+  } else {                                                                                   \
+    const int grid = grid_for(p2_near_kernel<KK, false>, sms, per_sm, a.nleaves, kNearThreads); \
+    p2_near_kernel<KK, false><<<grid, kNearThreads, 0, s>>>(a);                             \
   }
+  switch (a.kernel) {
+    case kLaplace: H3D_P2N(kLaplace); break;
+    case kR4: H3D_P2N(kR4); break;
+    default: H3D_P2N(kHelmholtz); break;
+  }
+#undef H3D_P2N
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1361,9 +1207,12 @@ void configure_kernels() {
         reinterpret_cast<const void*>(p2_proxy_kernel<kLaplace>),
         reinterpret_cast<const void*>(p2_proxy_kernel<kR4>),
         reinterpret_cast<const void*>(p2_proxy_kernel<kHelmholtz>),
-        reinterpret_cast<const void*>(p2_near_kernel<kLaplace>),
-        reinterpret_cast<const void*>(p2_near_kernel<kR4>),
-        reinterpret_cast<const void*>(p2_near_kernel<kHelmholtz>),
+        reinterpret_cast<const void*>(p2_near_kernel<kLaplace, false>),
+        reinterpret_cast<const void*>(p2_near_kernel<kR4, false>),
+        reinterpret_cast<const void*>(p2_near_kernel<kHelmholtz, false>),
+        reinterpret_cast<const void*>(p2_near_kernel<kLaplace, true>),
+        reinterpret_cast<const void*>(p2_near_kernel<kR4, true>),
+        reinterpret_cast<const void*>(p2_near_kernel<kHelmholtz, true>),
         reinterpret_cast<const void*>(proxy_solve_kernel),
     };
     for (const void* f : fs)
@@ -1471,26 +1320,6 @@ void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* l
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_p2_compute(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
-  if (a.nleaves == 0) return;
-  const bool stored = a.NF != nullptr;
-#define H3D_P2C(KK)                                                                      \
-  if (stored) {                                                                          \
-    const int grid = grid_for(p2_compute_kernel<KK, true>, sms, per_sm, a.nleaves);      \
-    p2_compute_kernel<KK, true><<<grid, kThreads, 0, s>>>(a);                            \
-  } else {                                                                               \
-    const int grid = grid_for(p2_compute_kernel<KK, false>, sms, per_sm, a.nleaves);     \
-    p2_compute_kernel<KK, false><<<grid, kThreads, 0, s>>>(a);                           \
-  }
-  switch (a.kernel) {
-    case kLaplace: H3D_P2C(kLaplace); break;
-    case kR4: H3D_P2C(kR4); break;
-    default: H3D_P2C(kHelmholtz); break;
-  }
-#undef H3D_P2C
-  H3D_CUDA_CHECK(cudaGetLastError());
-}
-
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
   if (a.n_p2s_items == 0) return;
   const int grid = stream_grid(p2_stream_kernel, sms, per_sm, a.n_p2s_items);
@@ -1545,9 +1374,9 @@ void launch_near_scan(const Phase2Args& a, double* NF_out, unsigned* flags, cuda
   const unsigned grid = static_cast<unsigned>(a.nleaves);
   if (grid == 0) return;
   switch (a.kernel) {
-    case kLaplace: near_scan_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
-    case kR4: near_scan_kernel<kR4><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
-    default: near_scan_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
+    case kLaplace: near_store_kernel<kLaplace><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
+    case kR4: near_store_kernel<kR4><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
+    default: near_store_kernel<kHelmholtz><<<grid, kThreads, 0, s>>>(a, NF_out, flags); break;
   }
   H3D_CUDA_CHECK(cudaGetLastError());
 }

@@ -519,12 +519,9 @@ void Planner::layout() {
   near_off.assign(nl + 1, 0);
   near_dense.assign(nl + 1, 0);
   near_ids.clear();
-  nf_off.assign(nl + 1, 0);
-  nf_total = 0;
   S.near_blocks = S.near_entries = S.direct_evals = 0;
   for (std::int64_t x = 0; x < nl; ++x) {
     near_off[x] = static_cast<std::int32_t>(near_ids.size());
-    nf_off[x] = nf_total;
     const std::int64_t mx = node_size(L_, x);
     if (mx == 0 || x < leaf0 || x >= leaf1) continue;
     std::int64_t ndense_pts = 0;
@@ -552,16 +549,18 @@ void Planner::layout() {
           add(lists_[L_].ids[0][e], false);
     }
     near_dense[x] = nd;
-    nf_total += mx * ndense_pts;
+    (void)ndense_pts;
   }
   near_off[nl] = static_cast<std::int32_t>(near_ids.size());
-  nf_off[nl] = nf_total;
 
   // symmetric matrix-free lists (see planner.h)
   sym_off.assign(nl + 1, 0);
   sym_ids.clear();
   sym_cnt.assign(4 * nl, 0);
   out_off.assign(nl + 1, 0);
+  nf_off.assign(nl + 1, 0);
+  nf_cols.assign(nl + 1, 0);
+  nf_total = 0;
   std::vector<std::vector<std::int64_t>> incoming(nl);
   std::int64_t otot = 0;
   auto own = [&](std::int64_t y) { return y >= leaf0 && y < leaf1; };
@@ -571,6 +570,7 @@ void Planner::layout() {
   for (std::int64_t x = 0; x < nl; ++x) {
     sym_off[x] = static_cast<std::int32_t>(sym_ids.size());
     out_off[x] = otot;
+    nf_off[x] = nf_total;
     if (node_size(L_, x) == 0 || !own(x)) continue;
     std::vector<std::int32_t> cat[4];  // dense one-way, direct one-way, dense sym, direct sym
     auto put = [&](std::int64_t y, bool dense) {
@@ -588,6 +588,11 @@ void Planner::layout() {
           put(lists_[L_].ids[0][e], false);
     }
     sym_ids.push_back(static_cast<std::int32_t>(x));
+    std::int64_t ncols = node_size(L_, x);  // self, then the dense categories 0 and 2
+    for (int c : {0, 2})
+      for (std::int32_t y : cat[c]) ncols += node_size(L_, y);
+    nf_cols[x] = static_cast<std::int32_t>(ncols);
+    nf_total += node_size(L_, x) * ncols;
     for (int c = 0; c < 4; ++c) {
       sym_cnt[4 * x + c] = static_cast<std::int32_t>(cat[c].size());
       for (std::int32_t y : cat[c]) {
@@ -601,6 +606,7 @@ void Planner::layout() {
   }
   sym_off[nl] = static_cast<std::int32_t>(sym_ids.size());
   out_off[nl] = otot;
+  nf_off[nl] = nf_total;
   in_off.assign(nl + 1, 0);
   in_pos.clear();
   for (std::int64_t y = 0; y < nl; ++y) {

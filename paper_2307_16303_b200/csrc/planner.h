@@ -247,7 +247,12 @@ class Planner {
   std::vector<std::int64_t> out_off;  // nl + 1
   std::vector<std::int32_t> in_off;   // nl + 1
   std::vector<std::int64_t> in_pos;
-  std::vector<std::int64_t> nf_off;  // stored near field offsets (per leaf)
+  // stored near field (near_mode 0): per owned leaf X a row-major m x nf_cols[X]
+  // block at nf_off[X], one column per DENSE source of X's symmetric list in
+  // list order (self, dense one-way, dense sym) - exactly the values the
+  // matrix-free near pass evaluates, in its order (bitwise-equal results)
+  std::vector<std::int64_t> nf_off;
+  std::vector<std::int32_t> nf_cols;
   std::int64_t nf_total = 0;
   std::int64_t row0 = 0, row1 = 0;  // owned permuted rows
   std::vector<std::int64_t> rank_row0, rank_row1;

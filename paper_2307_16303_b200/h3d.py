@@ -119,6 +119,7 @@ _EXPORTS = [
     "h3d_dev_profile_read", "h3d_dev_profile_kernels", "h3d_plan_create", "h3d_plan_destroy", "h3d_plan_pairs",
     "h3d_plan_set_ranks", "h3d_plan_set_mode", "h3d_plan_layout", "h3d_plan_array",
     "h3d_dev_gmres", "h3d_dev_direct_matvec", "h3d_generate_grid_points", "h3d_cell_self_integral",
+    "h3d_dev_reference_error",
 ]
 
 
@@ -168,6 +169,8 @@ def _load():
     L.h3d_dev_gmres.argtypes = [P, P, P, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                 C.c_int, P, C.c_int, C.POINTER(_GmresInfo)]
     L.h3d_dev_direct_matvec.argtypes = [P, P, P, C.c_int]
+    L.h3d_dev_reference_error.argtypes = [P, P, P, C.c_int, C.c_int64, C.c_int64, C.c_uint64,
+                                          C.POINTER(C.c_double)]
     L.h3d_generate_grid_points.argtypes = [C.c_int64, P]
     L.h3d_cell_self_integral.argtypes = [C.c_double]
     L.h3d_cell_self_integral.restype = C.c_double
@@ -460,6 +463,20 @@ class HMatrixRep:
         return b
 
 
+    def reference_error(self, x, b_approx, exact_limit: int = 4096, sample_rows: int = 2000,
+                        seed: int = 7) -> float:
+        """Relative 2-norm error of b_approx against exact row sums, rows drawn
+        as the reference does (hmatrix.hpp:87-93, hmatrix.cpp:253-291)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        b = np.ascontiguousarray(b_approx, dtype=np.float64)
+        if x.shape != (self.n,) or b.shape != (self.n,):
+            raise ValueError("reference_error: length mismatch")
+        out = C.c_double(0.0)
+        _check(_L.h3d_dev_reference_error(self._h, _ptr(x), _ptr(b), 0, int(exact_limit),
+                                          int(sample_rows), int(seed), C.byref(out)))
+        return out.value
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_char * 128)()
     _check(_L.h3d_nccl_get_id(C.cast(buf, C.c_void_p)))
@@ -485,6 +502,12 @@ def matvec(rep: HMatrixRep, x, timing: Optional[MatvecTiming] = None) -> np.ndar
 
 def stats(rep: HMatrixRep) -> dict:
     return rep.stats()
+
+
+def reference_error(rep: HMatrixRep, x, b_approx, exact_limit: int = 4096, sample_rows: int = 2000,
+                    seed: int = 7) -> float:
+    """Reference hmatrix.hpp:87-93."""
+    return rep.reference_error(x, b_approx, exact_limit, sample_rows, seed)
 
 
 # ---------------------------------------------------------------- IE solver
