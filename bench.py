@@ -156,10 +156,17 @@ def reference_cpu_run(cfg_name: str, steps: int, warmup: int, n: int | None = No
                       near: str = "matrix-free"):
     """Time the reference CPU matvec (oracle/_ref) on all host cores; n=None:
     the workload's own N, else a bounded sample of that size."""
-    from oracle_lib import RefLib, have_ref
+    from oracle_lib import REF_REL_SO, RefLib, have_ref, host_has_avx512
+    build = "pinned parity build (-O3 -march=x86-64-v3 -ffp-contract=off)"
     if not have_ref():
         from oracle_lib import Oracle
         lib, kind = Oracle(), "port"
+        build = "C restatement oracle/h3d_oracle.c"
+    elif REF_REL_SO.exists() and host_has_avx512():
+        # the reference's release flags (proj/CMakeLists.txt:17: -O3 -march=native
+        # -fno-math-errno) for this AVX-512 host
+        lib, kind = RefLib(REF_REL_SO), "reference"
+        build = "release build (-O3 -march=x86-64-v4 -fno-math-errno, FP contraction on)"
     else:
         lib, kind = RefLib(), "reference"
     cores = os.cpu_count() or 1
@@ -196,7 +203,7 @@ def reference_cpu_run(cfg_name: str, steps: int, warmup: int, n: int | None = No
                 sample=(f"reference matvec (hmatrix.cpp:153-226, OpenMP {cores} threads on {model}) at N={n}, "
                         f"{what} (same generator/kernel/tol/n_max, depth {rep.depth}); "
                         f"mean of {steps} steps after {warmup} warm-up; initialize {init_s:.1f} s untimed"),
-                init_s=init_s, ms_per_step=mean * 1e3, n=n, cpu_model=model, depth=rep.depth)
+                init_s=init_s, ms_per_step=mean * 1e3, n=n, cpu_model=model, depth=rep.depth, build=build)
 
 
 # ------------------------------------------------------------------ main
@@ -232,7 +239,8 @@ def main():
                 "detail": {"n": r["n"], "depth": r["depth"], "initialize_s": round(r["init_s"], 2),
                            "threads": r["cores"], "cpu_model": r["cpu_model"],
                            "build": "oracle/Makefile: unmodified /root/reference/proj/src compiled "
-                                    "in place (-O3, OpenMP) against the Eigen/doctest API shims"},
+                                    "in place with OpenMP against the Eigen/doctest API shims, "
+                                    + r["build"]},
                 "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": r["value"], "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}

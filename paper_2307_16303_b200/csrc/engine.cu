@@ -152,6 +152,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "nf") tune_.nf = v;
         else if (k == "nfc") tune_.nfc = v;
         else if (k == "fw") tune_.fw = v;
+        else if (k == "sol") tune_.sol = v;
         else if (k == "pps") tune_.pps = v;
         else if (k == "graphs") tune_.graphs = v;
       }
@@ -664,6 +665,9 @@ void Engine::upload_plan() {
   std::vector<ProxySeg> solve;
   for (const auto& s : P.proxy_segs)
     if (s.solve) solve.push_back(s);
+  // largest blocks first: the solve kernel hands segments round-robin to its
+  // warps, so the long ones start early and the short ones fill in
+  std::stable_sort(solve.begin(), solve.end(), [](const ProxySeg& a, const ProxySeg& b) { return a.r > b.r; });
   n_segs_all_ = static_cast<std::int64_t>(P.proxy_segs.size());
   n_segs_solve_ = static_cast<std::int64_t>(solve.size());
   segs_all_.upload(P.proxy_segs, stream_);
@@ -1017,7 +1021,8 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   }
   if (n_segs_solve_ > 0) {
     kb(H3D_K_SOLVE, stream4_);
-    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), stream4_);
+    launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), sms_, tune_.sol,
+                       stream4_);
     ke(H3D_K_SOLVE, stream4_);
     ++launches;
   }

@@ -114,9 +114,10 @@ class Engine {
   // results are wrong; honoured only in a -DH3D_DEVTOOLS build)
   // ("nf=0": near field after p2_proxy instead of forked beside the solves;
   // "nfc": CTAs per SM of the forked near kernel; "fw=0": p2_stream does not
-  // wait for the solves-done flag)
+  // wait for the solves-done flag; "sol": CTAs per SM of the proxy solve)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1, fw = 1;
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1, fw = 1,
+        sol = 4;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;

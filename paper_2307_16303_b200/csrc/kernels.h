@@ -142,9 +142,11 @@ void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int
                          const double* px, const double* py, const double* pz, const double* cen,
                          double* q4, double* q4c, cudaStream_t s);
 // lu holds 2 x lu_total doubles: the packed inverses row-major, then column-major
-// in place on S: v (phase-1 output) -> the solved t-vector
-void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
-                        std::int64_t lu_total, double* S, cudaStream_t s);
+// in place on S: v (phase-1 output) -> the solved t-vector; persistent CTAs
+// (per_sm per SM at most), segments round-robin over the warps (host-sorted
+// by decreasing rank), r <= 320
+void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, std::int64_t lu_total,
+                        double* S, int sms, int per_sm, cudaStream_t s);
 // build time: replace every pair's packed LU by its triangular inverses
 // (strict lower L^-1, upper R^-1), row-major at lu and column-major at lu + lu_total
 void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::int64_t lu_total,

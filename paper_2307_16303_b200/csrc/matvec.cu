@@ -453,113 +453,200 @@ __global__ void lu_invert_kernel(const ProxySeg* __restrict__ segs, std::int64_t
   }
 }
 
-// One ordered proxy block per warp, in place on S; lane owns outputs
-// i = lane + 32 k (k < NK), the loop runs over the other index so every
-// matrix access is a coalesced row (side 1, row-major P) or column (side 0,
-// column-major PT) and the only cross-lane traffic is a shared broadcast.
+// ---- proxy solves: one ordered proxy block per warp, in place on S -------
+// Lane owns outputs i = lane + 32 k (k < NK = ceil(r / 32)). Both triangular
+// factors are applied in ONE pass over the rows of the r x r inverse block
+// (column-major PT for side 0, row-major P for side 1), so every block is
+// read from HBM once per orientation (2 x 8 r^2 bytes per pair):
 //   side 0 (target = pair's row side X):  s = R^-1 (L^-1 v)       (lowrank.cpp:310-320)
+//     row j of PT: w_j = v_j + (tail sums so far) is complete (rows < j added
+//     their strictly-lower parts), then head i <= j: s_i += PT[j][i] w_j and
+//     tail i > j: t_i += PT[j][i] v_j
 //   side 1 (target = pair's col side Y):  s = L^-T (R^-T v)       (the transposed block)
-// One GEMV sweep of the solve: acc[k] (lane output i = lane + 32 k) +=
-// M[j][i] x[j] over rows j of M with pred(i, j). The loads of B rows are
-// issued unconditionally (clamped indices, distinct registers) before any
-// FMA, so a warp keeps B x NK loads in flight instead of waiting one memory
-// latency per row (the predicated load -> FMA form serialises).
-template <int NK, int B, class Pred>
-__device__ __forceinline__ void tri_sweep(const double* __restrict__ M, int r, int j0, const double* x,
-                                          double (&acc)[NK], int lane, Pred pred) {
-  for (int jb = j0; jb < r; jb += B) {
-    double c[B][NK], xv[B];
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int j = min(jb + u, r - 1);
-      xv[u] = x[j];
-      const double* row = M + static_cast<std::int64_t>(j) * r;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) c[u][k] = row[min(lane + 32 * k, r - 1)];
-    }
-#pragma unroll
-    for (int u = 0; u < B; ++u) {
-      const int j = jb + u;
-#pragma unroll
-      for (int k = 0; k < NK; ++k) {
-        const int i = lane + 32 * k;
-        if (j < r && i < r && pred(i, j)) acc[k] = fma(c[u][k], xv[u], acc[k]);
-      }
-    }
+//     row i of P: tail j >= i: u_j += P[i][j] v_i (u_i is then complete),
+//     head j < i: s_j += P[i][j] u_i; finally s_j += u_j
+// The completed value of row j lives in lane j % 32's register j / 32 and is
+// broadcast with one shuffle. Fixed order per output: deterministic.
+//
+// The rows stream through shared memory: every warp runs its own bulk-copy
+// ring (kSolveStages stages of up to kSolveStageD doubles, blocks of whole
+// rows, lane 0 issues cp.async.bulk into the stage it just consumed), so the
+// copies of the next blocks - across segment boundaries - are in flight while
+// the warp works through the current rows from shared memory. Segments are
+// assigned round-robin over all warps of the grid (host-sorted by
+// decreasing rank for balance).
+#ifndef H3D_SOLVE_STAGES
+#define H3D_SOLVE_STAGES 2
+#endif
+constexpr int kSolveWarps = 4;
+constexpr int kSolveStages = H3D_SOLVE_STAGES;
+constexpr int kSolveStageD = 640;  // 5 KB per stage: two rows of the largest block (r <= 320)
+constexpr int kSolveMaxR = 320;
+static_assert(kSolveStageD >= 2 * kSolveMaxR, "a stage holds at least two rows");
+
+struct SolveSmem {
+  double ring[kSolveWarps][kSolveStages][kSolveStageD];
+  double v[kSolveWarps][kSolveMaxR];
+  unsigned long long full[kSolveWarps][kSolveStages];
+};
+
+// rows per staged block (even, so every block starts 16-byte aligned)
+__device__ __forceinline__ int solve_block_rows(int r) { return max(2, (kSolveStageD / r) & ~1); }
+
+struct SolveIssue {
+  long long k;  // index in this warp's segment list
+  int row;      // next row of that segment to copy
+  unsigned n;   // blocks issued so far
+};
+
+struct SolveCtx {
+  const ProxySeg* segs;
+  std::int64_t nseg;
+  long long gw, nw;  // this warp's global index, warps in the grid
+  const double* lu;
+  std::int64_t lu_total;
+  unsigned long long pol;
+};
+
+// lane 0: copy the next row block of this warp's segment stream (if any) into
+// stage n % kSolveStages
+__device__ __forceinline__ void solve_issue(SolveSmem& sm, int w, SolveIssue& is, const SolveCtx& cx) {
+  const long long sidx = cx.gw + is.k * cx.nw;
+  if (sidx >= cx.nseg) return;
+  const ProxySeg sg = cx.segs[sidx];
+  const int r = sg.r, rb = solve_block_rows(r);
+  const int nrow = min(rb, r - is.row);
+  long long nd = static_cast<long long>(nrow) * r;
+  nd += nd & 1;  // 16-byte multiple (the packed slot has r^2 + (r & 1) doubles)
+  const double* src = cx.lu + sg.lu_off + (sg.side == 0 ? cx.lu_total : 0) + static_cast<long long>(is.row) * r;
+  const int st = is.n % kSolveStages;
+  mbar_arrive_tx(&sm.full[w][st], static_cast<unsigned>(nd * 8));
+  bulk_g2s(sm.ring[w][st], src, static_cast<unsigned>(nd * 8), &sm.full[w][st], cx.pol);
+  ++is.n;
+  is.row += nrow;
+  if (is.row >= r) {
+    is.row = 0;
+    ++is.k;
   }
 }
 
-template <int NK>
-__device__ __forceinline__ void solve_seg(const ProxySeg& sg, const double* __restrict__ P,
-                                          const double* __restrict__ PT, double* v, double* w,
-                                          double* __restrict__ out, int lane) {
-  constexpr int B = NK <= 2 ? 8 : NK <= 4 ? 4 : 2;
-  const int r = sg.r;
-  double acc[NK];
+template <int NK, bool SIDE1>
+__device__ __forceinline__ void solve_rows(SolveSmem& sm, int w, int lane, int r, const double* v,
+                                           double* __restrict__ out, unsigned& c, SolveIssue& is,
+                                           const SolveCtx& cx) {
+  double t[NK], acc[NK];
 #pragma unroll
-  for (int k = 0; k < NK; ++k) acc[k] = 0.0;
-  if (sg.side == 0) {
-    // w = L^-1 v: w_i = v_i + sum_{j<i} PT[j][i] v_j
-    tri_sweep<NK, B>(PT, r, 0, v, acc, lane, [](int i, int j) { return i > j; });
+  for (int k = 0; k < NK; ++k) {
+    t[k] = 0.0;
+    acc[k] = 0.0;
+  }
+  const int rb = solve_block_rows(r);
+  for (int j0 = 0; j0 < r; j0 += rb) {
+    const int st = c % kSolveStages;
+    mbar_wait(&sm.full[w][st], (c / kSolveStages) & 1);
+    const double* blk = sm.ring[w][st];
+    const int j1 = min(r, j0 + rb);
+    for (int j = j0; j < j1; ++j) {
+      const double* row = blk + (j - j0) * r;
+      const double vj = v[j];
+      const int kj = j >> 5, lj = j & 31;
+      double cv[NK];
 #pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      const int i = lane + 32 * k;
-      if (i < r) w[i] = v[i] + acc[k];
-      acc[k] = 0.0;
+      for (int k = 0; k < NK; ++k) {
+        const int i = lane + 32 * k;
+        cv[k] = i < r ? row[i] : 0.0;
+      }
+      if constexpr (!SIDE1) {
+        double tj = t[0];
+#pragma unroll
+        for (int k = 1; k < NK; ++k) tj = k == kj ? t[k] : tj;
+        const double wj = vj + __shfl_sync(0xffffffffu, tj, lj);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int i = lane + 32 * k;
+          if (i <= j) acc[k] = fma(cv[k], wj, acc[k]);
+          else t[k] = fma(cv[k], vj, t[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int i = lane + 32 * k;
+          if (i >= j) t[k] = fma(cv[k], vj, t[k]);
+        }
+        double tj = t[0];
+#pragma unroll
+        for (int k = 1; k < NK; ++k) tj = k == kj ? t[k] : tj;
+        const double uj = __shfl_sync(0xffffffffu, tj, lj);
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+          const int i = lane + 32 * k;
+          if (i < j) acc[k] = fma(cv[k], uj, acc[k]);
+        }
+      }
     }
-    __syncwarp();
-    // s = R^-1 w: s_i = sum_{j>=i} PT[j][i] w_j
-    tri_sweep<NK, B>(PT, r, 0, w, acc, lane, [](int i, int j) { return i <= j; });
-  } else {
-    // u = R^-T v: u_j = sum_{i<=j} P[i][j] v_i   (here: lane output j, rows i)
-    tri_sweep<NK, B>(P, r, 0, v, acc, lane, [](int j, int i) { return j >= i; });
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      const int j = lane + 32 * k;
-      if (j < r) w[j] = acc[k];
-    }
-    __syncwarp();
-    // s = L^-T u: s_j = u_j + sum_{i>j} P[i][j] u_i
-    tri_sweep<NK, B>(P, r, 1, w, acc, lane, [](int j, int i) { return j < i; });
+    __syncwarp();  // every lane is done with this stage
+    ++c;
+    if (lane == 0) solve_issue(sm, w, is, cx);
   }
 #pragma unroll
   for (int k = 0; k < NK; ++k) {
     const int i = lane + 32 * k;
-    if (i < r) out[i] = acc[k];  // in place over v
+    if (i < r) out[i] = SIDE1 ? t[k] + acc[k] : acc[k];  // in place over v
   }
 }
 
-__global__ void __launch_bounds__(128) proxy_solve_kernel(const ProxySeg* __restrict__ segs,
-                                                          std::int64_t nseg,
-                                                          const double* __restrict__ lu,
-                                                          std::int64_t lu_total,
-                                                          double* __restrict__ S) {
-  __shared__ double sh[4][640];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const std::int64_t s = blockIdx.x * static_cast<std::int64_t>(blockDim.x >> 5) + warp;
-  if (s >= nseg) return;
-  const ProxySeg sg = segs[s];
-  const int r = sg.r;
-  double* v = sh[warp];  // v and w, r <= 320 (enforced on the host)
-  double* w = v + 320;
-  double* Sg = S + sg.so;
-  double* out = Sg;
-  for (int q = lane; q < r; q += 32) v[q] = Sg[q];
+template <int NK>
+__device__ __noinline__ void solve_seg(SolveSmem& sm, int w, int lane, const ProxySeg& sg, const double* v,
+                                       double* out, unsigned& c, SolveIssue& is, const SolveCtx& cx) {
+  if (sg.side == 0) solve_rows<NK, false>(sm, w, lane, sg.r, v, out, c, is, cx);
+  else solve_rows<NK, true>(sm, w, lane, sg.r, v, out, c, is, cx);
+}
+
+__global__ void __launch_bounds__(32 * kSolveWarps) proxy_solve_kernel(const ProxySeg* __restrict__ segs,
+                                                                        std::int64_t nseg,
+                                                                        const double* __restrict__ lu,
+                                                                        std::int64_t lu_total,
+                                                                        double* __restrict__ S) {
+  extern __shared__ __align__(128) unsigned char solve_smem[];
+  SolveSmem& sm = *reinterpret_cast<SolveSmem*>(solve_smem);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SolveCtx cx;
+  cx.segs = segs;
+  cx.nseg = nseg;
+  cx.nw = static_cast<long long>(gridDim.x) * kSolveWarps;
+  cx.gw = static_cast<long long>(blockIdx.x) * kSolveWarps + w;
+  cx.lu = lu;
+  cx.lu_total = lu_total;
+  cx.pol = l2_evict_first();
+  if (lane == 0) {
+    for (int st = 0; st < kSolveStages; ++st) mbar_init(&sm.full[w][st], 1);
+    mbar_fence_init();
+  }
   __syncwarp();
-  const double* P = lu + sg.lu_off;
-  const double* PT = P + lu_total;
-  switch ((r + 31) >> 5) {
-    case 0: break;
-    case 1: solve_seg<1>(sg, P, PT, v, w, out, lane); break;
-    case 2: solve_seg<2>(sg, P, PT, v, w, out, lane); break;
-    case 3: solve_seg<3>(sg, P, PT, v, w, out, lane); break;
-    case 4: solve_seg<4>(sg, P, PT, v, w, out, lane); break;
-    case 5: solve_seg<5>(sg, P, PT, v, w, out, lane); break;
-    case 6: solve_seg<6>(sg, P, PT, v, w, out, lane); break;
-    case 7: solve_seg<7>(sg, P, PT, v, w, out, lane); break;
-    case 8: solve_seg<8>(sg, P, PT, v, w, out, lane); break;
-    case 9: solve_seg<9>(sg, P, PT, v, w, out, lane); break;
-    default: solve_seg<10>(sg, P, PT, v, w, out, lane); break;
+  SolveIssue is{0, 0, 0};
+  if (lane == 0)
+    for (int st = 0; st < kSolveStages; ++st) solve_issue(sm, w, is, cx);
+  unsigned c = 0;
+  double* v = sm.v[w];
+  for (long long sidx = cx.gw; sidx < nseg; sidx += cx.nw) {
+    const ProxySeg sg = segs[sidx];
+    double* Sg = S + sg.so;
+    for (int q = lane; q < sg.r; q += 32) v[q] = Sg[q];
+    __syncwarp();
+    switch ((sg.r + 31) >> 5) {
+      case 0: break;
+      case 1: solve_seg<1>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 2: solve_seg<2>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 3: solve_seg<3>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 4: solve_seg<4>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 5: solve_seg<5>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 6: solve_seg<6>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 7: solve_seg<7>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 8: solve_seg<8>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      case 9: solve_seg<9>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+      default: solve_seg<10>(sm, w, lane, sg, v, Sg, c, is, cx); break;
+    }
+    __syncwarp();  // v is reused by the next segment
   }
 }
 
@@ -1198,6 +1285,8 @@ void configure_kernels() {
                                         static_cast<int>(sizeof(StreamSmem))));
     H3D_CUDA_CHECK(cudaFuncSetAttribute(p2_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         static_cast<int>(sizeof(StreamSmem))));
+    H3D_CUDA_CHECK(cudaFuncSetAttribute(proxy_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(SolveSmem))));
     const void* fs[] = {
         reinterpret_cast<const void*>(p1_stream_kernel),
         reinterpret_cast<const void*>(p2_stream_kernel),
@@ -1311,12 +1400,17 @@ void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::
   H3D_CUDA_CHECK(cudaFreeAsync(scratch, s));
 }
 
-void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu,
-                        std::int64_t lu_total, double* S, cudaStream_t s) {
+void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, std::int64_t lu_total,
+                        double* S, int sms, int per_sm, cudaStream_t s) {
   if (nseg == 0) return;
-  constexpr int warps = 4;
-  proxy_solve_kernel<<<static_cast<unsigned>((nseg + warps - 1) / warps), 32 * warps, 0, s>>>(
-      segs, nseg, lu, lu_total, S);
+  configure_kernels();
+  int nb = 0;
+  H3D_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, proxy_solve_kernel, 32 * kSolveWarps,
+                                                               sizeof(SolveSmem)));
+  const std::int64_t want = (nseg + kSolveWarps - 1) / kSolveWarps;
+  const int grid = static_cast<int>(std::max<std::int64_t>(
+      1, std::min<std::int64_t>(want, static_cast<std::int64_t>(sms) * std::max(1, std::min(nb, per_sm)))));
+  proxy_solve_kernel<<<grid, 32 * kSolveWarps, sizeof(SolveSmem), s>>>(segs, nseg, lu, lu_total, S);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -19,6 +19,16 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[1]
 ORACLE_SO = ROOT / "oracle" / "liboracle.so"
 REF_SO = ROOT / "oracle" / "_ref" / "libh3dref.so"
+# the same reference sources with release flags for an AVX-512 host (timing only)
+REF_REL_SO = ROOT / "oracle" / "_ref" / "libh3dref_rel.so"
+
+
+def host_has_avx512() -> bool:
+    try:
+        flags = next(l for l in open("/proc/cpuinfo") if l.startswith("flags")).split()
+    except (OSError, StopIteration):
+        return False
+    return all(f in flags for f in ("avx512f", "avx512dq", "avx512cd", "avx512bw", "avx512vl"))
 
 KERNELS = {"laplace3d": 0, "r4": 1, "helmholtz-re": 2}
 VARIANTS = {"hodlr3d": 0, "hodlr": 1, "hstrong": 2}  # h3d::Variant order (octree.hpp:80)

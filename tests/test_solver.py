@@ -36,6 +36,15 @@ def test_unit_cell_constant_frozen():
     assert h3d.cell_self_integral(0.125) == pytest.approx(h3d.cell_self_integral(0.25) / 4, rel=1e-15)
 
 
+def test_unit_cell_constant_against_closed_form():
+    # integral of 1/|u| over [-1/2, 1/2]^3 = 3 ln(2 + sqrt 3) - pi/2 (the
+    # reference's quadrature value is within a few ulp of it)
+    import math
+    h3d = _pkg()
+    exact = 3 * math.log(2 + math.sqrt(3)) - math.pi / 2
+    assert h3d.cell_self_integral(1.0) == pytest.approx(exact, rel=1e-14)
+
+
 def test_cell_self_integral_scales_as_h_squared():
     h3d = _pkg()
     c = h3d.cell_self_integral(1.0)
