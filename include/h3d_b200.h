@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define H3D_B200_ABI_VERSION 4
+#define H3D_B200_ABI_VERSION 5
 
 enum h3d_status {
   H3D_OK = 0,
@@ -82,7 +82,12 @@ typedef struct {
   int mode_policy;
   int level_modes[16];
   int variant;          /* h3d_variant (Variant argument of initialize, hmatrix.hpp:57-58) */
-  int64_t reserved[4];
+  /* Multi-GPU: 1 = every rank returns the FULL b, as parallel_matvec does
+   * (its final gather in fixed worker order, parallel.cpp:284-290): the owned
+   * Morton slices are all-gathered over NCCL after the matvec. 0 (default):
+   * each rank writes only its owned rows of b. */
+  int64_t gather_b;
+  int64_t reserved[3];
 } h3d_options;
 
 /* Per-call matvec timing, milliseconds (CUDA events on the engine stream);
@@ -249,6 +254,18 @@ int h3d_dev_export_pairs(const h3d_dev* dev, int level, int32_t* x, int32_t* y, 
  * broadcasts the 128 bytes; every rank attaches before its first matvec. */
 int h3d_nccl_get_id(void* id128);
 int h3d_dev_attach_nccl(h3d_dev* dev, const void* id128, int rank, int world);
+/* Exchange volume of this rank (analogue of h3d::CommLedger,
+ * parallel.hpp:38-51): doubles received per matvec by the x all-gather and
+ * (gather_b) the b all-gather, NCCL collectives per matvec, and matvecs run
+ * with the communicator attached. Zero with no communicator. */
+typedef struct {
+  int64_t x_gather_doubles;
+  int64_t b_gather_doubles;
+  int64_t collectives;
+  int64_t matvecs;
+  int64_t reserved[4];
+} h3d_comm_ledger;
+int h3d_dev_comm_ledger(const h3d_dev* dev, h3d_comm_ledger* out);
 
 /* Host planner (no GPU): the shard ownership, column layout, work items and
  * leaf lists the engine derives from the tree, for CPU verification of the

@@ -96,6 +96,7 @@ struct HmatOptions {
   // 1 auto, 2 explicit level_modes).
   int device = 0;
   int mode_policy = 1;
+  int gather_b = 0;  // multi-GPU: every rank returns the full b (h3d_options.gather_b)
 };
 
 /// Raised on CUDA / NCCL / allocation failures inside the engine.

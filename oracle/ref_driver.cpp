@@ -117,6 +117,20 @@ int h3dref_initialize(const double* xyz, std::int64_t n, int kernel_id, double d
   });
 }
 
+// octree.cpp:76-171 + 197-260 only (no ACA): the tree and lists of a large
+// configuration for the bit-exact digest (tests/golden/make_golden_large.py)
+int h3dref_tree_lists(const double* xyz, std::int64_t n, int n_max, int variant, void** out) {
+  *out = nullptr;
+  return guarded([&] {
+    const PointSet ps = pointset_of(xyz, n);
+    auto h = std::make_unique<RefHandle>();
+    h->rep.variant = static_cast<Variant>(variant);
+    h->rep.tree = build_tree(ps, n_max);
+    h->rep.lists = build_interaction_lists(h->rep.tree, h->rep.variant);
+    *out = h.release();
+  });
+}
+
 void h3dref_free(void* h) { delete static_cast<RefHandle*>(h); }
 
 // hmatrix.cpp:153-226; timing = {wall, dense_gen, matvec_seconds}

@@ -68,6 +68,7 @@ void h3d_default_options(h3d_options* o) {
   o->shard_rank = 0;
   o->shard_world = 1;
   o->mode_policy = 1;  // auto: direct leaf level, stream/proxy split by the cost model
+  o->gather_b = 0;
 }
 
 // generate_points(UniformRandom, n, seed) (kernel.cpp:88-95) with the same
@@ -161,6 +162,13 @@ int h3d_dev_direct_matvec(h3d_dev* dev, const double* x, double* b, int where) {
     if (!dev || !x || !b) throw h3db::InvalidArgument("direct_matvec: null argument");
     std::lock_guard<std::mutex> lk(eng(dev)->mu);
     eng(dev)->direct_matvec(x, b, where == 0);
+  });
+}
+
+int h3d_dev_comm_ledger(const h3d_dev* dev, h3d_comm_ledger* out) {
+  return guarded([&] {
+    if (!dev || !out) throw h3db::InvalidArgument("comm_ledger: null argument");
+    eng(dev)->comm_ledger(out);
   });
 }
 

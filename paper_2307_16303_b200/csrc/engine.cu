@@ -929,6 +929,10 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // HBM near peak, the FP64 kernels fill the remaining registers.
   const bool has_p2 = P.leaf1 > P.leaf0;
   const bool parts = n_lvl_ > 0 || sym_near_;  // near pass writes partials, combine sums them
+  // (with a 1-rank communicator the gather runs too: the path is exercised on one GPU)
+  const bool gather_b = (opt_.gather_b != 0 || force_gather_) && nccl_comm_ != nullptr;
+  if (opt_.gather_b != 0 && nccl_comm_ == nullptr && world_ > 1)
+    throw InvalidArgument("matvec: gather_b needs a communicator (attach_nccl) on a sharded handle");
   const bool pair_lv = pd_level_.size() > 1 && pd_level_.back() > 0;
   const bool hbm = n_p1s_ > 0 || n_p2s_ > 0 || pair_lv;
   const bool fused_lv = fd_level_.size() > 1 && fd_level_.back() > 0;
@@ -1088,10 +1092,27 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     kb(H3D_K_COMBINE, s);
     launch_combine(cpart_.get(), lvl_part_.get(), n_lvl_, n_, leaf_off_.get(), P.leaf0, P.leaf1 - P.leaf0,
                    sym_near_ ? in_off_.get() : nullptr, sym_near_ ? in_pos_.get() : nullptr,
-                   sym_near_ ? pairbuf_.get() : nullptr, perm_.get(), bout, s);
+                   sym_near_ ? pairbuf_.get() : nullptr, perm_.get(), bout,
+                   gather_b ? bm_.get() : nullptr, s);
     ke(H3D_K_COMBINE, s);
     ++launches;
   }
+  if (gather_b) {
+    // the full b on every rank (parallel.cpp:284-290): each rank's owned
+    // Morton slice to all, then the other ranks' rows to the original order
+    auto comm = static_cast<ncclComm_t>(nccl_comm_);
+    NCCL_CHECK(nccl().GroupStart());
+    for (int r = 0; r < world_; ++r) {
+      const std::int64_t c = P.rank_row1[r] - P.rank_row0[r];
+      if (c > 0)
+        NCCL_CHECK(nccl().Broadcast(bm_.get() + P.rank_row0[r], bm_.get() + P.rank_row0[r],
+                                 static_cast<std::size_t>(c), ncclDouble, r, comm, s));
+    }
+    NCCL_CHECK(nccl().GroupEnd());
+    launch_unpermute_rest(bm_.get(), perm_.get(), n_, P.row0, P.row1, bout, s);
+    ++launches;
+  }
+  if (nccl_comm_ != nullptr) ++comm_matvecs_;
   if (ev) cudaEventRecord(ev[3], s);
   return launches;
 }
@@ -1289,6 +1310,24 @@ void Engine::attach_nccl(const void* id128, int rank, int world) {
   ncclComm_t comm;
   NCCL_CHECK(nccl().CommInitRank(&comm, world, id, rank));
   nccl_comm_ = comm;
+  if (opt_.gather_b != 0) bm_.alloc(static_cast<std::size_t>(n_));
+  // captured graphs of an unattached handle must not be replayed (no exchange)
+  for (auto& g : graphs_)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  graphs_.clear();
+}
+
+void Engine::comm_ledger(h3d_comm_ledger* out) const {
+  std::memset(out, 0, sizeof(*out));
+  if (nccl_comm_ == nullptr) return;
+  const Planner& P = *plan_;
+  const std::int64_t owned = P.row1 - P.row0;
+  int slices = 0;
+  for (int r = 0; r < world_; ++r) slices += P.rank_row1[r] > P.rank_row0[r] ? 1 : 0;
+  out->x_gather_doubles = n_ - owned;
+  out->b_gather_doubles = opt_.gather_b != 0 ? n_ - owned : 0;
+  out->collectives = slices * (opt_.gather_b != 0 ? 2 : 1);
+  out->matvecs = comm_matvecs_;
 }
 
 void Engine::stats(h3d_stats* s) const {
@@ -1377,7 +1416,7 @@ namespace h3db {
 // ---------------------------------------------------------------- solver
 void Engine::direct_matvec(const double* x, double* b, bool host) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
-  if (world_ != 1) throw InvalidArgument("direct_matvec: single-shard handles only");
+  // every point is resident on every shard: the exact product runs whole here
   begin_call(stream_);
   const double* xin = x;
   if (host) {
@@ -1448,7 +1487,19 @@ void Engine::gmres(const double* rhs, double* xout, bool host, double alpha, dou
                    int restart, int max_iter, double* hist, int hist_cap, h3d_gmres_info* info) {
   H3D_CUDA_CHECK(cudaSetDevice(opt_.device));
   if (!(tol > 0)) throw InvalidArgument("gmres: tol must be positive");
-  if (world_ != 1) throw InvalidArgument("gmres: single-shard handles only (Krylov vectors are not sharded)");
+  // sharded handles: the Krylov vectors are replicated on every rank and each
+  // operator application all-gathers b (force_gather_), so every rank runs
+  // the same deterministic iteration on full vectors
+  if (world_ != 1 && nccl_comm_ == nullptr)
+    throw InvalidArgument("gmres: a sharded handle needs its communicator (attach_nccl)");
+  struct GatherScope {
+    Engine* e;
+    explicit GatherScope(Engine* en) : e(en) {
+      if (e->nccl_comm_ != nullptr && e->bm_.size() == 0) e->bm_.alloc(static_cast<std::size_t>(e->n_));
+      e->force_gather_ = e->nccl_comm_ != nullptr;
+    }
+    ~GatherScope() { e->force_gather_ = false; }
+  } gather_scope(this);
   const auto t0 = Clock::now();
   const std::int64_t n = n_;
   max_iter = std::max(max_iter, 1);

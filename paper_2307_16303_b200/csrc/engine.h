@@ -64,6 +64,7 @@ class Engine {
   std::int64_t export_list(int level, int kind, std::int32_t* offsets, std::int32_t* ids) const;
   std::int64_t export_pairs(int level, std::int32_t* x, std::int32_t* y, std::int32_t* rank) const;
   void attach_nccl(const void* id128, int rank, int world);
+  void comm_ledger(h3d_comm_ledger* out) const;
   // exact dense product b = K x (O(N^2), verification / manufactured RHS)
   void direct_matvec(const double* x, double* b, bool host);
   // relative 2-norm error of b against exact row sums (reference
@@ -204,6 +205,9 @@ class Engine {
 
   // multi-GPU
   void* nccl_comm_ = nullptr;
+  DevBuf<double> bm_;           // Morton-order b for the all-gather (gather_b)
+  bool force_gather_ = false;   // GMRES on a sharded handle: every matvec returns the full b
+  std::int64_t comm_matvecs_ = 0;
 
   // profiling ring for async matvecs (4 events per step)
   bool prof_on_ = false;

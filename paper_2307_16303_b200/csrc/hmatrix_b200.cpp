@@ -115,6 +115,7 @@ HMatrixRep initialize(const double* xyz, std::size_t n, const KernelSpec& kernel
   opt.near_mode = o.dense_mode == DenseMode::Cached ? H3D_NEAR_STORED : H3D_NEAR_MATRIX_FREE;
   opt.device = o.device;
   opt.mode_policy = o.mode_policy;
+  opt.gather_b = o.gather_b;
   opt.variant = static_cast<int>(variant);
   h3d_dev* dev = nullptr;
   check(h3d_dev_create(xyz, static_cast<std::int64_t>(n), &opt, &dev));

@@ -225,7 +225,10 @@ void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s);
 void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
                     const std::int64_t* leaf_off, std::int64_t leaf0, std::int64_t nleaves,
                     const std::int32_t* in_off, const std::int64_t* in_pos, const double* pairbuf,
-                    const std::int32_t* perm, double* b, cudaStream_t s);
+                    const std::int32_t* perm, double* b, double* bm, cudaStream_t s);
+// after the all-gather of the Morton-order b: the rows other shards own
+void launch_unpermute_rest(const double* bm, const std::int32_t* perm, std::int64_t n, std::int64_t row0,
+                           std::int64_t row1, double* b, cudaStream_t s);
 
 // ---------------------------------------------------------------- pair.cu
 constexpr int kPairMaxRp = 128;  // pair levels: ranks above this stay two-phase

@@ -1139,7 +1139,8 @@ __global__ void combine_kernel(const double* __restrict__ cpart, const double* _
                                const std::int32_t* __restrict__ in_off,
                                const std::int64_t* __restrict__ in_pos,
                                const double* __restrict__ pairbuf,
-                               const std::int32_t* __restrict__ perm, double* __restrict__ b) {
+                               const std::int32_t* __restrict__ perm, double* __restrict__ b,
+                               double* __restrict__ bm) {
   const std::int64_t t = (blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= nleaves) return;
@@ -1153,6 +1154,7 @@ __global__ void combine_kernel(const double* __restrict__ cpart, const double* _
     for (int e = i0; e < i1; ++e) v += pairbuf[in_pos[e] + i];
     for (int l = 0; l < n_lvl; ++l) v += lvl[static_cast<std::int64_t>(l) * n_total + p];
     b[perm[p]] = v;
+    if (bm) bm[p] = v;  // Morton copy for the all-gather of b
   }
 }
 
@@ -1456,11 +1458,28 @@ void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s) {
 void launch_combine(const double* cpart, const double* lvl_part, int n_lvl, std::int64_t n_total,
                     const std::int64_t* leaf_off, std::int64_t leaf0, std::int64_t nleaves,
                     const std::int32_t* in_off, const std::int64_t* in_pos, const double* pairbuf,
-                    const std::int32_t* perm, double* b, cudaStream_t s) {
+                    const std::int32_t* perm, double* b, double* bm, cudaStream_t s) {
   if (nleaves <= 0) return;
   const std::int64_t threads = nleaves * 32;
   combine_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
-      cpart, lvl_part, n_lvl, n_total, leaf_off, leaf0, nleaves, in_off, in_pos, pairbuf, perm, b);
+      cpart, lvl_part, n_lvl, n_total, leaf_off, leaf0, nleaves, in_off, in_pos, pairbuf, perm, b, bm);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+// rows outside [row0, row1) of the all-gathered Morton-order b to the
+// original order (the owned rows were written by combine)
+__global__ void unpermute_rest_kernel(const double* __restrict__ bm, const std::int32_t* __restrict__ perm,
+                                      std::int64_t n, std::int64_t row0, std::int64_t row1,
+                                      double* __restrict__ b) {
+  for (std::int64_t p = blockIdx.x * static_cast<std::int64_t>(blockDim.x) + threadIdx.x; p < n;
+       p += static_cast<std::int64_t>(gridDim.x) * blockDim.x)
+    if (p < row0 || p >= row1) b[perm[p]] = bm[p];
+}
+
+void launch_unpermute_rest(const double* bm, const std::int32_t* perm, std::int64_t n, std::int64_t row0,
+                           std::int64_t row1, double* b, cudaStream_t s) {
+  const unsigned grid = static_cast<unsigned>(std::min<std::int64_t>((n + 255) / 256, 148 * 8));
+  unpermute_rest_kernel<<<grid, 256, 0, s>>>(bm, perm, n, row0, row1, b);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -58,6 +58,17 @@ class _Options(C.Structure):
         ("mode_policy", C.c_int),
         ("level_modes", C.c_int * 16),
         ("variant", C.c_int),
+        ("gather_b", C.c_int64),
+        ("reserved", C.c_int64 * 3),
+    ]
+
+
+class _CommLedger(C.Structure):
+    _fields_ = [
+        ("x_gather_doubles", C.c_int64),
+        ("b_gather_doubles", C.c_int64),
+        ("collectives", C.c_int64),
+        ("matvecs", C.c_int64),
         ("reserved", C.c_int64 * 4),
     ]
 
@@ -119,7 +130,7 @@ _EXPORTS = [
     "h3d_dev_profile_read", "h3d_dev_profile_kernels", "h3d_plan_create", "h3d_plan_destroy", "h3d_plan_pairs",
     "h3d_plan_set_ranks", "h3d_plan_set_mode", "h3d_plan_layout", "h3d_plan_array",
     "h3d_dev_gmres", "h3d_dev_direct_matvec", "h3d_generate_grid_points", "h3d_cell_self_integral",
-    "h3d_dev_reference_error",
+    "h3d_dev_reference_error", "h3d_dev_comm_ledger",
 ]
 
 
@@ -169,6 +180,7 @@ def _load():
     L.h3d_dev_gmres.argtypes = [P, P, P, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
                                 C.c_int, P, C.c_int, C.POINTER(_GmresInfo)]
     L.h3d_dev_direct_matvec.argtypes = [P, P, P, C.c_int]
+    L.h3d_dev_comm_ledger.argtypes = [P, C.POINTER(_CommLedger)]
     L.h3d_dev_reference_error.argtypes = [P, P, P, C.c_int, C.c_int64, C.c_int64, C.c_uint64,
                                           C.POINTER(C.c_double)]
     L.h3d_generate_grid_points.argtypes = [C.c_int64, P]
@@ -261,6 +273,9 @@ class HmatOptions:
     # one fused read per pair)
     mode_policy: str = "auto"
     level_modes: tuple = ()
+    # multi-GPU (B200 extension): every rank returns the full b, all-gathered
+    # over NCCL after the matvec (parallel_matvec's final gather, parallel.cpp:284-290)
+    gather_b: bool = False
 
 
 @dataclasses.dataclass
@@ -306,6 +321,7 @@ class HMatrixRep:
         if variant not in VARIANTS:
             raise ValueError(f"unknown variant: {variant}")
         o.variant = VARIANTS[variant]
+        o.gather_b = 1 if options.gather_b else 0
         h = C.c_void_p()
         self._h = None
         _check(_L.h3d_dev_create(_ptr(pts), len(pts), C.byref(o), C.byref(h)))
@@ -432,6 +448,13 @@ class HMatrixRep:
         buf = (C.c_char * 128).from_buffer_copy(unique_id)
         _check(_L.h3d_dev_attach_nccl(self._h, C.cast(buf, C.c_void_p), rank, world))
 
+
+    def comm_ledger(self) -> dict:
+        """Per-rank exchange volume per matvec (analogue of h3d::CommLedger,
+        parallel.hpp:38-51)."""
+        c = _CommLedger()
+        _check(_L.h3d_dev_comm_ledger(self._h, C.byref(c)))
+        return {f: getattr(c, f) for f, _ in _CommLedger._fields_ if f != "reserved"}
 
     # --- solver -------------------------------------------------------------
     def gmres(self, rhs, alpha: float = 0.0, beta: float = 1.0,

@@ -7,9 +7,12 @@
 * the reference matvec b_ref and the exact sum b_exact on 2000 rows drawn by
   reference_error's rule (mt19937_64(7), hmatrix.cpp:263-266), plus the
   reference's own reference_error value,
-* per-level rank summaries (count, sum, max of the ordered block ranks).
+* per-level rank summaries (count, sum, max of the ordered block ranks),
+* the reference's full matvec output b_ref (every config up to C3: 8 MB),
+* C5 (N = 4,194,304): the tree/list digest only (the reference's
+  build_tree + build_interaction_lists; its initialize would need ~66 GB).
 
-    python tests/golden/make_golden_large.py c2 c4 c3
+    python tests/golden/make_golden_large.py c2 c4 c3 c5
 """
 import hashlib
 import sys
@@ -26,7 +29,9 @@ CONFIGS = {
     "c2": (65536, "laplace3d", 64, 1e-10, 1),
     "c3": (1048576, "laplace3d", 64, 1e-8, 1),
     "c4": (262144, "r4", 64, 1e-8, 1),
+    "c5": (4194304, "laplace3d", 64, 1e-6, 1),  # tree / lists only
 }
+TREE_ONLY = {"c5"}
 
 
 def tree_digest(rep):
@@ -56,6 +61,14 @@ def main(names):
         n, kern, n_max, eps, seed = CONFIGS[name]
         pts = ref.generate_points(n, seed)
         x = ref.random_vector(n, seed + 17)
+        if name in TREE_ONLY:
+            t0 = time.time()
+            rep = ref.tree_lists(pts, n_max=n_max)
+            out = dict(n=n, kernel=kern, n_max=n_max, eps=eps, seed=seed, depth=rep.depth,
+                       tree_digest=tree_digest(rep), tree_only=True)
+            np.savez_compressed(HERE / f"large_{name}.npz", **out)
+            print(name, "depth", rep.depth, "tree+lists", round(time.time() - t0, 1), "s", flush=True)
+            continue
         t0 = time.time()
         rep = ref.initialize(pts, kern, n_max=n_max, eps=eps)
         t1 = time.time()
@@ -72,12 +85,11 @@ def main(names):
                    tree_digest=tree_digest(rep), rows=rows, b_ref_rows=b[rows],
                    b_exact_rows=ex, ref_error=ref_err, ranks=np.array(ranks, dtype=np.int64),
                    ref_init_s=t1 - t0)
-        if n <= 65536:
-            out["b_ref"] = b
+        out["b_ref"] = b
         np.savez_compressed(HERE / f"large_{name}.npz", **out)
         print(name, "depth", rep.depth, "init", round(t1 - t0, 1), "ref_error", ref_err,
               flush=True)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c2", "c4", "c3"])
+    main(sys.argv[1:] or ["c2", "c4", "c3", "c5"])

@@ -233,6 +233,7 @@ class RefLib:
         L.h3dref_initialize.argtypes = [_D, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int,
                                         C.c_double, C.c_int, C.c_int, C.c_int64, C.POINTER(_P)]
         L.h3dref_free.argtypes = [_P]
+        L.h3dref_tree_lists.argtypes = [_D, C.c_int64, C.c_int, C.c_int, C.POINTER(_P)]
         L.h3dref_matvec.argtypes = [_P, _D, _D, _P]
         L.h3dref_parallel_matvec.argtypes = [_P, _D, C.c_int, _D, _P]
         L.h3dref_reference_error.argtypes = [_P, _D, _D, C.POINTER(C.c_double)]
@@ -309,6 +310,13 @@ class RefLib:
                                             lu, cap, C.byref(r)))
         k = r.value
         return rp[:k].copy(), cp[:k].copy(), lu[: k * k].reshape(k, k).copy()
+
+    def tree_lists(self, pts, n_max=216, variant=0) -> "RefRep":
+        """build_tree + build_interaction_lists only (octree.cpp:76-260)."""
+        pts = np.ascontiguousarray(pts, dtype=np.float64).reshape(-1)
+        h = _P()
+        self._check(self.L.h3dref_tree_lists(pts, len(pts) // 3, n_max, _variant(variant), C.byref(h)))
+        return RefRep(self, h, len(pts) // 3)
 
     def initialize(self, pts, kernel="laplace3d", n_max=216, eps=1e-7, depth_cap=12,
                    max_rank=0, diag=0.0, variant=0, cached=False) -> "RefRep":

@@ -39,7 +39,7 @@ def test_python_binding_lists_every_export():
 
 def test_abi_version_and_defaults():
     lib = ctypes.CDLL(str(LIB))
-    assert lib.h3d_abi_version() == 4
+    assert lib.h3d_abi_version() == 5
     from paper_2307_16303_b200 import h3d
     o = h3d._Options()
     h3d._L.h3d_default_options(ctypes.byref(o))

@@ -1,11 +1,14 @@
 """GPU parity at the BASELINE sizes against fixtures produced by the
 reference itself (tests/golden/make_golden_large.py -> oracle/_ref):
 
-* tree + interaction lists bit-exact (SHA-256 digest of perm, offsets, lists);
-* matvec within 10 x eps of the reference's matvec on 2000 rows drawn by the
-  reference's own sampling rule (full vector at C2);
-* error against the exact dense product no worse than 2 x the reference's on
-  those rows.
+* tree + interaction lists bit-exact (SHA-256 digest of perm, offsets, lists),
+  C2-C5 (C5: the reference's build_tree + build_interaction_lists only);
+* matvec within relative 2-norm 10 x eps of the reference's full matvec
+  output (C2, C3, C4), and on the 2000 rows drawn by the reference's own
+  sampling rule;
+* error against the exact dense product no worse than 2 x the reference's,
+  on those rows and through the device reference_error (the same estimator,
+  hmatrix.cpp:253-291).
 """
 import hashlib
 
@@ -38,6 +41,8 @@ def rel(a, b):
 @pytest.mark.parametrize("name", LARGE_NAMES)
 def test_large_config_against_reference(h3d, name, policy):
     g = load_golden(f"large_{name}")
+    if "tree_only" in g:
+        pytest.skip("tree/list digest only (test_c5_on_one_gpu)")
     n, seed, eps = int(g["n"]), int(g["seed"]), float(g["eps"])
     pts = h3d.generate_points(n, seed)
     x = h3d.random_vector(n, seed + 17)
@@ -56,6 +61,9 @@ def test_large_config_against_reference(h3d, name, policy):
     # 1/sqrt(r^2) rows instead of eval_pair's 1/r: equal to ~1e-5 relative)
     assert abs(ref_err - float(g["ref_error"])) <= 1e-2 * float(g["ref_error"]) + 1e-14
     assert err <= 2 * ref_err, (err, ref_err)
+    # the reference's estimator on the device (same 2000 rows, exact sums)
+    dev_err = rep.reference_error(x, b)
+    assert dev_err <= 2 * float(g["ref_error"]), (dev_err, float(g["ref_error"]))
     if policy == "stream":
         # ACA ranks per level against the reference's census (count, sum and
         # max of its ordered-block ranks). The reference compresses (X, Y) and
@@ -75,25 +83,31 @@ def test_large_config_against_reference(h3d, name, policy):
     rep.close()
 
 
-def test_c5_on_one_gpu_sampled_rows(h3d, oracle):
+def test_c5_on_one_gpu(h3d, oracle):
     # BASELINE configs[4] (N = 4,194,304, Laplace, tol 1e-6, matrix-free near
     # field), the reference's 8-GPU case, fits one B200 in the hybrid
-    # representation. No reference run exists at this size (its initialize
-    # needs ~66 GB and ~12 CPU-minutes of ACA), so the check is the
-    # reference's own acceptance form: sampled rows of the exact product
-    # (reference_error's seed-7 rule, hmatrix.cpp:253-291) within 10 x tol.
-    n, eps = 4194304, 1e-6
-    pts = h3d.generate_points(n, 1)
-    x = h3d.random_vector(n, 18)
+    # representation. The reference's full initialize needs ~66 GB and ~12
+    # CPU-minutes of ACA, so the fixture holds its tree/list digest only
+    # (bit-exact here); the matvec is checked by the reference's acceptance
+    # form: reference_error (2000 rows of mt19937_64(7), exact sums,
+    # hmatrix.cpp:253-291) within 10 x tol, cross-checked on 100 of those
+    # rows by the CPU checker.
+    g = load_golden("large_c5")
+    n, eps = int(g["n"]), float(g["eps"])
+    pts = h3d.generate_points(n, int(g["seed"]))
+    x = h3d.random_vector(n, int(g["seed"]) + 17)
     rep = h3d.initialize(pts, h3d.make_kernel("laplace3d"), "hodlr3d",
-                         h3d.HmatOptions(n_max=64, epsilon=eps, dense_mode="on-the-fly"))
-    assert rep.depth == 6
+                         h3d.HmatOptions(n_max=int(g["n_max"]), epsilon=eps, dense_mode="on-the-fly"))
+    assert rep.depth == int(g["depth"]) == 6
+    assert digest(rep) == str(g["tree_digest"]), "tree/lists must be bit-exact"
     b = rep.matvec(x)
-    rows = np.random.default_rng(7).integers(0, n, 200)
+    err = rep.reference_error(x, b)
+    print(f"C5 reference_error {err:.3e} (tol {eps:g}), modes {rep.stats()['level_modes'][:7]}")
+    assert err <= 10 * eps
+    u = (h3d.random_vector(100, 7) + 1.0) / 2.0  # the first 100 of the reference's draws
+    rows = rep.perm()[(u * n).astype(np.int64)]
     import os
     oracle.set_threads(os.cpu_count() or 1)
     ex = oracle.exact_rows(pts, x, rows)
-    err = rel(b[rows], ex)
-    print(f"C5 sampled-row error {err:.3e} (tol {eps:g}), modes {rep.stats()['level_modes'][:7]}")
-    assert err <= 10 * eps
+    assert rel(b[rows], ex) <= 10 * eps
     rep.close()

@@ -82,3 +82,48 @@ def test_nccl_exchange_path_world1(h3d):
     rep.attach_nccl(h3d.nccl_unique_id(), 0, 1)
     b1 = rep.matvec(x)
     assert np.array_equal(b0, b1)
+    led = rep.comm_ledger()
+    assert led["x_gather_doubles"] == 0 and led["b_gather_doubles"] == 0 and led["matvecs"] >= 1
+
+
+def test_nccl_b_allgather_path_world1(h3d):
+    # parallel_matvec's full result (parallel.cpp:284-290): with gather_b the
+    # owned Morton slices of b are all-gathered after the matvec and the other
+    # ranks' rows un-permuted; on a 1-rank communicator the same path runs
+    # (broadcast of the one slice + the un-permute pass) and must not change b
+    pts = h3d.generate_points(N, SEED)
+    x = h3d.random_vector(N, 9)
+    lap = h3d.make_kernel("laplace3d")
+    ref = h3d.initialize(pts, lap, options=h3d.HmatOptions(n_max=64, epsilon=1e-7)).matvec(x)
+    rep = h3d.initialize(pts, lap, options=h3d.HmatOptions(n_max=64, epsilon=1e-7, gather_b=True),
+                         shard_rank=0, shard_world=1)
+    rep.attach_nccl(h3d.nccl_unique_id(), 0, 1)
+    for _ in range(3):
+        assert np.array_equal(rep.matvec(x), ref)
+    led = rep.comm_ledger()
+    assert led["collectives"] == 2 and led["b_gather_doubles"] == 0
+
+
+def test_gather_b_without_communicator_is_refused(h3d):
+    pts = h3d.generate_points(N, SEED)
+    rep = h3d.initialize(pts, h3d.make_kernel("laplace3d"),
+                         options=h3d.HmatOptions(n_max=64, epsilon=1e-7, gather_b=True),
+                         shard_rank=0, shard_world=2)
+    with pytest.raises(ValueError):
+        rep.matvec(h3d.random_vector(N, 9))
+
+
+def test_gmres_on_an_attached_shard_world1(h3d):
+    # GMRES on a sharded handle: replicated Krylov vectors, every operator
+    # application all-gathers b (1-rank communicator here) - the same iterate
+    # as the single-GPU solve, bit for bit
+    pts = h3d.generate_points(N, SEED)
+    lap = h3d.make_kernel("laplace3d")
+    opt = h3d.HmatOptions(n_max=64, epsilon=1e-7)
+    f = h3d.random_vector(N, 5)
+    one = h3d.initialize(pts, lap, options=opt).gmres(f, alpha=2.0, beta=1e-3)
+    rep = h3d.initialize(pts, lap, options=opt, shard_rank=0, shard_world=1)
+    rep.attach_nccl(h3d.nccl_unique_id(), 0, 1)
+    res = rep.gmres(f, alpha=2.0, beta=1e-3)
+    assert res.converged and res.iterations == one.iterations
+    assert np.array_equal(res.x, one.x)
