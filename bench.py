@@ -263,6 +263,10 @@ def main():
     opt = h3d.HmatOptions(n_max=cfg["n_max"], epsilon=cfg["eps"],
                           dense_mode="cached" if args.near == "stored" else "on-the-fly",
                           mode_policy=args.policy)
+    # process warm-up (lazy module loading, allocator): a small build first, so
+    # aca_build_s is the workload's own build
+    h3d.initialize(h3d.generate_points(20000, 3), h3d.make_kernel(cfg["kernel"]), "hodlr3d",
+                   h3d.HmatOptions(n_max=cfg["n_max"], epsilon=cfg["eps"]), device=local_rank).close()
     t0 = time.time()
     rep = h3d.initialize(pts, h3d.make_kernel(cfg["kernel"]), "hodlr3d", opt, device=local_rank,
                          shard_rank=rank, shard_world=world)

@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
   __shared__ double s_c1;
   __shared__ long long s_c2;
   __shared__ long long s_pair;
+  __shared__ long long s_off;
   int CL = 1, crank = 0;
   if constexpr (CLU) {
     CL = static_cast<int>(cg::this_cluster().num_blocks());
@@ -402,7 +403,40 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
       continue;
     }
     if (crank == 0 && tid == 0) a.rank_out[p] = rank;
-    cx.bar();
+    cx.bar();  // every CTA's u / v columns are complete
+    if (a.pool != nullptr && crank == 0) {
+      // single-pass build: the pair's pivots + packed LU into the pool
+      if (tid == 0) {
+        long long off = -2;
+        if (rank > 0) {
+          const long long need = static_cast<long long>(rank) * rank + rank;
+          off = static_cast<long long>(atomicAdd(a.pool_ctr, static_cast<unsigned long long>(need)));
+          if (off + need > a.pool_cap) {
+            off = -1;
+            atomicOr(a.flags, kFlagPoolFull);
+          }
+        }
+        a.pool_off[p] = off;
+        s_off = off;
+      }
+      __syncthreads();
+      const long long off = s_off;
+      if (off >= 0) {
+        double* lu = a.pool + off;
+        int* pv = reinterpret_cast<int*>(lu + static_cast<long long>(rank) * rank);
+        for (int q = tid; q < rank; q += NT) {
+          pv[q] = s_prow[q];
+          pv[rank + q] = s_pcol[q];
+        }
+        for (int e = tid; e < rank * rank; e += NT) {
+          const int row = e / rank, col = e % rank;
+          double v;
+          if (row > col) v = U[static_cast<std::int64_t>(col) * a.ms + s_prow[row]] / s_delta[col];
+          else v = s_delta[row] * V[static_cast<std::int64_t>(row) * a.ns + s_pcol[col]];
+          lu[e] = v;
+        }
+      }
+    }
     if (a.W != nullptr && rank > 0) {
       write_rows<NT>(U + r0, a.ms, r1 - r0, rank, a.W + a.wx[p], r0, a.cx[p], a.rx[p], s_tile,
                      a.row_major != 0);
@@ -447,7 +481,121 @@ const void* kernel_for(int threads, int kernel, bool cluster) {
   }
 }
 
+// pool -> final pivot / LU arrays (single-pass build)
+__global__ void aca_compact_kernel(const double* __restrict__ pool, const std::int64_t* __restrict__ pool_off,
+                                   const std::int32_t* __restrict__ rank, std::int32_t* __restrict__ piv,
+                                   const std::int64_t* __restrict__ piv_off, double* __restrict__ lu,
+                                   const std::int64_t* __restrict__ lu_off) {
+  const std::int64_t p = blockIdx.x;
+  const int r = rank[p];
+  const std::int64_t off = pool_off[p];
+  if (r <= 0 || off < 0) return;
+  const double* src = pool + off;
+  const int* pv = reinterpret_cast<const int*>(src + static_cast<std::int64_t>(r) * r);
+  for (int q = threadIdx.x; q < 2 * r; q += blockDim.x) piv[piv_off[p] + q] = pv[q];
+  double* dst = lu + lu_off[p];
+  for (int e = threadIdx.x; e < r * r; e += blockDim.x) dst[e] = src[e];
+}
+
+__device__ __forceinline__ std::int64_t w_index(int row, int col, int nct, bool row_major) {
+  return row_major ? static_cast<std::int64_t>(row) * nct + col : tile_index(row, col, nct);
+}
+
+// One side of a pair's explicit factor (rc-row chunks): out[i][b] for the node's rows
+// (points pts + base, count rows) against the partner's pivot points
+// (pivot indices piv[a], local in the partner, base pbase):
+//   upper (U side): out[i][b] = sum_{a <= b} E[i][a] C[b][a], C = column-major R^-1
+//   lower (V side): out[i][b] = E[i][b] + sum_{a < b} E[i][a] C[b][a], C = row-major L^-1
+// with E[i][a] = K(point i, pivot point a). 32-row chunks: E and the output
+// tile staged in shared memory (rows padded to r + 1), the output written
+// column-fastest into the node's pool (coalesced).
+template <int K>
+__device__ void factor_side(const FactorGenArgs& a, std::int64_t base, int rows, std::int64_t pbase,
+                            const std::int32_t* __restrict__ piv, int r, const double* __restrict__ C,
+                            bool upper, double* __restrict__ Wn, int col0, int nct, double* sm, int rc) {
+  const int ld = r + 1;
+  double* E = sm;            // [rc][ld]
+  double* O = sm + rc * ld;  // [rc][ld]
+  double* Q = O + rc * ld;   // [r][3] pivot points
+  for (int q = threadIdx.x; q < r; q += blockDim.x) {
+    const std::int64_t k = pbase + piv[q];
+    Q[3 * q] = a.px[k];
+    Q[3 * q + 1] = a.py[k];
+    Q[3 * q + 2] = a.pz[k];
+  }
+  __syncthreads();
+  for (int i0 = 0; i0 < rows; i0 += rc) {
+    const int nr = min(rc, rows - i0);
+    for (int e = threadIdx.x; e < nr * r; e += blockDim.x) {
+      const int i = e / r, q = e % r;
+      const std::int64_t k = base + i0 + i;
+      E[i * ld + q] = kernel_r2_fast<K>(sq3(a.px[k] - Q[3 * q], a.py[k] - Q[3 * q + 1], a.pz[k] - Q[3 * q + 2]));
+    }
+    __syncthreads();
+    // (b, i) with i fastest: a warp shares b, so its C row is one broadcast stream
+    for (int e = threadIdx.x; e < nr * r; e += blockDim.x) {
+      const int b = e / nr, i = e % nr;
+      const double* cb = C + static_cast<std::int64_t>(b) * r;
+      const double* ei = E + i * ld;
+      double acc = 0.0;
+      if (upper) {
+        for (int q = 0; q <= b; ++q) acc = fma(ei[q], __ldg(cb + q), acc);
+      } else {
+        for (int q = 0; q < b; ++q) acc = fma(ei[q], __ldg(cb + q), acc);
+        acc += ei[b];
+      }
+      O[i * ld + b] = acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * r; e += blockDim.x) {
+      const int i = e / r, b = e % r;
+      Wn[w_index(i0 + i, col0 + b, nct, a.row_major != 0)] = O[i * ld + b];
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) factor_gen_kernel(const FactorGenArgs a) {
+  extern __shared__ double fg_smem[];
+  const std::int64_t p = blockIdx.x;
+  const int r = a.rank[p];
+  if (r <= 0) return;
+  const std::int32_t* pv = a.piv + a.piv_off[p];
+  const double* inv = a.inv + a.inv_off[p];
+  // U = K(X, tau) R^-1: R^-1 column b = row b of the column-major copy
+  factor_side<K>(a, a.xb[p], a.m[p], a.yb[p], pv + r, r, inv + a.inv_total, true, a.W + a.wx[p], a.cx[p],
+                 a.rx[p], fg_smem, a.rc);
+  // V = K(Y, sigma) L^-T: L^-1 row b (strict lower part of the row-major block)
+  factor_side<K>(a, a.yb[p], a.n[p], a.xb[p], pv, r, inv, false, a.W + a.wy[p], a.cy[p], a.ry[p], fg_smem,
+                 a.rc);
+}
+
 }  // namespace
+
+void launch_aca_compact(const double* pool, const std::int64_t* pool_off, const std::int32_t* rank,
+                        std::int64_t npairs, std::int32_t* piv, const std::int64_t* piv_off, double* lu,
+                        const std::int64_t* lu_off, cudaStream_t s) {
+  if (npairs == 0) return;
+  aca_compact_kernel<<<static_cast<unsigned>(npairs), 256, 0, s>>>(pool, pool_off, rank, piv, piv_off, lu, lu_off);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_factor_gen(const FactorGenArgs& a0, cudaStream_t s) {
+  if (a0.npairs == 0 || a0.max_r == 0) return;
+  FactorGenArgs a = a0;
+  // rows per staged chunk: 32, halved until E + out tiles fit 200 KB
+  a.rc = 32;
+  auto bytes = [&](int rc) { return sizeof(double) * (2 * rc * static_cast<std::size_t>(a.max_r + 1) + 3 * a.max_r); };
+  while (a.rc > 1 && bytes(a.rc) > 200u * 1024u) a.rc >>= 1;
+  const std::size_t smem = bytes(a.rc);
+  const void* f = a.kernel == kLaplace ? reinterpret_cast<const void*>(factor_gen_kernel<kLaplace>)
+                  : a.kernel == kR4    ? reinterpret_cast<const void*>(factor_gen_kernel<kR4>)
+                                       : reinterpret_cast<const void*>(factor_gen_kernel<kHelmholtz>);
+  H3D_CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  void* args[] = {const_cast<FactorGenArgs*>(&a)};
+  H3D_CUDA_CHECK(cudaLaunchKernel(f, dim3(static_cast<unsigned>(a.npairs)), dim3(256), args, smem, s));
+}
 
 std::size_t aca_smem_bytes(int /*threads*/, int cap_ws) {
   return sizeof(double) * (4 * static_cast<std::size_t>(cap_ws) + 32 * 33) +

@@ -19,6 +19,7 @@ enum DevFlag : unsigned {
   kFlagDegenGeom = 1u,    // r < 1e-14 between distinct points (kernel.cpp:59-71)
   kFlagAcaOverflow = 2u,  // ACA workspace rank capacity exhausted
   kFlagOutOfDomain = 4u,  // point outside [-1,1]^3 (octree.cpp:91-97)
+  kFlagPoolFull = 8u,     // single-pass ACA: the rank pass's LU pool is exhausted
 };
 
 constexpr double kCoincidentTol2 = 1e-14 * 1e-14;
@@ -273,5 +274,8 @@ struct PerDeviceOnce {
 #define H3D_CUDA_CHECK(expr)                                                   \
   do {                                                                         \
     cudaError_t e_ = (expr);                                                   \
-    if (e_ != cudaSuccess) throw ::h3db::CudaError(e_, #expr, __FILE__, __LINE__); \
+    if (e_ != cudaSuccess) {                                                   \
+      cudaGetLastError(); /* clear a non-sticky error so later checks see their own */ \
+      throw ::h3db::CudaError(e_, #expr, __FILE__, __LINE__);                  \
+    }                                                                          \
   } while (0)

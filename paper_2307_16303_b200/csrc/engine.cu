@@ -153,6 +153,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "nfc") tune_.nfc = v;
         else if (k == "fw") tune_.fw = v;
         else if (k == "sol") tune_.sol = v;
+        else if (k == "p2o") tune_.p2o = v;
         else if (k == "pps") tune_.pps = v;
         else if (k == "graphs") tune_.graphs = v;
       }
@@ -203,7 +204,8 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   plan_->layout();
   upload_plan();
   t = Clock::now();
-  run_aca(true);
+  single_pass_ = finish_single_pass();
+  if (!single_pass_) run_aca(true);
   ms_aca_write_ = ms_since(t);
   if (n_segs_all_ > 0) {
     launch_proxy_gather(segs_all_.get(), n_segs_all_, piv_.get(), px_.get(), py_.get(), pz_.get(),
@@ -384,6 +386,17 @@ void Engine::run_aca(bool write) {
   std::size_t free_b = 0, total_b = 0;
   H3D_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
   if (!write) free_mem_ = free_b;
+  if (!write && std::getenv("H3D_TWO_PASS") == nullptr) {
+    // single-pass build: a bump pool for every pair's pivots + packed LU
+    // (sum r^2 + r doubles; C3 ~3.6 GB, C5 ~35 GB), a fifth of free memory
+    const std::size_t cap_b = free_b / 5;
+    pool_.alloc(std::max<std::size_t>(cap_b / 8, 1));
+    pool_ctr_.alloc(1);
+    H3D_CUDA_CHECK(cudaMemsetAsync(pool_ctr_.get(), 0, 8, stream_));
+    pool_off_.clear();
+    pool_off_.resize(static_cast<std::size_t>(L_) + 1);
+    pool_ok_ = true;
+  }
   for (int l = 1; l <= L_; ++l) {
     auto& P = plan_->pairs(l);
     const std::int64_t np = static_cast<std::int64_t>(P.X.size());
@@ -497,6 +510,15 @@ void Engine::run_aca(bool write) {
       }
       a.flags = flags_.get();
       a.counter = counter.get();
+      if (!write && pool_ok_) {
+        auto& po = pool_off_[static_cast<std::size_t>(l)];
+        if (!po) po = std::make_unique<DevBuf<std::int64_t>>();
+        if (po->size() != static_cast<std::size_t>(np)) po->alloc(static_cast<std::size_t>(np));
+        a.pool = pool_.get();
+        a.pool_ctr = pool_ctr_.get();
+        a.pool_cap = static_cast<std::int64_t>(pool_.size());
+        a.pool_off = po->get();
+      }
       if (P.cluster > 1)
         launch_aca_cluster(a, P.threads, P.cluster, static_cast<int>(slots), stream_);
       else
@@ -505,6 +527,7 @@ void Engine::run_aca(bool write) {
       H3D_CUDA_CHECK(cudaMemcpyAsync(&f, flags_.get(), 4, cudaMemcpyDeviceToHost, stream_));
       H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
       if (f & kFlagDegenGeom) throw DegenerateGeometry("coincident distinct points in block");
+      if (f & kFlagPoolFull) pool_ok_ = false;  // the write pass recomputes the factors instead
       if (f & kFlagAcaOverflow) {
         if (write || cap_ws >= P.max_mn)
           throw std::logic_error("ACA workspace overflow in the write pass");
@@ -523,6 +546,134 @@ void Engine::run_aca(bool write) {
       P.rank = std::move(rk);
     }
   }
+  if (!write && pool_ok_) {
+    // keep only the used part of the pool (the planner sizes W from the
+    // memory that is free after the rank pass)
+    unsigned long long used = 0;
+    H3D_CUDA_CHECK(cudaMemcpyAsync(&used, pool_ctr_.get(), 8, cudaMemcpyDeviceToHost, stream_));
+    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    DevBuf<double> exact;
+    exact.alloc(std::max<std::size_t>(static_cast<std::size_t>(used), 1));
+    if (used > 0)
+      H3D_CUDA_CHECK(cudaMemcpyAsync(exact.get(), pool_.get(), used * 8, cudaMemcpyDeviceToDevice, stream_));
+    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    pool_.swap(exact);
+    free_mem_ -= std::min<std::size_t>(free_mem_, static_cast<std::size_t>(used) * 8);
+  }
+  if (!write && !pool_ok_) {
+    pool_.reset();
+    pool_off_.clear();
+  }
+}
+
+// Single-pass build, after the layout: proxy / fused levels take their pivots
+// and packed LU from the rank pass's pool (compaction into the planner's
+// offsets); stream / pair levels get explicit factors generated from the same
+// pivots + LU (triangular inverses, U = K(X, tau) R^-1, V = K(Y, sigma) L^-T)
+// instead of a second ACA pass. Returns false when the pool overflowed (the
+// caller runs the ACA write pass).
+bool Engine::finish_single_pass() {
+  if (!pool_ok_) {
+    pool_.reset();
+    pool_off_.clear();
+    return false;
+  }
+  for (int l = 1; l <= L_; ++l) {
+    auto& P = plan_->pairs(l);
+    const std::int64_t np = static_cast<std::int64_t>(P.X.size());
+    if (np == 0) continue;
+    const int mode = plan_->mode(l);
+    DevBuf<std::int32_t> d_rank;
+    d_rank.upload(P.rank, stream_);
+    const std::int64_t* poff = pool_off_[static_cast<std::size_t>(l)]->get();
+    if (mode == kModeProxy || mode == kModeFused) {
+      DevBuf<std::int64_t> d_po, d_lo;
+      d_po.upload(plan_->pair_piv[l], stream_);
+      d_lo.upload(plan_->pair_lu[l], stream_);
+      launch_aca_compact(pool_.get(), poff, d_rank.get(), np, piv_.get(), d_po.get(), lu_.get(), d_lo.get(),
+                         stream_);
+      H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+      continue;
+    }
+    // stream / pair level: pivots + LU into a temporary block array, its
+    // triangular inverses, then the explicit factors straight into W
+    std::vector<std::int64_t> po(np), lo(np), xb(np), yb(np);
+    std::vector<std::int32_t> m(np), nn(np);
+    std::vector<ProxySeg> segs(np);
+    std::int64_t ptot = 0, ltot = 0;
+    int max_r = 0;
+    for (std::int64_t p = 0; p < np; ++p) {
+      const std::int64_t r = P.rank[p];
+      po[p] = ptot;
+      lo[p] = ltot;
+      ptot += 2 * r;
+      ltot += r * r + (r & 1);
+      max_r = std::max<int>(max_r, static_cast<int>(r));
+      xb[p] = off_[l][P.X[p]];
+      yb[p] = off_[l][P.Y[p]];
+      m[p] = static_cast<std::int32_t>(node_size(l, P.X[p]));
+      nn[p] = static_cast<std::int32_t>(node_size(l, P.Y[p]));
+      segs[p] = ProxySeg{};
+      segs[p].lu_off = lo[p];
+      segs[p].piv_off = po[p];
+      segs[p].r = static_cast<std::int32_t>(r);
+      segs[p].side = 0;
+    }
+    if (max_r == 0) continue;
+    DevBuf<std::int32_t> tpiv, d_m, d_n;
+    DevBuf<double> tlu;
+    DevBuf<std::int64_t> d_po, d_lo, d_xb, d_yb, d_wx, d_wy;
+    DevBuf<std::int32_t> d_rx, d_ry, d_cx, d_cy;
+    DevBuf<ProxySeg> d_segs;
+    tpiv.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ptot, 1)));
+    tlu.alloc(static_cast<std::size_t>(std::max<std::int64_t>(2 * ltot, 1)));
+    d_po.upload(po, stream_);
+    d_lo.upload(lo, stream_);
+    launch_aca_compact(pool_.get(), poff, d_rank.get(), np, tpiv.get(), d_po.get(), tlu.get(), d_lo.get(),
+                       stream_);
+    d_segs.upload(segs, stream_);
+    launch_lu_invert(d_segs.get(), np, tlu.get(), ltot, max_r, stream_);
+    d_xb.upload(xb, stream_);
+    d_yb.upload(yb, stream_);
+    d_m.upload(m, stream_);
+    d_n.upload(nn, stream_);
+    d_wx.upload(plan_->pair_wx[l], stream_);
+    d_wy.upload(plan_->pair_wy[l], stream_);
+    d_rx.upload(plan_->pair_rx[l], stream_);
+    d_ry.upload(plan_->pair_ry[l], stream_);
+    d_cx.upload(plan_->pair_cx[l], stream_);
+    d_cy.upload(plan_->pair_cy[l], stream_);
+    FactorGenArgs fa;
+    fa.npairs = np;
+    fa.xb = d_xb.get();
+    fa.m = d_m.get();
+    fa.yb = d_yb.get();
+    fa.n = d_n.get();
+    fa.rank = d_rank.get();
+    fa.piv = tpiv.get();
+    fa.piv_off = d_po.get();
+    fa.inv = tlu.get();
+    fa.inv_total = ltot;
+    fa.inv_off = d_lo.get();
+    fa.px = px_.get();
+    fa.py = py_.get();
+    fa.pz = pz_.get();
+    fa.kernel = opt_.kernel_id;
+    fa.W = W_.get();
+    fa.wx = d_wx.get();
+    fa.cx = d_cx.get();
+    fa.rx = d_rx.get();
+    fa.wy = d_wy.get();
+    fa.cy = d_cy.get();
+    fa.ry = d_ry.get();
+    fa.row_major = mode == kModePair ? 1 : 0;
+    fa.max_r = max_r;
+    launch_factor_gen(fa, stream_);
+    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  }
+  pool_.reset();
+  pool_off_.clear();
+  return true;
 }
 
 // ---------------------------------------------------------------- modes
@@ -991,6 +1142,8 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       ke(H3D_K_RED_STREAM, stream2_);
       ++launches;
     }
+    // phase 1 of the HBM lane done: p2_stream is next on this lane
+    H3D_CUDA_CHECK(cudaEventRecord(fork_[1], stream2_));
   }
   // FP64 lane: phase 1 proxy levels -> reductions -> solves
   H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[0], 0));
@@ -1056,6 +1209,12 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // blocks (one persistent FP64 kernel resident at a time next to the HBM
   // lane's bulk-copy CTA)
   if (has_p2) {
+    // the FP64 lane's persistent phase-2 kernels start only once the HBM
+    // lane's phase 1 is done, so p2_stream (launched first) takes its SM slots
+    // before them: when the solves finish early, a p2_proxy launched ahead of
+    // p2_stream holds the SMs for its whole run and the stream loses
+    // bandwidth (measured: C3 p2_stream 10.3 -> 12.3 ms)
+    if (hbm && tune_.p2o) H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[1], 0));
     if (fused_lv) {
       kb(H3D_K_FUSED, stream4_);
       FusedArgs fa;

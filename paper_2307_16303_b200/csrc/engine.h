@@ -43,6 +43,10 @@ class DevBuf {
   std::size_t size() const { return n_; }
   void upload(const T* h, std::size_t n, cudaStream_t s);
   void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  void swap(DevBuf& o) {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+  }
 
  private:
   T* p_ = nullptr;
@@ -82,6 +86,14 @@ class Engine {
   void build_tree(const double* xyz);
   void build_lists();
   void run_aca(bool write);
+  // single-pass build: the rank pass leaves every pair's pivots + packed LU in
+  // a bump pool; afterwards proxy levels compact it into place and stream /
+  // pair levels generate their explicit factors from it (factor_gen)
+  bool finish_single_pass();
+  DevBuf<double> pool_;
+  DevBuf<unsigned long long> pool_ctr_;
+  std::vector<std::unique_ptr<DevBuf<std::int64_t>>> pool_off_;  // per level
+  bool pool_ok_ = false;
   void choose_modes();
   void upload_plan();
   void near_scan();
@@ -115,10 +127,11 @@ class Engine {
   // results are wrong; honoured only in a -DH3D_DEVTOOLS build)
   // ("nf=0": near field after p2_proxy instead of forked beside the solves;
   // "nfc": CTAs per SM of the forked near kernel; "fw=0": p2_stream does not
-  // wait for the solves-done flag; "sol": CTAs per SM of the proxy solve)
+  // wait for the solves-done flag; "sol": CTAs per SM of the proxy solve;
+  // "p2o=0": phase-2 FP64 kernels do not wait for the HBM lane's phase 1)
   struct Tune {
     int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1, fw = 1,
-        sol = 4;
+        sol = 2, p2o = 1;
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
@@ -223,6 +236,7 @@ class Engine {
 
   // build timings
   double ms_tree_ = 0, ms_lists_ = 0, ms_aca_rank_ = 0, ms_aca_write_ = 0, ms_total_ = 0;
+  bool single_pass_ = false;  // the build skipped the ACA write pass
   double level_aca_ms_[16] = {};  // rank + write pass per level
 };
 

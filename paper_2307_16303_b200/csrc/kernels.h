@@ -84,6 +84,14 @@ struct AcaArgs {
   const std::int64_t* lu_off = nullptr;
   unsigned* flags = nullptr;
   unsigned long long* counter = nullptr;
+  // rank pass, single-pass build: every compressed pair also leaves the
+  // reference's own representation (packed LU, r^2 doubles, then its 2r
+  // int32 pivots packed into r doubles) in a bump-allocated pool; pool_off[p]
+  // = its offset (-1: pool full, kFlagPoolFull raised; -2: rank 0)
+  double* pool = nullptr;
+  unsigned long long* pool_ctr = nullptr;
+  std::int64_t pool_cap = 0;
+  std::int64_t* pool_off = nullptr;
 };
 // threads in {32, 128, 256, 512}; grid = number of workspace slots
 void launch_aca(const AcaArgs& a, int threads, int grid, cudaStream_t s);
@@ -92,6 +100,43 @@ int aca_blocks_per_sm(int threads, int kernel, std::size_t smem);
 // cluster tier (one pair per cluster of `cluster` CTAs, DSMEM reductions)
 int aca_max_clusters(int threads, int kernel, int cluster, std::size_t smem);
 void launch_aca_cluster(const AcaArgs& a, int threads, int cluster, int nclusters, cudaStream_t s);
+// rank-pass pool -> pivots at piv + piv_off[p] (2r int32) and packed LU at
+// lu + lu_off[p] (r^2 doubles), one CTA per pair
+void launch_aca_compact(const double* pool, const std::int64_t* pool_off, const std::int32_t* rank,
+                        std::int64_t npairs, std::int32_t* piv, const std::int64_t* piv_off, double* lu,
+                        const std::int64_t* lu_off, cudaStream_t s);
+// Explicit factors from the pivots and the triangular inverses of the packed
+// LU (lu_invert layout: row-major at inv + inv_off[p], column-major at
+// inv + inv_total + inv_off[p]): U = K(X, tau) R^-1 (m x r) and
+// V = K(Y, sigma) L^-T (n x r), U V^T = K(X, tau) (L R)^-1 K(sigma, Y), the
+// reference's cross approximation (lowrank.cpp:291-327). Written like the
+// ACA write pass (tile-major node pools, or row-major pair pools).
+struct FactorGenArgs {
+  std::int64_t npairs = 0;
+  const std::int64_t* xb = nullptr;
+  const std::int32_t* m = nullptr;
+  const std::int64_t* yb = nullptr;
+  const std::int32_t* n = nullptr;
+  const std::int32_t* rank = nullptr;
+  const std::int32_t* piv = nullptr;      // row pivots (local in X) then col pivots (local in Y)
+  const std::int64_t* piv_off = nullptr;
+  const double* inv = nullptr;
+  std::int64_t inv_total = 0;
+  const std::int64_t* inv_off = nullptr;
+  const double *px = nullptr, *py = nullptr, *pz = nullptr;
+  int kernel = 0;
+  double* W = nullptr;
+  const std::int64_t* wx = nullptr;
+  const std::int32_t* cx = nullptr;
+  const std::int32_t* rx = nullptr;
+  const std::int64_t* wy = nullptr;
+  const std::int32_t* cy = nullptr;
+  const std::int32_t* ry = nullptr;
+  int row_major = 0;
+  int max_r = 0;
+  int rc = 32;  // rows per staged chunk (set by the launcher)
+};
+void launch_factor_gen(const FactorGenArgs& a, cudaStream_t s);
 
 // -------------------------------------------------------------- matvec.cu
 // xp[p] = x[perm[p]], and the weight lane of the packed points p4 (x, y, z, w)

@@ -35,7 +35,12 @@ def main():
         rep.matvec(x)
     st = rep.stats()
     print({k: st[k] for k in ("depth", "level_modes", "build_ms_total", "build_ms_aca_rank",
-                              "build_ms_aca_write", "lu_doubles", "factor_doubles", "proxy_units")})
+                              "build_ms_aca_write", "lu_doubles", "factor_doubles", "proxy_units",
+                              "level_aca_ms", "level_units")})
+    for l in range(1, st["depth"] + 1):
+        x, y, r = rep.pairs(l)
+        if len(r):
+            print(f"level {l}: pairs {len(r)} mean rank {r.mean():.1f} max {r.max()}")
 
 
 if __name__ == "__main__":
