@@ -23,13 +23,16 @@ def main():
     ap.add_argument("--matvecs", type=int, default=2)
     ap.add_argument("--policy", default="auto")
     ap.add_argument("--near", default="matrix-free")
+    ap.add_argument("--levels", default="", help="explicit level-mode string, e.g. 011142")
     a = ap.parse_args()
     import paper_2307_16303_b200 as h3d
     cfg = CONFIGS[a.config]
+    lv = dict(mode_policy=a.policy) if not a.levels else dict(
+        mode_policy="explicit", level_modes=tuple(int(c) for c in a.levels))
     pts = h3d.generate_points(cfg["n"], cfg["seed"])
     x = h3d.random_vector(cfg["n"], cfg["seed"] + 17)
     rep = h3d.initialize(pts, h3d.make_kernel(cfg["kernel"]), "hodlr3d",
-                         h3d.HmatOptions(n_max=cfg["n_max"], epsilon=cfg["eps"], mode_policy=a.policy,
+                         h3d.HmatOptions(n_max=cfg["n_max"], epsilon=cfg["eps"], **lv,
                                          dense_mode="cached" if a.near == "stored" else "on-the-fly"))
     for _ in range(a.matvecs):
         rep.matvec(x)
