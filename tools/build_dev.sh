@@ -3,7 +3,7 @@
 # masks) into tools/lib_dev/ (git-ignored). Never the product path.
 set -e
 cd "$(dirname "$0")/../paper_2307_16303_b200/csrc"
-OUT=../../tools/lib_dev
+OUT=../../tools/${DEV_OUT:-lib_dev}
 mkdir -p $OUT/obj
 NV="/usr/local/cuda/bin/nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr -DH3D_DEVTOOLS $EXTRA"
 pids=()
