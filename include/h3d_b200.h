@@ -138,7 +138,10 @@ typedef struct {
   int64_t lu_doubles;         /* packed LU storage of proxy-level pairs */
   int64_t level_units[16];    /* per level: sum over pairs of r (m + n) */
   double level_aca_ms[16];    /* per level: ACA wall time (rank + write pass) */
-  int64_t reserved[4];
+  double build_ms_plan;       /* mode choice, layout, descriptor upload (host planner) */
+  double build_ms_post;       /* proxy pivot gather + LU triangular inverses */
+  double build_ms_near;       /* near-field symmetry scan */
+  int64_t reserved[1];
 } h3d_stats;
 
 typedef struct h3d_dev h3d_dev;

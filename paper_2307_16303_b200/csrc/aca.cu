@@ -210,7 +210,11 @@ __global__ void __launch_bounds__(NT) aca_kernel(const AcaArgs a) {
 
   for (;;) {
     cx.bar();
-    if (crank == 0 && tid == 0) s_pair = static_cast<long long>(atomicAdd(a.counter, 1ULL));
+    if (crank == 0 && tid == 0) {
+      const long long c = static_cast<long long>(atomicAdd(a.counter, 1ULL));
+      const long long nc = a.nclaims < 0 ? a.npairs : a.nclaims;
+      s_pair = c >= nc ? a.npairs : a.order != nullptr ? a.order[c] : c;
+    }
     cx.bar();
     const long long p = cx.remote(&s_pair, 0);
     cx.bar();  // no CTA may exit while a peer still reads its shared memory

@@ -9,6 +9,9 @@
 //   Engine::stats       <- h3d::stats (hmatrix.cpp:228-251)
 #include <cstdio>
 
+#include <exception>
+#include <thread>
+
 #include "engine.h"
 #include "common.cuh"
 
@@ -156,6 +159,11 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2o") tune_.p2o = v;
         else if (k == "pps") tune_.pps = v;
         else if (k == "graphs") tune_.graphs = v;
+        else if (k == "acab") tune_.acab = v;
+        else if (k.size() > 4 && k.compare(0, 4, "acat") == 0) {
+          const int lv = std::atoi(k.c_str() + 4);
+          if (lv > 0 && lv < 16 && (v == 32 || v == 128 || v == 256 || v == 512)) tune_.acat[lv] = v;
+        }
       }
       pos = end + 1;
     }
@@ -197,16 +205,36 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     }
   }
   plan_ = std::make_unique<Planner>(L_, n_, off_, lists_, rank_, world_, modes_);
+  // the rank-independent part of the layout (leaf plan, near-field lists) on
+  // a host thread while the ACA rank pass runs on the device
+  std::exception_ptr leaf_err;
+  std::thread leaf_thread([this, &leaf_err] {
+    try {
+      plan_->layout_leaf();
+    } catch (...) {
+      leaf_err = std::current_exception();
+    }
+  });
   t = Clock::now();
-  run_aca(false);
+  try {
+    run_aca(false);
+  } catch (...) {
+    leaf_thread.join();
+    throw;
+  }
   ms_aca_rank_ = ms_since(t);
+  t = Clock::now();
+  leaf_thread.join();
+  if (leaf_err) std::rethrow_exception(leaf_err);
   choose_modes();
   plan_->layout();
   upload_plan();
+  ms_plan_ = ms_since(t);
   t = Clock::now();
   single_pass_ = finish_single_pass();
   if (!single_pass_) run_aca(true);
   ms_aca_write_ = ms_since(t);
+  t = Clock::now();
   if (n_segs_all_ > 0) {
     launch_proxy_gather(segs_all_.get(), n_segs_all_, piv_.get(), px_.get(), py_.get(), pz_.get(),
                         center_.get(), q4_.get(), q4c_.get(), stream_);
@@ -233,8 +261,12 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
                      stream_);
     H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   }
+  H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  ms_post_ = ms_since(t);
+  t = Clock::now();
   near_scan();
   H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+  ms_near_ = ms_since(t);
   ms_total_ = ms_since(t0);
 }
 
@@ -401,6 +433,7 @@ void Engine::run_aca(bool write) {
     auto& P = plan_->pairs(l);
     const std::int64_t np = static_cast<std::int64_t>(P.X.size());
     if (np == 0) continue;
+    if (!write && l < 16 && tune_.acat[l] > 0) P.threads = tune_.acat[l];
     const int mode = plan_->mode(l);
     const auto t_level = Clock::now();
     std::vector<std::int64_t> xb(np), yb(np);
@@ -412,7 +445,17 @@ void Engine::run_aca(bool write) {
       nn[p] = static_cast<std::int32_t>(node_size(l, P.Y[p]));
     }
     DevBuf<std::int64_t> d_xb, d_yb, d_wx, d_wy, d_po, d_lo;
-    DevBuf<std::int32_t> d_m, d_n, d_rank, d_rx, d_ry, d_cx, d_cy;
+    DevBuf<std::int32_t> d_m, d_n, d_rank, d_rx, d_ry, d_cx, d_cy, d_order;
+    {
+      std::vector<std::int32_t> order;
+      order.reserve(static_cast<std::size_t>(np));
+      // claim order: touching pairs (the highest ranks, r^2 (m + n) panel
+      // traffic each) first, so their long ACAs do not form the level's tail
+      for (int pass = 0; pass < 2; ++pass)
+        for (std::int64_t p = 0; p < np; ++p)
+          if (boxes_touch(P.X[p], P.Y[p]) == (pass == 0)) order.push_back(static_cast<std::int32_t>(p));
+      d_order.upload(order, stream_);
+    }
     d_xb.upload(xb, stream_);
     d_yb.upload(yb, stream_);
     d_m.upload(m, stream_);
@@ -438,7 +481,7 @@ void Engine::run_aca(bool write) {
     if (write) {
       cap_ws = std::max(1, level_max_rank);
     } else {
-      cap_ws = std::min(P.max_mn, P.threads == 32 ? 64 : 256);
+      cap_ws = std::min(P.max_mn, P.threads == 32 ? 128 : 256);
       if (opt_.max_rank > 0) cap_ws = static_cast<int>(std::min<std::int64_t>(cap_ws, opt_.max_rank));
       cap_ws = std::max(cap_ws, 1);
     }
@@ -460,19 +503,8 @@ void Engine::run_aca(bool write) {
         }
         P.cluster = cl;
       }
-      const int bps = P.cluster > 1 ? 1 : aca_blocks_per_sm(P.threads, opt_.kernel_id, smem);
       const std::int64_t budget = std::max<std::int64_t>(
           std::min<std::int64_t>(static_cast<std::int64_t>(free_b / 4), 24LL << 30), 256LL << 20);
-      std::int64_t slots =
-          P.cluster > 1
-              ? std::min<std::int64_t>(np, std::max(1, aca_max_clusters(P.threads, opt_.kernel_id,
-                                                                        P.cluster, smem)))
-              : std::min<std::int64_t>(np, static_cast<std::int64_t>(bps) * sms_);
-      slots = std::min<std::int64_t>(slots, std::max<std::int64_t>(1, budget / (slot_doubles * 8)));
-      DevBuf<double> ws;
-      ws.alloc(static_cast<std::size_t>(slots * slot_doubles));
-      H3D_CUDA_CHECK(cudaMemsetAsync(counter.get(), 0, 8, stream_));
-      H3D_CUDA_CHECK(cudaMemsetAsync(flags_.get(), 0, 4, stream_));
       AcaArgs a;
       a.npairs = np;
       a.xb = d_xb.get();
@@ -486,7 +518,6 @@ void Engine::run_aca(bool write) {
       a.diag = opt_.diagonal;
       a.eps = opt_.epsilon;
       a.max_rank = opt_.max_rank;
-      a.ws = ws.get();
       a.slot_doubles = slot_doubles;
       a.cap_ws = cap_ws;
       a.ms = ms;
@@ -519,10 +550,30 @@ void Engine::run_aca(bool write) {
         a.pool_cap = static_cast<std::int64_t>(pool_.size());
         a.pool_off = po->get();
       }
-      if (P.cluster > 1)
-        launch_aca_cluster(a, P.threads, P.cluster, static_cast<int>(slots), stream_);
-      else
-        launch_aca(a, P.threads, static_cast<int>(slots), stream_);
+      H3D_CUDA_CHECK(cudaMemsetAsync(flags_.get(), 0, 4, stream_));
+      // one launch: claims [c0, c0 + nc) of the order, cluster cl
+      auto launch_group = [&](std::int64_t c0, std::int64_t nc, int cl) {
+        if (nc <= 0) return;
+        int bps = cl > 1 ? 1 : aca_blocks_per_sm(P.threads, opt_.kernel_id, smem);
+        if (tune_.acab > 0 && cl <= 1) bps = std::min(bps, tune_.acab);
+        std::int64_t slots =
+            cl > 1 ? std::min<std::int64_t>(nc, std::max(1, aca_max_clusters(P.threads, opt_.kernel_id, cl, smem)))
+                   : std::min<std::int64_t>(nc, static_cast<std::int64_t>(bps) * sms_);
+        slots = std::min<std::int64_t>(slots, std::max<std::int64_t>(1, budget / (slot_doubles * 8)));
+        DevBuf<double> ws;
+        ws.alloc(static_cast<std::size_t>(slots * slot_doubles));
+        H3D_CUDA_CHECK(cudaMemsetAsync(counter.get(), 0, 8, stream_));
+        AcaArgs g = a;
+        g.ws = ws.get();
+        g.order = d_order.get() + c0;
+        g.nclaims = nc;
+        if (cl > 1)
+          launch_aca_cluster(g, P.threads, cl, static_cast<int>(slots), stream_);
+        else
+          launch_aca(g, P.threads, static_cast<int>(slots), stream_);
+        H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));  // ws is freed on return
+      };
+      launch_group(0, np, P.cluster);
       unsigned f = 0;
       H3D_CUDA_CHECK(cudaMemcpyAsync(&f, flags_.get(), 4, cudaMemcpyDeviceToHost, stream_));
       H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -1516,6 +1567,9 @@ void Engine::stats(h3d_stats* s) const {
   s->build_ms_aca_rank = ms_aca_rank_;
   s->build_ms_aca_write = ms_aca_write_;
   s->build_ms_total = ms_total_;
+  s->build_ms_plan = ms_plan_;
+  s->build_ms_post = ms_post_;
+  s->build_ms_near = ms_near_;
   s->phase1_items = n_p1s_ + n_p1p_;
   s->owned_row_begin = P.row0;
   s->owned_row_end = P.row1;

@@ -128,10 +128,13 @@ class Engine {
   // ("nf=0": near field after p2_proxy instead of forked beside the solves;
   // "nfc": CTAs per SM of the forked near kernel; "fw=0": p2_stream does not
   // wait for the solves-done flag; "sol": CTAs per SM of the proxy solve;
-  // "p2o=0": phase-2 FP64 kernels do not wait for the HBM lane's phase 1)
+  // "p2o=0": phase-2 FP64 kernels do not wait for the HBM lane's phase 1;
+  // "acab": cap on the ACA CTAs per SM, 0 = occupancy limit; "acat<l>=<n>":
+  // ACA CTA size of level l)
   struct Tune {
     int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1, fw = 1,
-        sol = 2, p2o = 1;
+        sol = 2, p2o = 1, acab = 0;
+    int acat[16] = {};  // per-level ACA CTA size override (32 / 128 / 256 / 512)
   } tune_;
   std::size_t free_mem_ = 0;
   cudaStream_t stream_ = nullptr;
@@ -235,7 +238,8 @@ class Engine {
   std::int64_t prof_launches_ = 0;
 
   // build timings
-  double ms_tree_ = 0, ms_lists_ = 0, ms_aca_rank_ = 0, ms_aca_write_ = 0, ms_total_ = 0;
+  double ms_tree_ = 0, ms_lists_ = 0, ms_aca_rank_ = 0, ms_aca_write_ = 0, ms_total_ = 0, ms_plan_ = 0,
+         ms_post_ = 0, ms_near_ = 0;
   bool single_pass_ = false;  // the build skipped the ACA write pass
   double level_aca_ms_[16] = {};  // rank + write pass per level
 };

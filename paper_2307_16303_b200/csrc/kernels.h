@@ -52,6 +52,7 @@ void exclusive_scan_i32(void* tmp, std::size_t tmp_bytes, const std::int32_t* in
 // ----------------------------------------------------------------- aca.cu
 struct AcaArgs {
   std::int64_t npairs = 0;
+  std::int64_t nclaims = -1;  // pairs this launch claims (order[0 .. nclaims)); < 0: npairs
   const std::int64_t* xb = nullptr;  // row range begin (permuted index)
   const std::int32_t* m = nullptr;
   const std::int64_t* yb = nullptr;  // column range begin
@@ -84,6 +85,9 @@ struct AcaArgs {
   const std::int64_t* lu_off = nullptr;
   unsigned* flags = nullptr;
   unsigned long long* counter = nullptr;
+  // claim order (claim c -> pair order[c]; nullptr = identity): the costly
+  // touching pairs first, so their long ACAs do not form the level's tail
+  const std::int32_t* order = nullptr;
   // rank pass, single-pass build: every compressed pair also leaves the
   // reference's own representation (packed LU, r^2 doubles, then its 2r
   // int32 pivots packed into r doubles) in a bump-allocated pool; pool_off[p]

@@ -14,18 +14,30 @@ namespace h3db {
 namespace {
 // Morton ids at one level (bit b of ix / iy / iz -> bit 3b / 3b+1 / 3b+2,
 // reference octree.cpp:30-38): Chebyshev distance 1 between distinct boxes
+// every third bit (0, 3, 6, ...) of a 63-bit Morton id, compacted
+inline std::int64_t compact3(std::uint64_t x) {
+  x &= 0x1249249249249249ULL;
+  x = (x ^ (x >> 2)) & 0x10c30c30c30c30c3ULL;
+  x = (x ^ (x >> 4)) & 0x100f00f00f00f00fULL;
+  x = (x ^ (x >> 8)) & 0x1f0000ff0000ffULL;
+  x = (x ^ (x >> 16)) & 0x1f00000000ffffULL;
+  x = (x ^ (x >> 32)) & 0x1fffffULL;
+  return static_cast<std::int64_t>(x);
+}
 bool vertex_adjacent(std::int64_t a, std::int64_t b) {
   std::int64_t d = 0;
   for (int dim = 0; dim < 3; ++dim) {
-    std::int64_t ca = 0, cb = 0;
-    for (int bit = 0; bit < 21; ++bit) {
-      ca |= ((a >> (3 * bit + dim)) & 1) << bit;
-      cb |= ((b >> (3 * bit + dim)) & 1) << bit;
-    }
+    const std::int64_t ca = compact3(static_cast<std::uint64_t>(a) >> dim);
+    const std::int64_t cb = compact3(static_cast<std::uint64_t>(b) >> dim);
     d = std::max<std::int64_t>(d, ca > cb ? ca - cb : cb - ca);
   }
   return d == 1;
 }
+}  // namespace
+
+bool boxes_touch(std::int64_t a, std::int64_t b) { return vertex_adjacent(a, b); }
+
+namespace {
 constexpr std::int64_t kRowChunk = 2048;  // phase-1 stream: rows per item
 static_assert(kRowChunk % kTileRows == 0, "phase-1 stream items start on a row tile");
 constexpr int kColChunk = 256;            // phase-1: columns (targets) per item
@@ -147,7 +159,7 @@ void Planner::build_pairs() {
     }
     P.rank.assign(P.X.size(), 0);
     const double mbar = static_cast<double>(n_) / static_cast<double>(cnt);
-    P.threads = mbar <= 64 ? 32 : mbar <= 512 ? 128 : mbar <= 4096 ? 256 : 512;
+    P.threads = mbar <= 64 ? 32 : mbar <= 2048 ? 128 : mbar <= 8192 ? 256 : 512;
   }
   sizes.npairs = 0;
   for (const auto& P : pairs_) sizes.npairs += static_cast<std::int64_t>(P.X.size());
@@ -195,6 +207,7 @@ void Planner::layout() {
   pair_cy.assign(L_ + 1, {});
   pair_piv.assign(L_ + 1, {});
   pair_lu.assign(L_ + 1, {});
+  std::vector<std::int8_t> grp;
   for (int l = 1; l <= L_; ++l) {
     const auto& P = pairs_[l];
     const std::int64_t cnt = 1LL << (3 * l);
@@ -236,12 +249,16 @@ void Planner::layout() {
       // runs over [0, p1a) and [p1b, p1c) only. One shard: one range.
       const bool oz = owned(l, z);
       std::int32_t grp_end[4] = {0, 0, 0, 0};
+      // group of every entry (0: touching + consumed here, 1: touching,
+      // 2: consumed here, 3: rest; -1: no pair), computed once
+      grp.resize(static_cast<std::size_t>(off[z + 1] - off[z]));
+      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
+        grp[e - off[z]] = ep[e] < 0 ? -1
+                                    : (vertex_adjacent(z, lid[e]) ? 0 : 2) + ((!oz || owned(l, lid[e])) ? 0 : 1);
+      }
       for (int pass = 0; pass < 4; ++pass) {
-        const bool want_touch = pass < 2, want_need = (pass & 1) == 0;
         for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
-          if (ep[e] < 0) continue;
-          if (vertex_adjacent(z, lid[e]) != want_touch) continue;
-          if ((!oz || owned(l, lid[e])) != want_need) continue;
+          if (grp[e - off[z]] != pass) continue;
           ec[e] = cols;
           cols += P.rank[ep[e]];
           any = true;
@@ -505,6 +522,14 @@ void Planner::layout() {
   }
   pg_level[L_ + 1] = static_cast<std::int64_t>(pg_items.size());
 
+  if (!leaf_done_) layout_leaf();
+}
+
+// Leaf plan and the symmetric near-field lists. They depend on the tree, the
+// lists and the (fixed) leaf mode only, not on ranks, so the engine runs this
+// on a host thread while the ACA rank pass occupies the GPU.
+void Planner::layout_leaf() {
+  PlanSizes& S = sizes;
   // leaf plan: owned leaves; near lists = self, near_edge, near_face (the
   // reference's dense blocks), plus the leaf-level admissible partners when
   // that level is evaluated directly
@@ -561,7 +586,8 @@ void Planner::layout() {
   nf_off.assign(nl + 1, 0);
   nf_cols.assign(nl + 1, 0);
   nf_total = 0;
-  std::vector<std::vector<std::int64_t>> incoming(nl);
+  std::vector<std::pair<std::int32_t, std::int64_t>> incoming;  // (target leaf, pair-buffer run)
+  std::vector<std::int32_t> cat[4];  // dense one-way, direct one-way, dense sym, direct sym
   std::int64_t otot = 0;
   auto own = [&](std::int64_t y) { return y >= leaf0 && y < leaf1; };
   // a pair is evaluated once iff both leaves are owned and fit one pass of
@@ -572,7 +598,7 @@ void Planner::layout() {
     out_off[x] = otot;
     nf_off[x] = nf_total;
     if (node_size(L_, x) == 0 || !own(x)) continue;
-    std::vector<std::int32_t> cat[4];  // dense one-way, direct one-way, dense sym, direct sym
+    for (auto& c : cat) c.clear();
     auto put = [&](std::int64_t y, bool dense) {
       if (node_size(L_, y) == 0) return;
       const bool pair = sym(x) && sym(y);
@@ -598,7 +624,7 @@ void Planner::layout() {
       for (std::int32_t y : cat[c]) {
         sym_ids.push_back(y);
         if (c >= 2) {
-          incoming[y].push_back(otot);
+          incoming.emplace_back(y, otot);
           otot += node_size(L_, y);
         }
       }
@@ -607,13 +633,16 @@ void Planner::layout() {
   sym_off[nl] = static_cast<std::int32_t>(sym_ids.size());
   out_off[nl] = otot;
   nf_off[nl] = nf_total;
+  // incoming runs per leaf, in the order they were produced (counting sort)
   in_off.assign(nl + 1, 0);
-  in_pos.clear();
-  for (std::int64_t y = 0; y < nl; ++y) {
-    in_off[y] = static_cast<std::int32_t>(in_pos.size());
-    in_pos.insert(in_pos.end(), incoming[y].begin(), incoming[y].end());
+  for (const auto& iv : incoming) ++in_off[iv.first + 1];
+  for (std::int64_t y = 0; y < nl; ++y) in_off[y + 1] += in_off[y];
+  in_pos.assign(incoming.size(), 0);
+  {
+    std::vector<std::int32_t> fill(in_off.begin(), in_off.end() - 1);
+    for (const auto& iv : incoming) in_pos[fill[iv.first]++] = iv.second;
   }
-  in_off[nl] = static_cast<std::int32_t>(in_pos.size());
+  leaf_done_ = true;
 }
 
 }  // namespace h3db

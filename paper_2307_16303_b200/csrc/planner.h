@@ -71,6 +71,10 @@ struct PairDesc {
   std::int32_t m, n, rp, own;  // own: bit 0 = X owned here, bit 1 = Y owned
 };
 
+// Two boxes of one level touch (Chebyshev distance 1 between their Morton
+// ids' grid coordinates)
+bool boxes_touch(std::int64_t a, std::int64_t b);
+
 // Variants, h3d::Variant order (reference octree.hpp:80)
 constexpr int kVariantHodlr3d = 0;
 constexpr int kVariantHodlr = 1;
@@ -170,6 +174,9 @@ class Planner {
   const std::vector<int>& modes() const { return mode_; }
   // stream <-> proxy may change after the rank pass (direct cannot: it decides
   // which pairs exist)
+  // the rank-independent part of layout() (leaf plan, near-field lists);
+  // layout() runs it when it has not run yet
+  void layout_leaf();
   void set_mode(int l, int m) {
     if (mode_[l] == kModeDirect || m == kModeDirect)
       throw std::invalid_argument("planner: direct mode is fixed at construction");
@@ -262,6 +269,7 @@ class Planner {
   void build_pairs();
 
   int L_;
+  bool leaf_done_ = false;
   std::int64_t n_;
   std::vector<std::vector<std::int64_t>> off_;
   std::vector<LevelLists> lists_;

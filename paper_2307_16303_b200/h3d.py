@@ -118,7 +118,10 @@ class _Stats(C.Structure):
         ("lu_doubles", C.c_int64),
         ("level_units", C.c_int64 * 16),
         ("level_aca_ms", C.c_double * 16),
-        ("reserved", C.c_int64 * 4),
+        ("build_ms_plan", C.c_double),
+        ("build_ms_post", C.c_double),
+        ("build_ms_near", C.c_double),
+        ("reserved", C.c_int64 * 1),
     ]
 
 
