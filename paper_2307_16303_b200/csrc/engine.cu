@@ -1230,7 +1230,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   if (n_segs_solve_ > 0) {
     kb(H3D_K_SOLVE, stream4_);
     launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), sms_, tune_.sol,
-                       stream4_);
+                       counters_.get() + 5, stream4_);
     ke(H3D_K_SOLVE, stream4_);
     ++launches;
   }

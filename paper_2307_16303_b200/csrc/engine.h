@@ -205,7 +205,7 @@ class Engine {
   };
   std::vector<GraphEntry> graphs_;
   std::int64_t run_graph(const double* x, double* b, cudaStream_t s);
-  DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy]
+  DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy, solve, ...]
   // matvec lanes (priorities: the HBM lane and the FP64 critical chain above
   // the near field, which fills whatever the two leave idle)
   cudaStream_t stream2_ = nullptr;          // HBM lane: stream levels

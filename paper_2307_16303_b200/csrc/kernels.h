@@ -195,7 +195,7 @@ void launch_proxy_gather(const ProxySeg* segs, std::int64_t nseg, const std::int
 // (per_sm per SM at most), segments round-robin over the warps (host-sorted
 // by decreasing rank), r <= 320
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, std::int64_t lu_total,
-                        double* S, int sms, int per_sm, cudaStream_t s);
+                        double* S, int sms, int per_sm, unsigned* counter, cudaStream_t s);
 // build time: replace every pair's packed LU by its triangular inverses
 // (strict lower L^-1, upper R^-1), row-major at lu and column-major at lu + lu_total
 void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::int64_t lu_total,

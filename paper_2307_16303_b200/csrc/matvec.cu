@@ -484,36 +484,53 @@ constexpr int kSolveStageD = 640;  // 5 KB per stage: two rows of the largest bl
 constexpr int kSolveMaxR = 320;
 static_assert(kSolveStageD >= 2 * kSolveMaxR, "a stage holds at least two rows");
 
+constexpr int kSolveQ = 8;  // claimed segments queued per warp (issue runs <= kSolveStages ahead)
+
 struct SolveSmem {
   double ring[kSolveWarps][kSolveStages][kSolveStageD];
   double v[kSolveWarps][kSolveMaxR];
   unsigned long long full[kSolveWarps][kSolveStages];
+  long long queue[kSolveWarps][kSolveQ];  // segments in issue order (nseg: no more)
 };
 
 // rows per staged block (even, so every block starts 16-byte aligned)
 __device__ __forceinline__ int solve_block_rows(int r) { return max(2, (kSolveStageD / r) & ~1); }
 
+// Issue cursor of a warp (lane 0): segments are claimed dynamically (an
+// atomic counter over the rank-sorted list, so the largest blocks go first
+// and a CTA that starts late, beside other kernels, takes less), queued in
+// claim order for the consuming side.
 struct SolveIssue {
-  long long k;  // index in this warp's segment list
-  int row;      // next row of that segment to copy
-  unsigned n;   // blocks issued so far
+  long long seg;  // segment being issued (< 0: claim the next one)
+  int row;        // next row of that segment to copy
+  unsigned n;     // blocks issued so far
+  unsigned q;     // segments queued so far
+  bool done;      // the terminator is queued
 };
 
 struct SolveCtx {
   const ProxySeg* segs;
   std::int64_t nseg;
-  long long gw, nw;  // this warp's global index, warps in the grid
+  unsigned* counter;
   const double* lu;
   std::int64_t lu_total;
   unsigned long long pol;
 };
 
-// lane 0: copy the next row block of this warp's segment stream (if any) into
-// stage n % kSolveStages
+// lane 0: copy the next row block of this warp's segment stream (claiming a
+// segment when the previous one is fully issued) into stage n % kSolveStages
 __device__ __forceinline__ void solve_issue(SolveSmem& sm, int w, SolveIssue& is, const SolveCtx& cx) {
-  const long long sidx = cx.gw + is.k * cx.nw;
-  if (sidx >= cx.nseg) return;
-  const ProxySeg sg = cx.segs[sidx];
+  if (is.done) return;
+  if (is.seg < 0) {
+    is.seg = static_cast<long long>(atomicAdd(cx.counter, 1u));
+    if (is.seg >= cx.nseg) is.seg = cx.nseg;
+    sm.queue[w][is.q++ % kSolveQ] = is.seg;
+    if (is.seg >= cx.nseg) {
+      is.done = true;
+      return;
+    }
+  }
+  const ProxySeg sg = cx.segs[is.seg];
   const int r = sg.r, rb = solve_block_rows(r);
   const int nrow = min(rb, r - is.row);
   long long nd = static_cast<long long>(nrow) * r;
@@ -526,7 +543,7 @@ __device__ __forceinline__ void solve_issue(SolveSmem& sm, int w, SolveIssue& is
   is.row += nrow;
   if (is.row >= r) {
     is.row = 0;
-    ++is.k;
+    is.seg = -1;
   }
 }
 
@@ -606,15 +623,14 @@ __global__ void __launch_bounds__(32 * kSolveWarps) proxy_solve_kernel(const Pro
                                                                         std::int64_t nseg,
                                                                         const double* __restrict__ lu,
                                                                         std::int64_t lu_total,
-                                                                        double* __restrict__ S) {
+                                                                        double* __restrict__ S, unsigned* counter) {
   extern __shared__ __align__(128) unsigned char solve_smem[];
   SolveSmem& sm = *reinterpret_cast<SolveSmem*>(solve_smem);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   SolveCtx cx;
   cx.segs = segs;
   cx.nseg = nseg;
-  cx.nw = static_cast<long long>(gridDim.x) * kSolveWarps;
-  cx.gw = static_cast<long long>(blockIdx.x) * kSolveWarps + w;
+  cx.counter = counter;
   cx.lu = lu;
   cx.lu_total = lu_total;
   cx.pol = l2_evict_first();
@@ -623,12 +639,15 @@ __global__ void __launch_bounds__(32 * kSolveWarps) proxy_solve_kernel(const Pro
     mbar_fence_init();
   }
   __syncwarp();
-  SolveIssue is{0, 0, 0};
+  SolveIssue is{-1, 0, 0, 0, false};
   if (lane == 0)
     for (int st = 0; st < kSolveStages; ++st) solve_issue(sm, w, is, cx);
+  __syncwarp();
   unsigned c = 0;
   double* v = sm.v[w];
-  for (long long sidx = cx.gw; sidx < nseg; sidx += cx.nw) {
+  for (unsigned qh = 0;; ++qh) {
+    const long long sidx = sm.queue[w][qh % kSolveQ];
+    if (sidx >= nseg) break;
     const ProxySeg sg = segs[sidx];
     double* Sg = S + sg.so;
     for (int q = lane; q < sg.r; q += 32) v[q] = Sg[q];
@@ -646,7 +665,7 @@ __global__ void __launch_bounds__(32 * kSolveWarps) proxy_solve_kernel(const Pro
       case 9: solve_seg<9>(sm, w, lane, sg, v, Sg, c, is, cx); break;
       default: solve_seg<10>(sm, w, lane, sg, v, Sg, c, is, cx); break;
     }
-    __syncwarp();  // v is reused by the next segment
+    __syncwarp();  // v is reused by the next segment; the queue entry is read
   }
 }
 
@@ -1403,7 +1422,7 @@ void launch_lu_invert(const ProxySeg* segs, std::int64_t nseg, double* lu, std::
 }
 
 void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* lu, std::int64_t lu_total,
-                        double* S, int sms, int per_sm, cudaStream_t s) {
+                        double* S, int sms, int per_sm, unsigned* counter, cudaStream_t s) {
   if (nseg == 0) return;
   configure_kernels();
   int nb = 0;
@@ -1412,7 +1431,7 @@ void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* l
   const std::int64_t want = (nseg + kSolveWarps - 1) / kSolveWarps;
   const int grid = static_cast<int>(std::max<std::int64_t>(
       1, std::min<std::int64_t>(want, static_cast<std::int64_t>(sms) * std::max(1, std::min(nb, per_sm)))));
-  proxy_solve_kernel<<<grid, 32 * kSolveWarps, sizeof(SolveSmem), s>>>(segs, nseg, lu, lu_total, S);
+  proxy_solve_kernel<<<grid, 32 * kSolveWarps, sizeof(SolveSmem), s>>>(segs, nseg, lu, lu_total, S, counter);
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 
