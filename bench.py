@@ -461,11 +461,12 @@ def main():
         "config": workload_config(args.config, args.near),
         "detail": {
             "representation": {"policy": args.policy,
-                               "level_modes": {str(l): ["stream", "proxy", "direct", "pair", "fused"][m]
+                               "level_modes": {str(l): ["stream", "proxy", "direct", "pair", "fused", "half"][m]
                                                for l, m in enumerate(st["level_modes"]) if l > 0},
                                "note": "one ACA per unordered admissible pair; stream = explicit "
                                        "factors in HBM, proxy = pivots+LU regenerated in FP64, "
-                                       "direct = exact leaf blocks"},
+                                       "half = U' = K(X,tau)(LR)^-1 streamed + K(sigma,Y) "
+                                       "regenerated (no solves), direct = exact leaf blocks"},
             "streamed_factor_GB_per_phase": round(8 * F / 1e9, 3),
             "proxy_entries_per_phase": U,
             "lu_GB": round(8 * st["lu_doubles"] / 1e9, 3),

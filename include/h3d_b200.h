@@ -73,12 +73,14 @@ typedef struct {
    * 1 = auto (default): leaf level evaluated exactly, upper levels split
    *     between streamed factors and matrix-free proxies (pivots + LU, the
    *     reference's own storage, lowrank.cpp:291-327) by a HBM/FP64 cost model;
+   *     stream levels of >= 8 GB per phase become half levels (laplace3d, r4);
    * 2 = explicit per level from level_modes[l] (0 stream, 1 proxy, 2 direct,
    *     3 pair = explicit factors, one pair-major pass (U read once, V twice,
    *     the second time from L2), 4 fused = proxy storage, pair-major, each
-   *     regenerated entry evaluated once for both orientations; direct only at
-   *     the leaf level, pair and fused ranks <= 128, fused nodes <= 352
-   *     points). */
+   *     regenerated entry evaluated once for both orientations, 5 half =
+   *     U' = K(X, tau) (LR)^-1 streamed and K(sigma, Y) regenerated, no solves
+   *     (laplace3d and r4 only); direct only at the leaf level, pair and fused
+   *     ranks <= 128, fused nodes <= 352 points). */
   int mode_policy;
   int level_modes[16];
   int variant;          /* h3d_variant (Variant argument of initialize, hmatrix.hpp:57-58) */
@@ -132,7 +134,8 @@ typedef struct {
   int64_t phase1_items;
   int64_t owned_row_begin;    /* shard rows [begin, end) in Morton order */
   int64_t owned_row_end;
-  int level_modes[16];        /* applied mode per level (0 stream, 1 proxy, 2 direct, 3 pair, 4 fused) */
+  int level_modes[16];        /* applied mode per level (0 stream, 1 proxy, 2 direct, 3 pair, 4 fused,
+                                 5 half) */
   int64_t proxy_units;        /* sum over proxy-level pairs of r (m + n) */
   int64_t direct_evals;       /* leaf-level admissible entries evaluated exactly */
   int64_t lu_doubles;         /* packed LU storage of proxy-level pairs */

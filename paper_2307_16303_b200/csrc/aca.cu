@@ -497,6 +497,7 @@ __global__ void aca_compact_kernel(const double* __restrict__ pool, const std::i
   const double* src = pool + off;
   const int* pv = reinterpret_cast<const int*>(src + static_cast<std::int64_t>(r) * r);
   for (int q = threadIdx.x; q < 2 * r; q += blockDim.x) piv[piv_off[p] + q] = pv[q];
+  if (lu == nullptr) return;  // pivots only (half levels)
   double* dst = lu + lu_off[p];
   for (int e = threadIdx.x; e < r * r; e += blockDim.x) dst[e] = src[e];
 }
@@ -513,10 +514,14 @@ __device__ __forceinline__ std::int64_t w_index(int row, int col, int nct, bool 
 // with E[i][a] = K(point i, pivot point a). 32-row chunks: E and the output
 // tile staged in shared memory (rows padded to r + 1), the output written
 // column-fastest into the node's pool (coalesced).
+// full (half levels, U side): then out2[i][b] = out[i][b] + sum_{a > b}
+// out[i][a] C[b][a] with the strictly lower part of the same column-major
+// copy (L^-1), i.e. U' = K(X, tau) R^-1 L^-1.
 template <int K>
 __device__ void factor_side(const FactorGenArgs& a, std::int64_t base, int rows, std::int64_t pbase,
                             const std::int32_t* __restrict__ piv, int r, const double* __restrict__ C,
-                            bool upper, double* __restrict__ Wn, int col0, int nct, double* sm, int rc) {
+                            bool upper, double* __restrict__ Wn, int col0, int nct, double* sm, int rc,
+                            bool full = false) {
   const int ld = r + 1;
   double* E = sm;            // [rc][ld]
   double* O = sm + rc * ld;  // [rc][ld]
@@ -551,9 +556,22 @@ __device__ void factor_side(const FactorGenArgs& a, std::int64_t base, int rows,
       O[i * ld + b] = acc;
     }
     __syncthreads();
+    const double* R = O;
+    if (full) {
+      for (int e = threadIdx.x; e < nr * r; e += blockDim.x) {
+        const int b = e / nr, i = e % nr;
+        const double* cb = C + static_cast<std::int64_t>(b) * r;
+        const double* oi = O + i * ld;
+        double acc = oi[b];
+        for (int q = b + 1; q < r; ++q) acc = fma(oi[q], __ldg(cb + q), acc);
+        E[i * ld + b] = acc;
+      }
+      __syncthreads();
+      R = E;
+    }
     for (int e = threadIdx.x; e < nr * r; e += blockDim.x) {
       const int i = e / r, b = e % r;
-      Wn[w_index(i0 + i, col0 + b, nct, a.row_major != 0)] = O[i * ld + b];
+      Wn[w_index(i0 + i, col0 + b, nct, a.row_major != 0)] = R[i * ld + b];
     }
     __syncthreads();
   }
@@ -569,7 +587,8 @@ __global__ void __launch_bounds__(256) factor_gen_kernel(const FactorGenArgs a) 
   const double* inv = a.inv + a.inv_off[p];
   // U = K(X, tau) R^-1: R^-1 column b = row b of the column-major copy
   factor_side<K>(a, a.xb[p], a.m[p], a.yb[p], pv + r, r, inv + a.inv_total, true, a.W + a.wx[p], a.cx[p],
-                 a.rx[p], fg_smem, a.rc);
+                 a.rx[p], fg_smem, a.rc, a.full != 0);
+  if (a.full) return;  // half levels: the Y side is regenerated
   // V = K(Y, sigma) L^-T: L^-1 row b (strict lower part of the row-major block)
   factor_side<K>(a, a.yb[p], a.n[p], a.xb[p], pv, r, inv, false, a.W + a.wy[p], a.cy[p], a.ry[p], fg_smem,
                  a.rc);

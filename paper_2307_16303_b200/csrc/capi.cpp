@@ -343,6 +343,7 @@ int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, in
     else if (nm == "near_ids") put(P.near_ids, out, count);
     else if (nm == "near_dense") put(P.near_dense, out, count);
     else if (nm == "node_base") put(P.node_base(), out, count);
+    else if (nm == "vbase") put(P.vbase, out, count);
     else if (nm == "modes") put(P.modes(), out, count);
     else if (nm == "ranges") {
       const std::vector<int64_t> r{P.leaf0, P.leaf1, P.row0, P.row1};

@@ -44,6 +44,8 @@ constexpr int kMaxProxyRank = 320; // proxy_solve_kernel's per-warp shared buffe
 // lanes overlap imperfectly: T = max(H, D) + kOverlapLoss * min(H, D).
 constexpr double kStreamBW = 7.0e12;   // B/s, tile-pipeline read rate
 constexpr double kOverlapLoss = 0.35;
+constexpr double kStreamPower = 0.0;  // 1/s: power-cap slowdown ~ H^2 (model studies only)
+constexpr double kHalfStreamBytes = 8e9;  // B per phase: stream levels at least this large go half
 double proxy_rate(int kernel) {  // evaluations / s, Newton-form proxy kernels
   switch (kernel) {
     case kLaplace: return 1.4e12;
@@ -160,6 +162,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "pps") tune_.pps = v;
         else if (k == "graphs") tune_.graphs = v;
         else if (k == "acab") tune_.acab = v;
+        else if (k == "half_search") tune_.half_search = v;
         else if (k.size() > 4 && k.compare(0, 4, "acat") == 0) {
           const int lv = std::atoi(k.c_str() + 4);
           if (lv > 0 && lv < 16 && (v == 32 || v == 128 || v == 256 || v == 512)) tune_.acat[lv] = v;
@@ -198,7 +201,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     for (int l = 1; l <= L_ && l < 16; ++l) {
       const int m = opt_.level_modes[l];
       if (m < 0 || m > kModeLast)
-        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2, 3 or 4");
+        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2, 3, 4 or 5");
       if (m == kModeDirect && l != L_)
         throw InvalidArgument("initialize: direct mode is only valid at the leaf level");
       modes_[l] = m;
@@ -232,7 +235,13 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   ms_plan_ = ms_since(t);
   t = Clock::now();
   single_pass_ = finish_single_pass();
-  if (!single_pass_) run_aca(true);
+  if (!single_pass_) {
+    for (int l = 1; l <= L_; ++l)
+      if (plan_->mode(l) == kModeHalf)
+        throw InvalidArgument("initialize: half mode (5) needs the single-pass build, whose pivot / LU pool "
+                              "did not fit in device memory; use stream or proxy mode");
+    run_aca(true);
+  }
   ms_aca_write_ = ms_since(t);
   t = Clock::now();
   if (n_segs_all_ > 0) {
@@ -637,90 +646,108 @@ bool Engine::finish_single_pass() {
     DevBuf<std::int32_t> d_rank;
     d_rank.upload(P.rank, stream_);
     const std::int64_t* poff = pool_off_[static_cast<std::size_t>(l)]->get();
-    if (mode == kModeProxy || mode == kModeFused) {
+    if (mode == kModeProxy || mode == kModeFused || mode == kModeHalf) {
       DevBuf<std::int64_t> d_po, d_lo;
       d_po.upload(plan_->pair_piv[l], stream_);
       d_lo.upload(plan_->pair_lu[l], stream_);
-      launch_aca_compact(pool_.get(), poff, d_rank.get(), np, piv_.get(), d_po.get(), lu_.get(), d_lo.get(),
-                         stream_);
+      launch_aca_compact(pool_.get(), poff, d_rank.get(), np, piv_.get(), d_po.get(),
+                         mode == kModeHalf ? nullptr : lu_.get(), d_lo.get(), stream_);
       H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
-      continue;
+      // half levels also get the explicit U' = K(X, tau) R^-1 L^-1 (below)
+      if (mode != kModeHalf) continue;
     }
-    // stream / pair level: pivots + LU into a temporary block array, its
-    // triangular inverses, then the explicit factors straight into W
-    std::vector<std::int64_t> po(np), lo(np), xb(np), yb(np);
-    std::vector<std::int32_t> m(np), nn(np);
-    std::vector<ProxySeg> segs(np);
-    std::int64_t ptot = 0, ltot = 0;
-    int max_r = 0;
-    for (std::int64_t p = 0; p < np; ++p) {
-      const std::int64_t r = P.rank[p];
-      po[p] = ptot;
-      lo[p] = ltot;
-      ptot += 2 * r;
-      ltot += r * r + (r & 1);
-      max_r = std::max<int>(max_r, static_cast<int>(r));
-      xb[p] = off_[l][P.X[p]];
-      yb[p] = off_[l][P.Y[p]];
-      m[p] = static_cast<std::int32_t>(node_size(l, P.X[p]));
-      nn[p] = static_cast<std::int32_t>(node_size(l, P.Y[p]));
-      segs[p] = ProxySeg{};
-      segs[p].lu_off = lo[p];
-      segs[p].piv_off = po[p];
-      segs[p].r = static_cast<std::int32_t>(r);
-      segs[p].side = 0;
+    // stream / pair / half level: pivots + LU into a temporary block array,
+    // its triangular inverses, then the explicit factors straight into W - in
+    // chunks of pairs whose temporaries stay under ~2 GB (C5 level 5 alone
+    // would need ~20 GB beside the pool and W)
+    constexpr std::int64_t kChunkDoubles = 128LL << 20;
+    for (std::int64_t p0 = 0; p0 < np;) {
+      std::int64_t p1 = p0, ptot = 0, ltot = 0;
+      int max_r = 0;
+      std::vector<std::int64_t> po, lo, xb, yb, wx, wy;
+      std::vector<std::int32_t> m, nn, rx, ry, cx, cy;
+      std::vector<ProxySeg> segs;
+      while (p1 < np && (p1 == p0 || ltot < kChunkDoubles)) {
+        const std::int64_t p = p1++;
+        const std::int64_t r = P.rank[p];
+        po.push_back(ptot);
+        lo.push_back(ltot);
+        ptot += 2 * r;
+        ltot += r * r + (r & 1);
+        max_r = std::max<int>(max_r, static_cast<int>(r));
+        xb.push_back(off_[l][P.X[p]]);
+        yb.push_back(off_[l][P.Y[p]]);
+        m.push_back(static_cast<std::int32_t>(node_size(l, P.X[p])));
+        nn.push_back(static_cast<std::int32_t>(node_size(l, P.Y[p])));
+        wx.push_back(plan_->pair_wx[l][p]);
+        wy.push_back(plan_->pair_wy[l][p]);
+        rx.push_back(plan_->pair_rx[l][p]);
+        ry.push_back(plan_->pair_ry[l][p]);
+        cx.push_back(plan_->pair_cx[l][p]);
+        cy.push_back(plan_->pair_cy[l][p]);
+        ProxySeg sg{};
+        sg.lu_off = lo.back();
+        sg.piv_off = po.back();
+        sg.r = static_cast<std::int32_t>(r);
+        sg.side = 0;
+        segs.push_back(sg);
+      }
+      const std::int64_t nc = p1 - p0;
+      if (max_r > 0) {
+        DevBuf<std::int32_t> tpiv, d_m, d_n;
+        DevBuf<double> tlu;
+        DevBuf<std::int64_t> d_po, d_lo, d_xb, d_yb, d_wx, d_wy;
+        DevBuf<std::int32_t> d_rx, d_ry, d_cx, d_cy;
+        DevBuf<ProxySeg> d_segs;
+        tpiv.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ptot, 1)));
+        tlu.alloc(static_cast<std::size_t>(std::max<std::int64_t>(2 * ltot, 1)));
+        d_po.upload(po, stream_);
+        d_lo.upload(lo, stream_);
+        launch_aca_compact(pool_.get(), poff + p0, d_rank.get() + p0, nc, tpiv.get(), d_po.get(), tlu.get(),
+                           d_lo.get(), stream_);
+        d_segs.upload(segs, stream_);
+        launch_lu_invert(d_segs.get(), nc, tlu.get(), ltot, max_r, stream_);
+        d_xb.upload(xb, stream_);
+        d_yb.upload(yb, stream_);
+        d_m.upload(m, stream_);
+        d_n.upload(nn, stream_);
+        d_wx.upload(wx, stream_);
+        d_wy.upload(wy, stream_);
+        d_rx.upload(rx, stream_);
+        d_ry.upload(ry, stream_);
+        d_cx.upload(cx, stream_);
+        d_cy.upload(cy, stream_);
+        FactorGenArgs fa;
+        fa.npairs = nc;
+        fa.xb = d_xb.get();
+        fa.m = d_m.get();
+        fa.yb = d_yb.get();
+        fa.n = d_n.get();
+        fa.rank = d_rank.get() + p0;
+        fa.piv = tpiv.get();
+        fa.piv_off = d_po.get();
+        fa.inv = tlu.get();
+        fa.inv_total = ltot;
+        fa.inv_off = d_lo.get();
+        fa.px = px_.get();
+        fa.py = py_.get();
+        fa.pz = pz_.get();
+        fa.kernel = opt_.kernel_id;
+        fa.W = W_.get();
+        fa.wx = d_wx.get();
+        fa.cx = d_cx.get();
+        fa.rx = d_rx.get();
+        fa.wy = d_wy.get();
+        fa.cy = d_cy.get();
+        fa.ry = d_ry.get();
+        fa.row_major = mode == kModePair ? 1 : 0;
+        fa.full = mode == kModeHalf ? 1 : 0;
+        fa.max_r = max_r;
+        launch_factor_gen(fa, stream_);
+        H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
+      }
+      p0 = p1;
     }
-    if (max_r == 0) continue;
-    DevBuf<std::int32_t> tpiv, d_m, d_n;
-    DevBuf<double> tlu;
-    DevBuf<std::int64_t> d_po, d_lo, d_xb, d_yb, d_wx, d_wy;
-    DevBuf<std::int32_t> d_rx, d_ry, d_cx, d_cy;
-    DevBuf<ProxySeg> d_segs;
-    tpiv.alloc(static_cast<std::size_t>(std::max<std::int64_t>(ptot, 1)));
-    tlu.alloc(static_cast<std::size_t>(std::max<std::int64_t>(2 * ltot, 1)));
-    d_po.upload(po, stream_);
-    d_lo.upload(lo, stream_);
-    launch_aca_compact(pool_.get(), poff, d_rank.get(), np, tpiv.get(), d_po.get(), tlu.get(), d_lo.get(),
-                       stream_);
-    d_segs.upload(segs, stream_);
-    launch_lu_invert(d_segs.get(), np, tlu.get(), ltot, max_r, stream_);
-    d_xb.upload(xb, stream_);
-    d_yb.upload(yb, stream_);
-    d_m.upload(m, stream_);
-    d_n.upload(nn, stream_);
-    d_wx.upload(plan_->pair_wx[l], stream_);
-    d_wy.upload(plan_->pair_wy[l], stream_);
-    d_rx.upload(plan_->pair_rx[l], stream_);
-    d_ry.upload(plan_->pair_ry[l], stream_);
-    d_cx.upload(plan_->pair_cx[l], stream_);
-    d_cy.upload(plan_->pair_cy[l], stream_);
-    FactorGenArgs fa;
-    fa.npairs = np;
-    fa.xb = d_xb.get();
-    fa.m = d_m.get();
-    fa.yb = d_yb.get();
-    fa.n = d_n.get();
-    fa.rank = d_rank.get();
-    fa.piv = tpiv.get();
-    fa.piv_off = d_po.get();
-    fa.inv = tlu.get();
-    fa.inv_total = ltot;
-    fa.inv_off = d_lo.get();
-    fa.px = px_.get();
-    fa.py = py_.get();
-    fa.pz = pz_.get();
-    fa.kernel = opt_.kernel_id;
-    fa.W = W_.get();
-    fa.wx = d_wx.get();
-    fa.cx = d_cx.get();
-    fa.rx = d_rx.get();
-    fa.wy = d_wy.get();
-    fa.cy = d_cy.get();
-    fa.ry = d_ry.get();
-    fa.row_major = mode == kModePair ? 1 : 0;
-    fa.max_r = max_r;
-    launch_factor_gen(fa, stream_);
-    H3D_CUDA_CHECK(cudaStreamSynchronize(stream_));
   }
   pool_.reset();
   pool_off_.clear();
@@ -736,6 +763,11 @@ bool Engine::finish_single_pass() {
 void Engine::choose_modes() {
   if (opt_.mode_policy == 2) {
     for (int l = 1; l <= L_; ++l) {
+      if (plan_->mode(l) == kModeHalf && !plan_->pairs(l).X.empty() && opt_.kernel_id != kLaplace &&
+          opt_.kernel_id != kR4)
+        throw InvalidArgument("initialize: half mode (5) is for the smooth kernels (laplace3d, r4): with "
+                              "cos(r)/r the explicit U' = K(X, tau) (LR)^-1 loses accuracy; use proxy or "
+                              "stream mode there");
       if (plan_->mode(l) == kModePair) {
         const auto& rk = plan_->pairs(l).rank;
         if (!rk.empty() && *std::max_element(rk.begin(), rk.end()) > kPairMaxRp)
@@ -766,7 +798,8 @@ void Engine::choose_modes() {
   }
   if (opt_.mode_policy != 1) return;
   std::vector<int> cand;
-  std::vector<double> units(L_ + 1, 0.0), lu(L_ + 1, 0.0);
+  // per level: units (sum r (m + n)), the X-side part (sum r m), sum r^2
+  std::vector<double> units(L_ + 1, 0.0), ux(L_ + 1, 0.0), lu(L_ + 1, 0.0);
   std::vector<int> maxr(L_ + 1, 0);
   for (int l = 1; l <= L_; ++l) {
     const auto& P = plan_->pairs(l);
@@ -774,6 +807,7 @@ void Engine::choose_modes() {
     for (std::size_t p = 0; p < P.X.size(); ++p) {
       const double r = P.rank[p];
       units[l] += r * static_cast<double>(node_size(l, P.X[p]) + node_size(l, P.Y[p]));
+      ux[l] += r * static_cast<double>(node_size(l, P.X[p]));
       lu[l] += r * r;
       maxr[l] = std::max(maxr[l], P.rank[p]);
     }
@@ -802,39 +836,83 @@ void Engine::choose_modes() {
   const double budget = 0.8 * static_cast<double>(free_mem_) - 64.0 * static_cast<double>(n_) -
                         (2 << 30);
   const double Rp = proxy_rate(opt_.kernel_id), Rn = near_rate(opt_.kernel_id);
-  double best = 1e300;
-  unsigned best_mask = 0;
+  // half levels (mode 5) form U' = K(X, tau) (LR)^-1 explicitly: fine for the
+  // smooth kernels, unstable for the oscillatory cos(r)/r (an ill-conditioned
+  // R mixed into every column of U', measured 0.06-0.16 relative error on
+  // the Helmholtz goldens), so auto offers it for Laplace and 1/r^4 only,
+  // and only when the single-pass pool kept every pair's pivots + LU
+  const bool half_ok = (opt_.kernel_id == kLaplace || opt_.kernel_id == kR4) && pool_ok_;
+  // the search covers proxy / stream (H3D_TUNE half_search=1: half too, for
+  // model studies); half replaces large stream levels afterwards (below)
+  const int nopt = half_ok && tune_.half_search ? 3 : 2;  // 0 proxy, 1 stream, 2 half
   const unsigned ncand = static_cast<unsigned>(cand.size());
-  for (unsigned mask = 0; mask < (1u << ncand); ++mask) {  // bit set = stream
-    double sbytes = 0.0, comp = 0.0, lub = 0.0;
+  unsigned ncomb = 1;
+  for (unsigned i = 0; i < ncand; ++i) ncomb *= static_cast<unsigned>(nopt);
+  double best = 1e300;
+  unsigned best_code = 0;
+  const bool dbg = std::getenv("H3D_MODEL_PRINT") != nullptr;
+  // stream levels that will become half levels (below) need only U' in W
+  auto to_half = [&](int l) { return half_ok && l > 1 && 8.0 * units[l] >= kHalfStreamBytes; };
+  for (unsigned code = 0; code < ncomb; ++code) {
+    double sbytes = 0.0, evals = 0.0, lub = 0.0, wbytes = 0.0;
     bool ok = true;
-    for (unsigned i = 0; i < ncand; ++i) {
+    unsigned c = code;
+    for (unsigned i = 0; i < ncand; ++i, c /= nopt) {
       const int l = cand[i];
-      if (mask & (1u << i)) {
+      const unsigned o = c % nopt;
+      if (o == 1) {
         // level 1 (8 nodes of N/8 points) streams through long partial-sum
         // chains and few work items: measured slower than its model, keep it
         // regenerated unless its ranks exceed the solve kernel's capacity
         if (l == 1 && maxr[l] <= kMaxProxyRank) ok = false;
         sbytes += 8.0 * units[l];
+        wbytes += 8.0 * (to_half(l) ? ux[l] : units[l]);
+      } else if (o == 2) {
+        if (l == 1) ok = false;
+        sbytes += 8.0 * ux[l];
+        wbytes += 8.0 * ux[l];
+        evals += units[l] - ux[l];
       } else {
         if (maxr[l] > kMaxProxyRank) ok = false;
-        comp += 2.0 * units[l] / Rp;
+        evals += units[l];
         lub += 2.0 * 8.0 * lu[l];  // both orientations read the pair's inverses once
       }
     }
-    if (!ok || sbytes > budget) continue;
+    if (!ok || wbytes > budget) continue;
     const double H = 2.0 * sbytes / kStreamBW;
-    const double D = comp + fixed / Rn + lub / kStreamBW;
-    const double T = std::max(H, D) + kOverlapLoss * std::min(H, D);
+    const double D = 2.0 * evals / Rp + fixed / Rn + lub / kStreamBW;
+    // the factor stream slows both lanes beyond the overlap loss (it pulls
+    // the board to its power limit): a term growing with its square,
+    // calibrated on C3 (stream vs half level 4, profiles/r02_summary.md)
+    const double T = std::max(H, D) + kOverlapLoss * std::min(H, D) + kStreamPower * H * H;
+    if (dbg) {
+      std::fprintf(stderr, "model");
+      unsigned cc = code;
+      for (unsigned i = 0; i < ncand; ++i, cc /= nopt) std::fprintf(stderr, " L%d=%u", cand[i], cc % nopt);
+      std::fprintf(stderr, "  H %.3f ms D %.3f ms T %.3f ms sbytes %.4g evals %.4g fixed %.4g lub %.4g\n",
+                   H * 1e3, D * 1e3, T * 1e3, sbytes, evals, fixed, lub);
+    }
     if (T < best) {
       best = T;
-      best_mask = mask;
+      best_code = code;
     }
   }
   if (best == 1e300)
     throw std::runtime_error("initialize: no stream/proxy split fits in device memory");
-  for (unsigned i = 0; i < ncand; ++i)
-    plan_->set_mode(cand[i], (best_mask & (1u << i)) ? kModeStream : kModeProxy);
+  unsigned c = best_code;
+  for (unsigned i = 0; i < ncand; ++i, c /= nopt) {
+    const unsigned o = c % nopt;
+    int m = o == 1 ? kModeStream : o == 2 ? kModeHalf : kModeProxy;
+    // A large factor stream pulls the board to its power limit and slows both
+    // lanes beyond the bandwidth model (C3: 75 GB per matvec, SM clock 1700
+    // vs 1965 MHz): stream levels of >= 8 GB per phase go half explicit /
+    // half regenerated instead (U' streamed, the other side regenerated, no
+    // solves). Measured (profiles/r02_summary.md): C3 level 4 18.3 -> 17.6
+    // ms, C4 levels 2 + 4 8.65 -> 8.25 ms, C5 levels 2 + 5 81.5 -> 66.3 ms;
+    // C2's 2.3 GB level 3 stays streamed (1.04 vs 1.14 ms half).
+    if (m == kModeStream && to_half(cand[i])) m = kModeHalf;
+    plan_->set_mode(cand[i], m);
+  }
 }
 
 // ---------------------------------------------------------------- device plan

@@ -137,6 +137,7 @@ struct FactorGenArgs {
   const std::int32_t* cy = nullptr;
   const std::int32_t* ry = nullptr;
   int row_major = 0;
+  int full = 0;  // half levels: X side only, U' = K(X, tau) R^-1 L^-1
   int max_r = 0;
   int rc = 32;  // rows per staged chunk (set by the launcher)
 };

@@ -166,7 +166,15 @@ void Planner::build_pairs() {
 }
 
 void Planner::layout() {
-  const std::int64_t T = total_nodes();
+  // half levels: a second (virtual) node id per node for its regenerated
+  // column group
+  std::int64_t T = total_nodes();
+  vbase.assign(L_ + 1, -1);
+  for (int l = 1; l <= L_; ++l)
+    if (mode_[l] == kModeHalf) {
+      vbase[l] = T;
+      T += 1LL << (3 * l);
+    }
   woff.assign(T, 0);
   soff.assign(T, 0);
   rowbeg.assign(T, 0);
@@ -184,7 +192,10 @@ void Planner::layout() {
       std::int64_t c[3] = {0, 0, 0};
       for (int b = 0; b < l; ++b)
         for (int d = 0; d < 3; ++d) c[d] |= ((z >> (3 * b + d)) & 1) << b;
-      for (int d = 0; d < 3; ++d) center[4 * gid(l, z) + d] = -1.0 + (static_cast<double>(c[d]) + 0.5) * w;
+      for (int d = 0; d < 3; ++d) {
+        center[4 * gid(l, z) + d] = -1.0 + (static_cast<double>(c[d]) + 0.5) * w;
+        if (vbase[l] >= 0) center[4 * gv(l, z) + d] = center[4 * gid(l, z) + d];
+      }
     }
   }
   for (int l = 0; l <= L_; ++l) {
@@ -192,6 +203,10 @@ void Planner::layout() {
     for (std::int64_t z = 0; z < cnt; ++z) {
       rowbeg[gid(l, z)] = off_[l][z];
       rows[gid(l, z)] = static_cast<std::int32_t>(node_size(l, z));
+      if (vbase[l] >= 0) {
+        rowbeg[gv(l, z)] = off_[l][z];
+        rows[gv(l, z)] = static_cast<std::int32_t>(node_size(l, z));
+      }
     }
   }
   PlanSizes& S = sizes;
@@ -215,13 +230,19 @@ void Planner::layout() {
       const std::int64_t r = P.rank[p];
       const std::int64_t units = r * (node_size(l, P.X[p]) + node_size(l, P.Y[p]));
       S.sum_rank += r;
-      if (mode_[l] == kModeStream || mode_[l] == kModePair) S.factor_doubles += units;
-      else S.proxy_units += units;
+      if (mode_[l] == kModeStream || mode_[l] == kModePair) {
+        S.factor_doubles += units;
+      } else if (mode_[l] == kModeHalf) {  // U' streamed, the Y side regenerated
+        S.factor_doubles += r * node_size(l, P.X[p]);
+        S.proxy_units += r * node_size(l, P.Y[p]);
+      } else {
+        S.proxy_units += units;
+      }
       S.max_rank = std::max(S.max_rank, P.rank[p]);
       S.ref_float_count += 2ull * static_cast<std::uint64_t>(r * r);
       S.ref_int_count += 4ull * static_cast<std::uint64_t>(r);
     }
-    if (mode_[l] == kModeProxy || mode_[l] == kModeFused) {
+    if (mode_[l] == kModeProxy || mode_[l] == kModeFused || mode_[l] == kModeHalf) {
       pair_piv[l].resize(P.X.size());
       pair_lu[l].resize(P.X.size());
       for (std::size_t p = 0; p < P.X.size(); ++p) {
@@ -229,7 +250,8 @@ void Planner::layout() {
         pair_piv[l][p] = S.piv_total;
         pair_lu[l][p] = S.lu_total;
         S.piv_total += 2 * r;
-        S.lu_total += r * r + (r & 1);  // even: 16-B aligned slots (bulk-copied by fused.cu)
+        // half levels keep the pivots only (their LU lives in U')
+        if (mode_[l] != kModeHalf) S.lu_total += r * r + (r & 1);  // even: 16-B aligned slots (fused.cu)
       }
     }
     const auto& off = lists_[l].off[0];
@@ -237,51 +259,56 @@ void Planner::layout() {
     auto& ec = entry_col_[l];
     ec.assign(ep.size(), -1);
     const auto& lid = lists_[l].ids[0];
-    for (std::int64_t z = 0; z < cnt; ++z) {
-      std::int32_t cols = 0;
-      bool any = false;
-      const std::int64_t g = gid(l, z);
-      // column groups: touching partners (Chebyshev distance 1) first (the
-      // proxy kernels' difference form covers the prefix [0, vcols)); within
-      // each, partners whose phase-1 output is consumed on this shard first.
-      // An owned node's columns against a remote partner feed only phase 2
-      // (that partner's t-vector comes from its ghost pool here), so phase 1
-      // runs over [0, p1a) and [p1b, p1c) only. One shard: one range.
-      const bool oz = owned(l, z);
-      std::int32_t grp_end[4] = {0, 0, 0, 0};
-      // group of every entry (0: touching + consumed here, 1: touching,
-      // 2: consumed here, 3: rest; -1: no pair), computed once
-      grp.resize(static_cast<std::size_t>(off[z + 1] - off[z]));
-      for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
-        grp[e - off[z]] = ep[e] < 0 ? -1
-                                    : (vertex_adjacent(z, lid[e]) ? 0 : 2) + ((!oz || owned(l, lid[e])) ? 0 : 1);
-      }
-      for (int pass = 0; pass < 4; ++pass) {
+    const bool half = mode_[l] == kModeHalf;
+    for (std::int64_t z = 0; z < cnt; ++z)
+      for (int side = 0; side < (half ? 2 : 1); ++side) {
+        // half levels: side 0 = the pairs z is X of (explicit U', streamed,
+        // node id gid), side 1 = the pairs z is Y of (regenerated, node id gv)
+        std::int32_t cols = 0;
+        bool any = false;
+        const std::int64_t g = side == 0 ? gid(l, z) : gv(l, z);
+        // column groups: touching partners (Chebyshev distance 1) first (the
+        // proxy kernels' difference form covers the prefix [0, vcols)); within
+        // each, partners whose phase-1 output is consumed on this shard first.
+        // An owned node's columns against a remote partner feed only phase 2
+        // (that partner's t-vector comes from its ghost pool here), so phase 1
+        // runs over [0, p1a) and [p1b, p1c) only. One shard: one range.
+        const bool oz = owned(l, z);
+        std::int32_t grp_end[4] = {0, 0, 0, 0};
+        // group of every entry (0: touching + consumed here, 1: touching,
+        // 2: consumed here, 3: rest; -1: no pair / the other side), computed once
+        grp.resize(static_cast<std::size_t>(off[z + 1] - off[z]));
         for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
-          if (grp[e - off[z]] != pass) continue;
-          ec[e] = cols;
-          cols += P.rank[ep[e]];
-          any = true;
+          const bool mine = ep[e] >= 0 && (!half || (P.X[ep[e]] == z) == (side == 0));
+          grp[e - off[z]] = !mine ? -1
+                                  : (vertex_adjacent(z, lid[e]) ? 0 : 2) + ((!oz || owned(l, lid[e])) ? 0 : 1);
         }
-        grp_end[pass] = cols;
+        for (int pass = 0; pass < 4; ++pass) {
+          for (std::int32_t e = off[z]; e < off[z + 1]; ++e) {
+            if (grp[e - off[z]] != pass) continue;
+            ec[e] = cols;
+            cols += P.rank[ep[e]];
+            any = true;
+          }
+          grp_end[pass] = cols;
+        }
+        vcols[g] = grp_end[1];
+        p1a[g] = grp_end[0];
+        p1b[g] = grp_end[1];
+        p1c[g] = grp_end[2];
+        const bool stream = mode_[l] == kModeStream || (half && side == 0);
+        const std::int32_t rp = !any || mode_[l] == kModePair || mode_[l] == kModeFused
+                                    ? 0
+                                    : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols
+                                             : cols + (cols & 1);
+        rpad[g] = rp;
+        soff[g] = S.s_doubles;
+        S.s_doubles += rp;
+        if (stream) {
+          woff[g] = S.w_doubles;
+          S.w_doubles += (node_size(l, z) + kTileRows - 1) / kTileRows * kTileRows * rp;
+        }
       }
-      vcols[g] = grp_end[1];
-      p1a[g] = grp_end[0];
-      p1b[g] = grp_end[1];
-      p1c[g] = grp_end[2];
-      const bool stream = mode_[l] == kModeStream;
-      const std::int32_t rp = !any || mode_[l] == kModePair || mode_[l] == kModeFused
-                                  ? 0
-                                  : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols
-                                           : cols + (cols & 1);
-      rpad[g] = rp;
-      soff[g] = S.s_doubles;
-      S.s_doubles += rp;
-      if (stream) {
-        woff[g] = S.w_doubles;
-        S.w_doubles += (node_size(l, z) + kTileRows - 1) / kTileRows * kTileRows * rp;
-      }
-    }
     if (mode_[l] == kModePair) {
       // pair-major pool: F_p = [U_p; V_p], (m + n) x rp row-major
       pair_wx[l].resize(P.X.size());
@@ -298,6 +325,21 @@ void Planner::layout() {
         pair_rx[l][p] = rp;
         pair_ry[l][p] = rp;
         S.w_doubles += (m + nn) * rp;
+      }
+    }
+    if (mode_[l] == kModeHalf) {
+      // explicit U' of the X side only: W node base, first column, column tiles
+      pair_wx[l].resize(P.X.size());
+      pair_cx[l].resize(P.X.size());
+      pair_rx[l].resize(P.X.size());
+      pair_wy[l].assign(P.X.size(), 0);
+      pair_cy[l].assign(P.X.size(), 0);
+      pair_ry[l].assign(P.X.size(), 0);
+      for (std::size_t p = 0; p < P.X.size(); ++p) {
+        const std::int64_t gx = gid(l, P.X[p]);
+        pair_wx[l][p] = woff[gx];
+        pair_cx[l][p] = ec[P.eX[p]];
+        pair_rx[l][p] = rpad[gx] / kTileCols;
       }
     }
     if (mode_[l] == kModeStream) {
@@ -339,22 +381,30 @@ void Planner::layout() {
         if (p < 0) continue;
         const std::int32_t k = ids[e];
         const int r = P.rank[p];
-        const std::int64_t so = soff[gid(l, z)] + ec[e];
-        if (mode_[l] == kModeProxy) {
+        const bool zx = P.X[p] == z;
+        // half levels: z's column for k sits in z's stream group when z is
+        // the pair's X, in its regenerated (virtual) group when z is Y
+        const bool half = mode_[l] == kModeHalf;
+        const std::int64_t gz = half && !zx ? gv(l, z) : gid(l, z);
+        const std::int64_t so = soff[gz] + ec[e];
+        if (mode_[l] == kModeProxy || (half && !zx)) {
           ProxySeg sg{};
           sg.so = so;
           sg.base = off_[l][k];
           sg.piv_off = pair_piv[l][p];
           sg.lu_off = pair_lu[l][p];
           sg.r = r;
-          sg.side = (P.X[p] == z) ? 0 : 1;
-          sg.solve = owned(l, z) ? 1 : 0;
-          sg.node = static_cast<std::int32_t>(gid(l, z));
+          sg.side = zx ? 0 : 1;
+          // half levels: the phase-1 output of a regenerated column is the
+          // transposed block's weight as it is (U' carries (LR)^-1): no solve
+          sg.solve = !half && owned(l, z) ? 1 : 0;
+          sg.node = static_cast<std::int32_t>(gz);
           proxy_segs.push_back(sg);
         }
         if (!owned(l, k)) continue;
-        const std::int32_t e2 = (P.X[p] == z) ? P.eY[p] : P.eX[p];
-        const std::int64_t dst = soff[gid(l, k)] + ec[e2];
+        const std::int32_t e2 = zx ? P.eY[p] : P.eX[p];
+        const std::int64_t gk = half && zx ? gv(l, k) : gid(l, k);  // k is the pair's Y iff z is X
+        const std::int64_t dst = soff[gk] + ec[e2];
         for (int a = 0; a < r; ++a) spos[so + a] = static_cast<std::int32_t>(dst + a);
       }
     }
@@ -368,9 +418,14 @@ void Planner::layout() {
   for (int l = 1; l <= L_; ++l) {
     if (mode_[l] == kModeDirect || mode_[l] == kModePair || mode_[l] == kModeFused) continue;
     const std::int64_t cnt = 1LL << (3 * l);
-    const std::int64_t chunk = mode_[l] == kModeStream ? kRowChunk : kSrcChunk;
+    const bool half = mode_[l] == kModeHalf;
+    for (int side = 0; side < (half ? 2 : 1); ++side) {
+    // half levels: side 0 = the streamed groups (node ids gid), side 1 = the
+    // regenerated ones (node ids gv)
+    const int kind = half ? (side == 0 ? kModeStream : kModeProxy) : mode_[l];
+    const std::int64_t chunk = kind == kModeStream ? kRowChunk : kSrcChunk;
     for (std::int64_t z = 0; z < cnt; ++z) {
-      const std::int64_t g = gid(l, z);
+      const std::int64_t g = side == 0 ? gid(l, z) : gv(l, z);
       const int rp = rpad[g];
       if (rp == 0) continue;
       const std::int64_t nr = node_size(l, z);
@@ -378,11 +433,11 @@ void Planner::layout() {
       const std::int64_t pbase = ptot;
       if (nrc > 1) {
         ptot += nrc * rp;
-        reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rp, static_cast<std::int32_t>(nrc), mode_[l], pbase});
+        reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rp, static_cast<std::int32_t>(nrc), kind, pbase});
       }
       // column ranges whose t-vectors are consumed on this shard (see the
       // column groups above), tile-aligned on stream levels
-      const int al = mode_[l] == kModeStream ? kTileCols : 1;
+      const int al = kind == kModeStream ? kTileCols : 1;
       auto down = [&](int v) { return v / al * al; };
       auto up = [&](int v) { return std::min(rp, (v + al - 1) / al * al); };
       int rng[2][2] = {{0, up(p1a[g])}, {down(p1b[g]), up(p1c[g])}};
@@ -399,10 +454,11 @@ void Planner::layout() {
             it.nrows = static_cast<std::int32_t>(std::min<std::int64_t>(chunk, nr - k * chunk));
             it.col0 = c0;
             it.ncols = std::min(kColChunk, rg[1] - c0);
-            it.kind = mode_[l];
+            it.kind = kind;
             it.pslot = nrc > 1 ? pbase + k * rp + c0 : -1;
             items.push_back(it);
           }
+    }
     }
   }
   S.p_doubles = ptot;
@@ -501,23 +557,28 @@ void Planner::layout() {
       }
       continue;
     }
-    const bool stream = mode_[l] == kModeStream;
-    const std::int64_t cnt = 1LL << (3 * l);
-    const std::int64_t step = stream ? kTileRows : kColChunk;
-    auto& dst = stream ? p2s_items : p2_items;
-    int slot = -1;
-    for (std::int64_t z = 0; z < cnt; ++z) {
-      const std::int64_t g = gid(l, z);
-      if (rpad[g] == 0 || !owned(l, z)) continue;
-      if (slot < 0) slot = n_proxy_levels++;
-      const std::int64_t nr = node_size(l, z);
-      // proxy levels: even split into ceil(nr / 256) items (a 256 + small
-      // remainder split leaves most of the second item's target slots idle)
-      const std::int64_t per =
-          stream ? step : (nr + (nr + step - 1) / step - 1) / ((nr + step - 1) / step);
-      for (std::int64_t r0 = 0; r0 < nr; r0 += per)
-        dst.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
-                             static_cast<std::int32_t>(std::min<std::int64_t>(per, nr - r0)), slot});
+    const bool half = mode_[l] == kModeHalf;
+    // half levels: the streamed groups and the regenerated groups write a
+    // partial each (two output slots)
+    for (int side = 0; side < (half ? 2 : 1); ++side) {
+      const bool stream = half ? side == 0 : mode_[l] == kModeStream;
+      const std::int64_t cnt = 1LL << (3 * l);
+      const std::int64_t step = stream ? kTileRows : kColChunk;
+      auto& dst = stream ? p2s_items : p2_items;
+      int slot = -1;
+      for (std::int64_t z = 0; z < cnt; ++z) {
+        const std::int64_t g = side == 0 ? gid(l, z) : gv(l, z);
+        if (rpad[g] == 0 || !owned(l, z)) continue;
+        if (slot < 0) slot = n_proxy_levels++;
+        const std::int64_t nr = node_size(l, z);
+        // proxy levels: even split into ceil(nr / 256) items (a 256 + small
+        // remainder split leaves most of the second item's target slots idle)
+        const std::int64_t per =
+            stream ? step : (nr + (nr + step - 1) / step - 1) / ((nr + step - 1) / step);
+        for (std::int64_t r0 = 0; r0 < nr; r0 += per)
+          dst.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
+                               static_cast<std::int32_t>(std::min<std::int64_t>(per, nr - r0)), slot});
+      }
     }
   }
   pg_level[L_ + 1] = static_cast<std::int64_t>(pg_items.size());

@@ -44,8 +44,13 @@ enum LevelMode : int {
                     //   once (8 r(m+n) B), both products through a per-pair output buffer
   kModeFused = 4,   // matrix-free like kModeProxy, pair-major: r(m+n) kernel evaluations per
                     //   pair, each entry kept in shared memory for both orientations
+  kModeHalf = 5,    // half explicit, half regenerated, no solves: U' = K(X, tau) (LR)^-1
+                    //   (m x r) streamed, K(sigma, Y) regenerated; 2 x 8 r m B + 2 r n
+                    //   evaluations per pair. Every node carries two column groups: the
+                    //   pairs it is X of (stream kernels, its own node id) and the pairs
+                    //   it is Y of (proxy kernels, a virtual node id >= total_nodes())
 };
-constexpr int kModeLast = kModeFused;
+constexpr int kModeLast = kModeHalf;
 
 // Fused proxy pass (kModeFused levels, fused.cu): pivots sigma (row, in X) at
 // piv_off, tau (column, in Y) at piv_off + r; inverses at lu_off (row-major)
@@ -189,6 +194,10 @@ class Planner {
     return off_[level][m + 1] - off_[level][m];
   }
   std::int64_t total_nodes() const { return node_base_.back(); }
+  // half levels: node z's regenerated column group has node id vbase[l] + z
+  // (after every real node); -1 elsewhere. Valid after layout().
+  std::vector<std::int64_t> vbase;
+  std::int64_t gv(int level, std::int64_t m) const { return vbase[level] + m; }
   const std::vector<std::int64_t>& node_base() const { return node_base_; }
   const std::vector<std::vector<std::int64_t>>& offsets() const { return off_; }
   const std::vector<LevelLists>& lists() const { return lists_; }

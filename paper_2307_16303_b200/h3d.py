@@ -273,7 +273,8 @@ class HmatOptions:
     # B200 extension: "auto" (cost model), "stream"
     # (explicit factors everywhere) or "explicit" (level_modes[l]: 0 stream,
     # 1 proxy, 2 direct at the leaf level, 3 pair = explicit factors applied in
-    # one fused read per pair)
+    # one fused read per pair, 4 fused, 5 half = U' = K(X, tau) (LR)^-1
+    # streamed and K(sigma, Y) regenerated, laplace3d / r4 only)
     mode_policy: str = "auto"
     level_modes: tuple = ()
     # multi-GPU (B200 extension): every rank returns the full b, all-gathered
@@ -665,7 +666,7 @@ _PLAN_DTYPES = {
     "spos": np.int32, "pair_wx": np.int64, "pair_wy": np.int64, "pair_rx": np.int32,
     "pair_ry": np.int32, "pair_cx": np.int32, "pair_cy": np.int32, "pair_piv": np.int64, "pair_lu": np.int64, "near_off": np.int32,
     "near_ids": np.int32, "near_dense": np.int32, "sym_off": np.int32, "sym_ids": np.int32,
-    "sym_cnt": np.int32, "out_off": np.int64, "in_off": np.int32, "in_pos": np.int64, "node_base": np.int64, "modes": np.int32, "ranges": np.int64,
+    "sym_cnt": np.int32, "out_off": np.int64, "in_off": np.int32, "in_pos": np.int64, "node_base": np.int64, "vbase": np.int64, "modes": np.int32, "ranges": np.int64,
     "rank_rows": np.int64, "sizes": np.int64,
     # structs, decoded as int64 fields (see csrc/planner.h)
     "proxy_segs": np.dtype([("so", np.int64), ("base", np.int64), ("piv_off", np.int64),

@@ -82,11 +82,11 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
 
     for l in range(1, L + 1):
         X, Y = plan.pairs(l)
-        if md[l] in (0, 3):
+        if md[l] in (0, 3, 5):
             wx, wy = plan.array("pair_wx", l), plan.array("pair_wy", l)
             rx, ry = plan.array("pair_rx", l), plan.array("pair_ry", l)
             cx, cy = plan.array("pair_cx", l), plan.array("pair_cy", l)
-        elif md[l] in (1, 4):
+        if md[l] in (1, 4, 5):
             po, lo = plan.array("pair_piv", l), plan.array("pair_lu", l)
         for p, (a, b) in enumerate(zip(X, Y)):
             rp, cp, LU = pd[(l, int(a), int(b))]
@@ -107,9 +107,16 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
                 else:  # pair-major: U then V, row-major with stride rp
                     W[wx[p] + I * rx[p] + Q] = FX
                     W[wy[p] + J * ry[p] + Qy] = FY
-            elif md[l] in (1, 4):
+            if md[l] == 5:
+                # half level: U' = K(X, tau) (L R)^-1 explicit on X's stream
+                # group; the Y side regenerated from the row pivots
+                FX = np.linalg.solve((Lm @ Um).T, kernel_matrix(kind, Xp, Yp[cp]).T).T
+                I, Q = np.meshgrid(np.arange(len(Xp)), np.arange(r), indexing="ij")
+                W[wx[p] + tile_index(I, cx[p] + Q, rx[p])] = FX
+            if md[l] in (1, 4, 5):
                 piv[po[p]: po[p] + r] = rp
                 piv[po[p] + r: po[p] + 2 * r] = cp
+            if md[l] in (1, 4):  # half levels keep the pivots only
                 lu[lo[p]: lo[p] + r * r] = LU.reshape(-1)
     # proxy coordinates (padding far away, weight 0)
     Q = np.full((max(sizes[1], 1), 3), 1e100)
@@ -210,8 +217,12 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
                      [int(v) for v in pgit["slot"]] + [-1])
     lvl = np.zeros((nslots, n))
     hits = np.zeros((L + 1, n), np.int64)
+    shits = np.zeros((nslots, n), np.int64)
+    vb = plan.array("vbase")
 
     def level_of(g):
+        if g >= nb[-1]:  # half levels' regenerated groups (virtual node ids)
+            return max(l for l in range(L + 1) if 0 <= vb[l] <= g)
         return int(np.searchsorted(nb, g, side="right")) - 1
     for it in items2:
         g = int(it["node"])
@@ -220,7 +231,9 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         r0 = rowbeg[g] + it["row0"]
         lvl[it["slot"], r0: r0 + it["nrows"]] = kernel_matrix(kind, ppts[r0: r0 + it["nrows"]],
                                                               Q[so: so + R]) @ S[so: so + R]
-        hits[level_of(g), r0: r0 + it["nrows"]] += 1
+        shits[it["slot"], r0: r0 + it["nrows"]] += 1
+        if g < nb[-1]:
+            hits[level_of(g), r0: r0 + it["nrows"]] += 1
     for it in items2s:
         g = int(it["node"])
         R, so = int(rpad[g]), int(soff[g])
@@ -228,6 +241,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         Wn = node_matrix(W, woff[g], g, int(rows[g]), R)
         r0 = rowbeg[g] + it["row0"]
         lvl[it["slot"], r0: r0 + it["nrows"]] = Wn[it["row0"]: it["row0"] + it["nrows"]] @ S[so: so + R]
+        shits[it["slot"], r0: r0 + it["nrows"]] += 1
         hits[level_of(g), r0: r0 + it["nrows"]] += 1
     # pair levels: one fused pass per pair descriptor, gathered per node
     pdesc = plan.array("pair_descs")
@@ -269,8 +283,10 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         for q in pcpos[pcoff[g]: pcoff[g + 1]]:
             v += pout[int(q) + it["row0"]: int(q) + it["row0"] + it["nrows"]]
         lvl[it["slot"], r0: r0 + it["nrows"]] = v
+        shits[it["slot"], r0: r0 + it["nrows"]] += 1
         hits[level_of(g), r0: r0 + it["nrows"]] += 1
     assert hits.max(initial=0) <= 1, "a row written twice at one level"
+    assert shits.max(initial=0) <= 1, "a row written twice into one partial"
     # every owned row of a node with partners is covered once at its level
     for l in range(1, L + 1):
         if md[l] == 2:
