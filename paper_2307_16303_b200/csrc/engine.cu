@@ -163,6 +163,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "graphs") tune_.graphs = v;
         else if (k == "acab") tune_.acab = v;
         else if (k == "half_search") tune_.half_search = v;
+        else if (k == "nfd") tune_.nfd = v;
         else if (k.size() > 4 && k.compare(0, 4, "acat") == 0) {
           const int lv = std::atoi(k.c_str() + 4);
           if (lv > 0 && lv < 16 && (v == 32 || v == 128 || v == 256 || v == 512)) tune_.acat[lv] = v;
@@ -208,6 +209,9 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     }
   }
   plan_ = std::make_unique<Planner>(L_, n_, off_, lists_, rank_, world_, modes_);
+  // stored near field: the dense leaf blocks in cached mode (the reference's
+  // DenseMode::Cached); the direct leaf-level blocks with H3D_TUNE nfd=1
+  plan_->set_near_storage((opt_.near_mode == H3D_NEAR_STORED ? 1 : 0) | (tune_.nfd ? 2 : 0));
   // the rank-independent part of the layout (leaf plan, near-field lists) on
   // a host thread while the ACA rank pass runs on the device
   std::exception_ptr leaf_err;
@@ -1055,7 +1059,7 @@ void Engine::upload_plan() {
   counters_.alloc(5 + L_ + 1);
   sync_flag_.alloc(1);
   H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), stream_));
-  if (opt_.near_mode == H3D_NEAR_STORED) {
+  if (P.near_storage() != 0) {
     nf_off_.upload(P.nf_off, stream_);
     nf_cols_.upload(P.nf_cols, stream_);
     NF_.alloc(std::max<std::int64_t>(P.nf_total, 1));
@@ -1089,10 +1093,11 @@ Phase2Args Engine::phase2_args(double* bout) const {
   a.near_off = near_off_.get();
   a.near_ids = near_ids_.get();
   a.near_dense = near_dense_.get();
-  if (opt_.near_mode == H3D_NEAR_STORED) {
+  if (P.near_storage() != 0) {
     a.nf_off = nf_off_.get();
     a.nf_cols = nf_cols_.get();
     a.NF = NF_.get();
+    a.nf_mask = P.near_storage();
   }
   a.kernel = opt_.kernel_id;
   a.diag = opt_.diagonal;
@@ -1130,9 +1135,9 @@ void Engine::near_scan() {
   const Planner& P = *plan_;
   if (P.leaf1 <= P.leaf0) return;
   Phase2Args a = phase2_args(nullptr);
-  if (opt_.near_mode != H3D_NEAR_STORED) a.nf_off = nullptr;
+  if (P.near_storage() == 0) a.nf_off = nullptr;
   H3D_CUDA_CHECK(cudaMemsetAsync(flags_.get(), 0, 4, stream_));
-  launch_near_scan(a, opt_.near_mode == H3D_NEAR_STORED ? NF_.get() : nullptr, flags_.get(), stream_);
+  launch_near_scan(a, P.near_storage() != 0 ? NF_.get() : nullptr, flags_.get(), stream_);
   check_flags("near field");
 }
 
@@ -1633,7 +1638,7 @@ void Engine::stats(h3d_stats* s) const {
   s->tvec_doubles = Z.s_doubles;
   s->near_blocks = Z.near_blocks;
   s->near_entries = Z.near_entries;
-  s->near_bytes_stored = opt_.near_mode == H3D_NEAR_STORED ? P.nf_total * 8 : 0;
+  s->near_bytes_stored = P.near_storage() != 0 ? P.nf_total * 8 : 0;
   // reference RepStats convention (hmatrix.cpp:228-251): r^2 per ordered
   // block + dense leaf areas (directly evaluated leaf blocks count as dense)
   s->ref_float_count = Z.ref_float_count + static_cast<std::uint64_t>(Z.near_entries + Z.direct_evals);

@@ -234,6 +234,7 @@ struct Phase2Args {
   const std::int64_t* nf_off = nullptr;
   const std::int32_t* nf_cols = nullptr;
   const double* NF = nullptr;
+  int nf_mask = 0;  // planner.h set_near_storage: bit 0 dense, bit 1 direct sources stored
   int kernel = 0;
   double diag = 0.0;
   double* b = nullptr;          // output, original order

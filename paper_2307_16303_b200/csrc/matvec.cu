@@ -750,14 +750,21 @@ __device__ __forceinline__ void near_seg(const double4* __restrict__ st, int lo,
     } else {
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-        const double r2 = sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z);
-        if constexpr (SYM) {
-          // the Newton-form value once, for both sums
-          const double g = far_acc<K>(r2, 1.0, 0.0);
+        if constexpr (STORED) {
+          // the stored Newton-form value (near_store_kernel), both sums
+          const double g = r < nvalid ? ldg_stream(nf0 + r * nds + j + dbias) : 0.0;
           acc[r] = fma(g, q.w, acc[r]);
-          cp = fma(g, tw[r], cp);
+          if constexpr (SYM) cp = fma(g, tw[r], cp);
         } else {
-          acc[r] = far_acc<K>(r2, q.w, acc[r]);
+          const double r2 = sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z);
+          if constexpr (SYM) {
+            // the Newton-form value once, for both sums
+            const double g = far_acc<K>(r2, 1.0, 0.0);
+            acc[r] = fma(g, q.w, acc[r]);
+            cp = fma(g, tw[r], cp);
+          } else {
+            acc[r] = far_acc<K>(r2, q.w, acc[r]);
+          }
         }
       }
       if constexpr (SYM) col[j] = cp;
@@ -776,12 +783,18 @@ __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const
                                            const double (&tx)[RPW], const double (&ty)[RPW],
                                            const double (&tz)[RPW], const double (&tw)[RPW],
                                            double (&acc)[RPW], double* __restrict__ col, double diag,
-                                           int lane, const double* __restrict__ nf0, int nvalid) {
+                                           int lane, const double* __restrict__ nf0, int nvalid, int mask) {
   constexpr double inv = 1.0 / far_scale<K>();
   const int h = (lane >> 2) & 1;
   const int base = mt.base, cnt = mt.cnt;
   auto cut = [&](int e) { return max(0, min(cnt, e - base)); };
   const int c0 = cut(mt.e0), c1 = cut(mt.e1), c2 = cut(mt.e2), c3 = cut(mt.e3);
+  // NF column of flattened source f (planner.h): the unstored categories
+  // before it are skipped
+  const bool sd = STORED && (mask & 1), sx = STORED && (mask & 2);
+  const int bd1 = sd ? 0 : mt.e1;                            // direct one-way
+  const int bs2 = sx ? 0 : mt.e2 - mt.e1;                    // dense sym
+  const int bx2 = sd ? 0 : mt.e1 + (mt.e3 - mt.e2);           // direct sym
   // self block, diagonal rule
   for (int j = lane; j < c0; j += 32) {
     const double4 q = ld_src(st, j, h);
@@ -789,16 +802,22 @@ __device__ __forceinline__ void near_chunk(const double4* __restrict__ st, const
 #pragma unroll
     for (int r = 0; r < RPW; ++r) {
       double k;
-      if constexpr (STORED) k = r < nvalid ? ldg_stream(nf0 + r * mt.nds + base + j) : 0.0;
+      if (sd) k = r < nvalid ? ldg_stream(nf0 + r * mt.nds + base + j) : 0.0;
       else k = (row0 + r == base + j) ? diag : kernel_r2_fast<K>(sq3(tx[r] - q.x, ty[r] - q.y, tz[r] - q.z));
       acc[r] = fma(k, w, acc[r]);
     }
   }
-  near_seg<K, RPW, true, false, STORED>(st, c0, c1, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid, base);
-  near_seg<K, RPW, false, false, false>(st, c1, c2, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
-  near_seg<K, RPW, true, true, STORED>(st, c2, c3, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid,
-                                       base - (mt.e2 - mt.e1));
-  near_seg<K, RPW, false, true, false>(st, c3, cnt, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
+  if (sd) near_seg<K, RPW, true, false, true>(st, c0, c1, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid, base);
+  else near_seg<K, RPW, true, false, false>(st, c0, c1, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
+  if (sx)
+    near_seg<K, RPW, false, false, true>(st, c1, c2, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid, base - bd1);
+  else near_seg<K, RPW, false, false, false>(st, c1, c2, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
+  if (sd)
+    near_seg<K, RPW, true, true, true>(st, c2, c3, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid, base - bs2);
+  else near_seg<K, RPW, true, true, false>(st, c2, c3, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
+  if (sx)
+    near_seg<K, RPW, false, true, true>(st, c3, cnt, tx, ty, tz, tw, acc, col, lane, nf0, mt.nds, nvalid, base - bx2);
+  else near_seg<K, RPW, false, true, false>(st, c3, cnt, tx, ty, tz, tw, acc, col, lane, nf0, 0, 0, 0);
 }
 
 // Consumer warp: one row pass of one leaf, starting at the (already waited)
@@ -827,7 +846,7 @@ __device__ unsigned near_consume(NearSmem& sm, const Phase2Args& a, unsigned t) 
     const int s = t % 2;
     const NearMeta mt = sm.meta[s];
     near_chunk<K, RPW, STORED>(sm.stage[s], mt, row0, tx, ty, tz, tw, acc, sm.col[warp], a.diag, lane, nf0,
-                               nvalid);
+                               nvalid, a.nf_mask);
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[s]);
     if (mt.base + mt.cnt > mt.e2) {  // chunk holds sym sources: column sums in warp order
@@ -1180,44 +1199,59 @@ __global__ void combine_kernel(const double* __restrict__ cpart, const double* _
 // Build-time pass over every owned leaf's dense sources in its symmetric
 // list order (self | dense one-way | dense sym; planner.cpp): the reference
 // forms all dense leaf blocks during initialize (hmatrix.cpp:124-147), so
-// coincident points raise DegenerateGeometryError here. With NF set (cached
-// near field) it stores, row-major per leaf, exactly the value the
-// matrix-free near pass computes for each (row, dense source) from the same
-// packed points: diag on the self block's diagonal, kernel_r2_fast of the
-// same sq3 operands elsewhere.
+// coincident points raise DegenerateGeometryError here. With NF set (stored
+// near field, planner.h set_near_storage) it stores, row-major per leaf,
+// exactly the value the matrix-free near pass computes for each (row,
+// stored source) from the same packed points: diag on the self block's
+// diagonal, kernel_r2_fast of the same sq3 operands for dense sources, the
+// Newton-form far_acc value for direct (leaf-level admissible) ones.
 template <int K>
 __global__ void __launch_bounds__(kThreads) near_store_kernel(const Phase2Args a, double* __restrict__ NF,
                                                               unsigned* flags) {
   __shared__ long long rs[kMaxNearRanges];
-  __shared__ int rpre[kMaxNearRanges + 1];
+  __shared__ int rpre[kMaxNearRanges + 1];   // visited-column prefix
+  __shared__ int rsto[kMaxNearRanges];       // stored-column prefix (-1: not stored)
+  __shared__ unsigned char rdir[kMaxNearRanges];
   __shared__ int nr;
   const std::int64_t X = a.leaf0 + blockIdx.x;
   const std::int64_t xb = a.leaf_off[X];
   const int m = static_cast<int>(a.leaf_off[X + 1] - xb);
   if (m == 0) return;
   const std::int32_t nb = a.sym_off[X];
+  const int mask = NF ? a.nf_mask : 0;
   if (threadIdx.x == 0) {
-    const int c0 = a.sym_cnt[4 * X], c1 = a.sym_cnt[4 * X + 1], c2 = a.sym_cnt[4 * X + 2];
-    int n = 0, pre = 0;
-    auto add = [&](std::int32_t e) {
+    const int c[4] = {a.sym_cnt[4 * X], a.sym_cnt[4 * X + 1], a.sym_cnt[4 * X + 2], a.sym_cnt[4 * X + 3]};
+    int n = 0, pre = 0, sto = 0;
+    // every dense source (the coincident-point scan) and, when stored, the
+    // direct ones, in symmetric-list order: self, dense one-way, direct
+    // one-way, dense sym, direct sym
+    auto add = [&](std::int32_t e, bool direct) {
+      const bool stored = (mask & (direct ? 2 : 1)) != 0;
+      if (direct && !stored) return;
       const std::int32_t Y = a.sym_ids[nb + e];
+      const int len = static_cast<int>(a.leaf_off[Y + 1] - a.leaf_off[Y]);
       rs[n] = a.leaf_off[Y];
       rpre[n] = pre;
-      pre += static_cast<int>(a.leaf_off[Y + 1] - a.leaf_off[Y]);
+      rsto[n] = stored ? sto : -1;
+      rdir[n] = direct ? 1 : 0;
+      pre += len;
+      if (stored) sto += len;
       ++n;
     };
-    add(0);                                               // self
-    for (int e = 0; e < c0; ++e) add(1 + e);              // dense one-way
-    for (int e = 0; e < c2; ++e) add(1 + c0 + c1 + e);    // dense sym
+    add(0, false);  // self
+    int e = 1;
+    for (int k = 0; k < 4; ++k)
+      for (int q = 0; q < c[k]; ++q, ++e) add(e, (k & 1) != 0);
     rpre[n] = pre;
     nr = n;
   }
   __syncthreads();
-  const int nds = rpre[nr];
+  const int nvis = rpre[nr];
+  const int nds = NF ? a.nf_cols[X] : 0;
   const double4* P4 = reinterpret_cast<const double4*>(a.p4);
   unsigned f = 0;
-  for (long long q = threadIdx.x; q < static_cast<long long>(m) * nds; q += blockDim.x) {
-    const int i = static_cast<int>(q / nds), d = static_cast<int>(q % nds);
+  for (long long q = threadIdx.x; q < static_cast<long long>(m) * nvis; q += blockDim.x) {
+    const int i = static_cast<int>(q / nvis), d = static_cast<int>(q % nvis);
     int lo = 0;
     while (lo + 1 < nr && rpre[lo + 1] <= d) ++lo;
     const double4 t = P4[xb + i];
@@ -1228,9 +1262,11 @@ __global__ void __launch_bounds__(kThreads) near_store_kernel(const Phase2Args a
     } else {
       const double r2 = sq3(t.x - sp.x, t.y - sp.y, t.z - sp.z);
       if (r2 < kCoincidentTol2) f |= kFlagDegenGeom;
-      v = kernel_r2_fast<K>(r2);
+      // the values the matrix-free pass evaluates: full accuracy for the
+      // dense blocks, the Newton form for the direct (admissible) ones
+      v = rdir[lo] ? far_acc<K>(r2, 1.0, 0.0) : kernel_r2_fast<K>(r2);
     }
-    if (NF) NF[a.nf_off[X] + q] = v;
+    if (NF && rsto[lo] >= 0) NF[a.nf_off[X] + static_cast<long long>(i) * nds + rsto[lo] + (d - rpre[lo])] = v;
   }
   if (f) atomicOr(flags, f);
 }

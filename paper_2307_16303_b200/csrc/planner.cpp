@@ -675,9 +675,12 @@ void Planner::layout_leaf() {
           put(lists_[L_].ids[0][e], false);
     }
     sym_ids.push_back(static_cast<std::int32_t>(x));
-    std::int64_t ncols = node_size(L_, x);  // self, then the dense categories 0 and 2
-    for (int c : {0, 2})
-      for (std::int32_t y : cat[c]) ncols += node_size(L_, y);
+    // stored columns: self + dense categories 0 and 2 (bit 0), direct
+    // categories 1 and 3 (bit 1)
+    std::int64_t ncols = (nf_mask_ & 1) ? node_size(L_, x) : 0;
+    for (int c = 0; c < 4; ++c)
+      if (nf_mask_ & ((c & 1) ? 2 : 1))
+        for (std::int32_t y : cat[c]) ncols += node_size(L_, y);
     nf_cols[x] = static_cast<std::int32_t>(ncols);
     nf_total += node_size(L_, x) * ncols;
     for (int c = 0; c < 4; ++c) {

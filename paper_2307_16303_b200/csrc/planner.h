@@ -182,6 +182,11 @@ class Planner {
   // the rank-independent part of layout() (leaf plan, near-field lists);
   // layout() runs it when it has not run yet
   void layout_leaf();
+  // stored near field (nf_*): bit 0 = the dense leaf blocks (self, edge,
+  // face: the reference's DenseMode::Cached), bit 1 = the direct leaf-level
+  // admissible blocks; set before layout_leaf()
+  void set_near_storage(int mask) { nf_mask_ = mask; }
+  int near_storage() const { return nf_mask_; }
   void set_mode(int l, int m) {
     if (mode_[l] == kModeDirect || m == kModeDirect)
       throw std::invalid_argument("planner: direct mode is fixed at construction");
@@ -263,9 +268,10 @@ class Planner {
   std::vector<std::int64_t> out_off;  // nl + 1
   std::vector<std::int32_t> in_off;   // nl + 1
   std::vector<std::int64_t> in_pos;
-  // stored near field (near_mode 0): per owned leaf X a row-major m x nf_cols[X]
-  // block at nf_off[X], one column per DENSE source of X's symmetric list in
-  // list order (self, dense one-way, dense sym) - exactly the values the
+  // stored near field: per owned leaf X a row-major m x nf_cols[X] block at
+  // nf_off[X], one column per STORED source of X's symmetric list in list
+  // order (self, dense one-way, direct one-way, dense sym, direct sym; dense
+  // ones with storage bit 0, direct ones with bit 1) - exactly the values the
   // matrix-free near pass evaluates, in its order (bitwise-equal results)
   std::vector<std::int64_t> nf_off;
   std::vector<std::int32_t> nf_cols;
@@ -279,6 +285,7 @@ class Planner {
 
   int L_;
   bool leaf_done_ = false;
+  int nf_mask_ = 1;
   std::int64_t n_;
   std::vector<std::vector<std::int64_t>> off_;
   std::vector<LevelLists> lists_;
