@@ -67,6 +67,10 @@ FP64_TFLOPS = 2 * FP64_INSTR_PEAK / 1e12
 # dense-near (third-order rsqrt) 6 more; 1/r^4 and cos(r)/r use the exact
 # radial maps (reciprocal / sincos sequences).
 INSTR_FAR = {"laplace3d": 10, "r4": 12, "helmholtz-re": 40}
+# half levels' regenerated side (matvec.cu half2_kernel): one evaluation (the
+# far value without the accumulate) feeding two FMAs, plus ~0.6 DADD of the
+# 8-source warp reduce-scatter per entry
+INSTR_HALF = {"laplace3d": 10, "r4": 12, "helmholtz-re": 42}
 INSTR_NEAR = {"laplace3d": 12, "r4": 14, "helmholtz-re": 40}
 
 
@@ -382,7 +386,8 @@ def main():
     # CUDA-event duration (lanes overlap, so shares are of the summed kernel time).
     hbm, peak_src = peaks()
     F = st["factor_doubles"]           # streamed factor doubles per phase (stream levels)
-    U = st["proxy_units"]              # regenerated entries per phase (proxy levels)
+    HU = st["half_units"]              # half levels: regenerated entries, evaluated once for both phases
+    U = st["proxy_units"] - HU         # regenerated entries per phase (proxy levels)
     NEAR, DIRECT = st["near_entries"], st["direct_evals"]
     LU = st["lu_doubles"]
     kf, kn = INSTR_FAR[cfg["kernel"]], INSTR_NEAR[cfg["kernel"]]
@@ -393,6 +398,7 @@ def main():
         "near": ("fp64", kn * NEAR + kf * DIRECT), "solve": ("hbm", 2 * 8.0 * LU),
         "gather": ("hbm", 8.0 * (4 * n)), "combine": ("hbm", 8.0 * n * (2 + nlev)),
         "red_stream": ("hbm", 0.0), "red_proxy": ("hbm", 0.0),
+        "half": ("fp64", INSTR_HALF[cfg["kernel"]] * HU),
     }
     kstats = {}
     for k, (tot, cnt, start) in kern.items():

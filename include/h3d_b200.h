@@ -144,7 +144,7 @@ typedef struct {
   double build_ms_plan;       /* mode choice, layout, descriptor upload (host planner) */
   double build_ms_post;       /* proxy pivot gather + LU triangular inverses */
   double build_ms_near;       /* near-field symmetry scan */
-  int64_t reserved[1];
+  int64_t half_units;         /* half levels: sum over pairs of r n (the regenerated side) */
 } h3d_stats;
 
 typedef struct h3d_dev h3d_dev;
@@ -197,6 +197,7 @@ typedef enum {
   H3D_K_COMBINE,       /* sum of the per-level partials, un-permute */
   H3D_K_PAIR,          /* pair levels: fused one-read pass + per-node gather (HBM) */
   H3D_K_FUSED,         /* fused levels: one evaluation per entry, both orientations (FP64) */
+  H3D_K_HALF,          /* half levels, regenerated side: both uses per entry (FP64) */
   H3D_K_COUNT
 } h3d_kernel_slot;
 int h3d_dev_profile_kernels(const h3d_dev* dev, double* ms_sum, int64_t* launches, double* start_sum,

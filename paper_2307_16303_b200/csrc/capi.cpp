@@ -320,6 +320,7 @@ int h3d_plan_array(const h3d_plan* p, const char* name, int level, void* out, in
     else if (nm == "pair_cy") put(P.pair_cy.at(level), out, count);
     else if (nm == "p2_items") put(P.p2_items, out, count);
     else if (nm == "p2s_items") put(P.p2s_items, out, count);
+    else if (nm == "h2_items") put(P.h2_items, out, count);
     else if (nm == "sym_off") put(P.sym_off, out, count);
     else if (nm == "sym_ids") put(P.sym_ids, out, count);
     else if (nm == "sym_cnt") put(P.sym_cnt, out, count);

@@ -92,6 +92,25 @@ __device__ __forceinline__ double far_acc(double r2, double w, double acc) {
     return fma(kernel_r2<K>(r2), w, acc);
   }
 }
+// the admissible-path value itself, far_scale-scaled like far_acc (no
+// accumulate: one FP64 instruction fewer than far_acc(r2, 1.0, 0.0))
+template <int K>
+__device__ __forceinline__ double far_val(double r2) {
+  if constexpr (K == kLaplace || K == kR4) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+    const double g = y * fma(r2 * y, y, -3.0);
+    if constexpr (K == kLaplace) {
+      return g;
+    } else {
+      const double g2 = g * g;
+      return g2 * g2;
+    }
+  } else {
+    return kernel_r2<K>(r2);
+  }
+}
+
 template <int K>
 __device__ __forceinline__ constexpr double far_scale() {
   return K == kLaplace ? kNewtonScale : K == kR4 ? 1.0 / 16.0 : 1.0;

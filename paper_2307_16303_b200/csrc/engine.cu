@@ -182,6 +182,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
   }
   for (auto& e : ev_) H3D_CUDA_CHECK(cudaEventCreate(&e));
   H3D_CUDA_CHECK(cudaEventCreateWithFlags(&done_ev_, cudaEventDisableTiming));
+  H3D_CUDA_CHECK(cudaEventCreateWithFlags(&h2_done_, cudaEventDisableTiming));
   for (int k = 0; k < 3; ++k) {
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&fork_[k], cudaEventDisableTiming));
     H3D_CUDA_CHECK(cudaEventCreateWithFlags(&join_[k], cudaEventDisableTiming));
@@ -292,6 +293,7 @@ Engine::~Engine() {
   for (auto& e : ev_)
     if (e) cudaEventDestroy(e);
   if (done_ev_) cudaEventDestroy(done_ev_);
+  if (h2_done_) cudaEventDestroy(h2_done_);
   for (int k = 0; k < 3; ++k) {
     if (fork_[k]) cudaEventDestroy(fork_[k]);
     if (join_[k]) cudaEventDestroy(join_[k]);
@@ -983,12 +985,14 @@ void Engine::upload_plan() {
   n_p1s_ = static_cast<std::int64_t>(si.size());
   n_p1p_ = static_cast<std::int64_t>(pi.size());
   {
-    std::vector<P1Reduce> rs, rp;
-    for (const auto& r : P.reds) (r.kind == kModeStream ? rs : rp).push_back(r);
+    std::vector<P1Reduce> rs, rp, rh;
+    for (const auto& r : P.reds) (r.kind == kModeStream ? rs : r.kind == kModeHalf ? rh : rp).push_back(r);
     p1_red_s_.upload(rs, stream_);
     p1_red_p_.upload(rp, stream_);
+    p1_red_h_.upload(rh, stream_);
     n_red_s_ = static_cast<std::int64_t>(rs.size());
     n_red_p_ = static_cast<std::int64_t>(rp.size());
+    n_red_h_ = static_cast<std::int64_t>(rh.size());
   }
   for (std::size_t x = 0; x + 1 < P.near_off.size(); ++x)
     if (P.near_off[x + 1] - P.near_off[x] > kMaxNearRanges)
@@ -1015,6 +1019,8 @@ void Engine::upload_plan() {
   for (int l = 1; l <= L_; ++l)
     if (P.mode(l) == kModeStream && !P.pairs(l).X.empty()) has_stream_levels_ = true;
   p2_items_.upload(P.p2_items, stream_);
+  h2_items_.upload(P.h2_items.empty() ? std::vector<H2Item>{H2Item{}} : P.h2_items, stream_);
+  n_h2_ = static_cast<std::int64_t>(P.h2_items.size());
   n_p2_ = static_cast<std::int64_t>(P.p2_items.size());
   p2s_items_.upload(P.p2s_items, stream_);
   {
@@ -1122,6 +1128,14 @@ Phase2Args Engine::phase2_args(double* bout) const {
     a.p2_items = p2_items_.get();
     a.n_p2_items = n_p2_;
     a.lvl_part = lvl_part_.get();
+  }
+  if (n_h2_ > 0) {
+    a.h2_items = h2_items_.get();
+    a.n_h2_items = n_h2_;
+    a.lvl_part = lvl_part_.get();
+    a.spos = spos_.get();
+    a.Sw = S_.get();
+    a.P = P_.get();
   }
   a.n_total = n_;
   for (int l = 0; l <= L_ && l < 24; ++l) {
@@ -1310,6 +1324,20 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ke(H3D_K_RED_PROXY, stream4_);
     ++launches;
   }
+  // half levels, the regenerated side: both uses per entry in one pass, once
+  // the partners' streamed phase 1 (its t) is in S; p2_stream waits for its v
+  const bool h2 = n_h2_ > 0 && has_p2;
+  if (h2) {
+    if (hbm) H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[1], 0));
+    kb(H3D_K_HALF, stream4_);
+    a2.counter_h2 = counters_.get() + 6;
+    launch_half2(a2, sms_, hbm ? tune_.p2p : 8, stream4_);
+    if (n_red_h_ > 0)
+      launch_phase1_reduce(p1_red_h_.get(), n_red_h_, nt, spos_.get(), P_.get(), S_.get(), stream4_);
+    ke(H3D_K_HALF, stream4_);
+    launches += 1 + (n_red_h_ > 0 ? 1 : 0);
+    H3D_CUDA_CHECK(cudaEventRecord(h2_done_, stream4_));
+  }
   if (n_segs_solve_ > 0) {
     kb(H3D_K_SOLVE, stream4_);
     launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), sms_, tune_.sol,
@@ -1331,6 +1359,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       a2.wait_flag = sync_flag_.get();
       a2.wait_value = 1u;
     }
+    if (h2) H3D_CUDA_CHECK(cudaStreamWaitEvent(stream2_, h2_done_, 0));
     if (has_p2 && n_p2s_ > 0) {
       kb(H3D_K_P2_STREAM, stream2_);
       if (run(H3D_K_P2_STREAM)) launch_p2_stream(a2, sms_, fp ? tune_.p2s : 2, stream2_);
@@ -1658,6 +1687,7 @@ void Engine::stats(h3d_stats* s) const {
   s->owned_row_end = P.row1;
   for (int l = 0; l <= L_ && l < 16; ++l) s->level_modes[l] = P.mode(l);
   s->proxy_units = Z.proxy_units;
+  s->half_units = Z.half_units;
   s->direct_evals = Z.direct_evals;
   s->lu_doubles = Z.lu_total;
   for (int l = 1; l <= L_ && l < 16; ++l) {

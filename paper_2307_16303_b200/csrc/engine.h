@@ -169,8 +169,11 @@ class Engine {
   DevBuf<ProxySeg> segs_all_, segs_solve_;
   std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
   DevBuf<P1Item> p1_stream_items_, p1_proxy_items_;
-  DevBuf<P1Reduce> p1_red_s_, p1_red_p_;  // tall-node partial reductions, stream / proxy kind
-  std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_s_ = 0, n_red_p_ = 0;
+  DevBuf<P1Reduce> p1_red_s_, p1_red_p_, p1_red_h_;  // tall-node partial reductions, stream / proxy / half kind
+  std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_s_ = 0, n_red_p_ = 0, n_red_h_ = 0;
+  DevBuf<H2Item> h2_items_;  // half levels, regenerated side (both uses per entry)
+  std::int64_t n_h2_ = 0;
+  cudaEvent_t h2_done_ = nullptr;  // the half pass's v are in S (p2_stream waits)
   bool has_stream_levels_ = false;
   DevBuf<std::int32_t> near_off_, near_ids_, near_dense_;
   DevBuf<std::int32_t> sym_off_, sym_ids_, sym_cnt_, in_off_;

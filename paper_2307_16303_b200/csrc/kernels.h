@@ -247,6 +247,13 @@ struct Phase2Args {
   // the proxy ranges and p2_proxy writes one partial per proxy level
   const P2Item* p2_items = nullptr;
   std::int64_t n_p2_items = 0;
+  // half levels, regenerated side: both uses per entry (planner.h H2Item)
+  const H2Item* h2_items = nullptr;
+  std::int64_t n_h2_items = 0;
+  unsigned* counter_h2 = nullptr;
+  const std::int32_t* spos = nullptr;
+  double* Sw = nullptr;  // S, written by the half-level pass (its v)
+  double* P = nullptr;   // v partials of multi-chunk nodes
   // stream levels: one row tile per item, one partial per stream level
   const P2Item* p2s_items = nullptr;
   const StreamDesc* p2s_descs = nullptr;
@@ -267,6 +274,7 @@ constexpr int kMaxNearRanges = 256;
 // matrix-free near field + direct leaf blocks (near_mode on-the-fly)
 void launch_p2_near(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_stream(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
+void launch_half2(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 void launch_p2_proxy(const Phase2Args& a, int sms, int per_sm, cudaStream_t s);
 // *flag = value (release, device scope), stream-ordered
 void launch_set_flag(unsigned* flag, unsigned value, cudaStream_t s);

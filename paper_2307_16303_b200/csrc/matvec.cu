@@ -1171,6 +1171,155 @@ __global__ void __launch_bounds__(kProxyThreads, 5) p2_proxy_kernel(const Phase2
   }
 }
 
+// ---- half levels, the regenerated side (planner.h H2Item): one pass per
+// row chunk of a node's virtual group evaluates each entry e = K(row, proxy)
+// once for both uses: b_row += e t_proxy (t = the partner's streamed
+// U'^T x, in S) and v_proxy += e x_row (the partner's phase-2 weight). Same
+// evaluation core as p2_proxy_kernel (two targets per thread, box-centred
+// sources staged in shared memory); the v sums over the rows go through an
+// 8-source warp reduce-scatter (9 shuffles per 8 sources per lane, 2 targets
+// each) and a fixed-order sum over the 4 warps. Deterministic.
+__device__ __forceinline__ double h2_reduce8(const double (&v)[8], int lane) {
+  const int b = (lane >> 4) & 1, c = (lane >> 3) & 1, d = (lane >> 2) & 1;
+  double k4[4], k2[2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double send = b ? v[q] : v[4 + q];
+    const double keep = b ? v[4 + q] : v[q];
+    k4[q] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const double send = c ? k4[q] : k4[2 + q];
+    const double keep = c ? k4[2 + q] : k4[q];
+    k2[q] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  double r = (d ? k2[1] : k2[0]) + __shfl_xor_sync(0xffffffffu, d ? k2[0] : k2[1], 4);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;  // the total of source (lane >> 2) & 7
+}
+
+constexpr int kH2Warps = kProxyThreads / 32;
+
+template <int K, bool TRICK>
+__device__ __forceinline__ void h2_block(const Tgt (&tg)[2], const double (&xw)[2], double (&bacc)[2],
+                                         const double2* __restrict__ src, int j0, double* __restrict__ vw,
+                                         int lane) {
+  double prod[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int jj = j0 + u;
+    const double2 s0 = src[3 * jj], s1 = src[3 * jj + 1], s2 = src[3 * jj + 2];
+    double p = 0.0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      double r2;
+      if constexpr (TRICK) {
+        r2 = fma(tg[t].ax, s0.x, fma(tg[t].ay, s0.y, fma(tg[t].az, s1.x, tg[t].tt + s1.y)));
+      } else {
+        r2 = sq3(fma(-0.5, tg[t].ax, -s0.x), fma(-0.5, tg[t].ay, -s0.y), fma(-0.5, tg[t].az, -s1.x));
+      }
+      const double e = far_val<K>(r2);
+      bacc[t] = fma(e, s2.x, bacc[t]);
+      p = fma(e, xw[t], p);
+    }
+    prod[u] = p;
+  }
+  const double v = h2_reduce8(prod, lane);
+  if ((lane & 3) == 0) vw[j0 + ((lane >> 2) & 7)] = v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kProxyThreads, 4) half2_kernel(const Phase2Args a) {
+  __shared__ double2 src[3 * kChunk];
+  __shared__ double vw[kH2Warps][kChunk];
+  __shared__ double red[2 * kProxyThreads];
+  __shared__ long long s_k;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_k = static_cast<long long>(atomicAdd(a.counter_h2, 1u));
+    __syncthreads();
+    const long long k = s_k;
+    if (k >= a.n_h2_items) break;
+    const H2Item it = a.h2_items[k];
+    const std::int64_t g = it.node;
+    const std::int64_t so = a.nt.soff[g];
+    const int R = a.nt.rpad[g];
+    const int vc = a.vcols[g];
+    const double4 cen = reinterpret_cast<const double4*>(a.cen)[g];
+    const double4* P4 = reinterpret_cast<const double4*>(a.p4);
+    // items of <= 128 / <= 64 rows: G = 2 / 4 thread groups, each covering
+    // every row and taking a disjoint share of every staged chunk
+    const int G = it.nrows <= 64 ? 4 : it.nrows <= 128 ? 2 : 1;
+    const int tpg = kProxyThreads / G, wpg = tpg / 32;
+    const int grp = threadIdx.x / tpg, loc = threadIdx.x % tpg;
+    Tgt tg[2];
+    double xw[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int i = loc + t * tpg;
+      const double4 q = i < it.nrows ? P4[a.nt.rowbeg[g] + it.row0 + i] : make_double4(kFar, kFar, kFar, 0.0);
+      tg[t] = make_tgt(q.x, q.y, q.z, cen);
+      xw[t] = q.w;
+    }
+    double bacc[2] = {0.0, 0.0};
+    for (int j0 = 0; j0 < R; j0 += kChunk) {
+      const int nj = min(kChunk, R - j0);
+      const int sub = (((nj + G - 1) / G) + 7) & ~7;  // sources per group, whole blocks of 8
+      const int lo = min(kChunk, grp * sub), hi = min(kChunk, lo + sub);
+      const int nstage = min(kChunk, G * sub);
+      __syncthreads();  // the previous chunk's sources and v partials are consumed
+      for (int q = threadIdx.x; q < nstage; q += kProxyThreads) {
+        if (q < nj) {
+          const double4 c4 = reinterpret_cast<const double4*>(a.q4c)[so + j0 + q];
+          src[3 * q] = make_double2(c4.x, c4.y);
+          src[3 * q + 1] = make_double2(c4.z, c4.w);
+          src[3 * q + 2] = make_double2(a.S[so + j0 + q], 0.0);
+        } else {  // padding sources: far away (away from the padding rows too), weight 0
+          src[3 * q] = make_double2(-kFar, -kFar);
+          src[3 * q + 1] = make_double2(-kFar, 3.0 * kFar * kFar);
+          src[3 * q + 2] = make_double2(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+      // sources [0, vc) of the node (vertex-adjacent partners): difference form
+      const int jv = vc - j0;
+      for (int jb = lo; jb < hi; jb += 8) {
+        if (jb < jv) h2_block<K, false>(tg, xw, bacc, src, jb, vw[warp], lane);
+        else h2_block<K, true>(tg, xw, bacc, src, jb, vw[warp], lane);
+      }
+      __syncthreads();
+      // v of the chunk's sources: fixed-order sum over the owning group's warps
+      for (int c = threadIdx.x; c < nj; c += kProxyThreads) {
+        const int og = c / sub;
+        double v = 0.0;
+        for (int w = og * wpg; w < (og + 1) * wpg; ++w) v += vw[w][c];
+        v *= far_scale<K>();
+        if (it.pslot >= 0) {
+          a.P[it.pslot + j0 + c] = v;
+        } else {
+          const std::int32_t dst = a.spos[so + j0 + c];
+          if (dst >= 0) a.Sw[dst] = v;
+        }
+      }
+    }
+    if (it.slot >= 0) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = bacc[t];
+      __syncthreads();
+      for (int i = threadIdx.x; i < it.nrows; i += kProxyThreads) {
+        const int per = 2 * tpg;
+        double v = 0.0;
+        for (int q = 0; q < G; ++q) v += red[q * per + i];
+        a.lvl_part[static_cast<std::int64_t>(it.slot) * a.n_total + a.nt.rowbeg[g] + it.row0 + i] =
+            far_scale<K>() * v;
+      }
+    }
+  }
+}
+
 __global__ void combine_kernel(const double* __restrict__ cpart, const double* __restrict__ lvl,
                                int n_lvl, std::int64_t n_total, const std::int64_t* __restrict__ leaf_off,
                                std::int64_t leaf0, std::int64_t nleaves,
@@ -1468,6 +1617,26 @@ void launch_proxy_solve(const ProxySeg* segs, std::int64_t nseg, const double* l
   const int grid = static_cast<int>(std::max<std::int64_t>(
       1, std::min<std::int64_t>(want, static_cast<std::int64_t>(sms) * std::max(1, std::min(nb, per_sm)))));
   proxy_solve_kernel<<<grid, 32 * kSolveWarps, sizeof(SolveSmem), s>>>(segs, nseg, lu, lu_total, S, counter);
+  H3D_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_half2(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
+  if (a.n_h2_items == 0) return;
+  configure_kernels();
+  switch (a.kernel) {
+    case kLaplace: {
+      const int grid = grid_for(half2_kernel<kLaplace>, sms, per_sm, a.n_h2_items, kProxyThreads);
+      half2_kernel<kLaplace><<<grid, kProxyThreads, 0, s>>>(a);
+      break;
+    }
+    case kR4: {
+      const int grid = grid_for(half2_kernel<kR4>, sms, per_sm, a.n_h2_items, kProxyThreads);
+      half2_kernel<kR4><<<grid, kProxyThreads, 0, s>>>(a);
+      break;
+    }
+    default:
+      throw std::logic_error("half levels are for the smooth kernels only");
+  }
   H3D_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -211,7 +211,7 @@ void Planner::layout() {
   }
   PlanSizes& S = sizes;
   S.w_doubles = S.s_doubles = S.piv_total = S.lu_total = 0;
-  S.factor_doubles = S.proxy_units = S.sum_rank = 0;
+  S.factor_doubles = S.proxy_units = S.half_units = S.sum_rank = 0;
   S.max_rank = 0;
   S.ref_float_count = S.ref_int_count = 0;
   pair_wx.assign(L_ + 1, {});
@@ -235,6 +235,7 @@ void Planner::layout() {
       } else if (mode_[l] == kModeHalf) {  // U' streamed, the Y side regenerated
         S.factor_doubles += r * node_size(l, P.X[p]);
         S.proxy_units += r * node_size(l, P.Y[p]);
+        S.half_units += r * node_size(l, P.Y[p]);
       } else {
         S.proxy_units += units;
       }
@@ -419,10 +420,10 @@ void Planner::layout() {
     if (mode_[l] == kModeDirect || mode_[l] == kModePair || mode_[l] == kModeFused) continue;
     const std::int64_t cnt = 1LL << (3 * l);
     const bool half = mode_[l] == kModeHalf;
-    for (int side = 0; side < (half ? 2 : 1); ++side) {
-    // half levels: side 0 = the streamed groups (node ids gid), side 1 = the
-    // regenerated ones (node ids gv)
-    const int kind = half ? (side == 0 ? kModeStream : kModeProxy) : mode_[l];
+    // half levels: the streamed groups (node ids gid) here; the regenerated
+    // ones (node ids gv) run as h2_items in phase 2 (both uses at once)
+    for (int side = 0; side < 1; ++side) {
+    const int kind = half ? kModeStream : mode_[l];
     const std::int64_t chunk = kind == kModeStream ? kRowChunk : kSrcChunk;
     for (std::int64_t z = 0; z < cnt; ++z) {
       const std::int64_t g = side == 0 ? gid(l, z) : gv(l, z);
@@ -467,6 +468,7 @@ void Planner::layout() {
   // for every owned node A of a proxy level, rows in chunks of 256
   p2_items.clear();
   p2s_items.clear();
+  h2_items.clear();
   pg_items.clear();
   pair_descs.clear();
   pd_level.assign(L_ + 2, 0);
@@ -568,13 +570,35 @@ void Planner::layout() {
       int slot = -1;
       for (std::int64_t z = 0; z < cnt; ++z) {
         const std::int64_t g = side == 0 ? gid(l, z) : gv(l, z);
-        if (rpad[g] == 0 || !owned(l, z)) continue;
+        // half levels' regenerated groups: every shard that holds the group
+        // evaluates it (its v feeds the owned partners' streamed rows)
+        if (rpad[g] == 0 || (!owned(l, z) && !(half && side == 1))) continue;
         if (slot < 0) slot = n_proxy_levels++;
         const std::int64_t nr = node_size(l, z);
         // proxy levels: even split into ceil(nr / 256) items (a 256 + small
         // remainder split leaves most of the second item's target slots idle)
         const std::int64_t per =
             stream ? step : (nr + (nr + step - 1) / step - 1) / ((nr + step - 1) / step);
+        if (half && side == 1) {
+          // both uses in one pass; the node's v partials per chunk when it
+          // spans several. Chunks of 256 rows and the remainder (which runs
+          // on 2 / 4 thread groups when it is <= 128 / <= 64 rows): an even
+          // split of 257-320 rows would fill two 256-slot chunks half
+          const std::int64_t per = step;
+          const std::int64_t nch = (nr + per - 1) / per;
+          const std::int64_t pbase = S.p_doubles;
+          if (nch > 1) {
+            S.p_doubles += nch * rpad[g];
+            reds.push_back(P1Reduce{static_cast<std::int32_t>(g), rpad[g], static_cast<std::int32_t>(nch),
+                                    kModeHalf, pbase});
+          }
+          std::int64_t k = 0;
+          for (std::int64_t r0 = 0; r0 < nr; r0 += per, ++k)
+            h2_items.push_back(H2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
+                                      static_cast<std::int32_t>(std::min<std::int64_t>(per, nr - r0)),
+                                      owned(l, z) ? slot : -1, nch > 1 ? pbase + k * rpad[g] : -1});
+          continue;
+        }
         for (std::int64_t r0 = 0; r0 < nr; r0 += per)
           dst.push_back(P2Item{static_cast<std::int32_t>(g), static_cast<std::int32_t>(r0),
                                static_cast<std::int32_t>(std::min<std::int64_t>(per, nr - r0)), slot});

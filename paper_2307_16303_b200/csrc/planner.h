@@ -125,6 +125,20 @@ struct P2Item {
   std::int32_t slot;
 };
 
+// Half levels (kModeHalf), the regenerated side: one pass per row chunk of a
+// node's virtual group evaluates every entry E = K(sigma, rows) once for
+// both of its uses - b rows += E^T t (t = the partners' streamed U'^T x,
+// ready once p1_stream is done) and v = E x_rows (the partners' streamed
+// phase-2 weights, scattered through spos, or partials at pslot when the
+// node spans several chunks, summed by a P1Reduce of kind kModeHalf).
+struct H2Item {
+  std::int32_t node;   // virtual node id (planner: gv)
+  std::int32_t row0;
+  std::int32_t nrows;  // <= 256
+  std::int32_t slot;   // output partial of the rows
+  std::int64_t pslot;  // -1: v through spos; else this chunk's partial base
+};
+
 // Device descriptor of one stream-level work item (engine.cu, from P1Item /
 // P2Item + the node tables), so the bulk-copy producer needs one load per item.
 struct StreamDesc {
@@ -162,7 +176,7 @@ struct ProxySeg {
 
 struct PlanSizes {
   std::int64_t w_doubles = 0, s_doubles = 0, p_doubles = 0, piv_total = 0, lu_total = 0;
-  std::int64_t factor_doubles = 0, proxy_units = 0, direct_evals = 0, sum_rank = 0,
+  std::int64_t factor_doubles = 0, proxy_units = 0, half_units = 0, direct_evals = 0, sum_rank = 0,
                npairs = 0, nblocks_ordered = 0;
   std::int64_t near_blocks = 0, near_entries = 0;
   int max_rank = 0;
@@ -237,6 +251,7 @@ class Planner {
   std::vector<P1Reduce> reds;
   std::vector<P2Item> p2_items;   // owned nodes of proxy levels, <= 256 rows each
   std::vector<P2Item> p2s_items;  // owned nodes of stream levels, one row tile each
+  std::vector<H2Item> h2_items;   // half levels: the regenerated side, both uses in one pass
   // pair levels: one descriptor per pair with an owned side (grouped by level),
   // pd_level[l] .. pd_level[l + 1]; per owned node the output runs of its
   // pairs (pc_off over global nodes, pc_pos in pair order), gathered into the

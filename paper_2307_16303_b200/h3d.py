@@ -121,7 +121,7 @@ class _Stats(C.Structure):
         ("build_ms_plan", C.c_double),
         ("build_ms_post", C.c_double),
         ("build_ms_near", C.c_double),
-        ("reserved", C.c_int64 * 1),
+        ("half_units", C.c_int64),
     ]
 
 
@@ -659,7 +659,7 @@ def ie_experiment(n: int, kernel: KernelSpec, eps: float, variant: str = "hodlr3
 # ---------------------------------------------------------------- host planner
 # h3d_kernel_slot order (include/h3d_b200.h)
 KERNEL_SLOTS = ("gather", "p1_stream", "red_stream", "p2_stream", "p1_proxy", "red_proxy", "solve",
-                "p2_proxy", "near", "combine", "pair", "fused")
+                "p2_proxy", "near", "combine", "pair", "fused", "half")
 
 _PLAN_DTYPES = {
     "woff": np.int64, "soff": np.int64, "rowbeg": np.int64, "rpad": np.int32, "rows": np.int32,
@@ -669,6 +669,8 @@ _PLAN_DTYPES = {
     "sym_cnt": np.int32, "out_off": np.int64, "in_off": np.int32, "in_pos": np.int64, "node_base": np.int64, "vbase": np.int64, "modes": np.int32, "ranges": np.int64,
     "rank_rows": np.int64, "sizes": np.int64,
     # structs, decoded as int64 fields (see csrc/planner.h)
+    "h2_items": np.dtype([("node", np.int32), ("row0", np.int32), ("nrows", np.int32), ("slot", np.int32),
+                          ("pslot", np.int64)]),
     "proxy_segs": np.dtype([("so", np.int64), ("base", np.int64), ("piv_off", np.int64),
                             ("lu_off", np.int64), ("r", np.int32), ("side", np.int32),
                             ("solve", np.int32), ("pad", np.int32)]),

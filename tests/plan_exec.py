@@ -143,12 +143,36 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             S[dst[ok]] = v[ok]
         else:
             P[it["pslot"]: it["pslot"] + nc] = v
-    for rd in plan.array("reds"):
+    def reduce(rd):
         g, nc, k = int(rd["node"]), int(rd["ncols"]), int(rd["nchunks"])
         v = P[rd["pbase"]: rd["pbase"] + k * nc].reshape(k, nc).sum(axis=0)
         dst = spos[soff[g]: soff[g] + nc]
         ok = dst >= 0
         S[dst[ok]] = v[ok]
+    reds = plan.array("reds")
+    for rd in reds:
+        if rd["kind"] != 5:
+            reduce(rd)
+    # half levels, the regenerated side: both uses per entry (planner.h H2Item);
+    # its t (the partners' streamed phase 1) is in S, its v feeds their phase 2
+    h2 = plan.array("h2_items")
+    h2b = []
+    for it in h2:
+        g = int(it["node"])
+        R, so = int(rpad[g]), int(soff[g])
+        r0 = rowbeg[g] + it["row0"]
+        E = kernel_matrix(kind, ppts[r0: r0 + it["nrows"]], Q[so: so + R])
+        h2b.append((int(it["slot"]), r0, int(it["nrows"]), E @ S[so: so + R], g))
+        v = E.T @ xp[r0: r0 + it["nrows"]]
+        if it["pslot"] >= 0:
+            P[it["pslot"]: it["pslot"] + R] = v
+        else:
+            dst = spos[so: so + R]
+            ok = dst >= 0
+            S[dst[ok]] = v[ok]
+    for rd in reds:
+        if rd["kind"] == 5:
+            reduce(rd)
     # ---- proxy solves
     for sg in plan.array("proxy_segs"):
         if not sg["solve"]:
@@ -214,7 +238,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
     items2s = plan.array("p2s_items")
     pgit = plan.array("pg_items")
     nslots = 1 + max([int(v) for v in items2["slot"]] + [int(v) for v in items2s["slot"]] +
-                     [int(v) for v in pgit["slot"]] + [-1])
+                     [int(v) for v in pgit["slot"]] + [int(v) for v in h2["slot"]] + [-1])
     lvl = np.zeros((nslots, n))
     hits = np.zeros((L + 1, n), np.int64)
     shits = np.zeros((nslots, n), np.int64)
@@ -275,6 +299,10 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
         sY = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, EX @ xp[d["xrow"]: d["xrow"] + m_]))
         pout[d["out"]: d["out"] + m_] = EX.T @ sX
         pout[d["out"] + m_: d["out"] + m_ + n_] = EY.T @ sY
+    for slot, r0, nr, bv, g in h2b:
+        if slot >= 0:
+            lvl[slot, r0: r0 + nr] = bv
+            shits[slot, r0: r0 + nr] += 1
     pcoff, pcpos = plan.array("pc_off"), plan.array("pc_pos")
     for it in pgit:
         g = int(it["node"])

@@ -42,7 +42,7 @@ def main():
     bd = torch.empty_like(xd)
     st = torch.cuda.current_stream()
     names = ["gather", "p1_stream", "red_stream", "p2_stream", "p1_proxy", "red_proxy", "solve",
-             "p2_proxy", "near", "combine", "pair", "fused"]
+             "p2_proxy", "near", "combine", "pair", "fused", "half"]
     for lv in a.levels.split(","):
         pol = dict(mode_policy="auto") if lv == "auto" else dict(
             mode_policy="explicit", level_modes=tuple(int(c) for c in lv))
