@@ -467,7 +467,7 @@ def main():
         "config": workload_config(args.config, args.near),
         "detail": {
             "representation": {"policy": args.policy,
-                               "level_modes": {str(l): ["stream", "proxy", "direct", "pair", "fused", "half"][m]
+                               "level_modes": {str(l): ["stream", "proxy", "direct", "pair", "fused", "half", "split"][m]
                                                for l, m in enumerate(st["level_modes"]) if l > 0},
                                "note": "one ACA per unordered admissible pair; stream = explicit "
                                        "factors in HBM, proxy = pivots+LU regenerated in FP64, "

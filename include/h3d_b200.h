@@ -79,8 +79,10 @@ typedef struct {
    *     the second time from L2), 4 fused = proxy storage, pair-major, each
    *     regenerated entry evaluated once for both orientations, 5 half =
    *     U' = K(X, tau) (LR)^-1 streamed and K(sigma, Y) regenerated, no solves
-   *     (laplace3d and r4 only); direct only at the leaf level, pair and fused
-   *     ranks <= 128, fused nodes <= 352 points). */
+   *     (laplace3d and r4 only), 6 split = proxy storage in three passes: the
+   *     X-role entries twice, the Y-role entries once for both uses between two
+   *     solve rounds; direct only at the leaf level, pair and fused ranks <= 128,
+   *     fused nodes <= 352 points). */
   int mode_policy;
   int level_modes[16];
   int variant;          /* h3d_variant (Variant argument of initialize, hmatrix.hpp:57-58) */
@@ -135,7 +137,7 @@ typedef struct {
   int64_t owned_row_begin;    /* shard rows [begin, end) in Morton order */
   int64_t owned_row_end;
   int level_modes[16];        /* applied mode per level (0 stream, 1 proxy, 2 direct, 3 pair, 4 fused,
-                                 5 half) */
+                                 5 half, 6 split) */
   int64_t proxy_units;        /* sum over proxy-level pairs of r (m + n) */
   int64_t direct_evals;       /* leaf-level admissible entries evaluated exactly */
   int64_t lu_doubles;         /* packed LU storage of proxy-level pairs */

@@ -203,7 +203,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
     for (int l = 1; l <= L_ && l < 16; ++l) {
       const int m = opt_.level_modes[l];
       if (m < 0 || m > kModeLast)
-        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2, 3, 4 or 5");
+        throw InvalidArgument("initialize: level_modes entries must be 0, 1, 2, 3, 4, 5 or 6");
       if (m == kModeDirect && l != L_)
         throw InvalidArgument("initialize: direct mode is only valid at the leaf level");
       modes_[l] = m;
@@ -652,7 +652,7 @@ bool Engine::finish_single_pass() {
     DevBuf<std::int32_t> d_rank;
     d_rank.upload(P.rank, stream_);
     const std::int64_t* poff = pool_off_[static_cast<std::size_t>(l)]->get();
-    if (mode == kModeProxy || mode == kModeFused || mode == kModeHalf) {
+    if (mode == kModeProxy || mode == kModeFused || two_groups(mode)) {
       DevBuf<std::int64_t> d_po, d_lo;
       d_po.upload(plan_->pair_piv[l], stream_);
       d_lo.upload(plan_->pair_lu[l], stream_);
@@ -795,7 +795,7 @@ void Engine::choose_modes() {
         }
         continue;
       }
-      if (plan_->mode(l) != kModeProxy) continue;
+      if (plan_->mode(l) != kModeProxy && plan_->mode(l) != kModeSplit) continue;
       const auto& rk = plan_->pairs(l).rank;
       if (!rk.empty() && *std::max_element(rk.begin(), rk.end()) > kMaxProxyRank)
         throw InvalidArgument("initialize: level " + std::to_string(l) + " has ranks above " +
@@ -948,9 +948,13 @@ void Engine::upload_plan() {
   launch_fill_far(q4c_.get(), std::max<std::int64_t>(Z.s_doubles, 2), true, stream_);
   center_.upload(P.center, stream_);
   vcols_.upload(P.vcols, stream_);
-  std::vector<ProxySeg> solve;
+  std::vector<ProxySeg> solve, solve2;
   for (const auto& s : P.proxy_segs)
-    if (s.solve) solve.push_back(s);
+    if (s.solve == 2) solve2.push_back(s);
+    else if (s.solve) solve.push_back(s);
+  std::stable_sort(solve2.begin(), solve2.end(), [](const ProxySeg& a, const ProxySeg& b) { return a.r > b.r; });
+  n_segs_solve2_ = static_cast<std::int64_t>(solve2.size());
+  segs_solve2_.upload(solve2.empty() ? std::vector<ProxySeg>{ProxySeg{}} : solve2, stream_);
   // largest blocks first: the solve kernel hands segments round-robin to its
   // warps, so the long ones start early and the short ones fill in
   std::stable_sort(solve.begin(), solve.end(), [](const ProxySeg& a, const ProxySeg& b) { return a.r > b.r; });
@@ -1062,7 +1066,7 @@ void Engine::upload_plan() {
   pg_items_.upload(P.pg_items.empty() ? std::vector<P2Item>{P2Item{}} : P.pg_items, stream_);
   n_pg_ = static_cast<std::int64_t>(P.pg_items.size());
   pair_out_.alloc(std::max<std::int64_t>(P.pair_out_total, 1));
-  counters_.alloc(5 + L_ + 1);
+  counters_.alloc(kCounters);
   sync_flag_.alloc(1);
   H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), stream_));
   if (P.near_storage() != 0) {
@@ -1235,7 +1239,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   const bool pair_lv = pd_level_.size() > 1 && pd_level_.back() > 0;
   const bool hbm = n_p1s_ > 0 || n_p2s_ > 0 || pair_lv;
   const bool fused_lv = fd_level_.size() > 1 && fd_level_.back() > 0;
-  const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0 || fused_lv;
+  const bool fp = n_p1p_ > 0 || n_segs_solve_ > 0 || n_p2_ > 0 || fused_lv || n_h2_ > 0;
   // per-level gather of pair-major outputs into the level partials
   auto gather_levels = [&](int mode, cudaStream_t st) {
     for (int l = 1; l <= L_; ++l) {
@@ -1247,7 +1251,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
       ++launches;
     }
   };
-  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, (5 + L_ + 1) * sizeof(unsigned), s));
+  H3D_CUDA_CHECK(cudaMemsetAsync(counters_.get(), 0, kCounters * sizeof(unsigned), s));
   H3D_CUDA_CHECK(cudaMemsetAsync(sync_flag_.get(), 0, sizeof(unsigned), s));
   Phase2Args a2 = phase2_args(bout);
   a2.counter = counters_.get() + 2;
@@ -1327,6 +1331,14 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // half levels, the regenerated side: both uses per entry in one pass, once
   // the partners' streamed phase 1 (its t) is in S; p2_stream waits for its v
   const bool h2 = n_h2_ > 0 && has_p2;
+  if (h2 && n_segs_solve2_ > 0) {
+    // split levels: the Y-role columns' weights are solved before the pass
+    kb(H3D_K_SOLVE, stream4_);
+    launch_proxy_solve(segs_solve2_.get(), n_segs_solve2_, lu_.get(), lu_total_, S_.get(), sms_, tune_.sol,
+                       counters_.get() + 7, stream4_);
+    ke(H3D_K_SOLVE, stream4_);
+    ++launches;
+  }
   if (h2) {
     if (hbm) H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[1], 0));
     kb(H3D_K_HALF, stream4_);

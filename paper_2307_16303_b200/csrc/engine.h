@@ -166,8 +166,9 @@ class Engine {
   DevBuf<double> q4c_;  // the same points centred on their node's box (x', y', z', |.|^2)
   DevBuf<double> center_;  // box centre per global node
   DevBuf<std::int32_t> vcols_;  // leading vertex-partner columns per node
-  DevBuf<ProxySeg> segs_all_, segs_solve_;
-  std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0;
+  DevBuf<ProxySeg> segs_all_, segs_solve_, segs_solve2_;
+  // segs_solve2_: split levels' Y-role segments, solved before the two-use pass
+  std::int64_t n_segs_all_ = 0, n_segs_solve_ = 0, n_segs_solve2_ = 0;
   DevBuf<P1Item> p1_stream_items_, p1_proxy_items_;
   DevBuf<P1Reduce> p1_red_s_, p1_red_p_, p1_red_h_;  // tall-node partial reductions, stream / proxy / half kind
   std::int64_t n_p1s_ = 0, n_p1p_ = 0, n_red_s_ = 0, n_red_p_ = 0, n_red_h_ = 0;
@@ -208,7 +209,10 @@ class Engine {
   };
   std::vector<GraphEntry> graphs_;
   std::int64_t run_graph(const double* x, double* b, cudaStream_t s);
-  DevBuf<unsigned> counters_;  // [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy, solve, ...]
+  // work counters: [p1_stream, p1_proxy, p2_compute, p2_stream, p2_proxy, solve, two-use pass, solve 2,
+  // pair levels 8..]
+  static constexpr int kCounters = 32;
+  DevBuf<unsigned> counters_;
   // matvec lanes (priorities: the HBM lane and the FP64 critical chain above
   // the near field, which fills whatever the two leave idle)
   cudaStream_t stream2_ = nullptr;          // HBM lane: stream levels

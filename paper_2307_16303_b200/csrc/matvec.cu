@@ -1634,8 +1634,11 @@ void launch_half2(const Phase2Args& a, int sms, int per_sm, cudaStream_t s) {
       half2_kernel<kR4><<<grid, kProxyThreads, 0, s>>>(a);
       break;
     }
-    default:
-      throw std::logic_error("half levels are for the smooth kernels only");
+    default: {
+      const int grid = grid_for(half2_kernel<kHelmholtz>, sms, per_sm, a.n_h2_items, kProxyThreads);
+      half2_kernel<kHelmholtz><<<grid, kProxyThreads, 0, s>>>(a);
+      break;
+    }
   }
   H3D_CUDA_CHECK(cudaGetLastError());
 }

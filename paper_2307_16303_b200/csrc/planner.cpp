@@ -171,7 +171,7 @@ void Planner::layout() {
   std::int64_t T = total_nodes();
   vbase.assign(L_ + 1, -1);
   for (int l = 1; l <= L_; ++l)
-    if (mode_[l] == kModeHalf) {
+    if (two_groups(mode_[l])) {
       vbase[l] = T;
       T += 1LL << (3 * l);
     }
@@ -236,6 +236,9 @@ void Planner::layout() {
         S.factor_doubles += r * node_size(l, P.X[p]);
         S.proxy_units += r * node_size(l, P.Y[p]);
         S.half_units += r * node_size(l, P.Y[p]);
+      } else if (mode_[l] == kModeSplit) {  // X side twice, Y side once (two-use pass)
+        S.proxy_units += units;
+        S.half_units += r * node_size(l, P.Y[p]);
       } else {
         S.proxy_units += units;
       }
@@ -243,7 +246,7 @@ void Planner::layout() {
       S.ref_float_count += 2ull * static_cast<std::uint64_t>(r * r);
       S.ref_int_count += 4ull * static_cast<std::uint64_t>(r);
     }
-    if (mode_[l] == kModeProxy || mode_[l] == kModeFused || mode_[l] == kModeHalf) {
+    if (mode_[l] == kModeProxy || mode_[l] == kModeFused || two_groups(mode_[l])) {
       pair_piv[l].resize(P.X.size());
       pair_lu[l].resize(P.X.size());
       for (std::size_t p = 0; p < P.X.size(); ++p) {
@@ -260,7 +263,7 @@ void Planner::layout() {
     auto& ec = entry_col_[l];
     ec.assign(ep.size(), -1);
     const auto& lid = lists_[l].ids[0];
-    const bool half = mode_[l] == kModeHalf;
+    const bool half = two_groups(mode_[l]);  // two column groups per node
     for (std::int64_t z = 0; z < cnt; ++z)
       for (int side = 0; side < (half ? 2 : 1); ++side) {
         // half levels: side 0 = the pairs z is X of (explicit U', streamed,
@@ -297,7 +300,7 @@ void Planner::layout() {
         p1a[g] = grp_end[0];
         p1b[g] = grp_end[1];
         p1c[g] = grp_end[2];
-        const bool stream = mode_[l] == kModeStream || (half && side == 0);
+        const bool stream = mode_[l] == kModeStream || (mode_[l] == kModeHalf && side == 0);
         const std::int32_t rp = !any || mode_[l] == kModePair || mode_[l] == kModeFused
                                     ? 0
                                     : stream ? (cols + kTileCols - 1) / kTileCols * kTileCols
@@ -385,10 +388,11 @@ void Planner::layout() {
         const bool zx = P.X[p] == z;
         // half levels: z's column for k sits in z's stream group when z is
         // the pair's X, in its regenerated (virtual) group when z is Y
-        const bool half = mode_[l] == kModeHalf;
+        const bool half = two_groups(mode_[l]);
+        const bool split = mode_[l] == kModeSplit;
         const std::int64_t gz = half && !zx ? gv(l, z) : gid(l, z);
         const std::int64_t so = soff[gz] + ec[e];
-        if (mode_[l] == kModeProxy || (half && !zx)) {
+        if (mode_[l] == kModeProxy || split || (half && !zx)) {
           ProxySeg sg{};
           sg.so = so;
           sg.base = off_[l][k];
@@ -397,8 +401,10 @@ void Planner::layout() {
           sg.r = r;
           sg.side = zx ? 0 : 1;
           // half levels: the phase-1 output of a regenerated column is the
-          // transposed block's weight as it is (U' carries (LR)^-1): no solve
-          sg.solve = !half && owned(l, z) ? 1 : 0;
+          // transposed block's weight as it is (U' carries (LR)^-1): no solve.
+          // Split levels: the Y-role columns are solved before the two-use
+          // pass (2), the X-role ones after it, with the proxy levels (1)
+          sg.solve = !owned(l, z) ? 0 : split ? (zx ? 1 : 2) : half ? 0 : 1;
           sg.node = static_cast<std::int32_t>(gz);
           proxy_segs.push_back(sg);
         }
@@ -419,11 +425,11 @@ void Planner::layout() {
   for (int l = 1; l <= L_; ++l) {
     if (mode_[l] == kModeDirect || mode_[l] == kModePair || mode_[l] == kModeFused) continue;
     const std::int64_t cnt = 1LL << (3 * l);
-    const bool half = mode_[l] == kModeHalf;
-    // half levels: the streamed groups (node ids gid) here; the regenerated
-    // ones (node ids gv) run as h2_items in phase 2 (both uses at once)
+    // half / split levels: the X-role groups (node ids gid) here - streamed
+    // (half) or regenerated (split); the Y-role ones (node ids gv) run as
+    // h2_items (both uses at once)
     for (int side = 0; side < 1; ++side) {
-    const int kind = half ? kModeStream : mode_[l];
+    const int kind = mode_[l] == kModeHalf ? kModeStream : mode_[l] == kModeSplit ? kModeProxy : mode_[l];
     const std::int64_t chunk = kind == kModeStream ? kRowChunk : kSrcChunk;
     for (std::int64_t z = 0; z < cnt; ++z) {
       const std::int64_t g = side == 0 ? gid(l, z) : gv(l, z);
@@ -559,11 +565,11 @@ void Planner::layout() {
       }
       continue;
     }
-    const bool half = mode_[l] == kModeHalf;
-    // half levels: the streamed groups and the regenerated groups write a
+    const bool half = two_groups(mode_[l]);
+    // half / split levels: the X-role groups and the Y-role groups write a
     // partial each (two output slots)
     for (int side = 0; side < (half ? 2 : 1); ++side) {
-      const bool stream = half ? side == 0 : mode_[l] == kModeStream;
+      const bool stream = mode_[l] == kModeHalf ? side == 0 : mode_[l] == kModeStream;
       const std::int64_t cnt = 1LL << (3 * l);
       const std::int64_t step = stream ? kTileRows : kColChunk;
       auto& dst = stream ? p2s_items : p2_items;

@@ -49,8 +49,15 @@ enum LevelMode : int {
                     //   evaluations per pair. Every node carries two column groups: the
                     //   pairs it is X of (stream kernels, its own node id) and the pairs
                     //   it is Y of (proxy kernels, a virtual node id >= total_nodes())
+  kModeSplit = 6,   // matrix-free like kModeProxy, three passes: the pairs a node is X of
+                    //   (proxy kernels, node id gid) evaluated in phase 1 and phase 2, the
+                    //   pairs it is Y of (virtual node id gv) once, both uses in the two-use
+                    //   pass between two solve rounds: 1.5 r(m+n) evaluations per pair
 };
-constexpr int kModeLast = kModeHalf;
+constexpr int kModeLast = kModeSplit;
+// levels whose nodes carry two column groups (gid: the pairs a node is X of,
+// gv: the pairs it is Y of)
+inline bool two_groups(int mode) { return mode == kModeHalf || mode == kModeSplit; }
 
 // Fused proxy pass (kModeFused levels, fused.cu): pivots sigma (row, in X) at
 // piv_off, tau (column, in Y) at piv_off + r; inverses at lu_off (row-major)

@@ -274,7 +274,8 @@ class HmatOptions:
     # (explicit factors everywhere) or "explicit" (level_modes[l]: 0 stream,
     # 1 proxy, 2 direct at the leaf level, 3 pair = explicit factors applied in
     # one fused read per pair, 4 fused, 5 half = U' = K(X, tau) (LR)^-1
-    # streamed and K(sigma, Y) regenerated, laplace3d / r4 only)
+    # streamed and K(sigma, Y) regenerated, laplace3d / r4 only, 6 split =
+    # proxy storage, the Y-role entries evaluated once for both uses)
     mode_policy: str = "auto"
     level_modes: tuple = ()
     # multi-GPU (B200 extension): every rank returns the full b, all-gathered

@@ -86,7 +86,7 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
             wx, wy = plan.array("pair_wx", l), plan.array("pair_wy", l)
             rx, ry = plan.array("pair_rx", l), plan.array("pair_ry", l)
             cx, cy = plan.array("pair_cx", l), plan.array("pair_cy", l)
-        if md[l] in (1, 4, 5):
+        if md[l] in (1, 4, 5, 6):
             po, lo = plan.array("pair_piv", l), plan.array("pair_lu", l)
         for p, (a, b) in enumerate(zip(X, Y)):
             rp, cp, LU = pd[(l, int(a), int(b))]
@@ -113,10 +113,10 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
                 FX = np.linalg.solve((Lm @ Um).T, kernel_matrix(kind, Xp, Yp[cp]).T).T
                 I, Q = np.meshgrid(np.arange(len(Xp)), np.arange(r), indexing="ij")
                 W[wx[p] + tile_index(I, cx[p] + Q, rx[p])] = FX
-            if md[l] in (1, 4, 5):
+            if md[l] in (1, 4, 5, 6):
                 piv[po[p]: po[p] + r] = rp
                 piv[po[p] + r: po[p] + 2 * r] = cp
-            if md[l] in (1, 4):  # half levels keep the pivots only
+            if md[l] in (1, 4, 6):  # half levels keep the pivots only
                 lu[lo[p]: lo[p] + r * r] = LU.reshape(-1)
     # proxy coordinates (padding far away, weight 0)
     Q = np.full((max(sizes[1], 1), 3), 1e100)
@@ -153,6 +153,22 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
     for rd in reds:
         if rd["kind"] != 5:
             reduce(rd)
+
+    def solve_segs(which):
+        for sg in plan.array("proxy_segs"):
+            if sg["solve"] != which:
+                continue
+            r, so = int(sg["r"]), int(sg["so"])
+            LU = lu[sg["lu_off"]: sg["lu_off"] + r * r].reshape(r, r)
+            Lm = np.tril(LU, -1) + np.eye(r)
+            Um = np.triu(LU)
+            v = S[so: so + r]
+            if sg["side"] == 0:
+                S[so: so + r] = np.linalg.solve(Um, np.linalg.solve(Lm, v))
+            else:
+                S[so: so + r] = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, v))
+    # split levels: the Y-role weights are solved before the two-use pass
+    solve_segs(2)
     # half levels, the regenerated side: both uses per entry (planner.h H2Item);
     # its t (the partners' streamed phase 1) is in S, its v feeds their phase 2
     h2 = plan.array("h2_items")
@@ -173,19 +189,8 @@ def simulate(plan, inp, xp, kind, diag=0.0, modes=None):
     for rd in reds:
         if rd["kind"] == 5:
             reduce(rd)
-    # ---- proxy solves
-    for sg in plan.array("proxy_segs"):
-        if not sg["solve"]:
-            continue
-        r, so = int(sg["r"]), int(sg["so"])
-        LU = lu[sg["lu_off"]: sg["lu_off"] + r * r].reshape(r, r)
-        Lm = np.tril(LU, -1) + np.eye(r)
-        Um = np.triu(LU)
-        v = S[so: so + r]
-        if sg["side"] == 0:
-            S[so: so + r] = np.linalg.solve(Um, np.linalg.solve(Lm, v))
-        else:
-            S[so: so + r] = np.linalg.solve(Lm.T, np.linalg.solve(Um.T, v))
+    # ---- proxy solves (and the split levels' X-role ones, after the two-use pass)
+    solve_segs(1)
     # ---- phase 2: near field + direct leaf blocks per owned leaf (cpart),
     # proxy / stream levels per node row chunk into one partial per level
     leaf0, leaf1, row0, row1 = plan.array("ranges")

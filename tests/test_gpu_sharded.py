@@ -19,7 +19,7 @@ def rel(a, b):
 
 
 @pytest.mark.parametrize("levels", [(0, 0, 0, 0), (0, 1, 0, 2), (0, 1, 1, 1), (0, 3, 3, 2), (0, 1, 3, 3),
-                                    (0, 1, 4, 4), (0, 1, 4, 2), (0, 5, 1, 5), (0, 1, 5, 2)])
+                                    (0, 1, 4, 4), (0, 1, 4, 2), (0, 5, 1, 5), (0, 1, 5, 2), (0, 6, 6, 2), (0, 6, 1, 5)])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_shards_reproduce_single_gpu(h3d, oracle, world, levels):
     pts = h3d.generate_points(N, SEED)

@@ -119,7 +119,7 @@ def ref_inputs():
 
 
 @pytest.mark.parametrize("world", [1, 2])
-@pytest.mark.parametrize("modes_name", ["stream", "proxy", "hybrid", "pair", "fused", "half"])
+@pytest.mark.parametrize("modes_name", ["stream", "proxy", "hybrid", "pair", "fused", "half", "split"])
 def test_sharded_plan_reproduces_the_oracle(ref_inputs, world, modes_name):
     L = ref_inputs["L"]
     assert L == 3
@@ -128,7 +128,8 @@ def test_sharded_plan_reproduces_the_oracle(ref_inputs, world, modes_name):
              "hybrid": [0] + [1, 0] + [1] * (L - 3) + [2],
              "pair": [0, 1, 3, 3],
              "fused": [0, 1, 4, 4],
-             "half": [0, 5, 1, 5]}[modes_name]
+             "half": [0, 5, 1, 5],
+             "split": [0, 6, 6, 5]}[modes_name]
     b, sizes = _run_world(world, modes)
     # the plan reproduces the dense evaluation of the same representation
     # (one pivot/LU factorization per unordered pair, both orientations) to
