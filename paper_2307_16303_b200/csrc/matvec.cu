@@ -43,6 +43,8 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kP1Cols = 256;    // phase-1 columns per item
 constexpr int kChunk = 256;     // phase-1 proxy: sources staged per round
+constexpr int kHalfChunk = kChunk / 2;  // p1 / p2_proxy: two buffers of this many sources
+static_assert(kHalfChunk == 128, "one staged source per thread of a 128-thread proxy CTA");
 constexpr int kMaxRanges = 256; // phase-2 compute: source ranges per tile
 // p2_stream's solves-done throttle gives up after this long (the solves take
 // 0.3-2.5 ms; the flag orders nothing the kernel's results depend on)
@@ -350,20 +352,32 @@ __global__ void __launch_bounds__(kProxyThreads, 5) p1_proxy_kernel(const P1Args
                                      : make_double4(kFar, kFar, kFar, 0.0);
       tg[t] = make_tgt(q.x, q.y, q.z, cen);
     }
-    for (int j0 = 0; j0 < it.nrows; j0 += kChunk) {
-      const int nj = min(kChunk, it.nrows - j0);
-      __syncthreads();
-      for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
-        const double4 v = reinterpret_cast<const double4*>(a.p4)[rb + j0 + q];
-        const double px = v.x - cen.x, py = v.y - cen.y, pz = v.z - cen.z;
-        src[3 * q] = make_double2(px, py);
-        src[3 * q + 1] = make_double2(pz, fma(pz, pz, fma(py, py, px * px)));
-        src[3 * q + 2] = make_double2(v.w, 0.0);
-      }
-      __syncthreads();
+    // sources (the node's points) in chunks of kHalfChunk, double-buffered
+    // like p2_proxy_kernel: one barrier per chunk, the next chunk's loads in
+    // flight during the current chunk's evaluations
+    const double4* P4s = reinterpret_cast<const double4*>(a.p4) + rb;
+    const int nrw = it.nrows;
+    auto stage = [&](double2* d, const double4& v) {
+      const double px = v.x - cen.x, py = v.y - cen.y, pz = v.z - cen.z;
+      d[0] = make_double2(px, py);
+      d[1] = make_double2(pz, fma(pz, pz, fma(py, py, px * px)));
+      d[2] = make_double2(v.w, 0.0);
+    };
+    double4 nv = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (threadIdx.x < nrw) nv = P4s[threadIdx.x];
+    __syncthreads();  // the previous item is done with both buffers
+    stage(src + 3 * threadIdx.x, nv);
+    __syncthreads();
+    for (int j0 = 0, b = 0; j0 < nrw; j0 += kHalfChunk, b ^= 1) {
+      const int nj = min(kHalfChunk, nrw - j0);
+      const bool more = j0 + kHalfChunk < nrw;
+      const int qn = j0 + kHalfChunk + threadIdx.x;
+      if (more && qn < nrw) nv = P4s[qn];
       const int sub = (nj + G - 1) / G;
       const int lo = min(nj, grp * sub), hi = min(nj, lo + sub);
-      proxy_eval2<K>(tg, acc, src, lo, lo, hi, nt, vwarp);
+      proxy_eval2<K>(tg, acc, src + 3 * kHalfChunk * b, lo, lo, hi, nt, vwarp);
+      if (more && qn < nrw) stage(src + 3 * kHalfChunk * (b ^ 1) + 3 * threadIdx.x, nv);
+      __syncthreads();
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = acc[t][0] + acc[t][1];
@@ -1143,20 +1157,45 @@ __global__ void __launch_bounds__(kProxyThreads, 5) p2_proxy_kernel(const Phase2
       const double4 q = i < it.nrows ? P4[a.nt.rowbeg[g] + it.row0 + i] : make_double4(kFar, kFar, kFar, 0.0);
       tg[t] = make_tgt(q.x, q.y, q.z, cen);
     }
-    for (int j0 = 0; j0 < R; j0 += kChunk) {
-      const int nj = min(kChunk, R - j0);
-      __syncthreads();
-      for (int q = threadIdx.x; q < nj; q += kProxyThreads) {
-        const double4 c4 = reinterpret_cast<const double4*>(a.q4c)[so + j0 + q];
-        src[3 * q] = make_double2(c4.x, c4.y);
-        src[3 * q + 1] = make_double2(c4.z, c4.w);
-        src[3 * q + 2] = make_double2(a.S[so + j0 + q], 0.0);
+    // sources in chunks of kHalfChunk, double-buffered: each thread loads one
+    // source of the next chunk into registers before the current chunk's
+    // evaluations and stores it after them, one barrier per chunk
+    const double4* Q4 = reinterpret_cast<const double4*>(a.q4c) + so;
+    const double* Sv = a.S + so;
+    double4 nq = make_double4(0.0, 0.0, 0.0, 0.0);
+    double nw = 0.0;
+    if (threadIdx.x < R) {
+      nq = Q4[threadIdx.x];
+      nw = Sv[threadIdx.x];
+    }
+    __syncthreads();  // the previous item is done with both buffers
+    if (threadIdx.x < kHalfChunk) {
+      double2* d = src + 3 * threadIdx.x;
+      d[0] = make_double2(nq.x, nq.y);
+      d[1] = make_double2(nq.z, nq.w);
+      d[2] = make_double2(nw, 0.0);
+    }
+    __syncthreads();
+    for (int j0 = 0, b = 0; j0 < R; j0 += kHalfChunk, b ^= 1) {
+      const int nj = min(kHalfChunk, R - j0);
+      const bool more = j0 + kHalfChunk < R;
+      const int qn = j0 + kHalfChunk + threadIdx.x;
+      if (more && qn < R) {
+        nq = Q4[qn];
+        nw = Sv[qn];
       }
-      __syncthreads();
+      const double2* cur = src + 3 * kHalfChunk * b;
       const int sub = (nj + G - 1) / G;
       const int lo = min(nj, grp * sub), hi = min(nj, lo + sub);
       const int jv = max(lo, min(hi, vc - j0));
-      proxy_eval2<K>(tg, acc, src, lo, jv, hi, nt, false);
+      proxy_eval2<K>(tg, acc, cur, lo, jv, hi, nt, false);
+      if (more && threadIdx.x < kHalfChunk && qn < R) {
+        double2* d = src + 3 * kHalfChunk * (b ^ 1) + 3 * threadIdx.x;
+        d[0] = make_double2(nq.x, nq.y);
+        d[1] = make_double2(nq.z, nq.w);
+        d[2] = make_double2(nw, 0.0);
+      }
+      __syncthreads();
     }
 #pragma unroll
     for (int t = 0; t < 2; ++t) red[grp * 2 * tpg + loc + t * tpg] = acc[t][0] + acc[t][1];
