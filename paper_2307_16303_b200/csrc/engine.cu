@@ -1312,8 +1312,10 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
   // latency-bound solves (H3D_TUNE nf=0: after p2_proxy on the FP64 lane).
   // Measured with the batched-load solve: C2 / C3 / C4 3.5-5.5 % faster
   // (before it the solves lost more than the near field gained)
-  const bool near_fork = has_p2 && tune_.nf != 0;
-  if (near_fork) {
+  // the near field (x only) forks beside the latency-bound solves
+  const int nf_mode = tune_.nf >= 0 ? tune_.nf : (n_h2_ > 0 ? 2 : 1);
+  const bool near_fork = has_p2 && nf_mode != 0;
+  auto fork_near = [&] {
     H3D_CUDA_CHECK(cudaEventRecord(fork_[2], stream4_));
     H3D_CUDA_CHECK(cudaStreamWaitEvent(stream3_, fork_[2], 0));
     kb(H3D_K_NEAR, stream3_);
@@ -1321,7 +1323,10 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ke(H3D_K_NEAR, stream3_);
     ++launches;
     H3D_CUDA_CHECK(cudaEventRecord(join_[2], stream3_));
-  }
+  };
+  // nf 1: right after p1_proxy; nf 2 (default with a two-use pass): after
+  // that pass, so the near field overlaps the solves and p2_proxy as before
+  if (near_fork && nf_mode == 1) fork_near();
   if (n_red_p_ > 0) {
     kb(H3D_K_RED_PROXY, stream4_);
     launch_phase1_reduce(p1_red_p_.get(), n_red_p_, nt, spos_.get(), P_.get(), S_.get(), stream4_);
@@ -1350,6 +1355,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     launches += 1 + (n_red_h_ > 0 ? 1 : 0);
     H3D_CUDA_CHECK(cudaEventRecord(h2_done_, stream4_));
   }
+  if (near_fork && nf_mode == 2) fork_near();
   if (n_segs_solve_ > 0) {
     kb(H3D_K_SOLVE, stream4_);
     launch_proxy_solve(segs_solve_.get(), n_segs_solve_, lu_.get(), lu_total_, S_.get(), sms_, tune_.sol,

@@ -125,14 +125,16 @@ class Engine {
   // H3D_TUNE="p1s=1,p1p=4,p2c=2,p2s=1,p2p=4" (proxy kernels: 128-thread CTAs)
   // ("skip=<mask of h3d_kernel_slot>" drops kernels: timing experiments only,
   // results are wrong; honoured only in a -DH3D_DEVTOOLS build)
-  // ("nf=0": near field after p2_proxy instead of forked beside the solves;
+  // ("nf=0": near field after p2_proxy instead of forked beside the solves,
+  // "nf=1": forked right after p1_proxy, "nf=2": forked after the two-use
+  // pass (the default when there is one, else 1);
   // "nfc": CTAs per SM of the forked near kernel; "fw=0": p2_stream does not
   // wait for the solves-done flag; "sol": CTAs per SM of the proxy solve;
   // "p2o=0": phase-2 FP64 kernels do not wait for the HBM lane's phase 1;
   // "acab": cap on the ACA CTAs per SM, 0 = occupancy limit; "acat<l>=<n>":
   // ACA CTA size of level l)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = 1, nfc = 1, pps = 0, graphs = 1, fw = 1,
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1, nfc = 1, pps = 0, graphs = 1, fw = 1,
         sol = 2, p2o = 1, acab = 0, half_search = 0, nfd = 0;
     int acat[16] = {};  // per-level ACA CTA size override (32 / 128 / 256 / 512)
   } tune_;
