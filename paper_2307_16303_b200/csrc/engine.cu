@@ -153,6 +153,7 @@ Engine::Engine(const double* xyz, std::int64_t n, const h3d_options& opt) : opt_
         else if (k == "p2p") tune_.p2p = v;
 #ifdef H3D_DEVTOOLS
         else if (k == "skip") tune_.skip = v;
+        else if (k == "h2w") tune_.h2w = v;
 #endif
         else if (k == "nf") tune_.nf = v;
         else if (k == "nfc") tune_.nfc = v;
@@ -1345,7 +1346,7 @@ std::int64_t Engine::enqueue(const double* xin, double* bout, cudaStream_t s, cu
     ++launches;
   }
   if (h2) {
-    if (hbm) H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[1], 0));
+    if (hbm && tune_.h2w) H3D_CUDA_CHECK(cudaStreamWaitEvent(stream4_, fork_[1], 0));
     kb(H3D_K_HALF, stream4_);
     a2.counter_h2 = counters_.get() + 6;
     launch_half2(a2, sms_, hbm ? tune_.p2p : 8, stream4_);

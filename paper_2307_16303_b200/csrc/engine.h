@@ -134,7 +134,7 @@ class Engine {
   // "acab": cap on the ACA CTAs per SM, 0 = occupancy limit; "acat<l>=<n>":
   // ACA CTA size of level l)
   struct Tune {
-    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, nf = -1, nfc = 1, pps = 0, graphs = 1, fw = 1,
+    int p1s = 1, p1p = 4, p2c = 2, p2s = 1, p2p = 4, skip = 0, h2w = 1, nf = -1, nfc = 1, pps = 0, graphs = 1, fw = 1,
         sol = 2, p2o = 1, acab = 0, half_search = 0, nfd = 0;
     int acat[16] = {};  // per-level ACA CTA size override (32 / 128 / 256 / 512)
   } tune_;
