@@ -287,7 +287,7 @@ __device__ __forceinline__ void proxy_evalT(const Tgt (&tg)[2], double (&acc)[2]
     one(j + 2, 0);
     one(j + 3, 1);
   }
-  for (; j < nj; ++j) one(j, j & 1);
+  for (; j < nj; ++j) one(j, 0);  // a runtime accumulator index would put acc in local memory
 }
 
 // nt = targets of this warp that exist (warp-uniform: 0, 1 or 2 per thread;

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(128, 5) operand_probe(double* out, int iters) 
       if (KIND == 0) a[k] = fma(a[k], m, 1e-9);          // 1 register pair read + reuse
       else if (KIND == 1) a[k] = fma(b[k], m, a[k]);     // 2 distinct + 1 repeated
       else if (KIND == 2) a[k] = fma(b[k], c[k], a[k]);  // 3 distinct
-      else a[k] = fma(b[k], c[7 - k], a[k]);             // 3 distinct, other pairing
+      else if (KIND == 3) a[k] = fma(b[k], c[7 - k], a[k]);  // 3 distinct, other pairing
+      else a[k] = fma(b[k], b[k], a[k]);                 // one register in two slots + 1 distinct
     }
   }
   double s = 0;
@@ -129,6 +130,12 @@ __device__ __forceinline__ void one_src(const Tgt (&tg)[NT], double (&acc)[NT][2
       const double tt = r2 * y;
       const double h = fma(tt, y, -s2.y);
       acc[t][u] = fma(y, h, acc[t][u]);
+    } else if constexpr (FORM == 4) {  // FORM 0 with the Newton step through y * y (exact: y has 21 bits)
+      const double r2 = fma(tg[t].ax, s0.x, fma(tg[t].ay, s0.y, fma(tg[t].az, s1.x, tg[t].tt + s1.y)));
+      double y;
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r2));
+      const double h = fma(r2, y * y, -3.0);
+      acc[t][u] = fma(y * h, s2.x, acc[t][u]);
     } else if constexpr (FORM == 3) {  // FORM 0 with the seed from the fp32 MUFU.RSQ via bit moves
       const double r2 = fma(tg[t].ax, s0.x, fma(tg[t].ay, s0.y, fma(tg[t].az, s1.x, tg[t].tt + s1.y)));
       const int hi = __double2hiint(r2);
@@ -316,6 +323,88 @@ __global__ void __launch_bounds__(128, 5) core_mma(const double4* __restrict__ p
   out[blockIdx.x * blockDim.x + threadIdx.x] = -0.5 * s;
 }
 
+
+// ---- (4) r^2 stages written as PTX blocks, one per stage and source, the
+// targets adjacent (shared source operand in the same slot): does ptxas keep
+// them together and set .reuse?
+template <int NT>
+__device__ __forceinline__ void stage_add(double (&q)[NT], const Tgt (&tg)[NT], double ss) {
+  if constexpr (NT == 4)
+    asm("add.f64 %0, %4, %8;\n\tadd.f64 %1, %5, %8;\n\tadd.f64 %2, %6, %8;\n\tadd.f64 %3, %7, %8;"
+        : "=d"(q[0]), "=d"(q[1]), "=d"(q[2]), "=d"(q[3])
+        : "d"(tg[0].tt), "d"(tg[1].tt), "d"(tg[2].tt), "d"(tg[3].tt), "d"(ss));
+  else
+    asm("add.f64 %0, %2, %4;\n\tadd.f64 %1, %3, %4;" : "=d"(q[0]), "=d"(q[1]) : "d"(tg[0].tt), "d"(tg[1].tt), "d"(ss));
+}
+template <int NT>
+__device__ __forceinline__ void stage_fma(double (&q)[NT], double a0, double a1, double a2, double a3, double s) {
+  if constexpr (NT == 4)
+    asm("fma.rn.f64 %0, %4, %8, %0;\n\tfma.rn.f64 %1, %5, %8, %1;\n\tfma.rn.f64 %2, %6, %8, %2;\n\tfma.rn.f64 %3, %7, %8, %3;"
+        : "+d"(q[0]), "+d"(q[1]), "+d"(q[2]), "+d"(q[3])
+        : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(s));
+  else
+    asm("fma.rn.f64 %0, %2, %4, %0;\n\tfma.rn.f64 %1, %3, %4, %1;" : "+d"(q[0]), "+d"(q[1]) : "d"(a0), "d"(a1), "d"(s));
+}
+
+template <int NT, int NS>
+__global__ void __launch_bounds__(128, 4) core_ptx(const double4* __restrict__ pts, double* out, int reps) {
+  __shared__ double2 src[3 * kSrc];
+  {
+    const double4 v = pts[threadIdx.x];
+    const double ss = v.x * v.x + v.y * v.y + v.z * v.z;
+    src[3 * threadIdx.x] = make_double2(v.x, v.y);
+    src[3 * threadIdx.x + 1] = make_double2(v.z, ss);
+    src[3 * threadIdx.x + 2] = make_double2(v.w, 0.0);
+  }
+  Tgt tg[NT];
+  double acc[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const double4 q = pts[1024 + (blockIdx.x * NT + t) * 128 + threadIdx.x];
+    const double x = q.x + 3.0, y = q.y, z = q.z;
+    tg[t] = Tgt{-2.0 * x, -2.0 * y, -2.0 * z, x * x + y * y + z * z};
+    acc[t] = 0.0;
+  }
+  __syncthreads();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+    for (int j0 = 0; j0 < kSrc; j0 += NS) {
+      double q[NS][NT], w[NS];
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        const double2 s0 = src[3 * (j0 + j)], s1 = src[3 * (j0 + j) + 1], s2 = src[3 * (j0 + j) + 2];
+        w[j] = s2.x;
+        stage_add<NT>(q[j], tg, s1.y);
+        if constexpr (NT == 4) {
+          stage_fma<NT>(q[j], tg[0].az, tg[1].az, tg[2].az, tg[3].az, s1.x);
+          stage_fma<NT>(q[j], tg[0].ay, tg[1].ay, tg[2].ay, tg[3].ay, s0.y);
+          stage_fma<NT>(q[j], tg[0].ax, tg[1].ax, tg[2].ax, tg[3].ax, s0.x);
+        } else {
+          stage_fma<NT>(q[j], tg[0].az, tg[1].az, 0.0, 0.0, s1.x);
+          stage_fma<NT>(q[j], tg[0].ay, tg[1].ay, 0.0, 0.0, s0.y);
+          stage_fma<NT>(q[j], tg[0].ax, tg[1].ax, 0.0, 0.0, s0.x);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        double g[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          double y;
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q[j][t]));
+          const double h = fma(q[j][t] * y, y, -3.0);
+          g[t] = y * h;
+        }
+        stage_fma<NT>(acc, g[0], g[1], NT == 4 ? g[NT - 2] : 0.0, NT == 4 ? g[NT - 1] : 0.0, w[j]);
+      }
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) s += acc[t];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = -0.5 * s;
+}
+
 template <class F>
 float timed(F launch) {
   launch();
@@ -373,7 +462,7 @@ int main() {
     const float ms = timed([&] { operand_probe<KIND><<<blocks, 128>>>(out, iters); });    \
     printf("operand probe kind %d: %.3f ms, %.2f T DFMA/s\n", KIND, ms, double(blocks) * 128 * iters * 8 / ms / 1e9); \
   }
-    OPER(0) OPER(1) OPER(2) OPER(3)
+    OPER(0) OPER(1) OPER(2) OPER(3) OPER(4)
   }
   const int npts = 1024 + blocks * 4 * 128 + 64;
   double4* h = new double4[npts];
@@ -397,7 +486,7 @@ int main() {
   }
   CORE(0, 2, 4) CORE(0, 2, 8) CORE(0, 4, 4) CORE(0, 4, 2) CORE(0, 1, 8)
   CORE(1, 2, 4) CORE(1, 2, 8) CORE(1, 4, 4) CORE(1, 4, 2) CORE(1, 1, 8)
-  CORE(3, 2, 4) CORE(3, 4, 4)
+  CORE(4, 2, 4) CORE(4, 4, 4) CORE(4, 2, 8)
   CORE(2, 2, 4) CORE(2, 2, 8) CORE(2, 4, 4) CORE(2, 4, 2) CORE(2, 1, 8) CORE(2, 2, 2)
 #define BLK(NT, NS, ORD)                                                                            \
   {                                                                                                 \
@@ -419,6 +508,16 @@ int main() {
            NF, NF * 8, NACC, ms, ev / ms / 1e9, ho[5]);                                             \
   }
   MMA(8, 1) MMA(8, 2) MMA(4, 2) MMA(4, 1) MMA(2, 2)
+#define PTXC(NT, NS)                                                                                \
+  {                                                                                                 \
+    const int bl = blocks * 2 / NT;                                                                 \
+    const float ms = timed([&] { core_ptx<NT, NS><<<bl, 128>>>(pts, out, reps); });                 \
+    const double ev = double(bl) * 128 * NT * kSrc * reps;                                          \
+    cudaMemcpy(ho, out, sizeof(double) * 128, cudaMemcpyDeviceToHost);                              \
+    printf("ptx-staged core %d targets x %d sources per trip: %.3f ms, %.3f T evals/s (out[5] %.15g)\n", \
+           NT, NS, ms, ev / ms / 1e9, ho[5]);                                                       \
+  }
+  PTXC(2, 4) PTXC(4, 2) PTXC(4, 4) PTXC(2, 2) PTXC(4, 1)
   printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
