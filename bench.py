@@ -67,6 +67,13 @@ FP64_TFLOPS = 2 * FP64_INSTR_PEAK / 1e12
 # dense-near (third-order rsqrt) 6 more; 1/r^4 and cos(r)/r use the exact
 # radial maps (reciprocal / sincos sequences).
 INSTR_FAR = {"laplace3d": 10, "r4": 12, "helmholtz-re": 40}
+# What the register file lets the Laplace admissible core reach: a DFMA with
+# three distinct register operands takes 3 cycles per sub-partition, not 2
+# (one 64-bit operand read per cycle), and a broadcast LDS.128 ~1.4; the
+# kernels' loop (2 targets x 4 sources per trip, 18.0-18.6 operand reads + 1.5
+# LDS.128 per evaluation) runs at 1.76 T evaluations/s in isolation
+# (tools/eval_bench.cu, profiles/r02_eval_bench.log, profiles/r02_summary.md).
+CORE_EVALS_PER_S = {"laplace3d": 1.76e12}
 # half levels' regenerated side (matvec.cu half2_kernel): one evaluation (the
 # far value without the accumulate) feeding two FMAs, plus ~0.6 DADD of the
 # 8-source warp reduce-scatter per entry
@@ -412,6 +419,11 @@ def main():
             ach, pk, unit = 2 * w / (kms * 1e-3) / 1e12, FP64_TFLOPS, "TFLOP/s"
         kstats[k] = dict(ms=round(kms, 4), start_ms=round(start / cnt, 4), bound=bound,
                          achieved=round(ach, 3), peak=pk, unit=unit, frac=round(ach / pk, 4))
+        if k in ("p1_proxy", "p2_proxy") and cfg["kernel"] in CORE_EVALS_PER_S and U > 0:
+            # the same kernel against the operand-read bound of its evaluation core
+            ev = U / (kms * 1e-3)
+            kstats[k]["evals_per_s"] = round(ev / 1e12, 4)
+            kstats[k]["frac_of_operand_bound"] = round(ev / CORE_EVALS_PER_S[cfg["kernel"]], 4)
     ksum = sum(v["ms"] for v in kstats.values())
     for v in kstats.values():
         v["share"] = round(v["ms"] / ksum, 4) if ksum else None
@@ -510,7 +522,12 @@ def main():
                      "unit": kd["unit"], "frac": kd["frac"], "traffic": traffic,
                      "alg_work_per_launch": work[dom][1],
                      "alg_work_unit": "bytes" if kd["bound"] == "hbm" else "FP64-pipe instructions",
-                     "t_ms": kd["ms"], "share_of_kernel_time": kd["share"]},
+                     "t_ms": kd["ms"], "share_of_kernel_time": kd["share"],
+                     "note": "durations are CUDA events inside the concurrent step: p2_proxy shares "
+                             "the FP64 path with the near pass and p2_stream while it runs (its "
+                             "stand-alone ncu time is in profiles/); FP64 kernels are bound by "
+                             "register-operand reads (3-operand DFMA = 2/3 of the DFMA rate), see "
+                             "frac_of_operand_bound in detail.kernels and profiles/r02_summary.md"},
         "clocks": clk,
         "e2e": {"value": e2e_value, "unit": "Mpoints/s", "h2d_bytes_per_step": 8 * n,
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e_ms,
