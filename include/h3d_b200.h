@@ -157,7 +157,7 @@ void h3d_default_options(h3d_options* opt);
 
 /* Input generation, bit-identical to the reference:
  * generate_points(UniformRandom, n, seed) (kernel.cpp:88-95), AoS xyz[3n];
- * the CLI right-hand side mt19937_64(seed), 2u-1 (tools/h3d.cpp:135-137). */
+ * the CLI right-hand side mt19937_64(seed), 2u-1 (reference proj/tools/h3d.cpp:135-137). */
 int h3d_generate_points(int64_t n, uint64_t seed, double* xyz);
 void h3d_random_vector(int64_t n, uint64_t seed, double* out);
 
