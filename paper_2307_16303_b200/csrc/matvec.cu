@@ -986,6 +986,51 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
         e3 += __shfl_xor_sync(0xffffffffu, e3, o);
       }
       __syncwarp();
+      // Ranges that follow one another in the packed point array (the
+      // children of one parent cell are consecutive leaves) merge into one
+      // copy: the flattened source order is unchanged, the producer issues
+      // 3-5x fewer bulk copies per leaf (it is the bottleneck on small
+      // leaves: one lane issues them). In place, 32 ranges per step.
+      int nrun = 0;
+      {
+        long long carry_end = -1;
+        for (int base = 0; base < nrange; base += 32) {
+          const int e = base + lane;
+          const bool valid = e < nrange;
+          const long long rs = valid ? sm.rstart[e] : 0;
+          const int rl = valid ? sm.rlen[e] : 0;
+          const long long my_end = rs + rl;
+          long long prev_end = __shfl_up_sync(0xffffffffu, my_end, 1);
+          if (lane == 0) prev_end = carry_end;
+          const bool head = valid && rs != prev_end;
+          const unsigned heads = __ballot_sync(0xffffffffu, head);
+          const int nv = __popc(__ballot_sync(0xffffffffu, valid));
+          int cum = rl;  // inclusive prefix of the lengths
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int up = __shfl_up_sync(0xffffffffu, cum, o);
+            if (lane >= o) cum += up;
+          }
+          // ranges before the block's first head continue the previous run
+          const int first = heads ? __ffs(heads) - 1 : nv;
+          const int lead = __shfl_sync(0xffffffffu, cum, max(first - 1, 0));
+          // a head's run ends before the next head (or the block's end)
+          const unsigned after = lane == 31 ? 0u : heads & ~((2u << lane) - 1u);
+          const int nxt = after ? __ffs(after) - 1 : nv;
+          const int cum_end = __shfl_sync(0xffffffffu, cum, max(nxt - 1, 0));
+          const long long last_end = __shfl_sync(0xffffffffu, my_end, max(nv - 1, 0));
+          __syncwarp();
+          if (lane == 0 && first > 0) sm.rlen[nrun - 1] += lead;
+          if (head) {
+            const int w = nrun + __popc(heads & ((1u << lane) - 1u));
+            sm.rstart[w] = rs;
+            sm.rlen[w] = cum_end - cum + rl;
+          }
+          nrun += __popc(heads);
+          carry_end = last_end;
+          __syncwarp();
+        }
+      }
       const long long obase = a.out_off[X] - e2;
       const int nchunks = (tot + kNearStage - 1) / kNearStage;
       const long long nfb = STORED ? a.nf_off[X] : 0;
@@ -999,7 +1044,7 @@ __global__ void __launch_bounds__(kNearThreads, 2) p2_near_kernel(const Phase2Ar
           near_put(sm, t,
                    NearMeta{xb, obase, r0, mr, c * kNearStage, 0, m, e1, e2, e3,
                             c + 1 == nchunks ? 1 : 0, nds, nfb},
-                   P4, re, roff, nrange, lane);
+                   P4, re, roff, nrun, lane);
       }
       __syncwarp();
     }
