@@ -405,6 +405,63 @@ __global__ void __launch_bounds__(128, 4) core_ptx(const double4* __restrict__ p
   out[blockIdx.x * blockDim.x + threadIdx.x] = -0.5 * s;
 }
 
+
+// ---- (5) many targets per thread, one (or two) sources per trip, not unrolled
+// over sources: the only independent work in a trip is the NT targets of the
+// same source, so ptxas has little choice but to keep them adjacent
+template <int NT, int NS>
+__global__ void __launch_bounds__(128, 4) core_wide(const double4* __restrict__ pts, double* out, int reps) {
+  __shared__ double2 src[3 * kSrc];
+  {
+    const double4 v = pts[threadIdx.x];
+    const double ss = v.x * v.x + v.y * v.y + v.z * v.z;
+    src[3 * threadIdx.x] = make_double2(v.x, v.y);
+    src[3 * threadIdx.x + 1] = make_double2(v.z, ss);
+    src[3 * threadIdx.x + 2] = make_double2(v.w, 0.0);
+  }
+  Tgt tg[NT];
+  double acc[NT];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) {
+    const double4 q = pts[1024 + ((blockIdx.x * NT + t) * 128 + threadIdx.x) % (1 << 20)];
+    const double x = q.x + 3.0, y = q.y, z = q.z;
+    tg[t] = Tgt{-2.0 * x, -2.0 * y, -2.0 * z, x * x + y * y + z * z};
+    acc[t] = 0.0;
+  }
+  __syncthreads();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+    for (int j0 = 0; j0 < kSrc; j0 += NS) {
+#pragma unroll
+      for (int j = 0; j < NS; ++j) {
+        const double2 s0 = src[3 * (j0 + j)], s1 = src[3 * (j0 + j) + 1], s2 = src[3 * (j0 + j) + 2];
+        double q[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) q[t] = tg[t].tt + s1.y;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) q[t] = fma(tg[t].az, s1.x, q[t]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) q[t] = fma(tg[t].ay, s0.y, q[t]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) q[t] = fma(tg[t].ax, s0.x, q[t]);
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          double y;
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(q[t]));
+          const double h = fma(q[t] * y, y, -3.0);
+          q[t] = y * h;
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) acc[t] = fma(q[t], s2.x, acc[t]);
+      }
+    }
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) s += acc[t];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = -0.5 * s;
+}
+
 template <class F>
 float timed(F launch) {
   launch();
@@ -518,6 +575,15 @@ int main() {
            NT, NS, ms, ev / ms / 1e9, ho[5]);                                                       \
   }
   PTXC(2, 4) PTXC(4, 2) PTXC(4, 4) PTXC(2, 2) PTXC(4, 1)
+#define WIDE(NT, NS)                                                                                \
+  {                                                                                                 \
+    const int bl = blocks * 2 / NT;                                                                 \
+    const float ms = timed([&] { core_wide<NT, NS><<<bl, 128>>>(pts, out, reps); });                \
+    const double ev = double(bl) * 128 * NT * kSrc * reps;                                          \
+    printf("wide core %d targets/thread, %d sources per trip (no unroll): %.3f ms, %.3f T evals/s\n", NT, NS, ms, \
+           ev / ms / 1e9);                                                                          \
+  }
+  WIDE(4, 1) WIDE(8, 1) WIDE(8, 2) WIDE(4, 2) WIDE(6, 1) WIDE(6, 2)
   printf("status: %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
   return 0;
 }
