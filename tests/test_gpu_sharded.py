@@ -67,6 +67,38 @@ def test_shards_reproduce_single_gpu_variants(h3d, oracle, world, variant):
     assert rel(b, oracle.dense_matvec(pts, x)) <= 10 * opt.epsilon
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_shards_reproduce_single_gpu_clustered(h3d, oracle, world):
+    # clustered points: unbalanced Morton subtrees (some shards own few or no
+    # rows), empty leaves, leaves above one near pass, cross-shard near pairs
+    rng = np.random.default_rng(321)
+    centres = rng.uniform(-0.7, 0.7, size=(5, 3))
+    n = 8000
+    pts = centres[rng.integers(0, 5, n)] + 0.15 * rng.standard_normal((n, 3))
+    pts = np.ascontiguousarray(np.clip(pts, -0.999, 0.999))
+    x = h3d.random_vector(n, 19)
+    # the same explicit representation on every shard (auto scores each
+    # shard's own levels and may pick differently from the single-GPU build)
+    opt = h3d.HmatOptions(n_max=64, epsilon=1e-7, mode_policy="explicit", level_modes=(0,) + (1,) * 15)
+    lap = h3d.make_kernel("laplace3d")
+    ref = h3d.initialize(pts, lap, options=opt)
+    b1 = ref.matvec(x)
+    perm = ref.perm()
+    b = np.full(n, np.nan)
+    rows_seen = 0
+    for r in range(world):
+        rep = h3d.initialize(pts, lap, options=opt, shard_rank=r, shard_world=world)
+        st = rep.stats()
+        own = perm[st["owned_row_begin"]:st["owned_row_end"]]
+        rows_seen += len(own)
+        if len(own):
+            b[own] = rep.matvec(x)[own]
+        rep.close()
+    assert rows_seen == n and not np.isnan(b).any()
+    assert rel(b, b1) <= 1e-12
+    assert rel(b, oracle.dense_matvec(pts, x)) <= 10 * opt.epsilon
+
+
 def test_nccl_exchange_path_world1(h3d):
     # The multi-GPU exchange (own slice of x in Morton order, one NCCL
     # broadcast per rank slice in a group, repack of the source records) run
